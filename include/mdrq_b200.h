@@ -1,0 +1,168 @@
+/*
+ * mdrq_b200.h -- C ABI of the B200-native MDRQ scan engine (libmdrq_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (streams are passed as opaque `void*` = cudaStream_t, NULL = the store's
+ * own stream).  Every call returns MDRQ_OK (0) or a negative status; the
+ * message of the last failure on the calling thread is mdrq_last_error().
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/mdrq/):
+ *
+ *   Kernel-backend level (kernels.py:34-46, the MDRQ_BACKEND plugin slot):
+ *     mdrq_match_rows   <- _kernels_cy.pyx:49-55  match_row (batched)
+ *     mdrq_scan_rows    <- _kernels_cy.pyx:58-86  scan_rows
+ *     mdrq_scan_column  <- _kernels_cy.pyx:89-120 scan_column
+ *     mdrq_and_masks    <- scan.py:55-78          and_masks_chunked
+ *     mdrq_mask_popcount<- scan.py:81-82          mask_popcount
+ *     mdrq_mask_to_ids  <- scan.py:85-88          mask_to_ids
+ *
+ *   Access-method level (methods.py:20-47 build_method + the AccessMethod
+ *   protocol .search / .search_with_stats of scan.py:91-214, vafile.py:88-219):
+ *     mdrq_store_create   <- SequentialScan/VerticalScan.__init__ (scan.py:94,
+ *                            174-181), ColumnSet.from_dataset (scan.py:35-37),
+ *                            VaFile.build (vafile.py:106-147)
+ *     mdrq_query_count    <- len(method.search(q))  (bench.py:176)
+ *     mdrq_query_ids      <- method.search(q).ids   (scan.py:103-111, 187-211,
+ *                            vafile.py:201-219)
+ *     mdrq_query_stats    <- SearchStats counters of search_with_stats
+ *                            (core.py:218-237)
+ *     mdrq_store_va_boundaries <- VaGrid (vafile.py:25-64) -- here a quantile
+ *                            grid, see DESIGN.md
+ */
+#ifndef MDRQ_B200_H
+#define MDRQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDRQ_ABI_VERSION 1
+
+/* status codes */
+#define MDRQ_OK          0
+#define MDRQ_EINVAL     -1   /* bad argument (maps to ValueError)            */
+#define MDRQ_ECUDA      -2   /* CUDA runtime failure (RuntimeError)          */
+#define MDRQ_ENOMEM     -3   /* device/host allocation failed (MemoryError)  */
+#define MDRQ_ETRUNC     -4   /* output buffer too small; *total holds need   */
+#define MDRQ_ENODEV     -5   /* no CUDA device / bad ordinal                 */
+
+/* store layouts (bit set) */
+#define MDRQ_LAYOUT_COLUMNAR 1u   /* m contiguous float32 columns            */
+#define MDRQ_LAYOUT_ROWWISE  2u   /* row-major float32 n x m                 */
+#define MDRQ_LAYOUT_VAFILE   4u   /* per-dim quantile-grid codes (+columns)  */
+
+/* query paths */
+#define MDRQ_PATH_AUTO           0u
+#define MDRQ_PATH_COLUMNAR       1u  /* one query per pass, dim-at-a-time, skip */
+#define MDRQ_PATH_ROWWISE        2u  /* bulk-copy staged row tiles            */
+#define MDRQ_PATH_VAFILE         3u  /* quantile-code filter + exact refine   */
+#define MDRQ_PATH_COLUMNAR_BATCH 4u  /* many queries per pass over the columns */
+
+/* kernel modes (core.py:29-44 KernelMode; affect only early-break stats) */
+#define MDRQ_MODE_SCALAR  0
+#define MDRQ_MODE_BLOCKED 1
+
+typedef struct mdrq_store mdrq_store;
+
+typedef struct mdrq_store_info {
+    uint64_t n;            /* tuples in this store (shard)                  */
+    uint32_t m;            /* dimensions                                    */
+    uint32_t layouts;      /* MDRQ_LAYOUT_* bits present                    */
+    uint32_t va_bits;      /* bits per dimension of the VA-file codes (0 = none) */
+    int32_t  device;       /* CUDA ordinal                                  */
+    uint64_t n_pad;        /* padded tuple count of the device arrays       */
+    uint64_t device_bytes; /* HBM held by the store (data + scratch)        */
+} mdrq_store_info;
+
+/* per-query counters, mirroring SearchStats (core.py:218-237) */
+typedef struct mdrq_search_stats {
+    uint64_t objects_compared;
+    uint64_t nodes_visited;    /* VA-file: tuples refined (exact compares)  */
+    uint64_t columns_scanned;
+    uint64_t early_breaks;     /* row-wise path only                        */
+    uint64_t and_chunks;       /* tiles the fused AND ran over              */
+} mdrq_search_stats;
+
+/* -- library ------------------------------------------------------------ */
+const char* mdrq_last_error(void);
+int mdrq_abi_version(void);
+int mdrq_device_count(int* count);
+
+/* -- kernel-backend level: host buffers in and out (parity / tests) ------ */
+/* match_row for `nrows` rows against one query: out[r] = 1 match / 0 not.  */
+int mdrq_match_rows(const float* rows, uint64_t nrows, uint32_t m,
+                    const float* lower, const float* upper, int device,
+                    uint8_t* out);
+/* scan_rows: ascending local ids (int64, capacity n), match count, early
+ * breaks under `mode` exactly as _kernels_cy.pyx:23-46 counts them.        */
+int mdrq_scan_rows(const float* values, uint64_t n, uint32_t m,
+                   const float* lower, const float* upper, int mode, int device,
+                   int64_t* ids_out, uint64_t* count_out, uint64_t* early_out);
+/* scan_column: little-endian packed bitmask of lo <= v <= hi, ceil(n/8) B. */
+int mdrq_scan_column(const float* col, uint64_t n, float lo, float hi,
+                     int device, uint8_t* mask_out);
+/* AND of k masks of nbytes each (masks[j] are host pointers).              */
+int mdrq_and_masks(const uint8_t* const* masks, uint32_t k, uint64_t nbytes,
+                   int device, uint8_t* out);
+int mdrq_mask_popcount(const uint8_t* mask, uint64_t nbytes, int device,
+                       uint64_t* count_out);
+/* positions of the set bits among the first n, ascending, int64.          */
+int mdrq_mask_to_ids(const uint8_t* mask, uint64_t n, int device,
+                     int64_t* ids_out, uint64_t* count_out);
+
+/* -- device-resident store ------------------------------------------------ */
+/* rows: host, row-major float32 n x m (NaN-free; checked by the caller's
+ * DataSet).  id_base is added to every emitted id (row-sharded stores).    */
+int mdrq_store_create(const float* rows, uint64_t n, uint32_t m, int device,
+                      uint32_t layouts, uint32_t va_bits, uint64_t id_base,
+                      mdrq_store** out);
+int mdrq_store_destroy(mdrq_store* s);
+int mdrq_store_get_info(const mdrq_store* s, mdrq_store_info* info);
+/* VA-file boundaries, m x (2^va_bits - 1) float32, sorted per dimension.  */
+int mdrq_store_va_boundaries(const mdrq_store* s, float* out);
+/* observed per-dimension [min, max] (core.py:99-105), m x 2 float32.       */
+int mdrq_store_bounds(const mdrq_store* s, float* out);
+
+/* One batch of nq queries, lower/upper host float32 [nq][m] with the
+ * reference's +-inf sentinels for unqueried dimensions (core.py:25-26,125). */
+int mdrq_query_count(mdrq_store* s, const float* lower, const float* upper,
+                     uint32_t nq, uint32_t path, uint64_t* counts);
+/* ids mode: offsets[nq+1] (exclusive prefix), ids ascending per query.
+ * When *total > ids_cap the call returns MDRQ_ETRUNC after filling offsets
+ * and *total; the results stay cached and mdrq_fetch_ids() copies them.    */
+int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper,
+                   uint32_t nq, uint32_t path, uint64_t* offsets,
+                   uint32_t* ids, uint64_t ids_cap, uint64_t* total);
+int mdrq_fetch_ids(mdrq_store* s, uint32_t* ids, uint64_t ids_cap);
+/* SearchStats of the last count/ids call, one entry per query.            */
+int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats,
+                     uint32_t nq);
+
+/* -- prepared (device-resident) batches: the timed path of bench.py ------ */
+typedef struct mdrq_batch mdrq_batch;
+int mdrq_batch_prepare(mdrq_store* s, const float* lower, const float* upper,
+                       uint32_t nq, uint32_t path, mdrq_batch** out);
+int mdrq_batch_destroy(mdrq_batch* b);
+/* enqueue a count pass on `stream`; counts are device u64[nq] (no sync).   */
+int mdrq_batch_count_async(mdrq_store* s, mdrq_batch* b, uint64_t* d_counts,
+                           void* stream);
+/* enqueue an ids pass on `stream` into the store's result buffers; no sync.
+ * The output capacity is grown by mdrq_batch_reserve (a synchronising call). */
+int mdrq_batch_ids_async(mdrq_store* s, mdrq_batch* b, void* stream);
+/* run once synchronously, size the result buffers for this batch, and
+ * report the total ids it produces.                                        */
+int mdrq_batch_reserve(mdrq_store* s, mdrq_batch* b, uint64_t* total);
+/* device pointers to the last ids pass: ids u32[total], offsets u64[nq+1]. */
+int mdrq_result_device(mdrq_store* s, uint64_t* d_ids, uint64_t* d_offsets,
+                       uint64_t* total);
+/* number of kernels one count / ids pass of this batch launches.          */
+int mdrq_batch_launches(mdrq_batch* b, int ids_mode, uint32_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MDRQ_B200_H */

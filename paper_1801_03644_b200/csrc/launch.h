@@ -1,0 +1,94 @@
+// launch.h -- host-side launch wrappers shared between the kernel TUs and
+// the C-ABI layer (store.cu).  Internal; not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace mdrq {
+
+// Padding of the device arrays: every column / code plane holds n_pad
+// entries, n_pad a multiple of kPadTuples; pad values are NaN (columns and
+// rows) so they never satisfy lo <= v <= hi, codes are 0 (they are also
+// masked by n).
+constexpr uint64_t kPadTuples = 8192;
+
+struct ScanArgs {
+    const float* cols;       // columnar store [m][stride]
+    const float* rows;       // row store [n_pad_rows][m]
+    const uint8_t* codes;    // VA codes [m][stride]
+    uint64_t stride;         // n_pad
+    uint64_t n;              // live tuples
+    uint32_t m;
+    uint32_t rows_per_tile;  // row-wise tile height
+    const QueryDesc* descs;  // device descriptors [nq]
+    const DimPred* preds;    // device predicates, descs[q].off .. +k
+    uint32_t q;              // query index of this launch
+    uint32_t num_tiles;
+    uint32_t* tile_counters; // [nq] zeroed per batch
+    uint64_t* status;        // look-back status [num_tiles]
+    uint32_t epoch;
+    unsigned long long* counts;   // [nq]
+    unsigned long long* offsets;  // [nq+1] ids mode (chained bases)
+    uint32_t* ids;
+    uint64_t ids_cap;
+    uint32_t id_base;
+    unsigned long long* stats;    // [nq][4]: early_scalar, early_blocked, refined, tiles
+};
+
+// multi-query pass over the columnar store (union dims, <= 32 queries)
+struct BatchArgs {
+    const float* cols;
+    uint64_t stride;
+    uint64_t n;
+    uint32_t kb;                 // union dims of this pass
+    uint32_t nqp;                // queries in this pass (<= 32)
+    const uint16_t* udims;       // [kb]
+    const float2* bounds;        // [nqp][kb] (lo, hi), +-inf where unconstrained
+    const unsigned long long* cmask;  // [nqp] constrained union dims (bit per union dim)
+    unsigned long long* counts;  // [nqp] (already offset to the pass)
+};
+
+constexpr int kColTile = 4096;     // tuples per CTA tile, single-query columnar
+constexpr int kVaTile = 8192;      // tuples per CTA tile, VA-file filter
+
+void launch_col_scan(const ScanArgs& a, bool ids, cudaStream_t st);
+void launch_row_scan(const ScanArgs& a, bool ids, cudaStream_t st);
+void launch_va_scan(const ScanArgs& a, bool ids, cudaStream_t st);
+void launch_col_batch_count(const BatchArgs& a, int num_sms, cudaStream_t st);
+int col_batch_max_dims();
+uint32_t row_tile_rows(uint32_t m);
+size_t row_scan_smem(uint32_t m);
+
+// store construction
+void launch_transpose_rows_to_cols(const float* rows, uint64_t n, uint32_t m, float* cols,
+                                   uint64_t stride, cudaStream_t st);
+void launch_fill_f32(float* p, uint64_t count, float v, cudaStream_t st);
+void launch_va_sample(const float* col, uint64_t n, uint64_t step, uint64_t count, float* out,
+                      cudaStream_t st);
+void launch_va_pick_boundaries(const float* sorted, uint64_t count, uint32_t nbins, float* out,
+                               cudaStream_t st);
+void launch_va_encode(const float* col, uint64_t n_pad, const float* bounds, uint32_t nb,
+                      uint8_t* codes, cudaStream_t st);
+// sort `count` floats (ascending), temp storage sized by the helper
+size_t va_sort_temp_bytes(uint64_t count);
+void va_sort(const float* in, float* out, uint64_t count, void* temp, size_t temp_bytes,
+             cudaStream_t st);
+void launch_min_max(const float* col, uint64_t n, float* out2, cudaStream_t st);
+
+// kernel-backend helpers (scan_column & mask algebra)
+void launch_scan_column_mask(const float* col, uint64_t n, float lo, float hi, uint32_t* mask_words,
+                             cudaStream_t st);
+void launch_and_masks(const uint32_t* const* masks, uint32_t k, uint64_t nwords, uint32_t* out,
+                      cudaStream_t st);
+void launch_popcount(const uint32_t* words, uint64_t nwords, unsigned long long* out,
+                     cudaStream_t st);
+void launch_mask_to_ids(const uint32_t* words, uint64_t n, uint32_t* status_scratch,
+                        uint64_t* status, uint32_t epoch, uint32_t* tile_counter,
+                        unsigned long long* count, int64_t* ids, cudaStream_t st);
+void launch_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lo,
+                       const float* hi, uint8_t* out, cudaStream_t st);
+
+}  // namespace mdrq

@@ -1,0 +1,182 @@
+// masks.cu -- the kernel-backend primitives of the reference's columnar scan
+// (the MDRQ_BACKEND plugin level, reference kernels.py:34-46) on sm_100a:
+//
+//   scan_column_mask   <- _kernels_cy.pyx:89-120  (lo <= v <= hi -> packed
+//                          little-endian bitmask; bit i of byte b = tuple 8b+i,
+//                          i.e. bit i of 32-bit word w = tuple 32w+i)
+//   and_masks          <- scan.py:55-78           (and_masks_chunked)
+//   popcount           <- scan.py:81-82           (mask_popcount)
+//   mask_to_ids        <- scan.py:85-88           (ordered compaction)
+//   match_rows         <- _kernels_cy.pyx:49-55   (match_row, one row/thread)
+//
+// The access-method executors never materialise these masks (the fused
+// kernels keep them in registers); these entry points exist so the
+// reference's kernel-level API and tests have a GPU backend.
+#include "launch.h"
+
+namespace mdrq {
+
+namespace {
+
+__global__ void scan_column_mask_kernel(const float* __restrict__ col, uint64_t n, float lo, float hi,
+                                        uint32_t* __restrict__ words) {
+    const uint64_t nwords = (n + 31) / 32;
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); w < nwords;
+         w += uint64_t(gridDim.x) * (blockDim.x / 32)) {
+        const uint64_t i = w * 32 + (threadIdx.x & 31u);
+        bool in = false;
+        if (i < n) {
+            const float v = col[i];
+            in = (lo <= v) & (v <= hi);
+        }
+        const uint32_t b = __ballot_sync(0xFFFFFFFFu, in);
+        if ((threadIdx.x & 31u) == 0) words[w] = b;
+    }
+}
+
+struct MaskList {
+    const uint32_t* p[16];
+};
+
+__global__ void and_masks_kernel(MaskList ml, uint32_t k, uint64_t nwords, uint32_t* __restrict__ out) {
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < nwords;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t acc = ml.p[0][w];
+        for (uint32_t j = 1; j < k; ++j) acc &= ml.p[j][w];
+        out[w] = acc;
+    }
+}
+
+__global__ void popcount_kernel(const uint32_t* __restrict__ words, uint64_t nwords,
+                                unsigned long long* out) {
+    unsigned long long c = 0;
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < nwords;
+         w += uint64_t(gridDim.x) * blockDim.x)
+        c += __popc(words[w]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if ((threadIdx.x & 31u) == 0 && c) atomicAdd(out, c);
+}
+
+// ordered mask -> ids: tile = 256 threads x 1 word (8192 tuples), per-warp
+// ballot-free ranks from popc, block scan, decoupled look-back.
+__global__ void __launch_bounds__(256) mask_to_ids_kernel(const uint32_t* __restrict__ words, uint64_t n,
+                                                          uint64_t* status, uint32_t epoch,
+                                                          uint32_t* tile_counter, uint32_t num_tiles,
+                                                          unsigned long long* count,
+                                                          int64_t* __restrict__ ids) {
+    __shared__ uint32_t s_tile, s_excl;
+    __shared__ uint32_t s_warp[8];
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t w = uint64_t(tile) * 256 + threadIdx.x;
+    const uint64_t nwords = (n + 31) / 32;
+    uint32_t bits = 0;
+    if (w < nwords) {
+        bits = words[w];
+        if ((w + 1) * 32 > n) bits &= (n % 32) ? ((1u << (n % 32)) - 1u) : 0xFFFFFFFFu;
+    }
+    const uint32_t c = __popc(bits);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= uint32_t(o)) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t v = lane < 8 ? s_warp[lane] : 0u;
+        uint32_t wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= uint32_t(o)) wi += t;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, wi, 31);
+        const uint32_t excl = lookback_exclusive(status, tile, epoch, total);
+        if (lane < 8) s_warp[lane] = wi - v;
+        if (lane == 0) {
+            s_excl = excl;
+            if (tile == num_tiles - 1) *count = excl + total;
+        }
+    }
+    __syncthreads();
+    uint64_t pos = uint64_t(s_excl) + s_warp[warp] + (incl - c);
+    while (bits) {
+        const int j = __ffs(bits) - 1;
+        bits &= bits - 1;
+        ids[pos++] = int64_t(w * 32 + j);
+    }
+}
+
+__global__ void match_rows_kernel(const float* __restrict__ rows, uint64_t nrows, uint32_t m,
+                                  const float* __restrict__ lo, const float* __restrict__ hi,
+                                  uint8_t* __restrict__ out) {
+    for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < nrows;
+         r += uint64_t(gridDim.x) * blockDim.x) {
+        bool ok = true;
+        for (uint32_t j = 0; j < m; ++j) {
+            const float v = rows[r * m + j];
+            ok = ok & (lo[j] <= v) & (v <= hi[j]);
+        }
+        out[r] = ok ? 1 : 0;
+    }
+}
+
+unsigned grid_for(uint64_t work, unsigned per_block) {
+    uint64_t b = (work + per_block - 1) / per_block;
+    if (b > 148ull * 32) b = 148ull * 32;
+    return unsigned(b ? b : 1);
+}
+
+}  // namespace
+
+void launch_scan_column_mask(const float* col, uint64_t n, float lo, float hi, uint32_t* mask_words,
+                             cudaStream_t st) {
+    if (!n) return;
+    scan_column_mask_kernel<<<grid_for((n + 31) / 32, 8), 256, 0, st>>>(col, n, lo, hi, mask_words);
+}
+
+void launch_and_masks(const uint32_t* const* masks, uint32_t k, uint64_t nwords, uint32_t* out,
+                      cudaStream_t st) {
+    if (!nwords) return;
+    // fold 16 at a time
+    MaskList ml{};
+    uint32_t done = 0;
+    bool first = true;
+    while (done < k) {
+        uint32_t c = 0;
+        if (!first) ml.p[c++] = out;
+        while (c < 16 && done < k) ml.p[c++] = masks[done++];
+        and_masks_kernel<<<grid_for(nwords, 256), 256, 0, st>>>(ml, c, nwords, out);
+        first = false;
+    }
+}
+
+void launch_popcount(const uint32_t* words, uint64_t nwords, unsigned long long* out, cudaStream_t st) {
+    cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+    if (!nwords) return;
+    popcount_kernel<<<grid_for(nwords, 256), 256, 0, st>>>(words, nwords, out);
+}
+
+void launch_mask_to_ids(const uint32_t* words, uint64_t n, uint32_t* /*unused*/, uint64_t* status,
+                        uint32_t epoch, uint32_t* tile_counter, unsigned long long* count, int64_t* ids,
+                        cudaStream_t st) {
+    const uint64_t nwords = (n + 31) / 32;
+    const uint32_t tiles = uint32_t((nwords + 255) / 256);
+    cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+    cudaMemsetAsync(tile_counter, 0, sizeof(uint32_t), st);
+    if (!tiles) return;
+    mask_to_ids_kernel<<<tiles, 256, 0, st>>>(words, n, status, epoch, tile_counter, tiles, count, ids);
+}
+
+void launch_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lo, const float* hi,
+                       uint8_t* out, cudaStream_t st) {
+    if (!nrows) return;
+    match_rows_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(rows, nrows, m, lo, hi, out);
+}
+
+}  // namespace mdrq

@@ -1,0 +1,1069 @@
+// store.cu -- the C ABI (include/mdrq_b200.h) of the B200 MDRQ scan engine:
+// device-resident stores, query preparation, launch orchestration and the
+// kernel-backend entry points.
+//
+// Reference anchors (relative to /root/reference/pkg/src/mdrq/):
+//   DataSet / RangeQuery validation         core.py:56-174
+//   queried dims = not (lo == -inf and hi == +inf)          core.py:125
+//   lo > hi on a queried dim raises                        core.py:126-132
+//   SequentialScan / HorizontalScan / VerticalScan         scan.py:91-214
+//   VaFile filter + refine                                 vafile.py:88-219
+//   SearchStats counters                                   core.py:218-237
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+#include "mdrq_b200.h"
+
+namespace mdrq {
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (e == cudaErrorMemoryAllocation) raise(MDRQ_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+        if (e == cudaErrorNoDevice || e == cudaErrorInvalidDevice || e == cudaErrorInsufficientDriver)
+            raise(MDRQ_ENODEV, std::string(what) + ": " + cudaGetErrorString(e));
+        raise(MDRQ_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+#define CK(expr) ck((expr), #expr)
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return MDRQ_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return MDRQ_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MDRQ_ECUDA;
+    }
+}
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    void reserve(size_t count) {
+        if (count <= cap && p) return;
+        release();
+        size_t c = count ? count : 1;
+        CK(cudaMalloc(reinterpret_cast<void**>(&p), c * sizeof(T)));
+        cap = c;
+    }
+    size_t bytes() const { return cap * sizeof(T); }
+};
+
+uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+// ----------------------------------------------------------------- kernels --
+namespace {
+
+__global__ void fill_f32_kernel(float* p, uint64_t count, float v) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+// rows [*, m] -> cols [m][stride]; one 32-row x 32-dim tile per block
+__global__ void transpose_kernel(const float* __restrict__ rows, uint64_t n, uint32_t m,
+                                 float* __restrict__ cols, uint64_t stride) {
+    __shared__ float tile[32][33];
+    const uint64_t r0 = uint64_t(blockIdx.x) * 32;
+    const uint32_t d0 = blockIdx.y * 32;
+    for (uint32_t r = threadIdx.y; r < 32; r += blockDim.y) {
+        const uint64_t row = r0 + r;
+        const uint32_t d = d0 + threadIdx.x;
+        if (row < n && d < m) tile[r][threadIdx.x] = rows[row * m + d];
+    }
+    __syncthreads();
+    for (uint32_t dd = threadIdx.y; dd < 32; dd += blockDim.y) {
+        const uint32_t d = d0 + dd;
+        const uint64_t row = r0 + threadIdx.x;
+        if (row < n && d < m) cols[uint64_t(d) * stride + row] = tile[threadIdx.x][dd];
+    }
+}
+
+}  // namespace
+
+void launch_fill_f32(float* p, uint64_t count, float v, cudaStream_t st) {
+    if (!count) return;
+    uint64_t b = (count + 255) / 256;
+    if (b > 148 * 32) b = 148 * 32;
+    fill_f32_kernel<<<unsigned(b), 256, 0, st>>>(p, count, v);
+}
+
+void launch_transpose_rows_to_cols(const float* rows, uint64_t n, uint32_t m, float* cols, uint64_t stride,
+                                   cudaStream_t st) {
+    if (!n) return;
+    dim3 grid(unsigned((n + 31) / 32), (m + 31) / 32);
+    transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, n, m, cols, stride);
+}
+
+}  // namespace mdrq
+
+using namespace mdrq;
+
+// ------------------------------------------------------------------ batches --
+namespace {
+
+struct Pass {
+    uint32_t q0 = 0, nqp = 0, kb = 0;
+    bool fallback = false;   // union too wide for the batch kernel
+    size_t udim_off = 0, bound_off = 0, cmask_off = 0;
+};
+
+}  // namespace
+
+struct mdrq_batch {
+    mdrq_store* owner = nullptr;
+    uint32_t nq = 0;
+    uint32_t path = 0;
+    std::vector<QueryDesc> descs;
+    std::vector<DimPred> preds;
+    std::vector<Pass> passes;
+    std::vector<uint16_t> udims;
+    std::vector<float2> bounds;
+    std::vector<unsigned long long> cmask;
+    // device copies + per-batch scratch
+    DBuf<QueryDesc> d_descs;
+    DBuf<DimPred> d_preds;
+    DBuf<uint16_t> d_udims;
+    DBuf<float2> d_bounds;
+    DBuf<unsigned long long> d_cmask;
+    DBuf<uint32_t> d_tile_counters;
+    DBuf<unsigned long long> d_counts;
+    DBuf<unsigned long long> d_offsets;
+    DBuf<unsigned long long> d_stats;
+};
+
+struct mdrq_store {
+    int device = 0;
+    int num_sms = 148;
+    uint64_t n = 0, n_pad = 0, n_pad_rows = 0;
+    uint32_t m = 0, layouts = 0, va_bits = 0, R = 0;
+    uint32_t id_base = 0;
+    cudaStream_t stream = nullptr;
+    DBuf<float> cols, rows;
+    DBuf<uint8_t> codes;
+    DBuf<float> va_bounds;
+    std::vector<float> h_va_bounds;  // [m][nb]
+    std::vector<float> h_minmax;     // [m][2]
+    DBuf<uint64_t> status;
+    uint32_t epoch = 0;
+    DBuf<uint32_t> ids;              // result pool
+    uint64_t last_total = 0;
+    uint32_t last_nq = 0;
+    uint32_t last_path = 0;
+    mdrq_batch* last_batch = nullptr;
+    mdrq_batch scratch;
+    std::mutex mu;
+
+    uint32_t nb() const { return va_bits ? ((1u << va_bits) - 1u) : 0u; }
+    uint32_t tiles_for(uint32_t path) const {
+        switch (path) {
+            case MDRQ_PATH_ROWWISE: return uint32_t((n + R - 1) / R);
+            case MDRQ_PATH_VAFILE: return uint32_t((n + kVaTile - 1) / kVaTile);
+            default: return uint32_t((n + kColTile - 1) / kColTile);
+        }
+    }
+    uint32_t next_epoch() {
+        ++epoch;
+        if (epoch >= (1u << 30)) {
+            CK(cudaMemsetAsync(status.p, 0, status.bytes(), stream));
+            epoch = 1;
+        }
+        return epoch;
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CK(cudaGetDevice(&prev));
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_neg_inf(float v) { return std::isinf(v) && v < 0; }
+bool is_pos_inf(float v) { return std::isinf(v) && v > 0; }
+
+uint16_t host_code(const float* b, uint32_t nb, float v) {
+    // #{b <= v}; b sorted ascending under float compare
+    return uint16_t(std::upper_bound(b, b + nb, v, [](float x, float y) { return x < y; }) - b);
+}
+
+// Build the host descriptors of a batch.  strict = reference RangeQuery
+// semantics (lo > hi on a queried dimension raises); the kernel-level entry
+// points pass strict = false (scan_rows accepts any bounds).
+void build_descs(const mdrq_store* s, const float* lo, const float* hi, uint32_t nq, uint32_t path, bool strict,
+                 mdrq_batch* b) {
+    const uint32_t m = s->m;
+    b->nq = nq;
+    b->path = path;
+    b->descs.assign(nq, QueryDesc{0, 0});
+    b->preds.clear();
+    b->passes.clear();
+    b->udims.clear();
+    b->bounds.clear();
+    b->cmask.clear();
+    const uint32_t nb = s->nb();
+    std::vector<std::pair<float, uint32_t>> order;
+    for (uint32_t q = 0; q < nq; ++q) {
+        const float* ql = lo + uint64_t(q) * m;
+        const float* qh = hi + uint64_t(q) * m;
+        order.clear();
+        for (uint32_t j = 0; j < m; ++j) {
+            const float l = ql[j], h = qh[j];
+            if (std::isnan(l) || std::isnan(h)) raise(MDRQ_EINVAL, "NaN query bounds are not allowed");
+            const bool queried = !(is_neg_inf(l) && is_pos_inf(h));
+            if (!queried) continue;
+            if (strict && l > h) {
+                char buf[160];
+                snprintf(buf, sizeof buf, "lower bound exceeds upper bound in dimension %u: %g > %g", j, double(l),
+                         double(h));
+                raise(MDRQ_EINVAL, buf);
+            }
+            // estimated pass fraction, used only to order the evaluation
+            float est = 1.0f;
+            if (nb && !s->h_va_bounds.empty()) {
+                const float* bd = s->h_va_bounds.data() + size_t(j) * nb;
+                est = float(int(host_code(bd, nb, h)) - int(host_code(bd, nb, l)) + 1) / float(nb + 1);
+            } else if (!s->h_minmax.empty()) {
+                const float mn = s->h_minmax[2 * j], mx = s->h_minmax[2 * j + 1];
+                const double w = double(mx) - double(mn);
+                if (w > 0 && std::isfinite(w)) {
+                    const double a = std::max(double(l), double(mn)), c = std::min(double(h), double(mx));
+                    est = float(std::max(0.0, c - a) / w);
+                }
+            }
+            order.emplace_back(path == MDRQ_PATH_ROWWISE ? float(j) : est, j);
+        }
+        std::stable_sort(order.begin(), order.end(),
+                         [](const std::pair<float, uint32_t>& x, const std::pair<float, uint32_t>& y) {
+                             return x.first < y.first;
+                         });
+        b->descs[q].k = uint32_t(order.size());
+        b->descs[q].off = uint32_t(b->preds.size());
+        for (auto& e : order) {
+            const uint32_t j = e.second;
+            DimPred p{};
+            p.lo = ql[j];
+            p.hi = qh[j];
+            p.dim = uint16_t(j);
+            if (nb) {
+                const float* bd = s->h_va_bounds.data() + size_t(j) * nb;
+                p.cl = host_code(bd, nb, p.lo);
+                p.ch = host_code(bd, nb, p.hi);
+                p.edge_lo = is_neg_inf(p.lo) ? 0 : 1;
+                p.edge_hi = is_pos_inf(p.hi) ? 0 : 1;
+                if (p.lo > p.hi) {  // kernel-level only: empty interval, reject every code
+                    p.cl = uint16_t(nb + 1);
+                    p.ch = 0;
+                }
+            }
+            b->preds.push_back(p);
+        }
+    }
+    if (path == MDRQ_PATH_COLUMNAR_BATCH) {
+        const int maxkb = col_batch_max_dims();
+        for (uint32_t q0 = 0; q0 < nq; q0 += 32) {
+            Pass ps;
+            ps.q0 = q0;
+            ps.nqp = std::min<uint32_t>(32, nq - q0);
+            std::vector<uint8_t> used(m, 0);
+            for (uint32_t q = q0; q < q0 + ps.nqp; ++q)
+                for (uint32_t i = 0; i < b->descs[q].k; ++i) used[b->preds[b->descs[q].off + i].dim] = 1;
+            std::vector<int> uidx(m, -1);
+            std::vector<uint16_t> ud;
+            for (uint32_t j = 0; j < m; ++j)
+                if (used[j]) {
+                    uidx[j] = int(ud.size());
+                    ud.push_back(uint16_t(j));
+                }
+            ps.kb = uint32_t(ud.size());
+            if (int(ps.kb) > maxkb) {
+                ps.fallback = true;
+                b->passes.push_back(ps);
+                continue;
+            }
+            ps.udim_off = b->udims.size();
+            ps.bound_off = b->bounds.size();
+            ps.cmask_off = b->cmask.size();
+            b->udims.insert(b->udims.end(), ud.begin(), ud.end());
+            for (uint32_t q = q0; q < q0 + ps.nqp; ++q) {
+                std::vector<float2> row(ps.kb, make_float2(-INFINITY, INFINITY));
+                unsigned long long cm = 0;
+                for (uint32_t i = 0; i < b->descs[q].k; ++i) {
+                    const DimPred& p = b->preds[b->descs[q].off + i];
+                    const int u = uidx[p.dim];
+                    row[u] = make_float2(p.lo, p.hi);
+                    cm |= 1ull << u;
+                }
+                b->bounds.insert(b->bounds.end(), row.begin(), row.end());
+                b->cmask.push_back(cm);
+            }
+            b->passes.push_back(ps);
+        }
+    }
+}
+
+template <class T>
+void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
+    d.reserve(h.size());
+    if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+void upload_batch(mdrq_store* s, mdrq_batch* b) {
+    upload(b->d_descs, b->descs, s->stream);
+    upload(b->d_preds, b->preds, s->stream);
+    upload(b->d_udims, b->udims, s->stream);
+    upload(b->d_bounds, b->bounds, s->stream);
+    upload(b->d_cmask, b->cmask, s->stream);
+    b->d_tile_counters.reserve(b->nq);
+    b->d_counts.reserve(b->nq);
+    b->d_offsets.reserve(size_t(b->nq) + 1);
+    b->d_stats.reserve(size_t(b->nq) * 4);
+    // H2D copies above may read pageable host vectors that a later rebuild
+    // mutates: make them complete before returning.
+    CK(cudaStreamSynchronize(s->stream));
+}
+
+uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
+    if (path == MDRQ_PATH_AUTO) {
+        if (!(s->layouts & MDRQ_LAYOUT_COLUMNAR)) return MDRQ_PATH_ROWWISE;
+        if (!ids && nq >= 2) return MDRQ_PATH_COLUMNAR_BATCH;
+        return MDRQ_PATH_COLUMNAR;
+    }
+    switch (path) {
+        case MDRQ_PATH_COLUMNAR:
+        case MDRQ_PATH_COLUMNAR_BATCH:
+            if (!(s->layouts & MDRQ_LAYOUT_COLUMNAR)) raise(MDRQ_EINVAL, "store has no columnar layout");
+            return path;
+        case MDRQ_PATH_ROWWISE:
+            if (!(s->layouts & MDRQ_LAYOUT_ROWWISE)) raise(MDRQ_EINVAL, "store has no row-wise layout");
+            return path;
+        case MDRQ_PATH_VAFILE:
+            if (!(s->layouts & MDRQ_LAYOUT_VAFILE)) raise(MDRQ_EINVAL, "store has no VA-file layout");
+            return path;
+        default: raise(MDRQ_EINVAL, "unknown query path " + std::to_string(path));
+    }
+}
+
+ScanArgs base_args(mdrq_store* s, mdrq_batch* b, uint32_t path) {
+    ScanArgs a{};
+    a.cols = s->cols.p;
+    a.rows = s->rows.p;
+    a.codes = s->codes.p;
+    a.stride = s->n_pad;
+    a.n = s->n;
+    a.m = s->m;
+    a.rows_per_tile = s->R;
+    a.descs = b->d_descs.p;
+    a.preds = b->d_preds.p;
+    a.num_tiles = s->tiles_for(path);
+    a.tile_counters = b->d_tile_counters.p;
+    a.status = s->status.p;
+    a.counts = b->d_counts.p;
+    a.offsets = b->d_offsets.p;
+    a.ids = s->ids.p;
+    a.ids_cap = s->ids.p ? s->ids.cap : 0;
+    a.id_base = s->id_base;
+    a.stats = b->d_stats.p;
+    return a;
+}
+
+// Enqueue one count / ids pass of a prepared batch.  Returns kernel launches.
+uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
+    const uint32_t nq = b->nq;
+    if (!nq) return 0;
+    CK(cudaMemsetAsync(b->d_tile_counters.p, 0, sizeof(uint32_t) * nq, st));
+    CK(cudaMemsetAsync(b->d_counts.p, 0, sizeof(unsigned long long) * nq, st));
+    CK(cudaMemsetAsync(b->d_stats.p, 0, sizeof(unsigned long long) * nq * 4, st));
+    if (ids) CK(cudaMemsetAsync(b->d_offsets.p, 0, sizeof(unsigned long long) * (nq + 1), st));
+    if (s->n == 0) return 0;
+    uint32_t launches = 0;
+    const uint32_t path = b->path;
+    auto single = [&](uint32_t sp, uint32_t q) {
+        ScanArgs a = base_args(s, b, sp);
+        a.q = q;
+        a.epoch = s->next_epoch();
+        if (sp == MDRQ_PATH_ROWWISE)
+            launch_row_scan(a, ids, st);
+        else if (sp == MDRQ_PATH_VAFILE)
+            launch_va_scan(a, ids, st);
+        else
+            launch_col_scan(a, ids, st);
+        ++launches;
+    };
+    if (path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
+        for (const Pass& ps : b->passes) {
+            if (ps.fallback) {
+                for (uint32_t q = ps.q0; q < ps.q0 + ps.nqp; ++q) single(MDRQ_PATH_COLUMNAR, q);
+                continue;
+            }
+            BatchArgs ba{};
+            ba.cols = s->cols.p;
+            ba.stride = s->n_pad;
+            ba.n = s->n;
+            ba.kb = ps.kb;
+            ba.nqp = ps.nqp;
+            ba.udims = b->d_udims.p + ps.udim_off;
+            ba.bounds = b->d_bounds.p + ps.bound_off;
+            ba.cmask = b->d_cmask.p + ps.cmask_off;
+            ba.counts = b->d_counts.p + ps.q0;
+            launch_col_batch_count(ba, s->num_sms, st);
+            ++launches;
+        }
+    } else {
+        const uint32_t sp = path == MDRQ_PATH_COLUMNAR_BATCH ? MDRQ_PATH_COLUMNAR : path;
+        for (uint32_t q = 0; q < nq; ++q) single(sp, q);
+    }
+    CK(cudaGetLastError());
+    return launches;
+}
+
+uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
+    if (!b->nq || s->n == 0) return 0;
+    if (b->path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
+        uint32_t l = 0;
+        for (const Pass& ps : b->passes) l += ps.fallback ? ps.nqp : 1;
+        return l;
+    }
+    return b->nq;
+}
+
+// Run an ids pass synchronously, growing the result pool until it fits.
+uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        enqueue(s, b, true, s->stream);
+        unsigned long long total = 0;
+        if (b->nq && s->n)
+            CK(cudaMemcpyAsync(&total, b->d_offsets.p + b->nq, sizeof(total), cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        if (total <= (s->ids.p ? s->ids.cap : 0)) {
+            s->last_total = total;
+            s->last_nq = b->nq;
+            s->last_path = b->path;
+            s->last_batch = b;
+            return total;
+        }
+        s->ids.reserve(size_t(total + total / 8 + 4096));
+    }
+    raise(MDRQ_ECUDA, "result pool did not converge");
+}
+
+void check_store(const mdrq_store* s) {
+    if (!s) raise(MDRQ_EINVAL, "null store");
+}
+
+}  // namespace
+
+// ==================================================================== C ABI ==
+extern "C" {
+
+const char* mdrq_last_error(void) { return g_err.c_str(); }
+
+int mdrq_abi_version(void) { return MDRQ_ABI_VERSION; }
+
+int mdrq_device_count(int* count) {
+    return guard([&] {
+        if (!count) raise(MDRQ_EINVAL, "null count");
+        int c = 0;
+        cudaError_t e = cudaGetDeviceCount(&c);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        *count = c;
+    });
+}
+
+int mdrq_store_create(const float* rows, uint64_t n, uint32_t m, int device, uint32_t layouts, uint32_t va_bits,
+                      uint64_t id_base, mdrq_store** out) {
+    return guard([&] {
+        if (!out) raise(MDRQ_EINVAL, "null out");
+        *out = nullptr;
+        if (m < 1) raise(MDRQ_EINVAL, "dimensionality must be at least 1");
+        if (m > uint32_t(kMaxDims)) raise(MDRQ_EINVAL, "at most 256 dimensions are supported on the GPU");
+        if (n && !rows) raise(MDRQ_EINVAL, "null rows");
+        if (n + id_base > 0xFFFFFFFFull) raise(MDRQ_EINVAL, "store ids must fit in uint32");
+        if (layouts == 0) layouts = MDRQ_LAYOUT_COLUMNAR;
+        if (layouts & ~7u) raise(MDRQ_EINVAL, "unknown layout bits");
+        if (layouts & MDRQ_LAYOUT_VAFILE) {
+            if (va_bits < 1 || va_bits > 8) raise(MDRQ_EINVAL, "va_bits must be in 1..8");
+            layouts |= MDRQ_LAYOUT_COLUMNAR;  // exact refine reads the columns
+        } else {
+            va_bits = 0;
+        }
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            raise(MDRQ_ENODEV, "no CUDA device available");
+        }
+        if (device < 0 || device >= ndev) raise(MDRQ_ENODEV, "bad device ordinal " + std::to_string(device));
+        DeviceGuard dg(device);
+        auto* s = new mdrq_store();
+        try {
+            s->device = device;
+            s->n = n;
+            s->m = m;
+            s->layouts = layouts;
+            s->va_bits = va_bits;
+            s->id_base = uint32_t(id_base);
+            CK(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device));
+            CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+            s->n_pad = round_up(std::max<uint64_t>(n, 1), kPadTuples);
+            s->R = row_tile_rows(m);
+            s->n_pad_rows = round_up(std::max<uint64_t>(n, 1), s->R);
+            cudaStream_t st = s->stream;
+            // stage rows on the device (kept as the row-wise layout if asked)
+            s->rows.reserve(s->n_pad_rows * m);
+            if (n) CK(cudaMemcpyAsync(s->rows.p, rows, n * m * sizeof(float), cudaMemcpyHostToDevice, st));
+            launch_fill_f32(s->rows.p + n * m, (s->n_pad_rows - n) * m, NAN, st);
+            if (layouts & MDRQ_LAYOUT_COLUMNAR) {
+                s->cols.reserve(s->n_pad * m);
+                for (uint32_t d = 0; d < m; ++d)
+                    launch_fill_f32(s->cols.p + uint64_t(d) * s->n_pad + n, s->n_pad - n, NAN, st);
+                launch_transpose_rows_to_cols(s->rows.p, n, m, s->cols.p, s->n_pad, st);
+            }
+            // observed bounds (core.py:99-105), used to order predicates
+            {
+                DBuf<float> mm;
+                mm.reserve(size_t(2) * m);
+                s->h_minmax.assign(size_t(2) * m, 0.f);
+                if (n && (layouts & MDRQ_LAYOUT_COLUMNAR)) {
+                    for (uint32_t d = 0; d < m; ++d)
+                        launch_min_max(s->cols.p + uint64_t(d) * s->n_pad, n, mm.p + 2 * d, st);
+                    CK(cudaMemcpyAsync(s->h_minmax.data(), mm.p, sizeof(float) * 2 * m, cudaMemcpyDeviceToHost, st));
+                }
+                CK(cudaStreamSynchronize(st));
+            }
+            if (layouts & MDRQ_LAYOUT_VAFILE) {
+                const uint32_t nb = s->nb();
+                s->va_bounds.reserve(size_t(nb) * m);
+                s->h_va_bounds.assign(size_t(nb) * m, 0.f);
+                s->codes.reserve(s->n_pad * m);
+                if (n) {
+                    const uint64_t cnt = std::min<uint64_t>(n, 1ull << 20);
+                    const uint64_t step = n / cnt;
+                    DBuf<float> samp, sorted;
+                    DBuf<unsigned char> temp;
+                    samp.reserve(cnt);
+                    sorted.reserve(cnt);
+                    const size_t tb = va_sort_temp_bytes(cnt);
+                    temp.reserve(tb);
+                    for (uint32_t d = 0; d < m; ++d) {
+                        const float* col = s->cols.p + uint64_t(d) * s->n_pad;
+                        launch_va_sample(col, n, step, cnt, samp.p, st);
+                        va_sort(samp.p, sorted.p, cnt, temp.p, tb, st);
+                        launch_va_pick_boundaries(sorted.p, cnt, nb + 1, s->va_bounds.p + size_t(d) * nb, st);
+                        launch_va_encode(col, s->n_pad, s->va_bounds.p + size_t(d) * nb, nb,
+                                         s->codes.p + uint64_t(d) * s->n_pad, st);
+                    }
+                    CK(cudaMemcpyAsync(s->h_va_bounds.data(), s->va_bounds.p, sizeof(float) * nb * m,
+                                       cudaMemcpyDeviceToHost, st));
+                } else {
+                    CK(cudaMemsetAsync(s->va_bounds.p, 0, sizeof(float) * nb * m, st));
+                    CK(cudaMemsetAsync(s->codes.p, 0, s->n_pad * m, st));
+                }
+                CK(cudaStreamSynchronize(st));
+            }
+            if (!(layouts & MDRQ_LAYOUT_ROWWISE)) s->rows.release();
+            uint64_t tiles = std::max<uint64_t>((n + kColTile - 1) / kColTile, (n + s->R - 1) / s->R);
+            s->status.reserve(std::max<uint64_t>(tiles, 1));
+            CK(cudaMemsetAsync(s->status.p, 0, s->status.bytes(), st));
+            CK(cudaStreamSynchronize(st));
+            CK(cudaGetLastError());
+        } catch (...) {
+            if (s->stream) cudaStreamDestroy(s->stream);
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+int mdrq_store_destroy(mdrq_store* s) {
+    return guard([&] {
+        if (!s) return;
+        DeviceGuard dg(s->device);
+        cudaStreamSynchronize(s->stream);
+        cudaStream_t st = s->stream;
+        delete s;
+        cudaStreamDestroy(st);
+    });
+}
+
+int mdrq_store_get_info(const mdrq_store* s, mdrq_store_info* info) {
+    return guard([&] {
+        check_store(s);
+        if (!info) raise(MDRQ_EINVAL, "null info");
+        info->n = s->n;
+        info->m = s->m;
+        info->layouts = s->layouts;
+        info->va_bits = s->va_bits;
+        info->device = s->device;
+        info->n_pad = s->n_pad;
+        info->device_bytes = s->cols.bytes() + s->rows.bytes() + s->codes.bytes() + s->va_bounds.bytes() +
+                             s->status.bytes() + s->ids.bytes();
+    });
+}
+
+int mdrq_store_va_boundaries(const mdrq_store* s, float* out) {
+    return guard([&] {
+        check_store(s);
+        if (!s->va_bits) raise(MDRQ_EINVAL, "store has no VA-file layout");
+        if (!out) raise(MDRQ_EINVAL, "null out");
+        std::memcpy(out, s->h_va_bounds.data(), s->h_va_bounds.size() * sizeof(float));
+    });
+}
+
+int mdrq_store_bounds(const mdrq_store* s, float* out) {
+    return guard([&] {
+        check_store(s);
+        if (!out) raise(MDRQ_EINVAL, "null out");
+        std::memcpy(out, s->h_minmax.data(), s->h_minmax.size() * sizeof(float));
+    });
+}
+
+int mdrq_query_count(mdrq_store* s, const float* lower, const float* upper, uint32_t nq, uint32_t path,
+                     uint64_t* counts) {
+    return guard([&] {
+        check_store(s);
+        if (nq && (!lower || !upper || !counts)) raise(MDRQ_EINVAL, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        mdrq_batch* b = &s->scratch;
+        b->owner = s;
+        build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false), true, b);
+        upload_batch(s, b);
+        enqueue(s, b, false, s->stream);
+        if (nq) CK(cudaMemcpyAsync(counts, b->d_counts.p, sizeof(uint64_t) * nq, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        s->last_batch = b;
+        s->last_nq = nq;
+        s->last_path = b->path;
+    });
+}
+
+int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper, uint32_t nq, uint32_t path,
+                   uint64_t* offsets, uint32_t* ids, uint64_t ids_cap, uint64_t* total) {
+    int trunc = 0;
+    int rc = guard([&] {
+        check_store(s);
+        if (!offsets || !total) raise(MDRQ_EINVAL, "null argument");
+        if (nq && (!lower || !upper)) raise(MDRQ_EINVAL, "null bounds");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        mdrq_batch* b = &s->scratch;
+        b->owner = s;
+        build_descs(s, lower, upper, nq, resolve_path(s, path, nq, true), true, b);
+        upload_batch(s, b);
+        const uint64_t tot = run_ids_sync(s, b);
+        *total = tot;
+        if (nq && s->n) {
+            CK(cudaMemcpyAsync(offsets, b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
+                               s->stream));
+        } else {
+            std::memset(offsets, 0, sizeof(uint64_t) * (size_t(nq) + 1));
+        }
+        if (tot > ids_cap) {
+            trunc = 1;
+        } else if (tot) {
+            if (!ids) raise(MDRQ_EINVAL, "null ids");
+            CK(cudaMemcpyAsync(ids, s->ids.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost, s->stream));
+        }
+        CK(cudaStreamSynchronize(s->stream));
+    });
+    if (rc == MDRQ_OK && trunc) {
+        g_err = "ids buffer too small";
+        return MDRQ_ETRUNC;
+    }
+    return rc;
+}
+
+int mdrq_fetch_ids(mdrq_store* s, uint32_t* ids, uint64_t ids_cap) {
+    return guard([&] {
+        check_store(s);
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        if (s->last_total > ids_cap) raise(MDRQ_ETRUNC, "ids buffer too small");
+        if (s->last_total) {
+            if (!ids) raise(MDRQ_EINVAL, "null ids");
+            CK(cudaMemcpyAsync(ids, s->ids.p, sizeof(uint32_t) * s->last_total, cudaMemcpyDeviceToHost, s->stream));
+            CK(cudaStreamSynchronize(s->stream));
+        }
+    });
+}
+
+int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats, uint32_t nq) {
+    return guard([&] {
+        check_store(s);
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        mdrq_batch* b = s->last_batch;
+        if (!b || b->nq != nq) raise(MDRQ_EINVAL, "no query batch of that size to report");
+        if (nq && !stats) raise(MDRQ_EINVAL, "null stats");
+        std::vector<unsigned long long> dev(size_t(nq) * 4, 0);
+        if (nq && s->n)
+            CK(cudaMemcpyAsync(dev.data(), b->d_stats.p, sizeof(unsigned long long) * 4 * nq, cudaMemcpyDeviceToHost,
+                               s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        const uint32_t path = b->path;
+        for (uint32_t q = 0; q < nq; ++q) {
+            mdrq_search_stats& o = stats[q];
+            const uint64_t k = b->descs[q].k;
+            o = mdrq_search_stats{};
+            if (path == MDRQ_PATH_ROWWISE) {
+                o.objects_compared = s->n;
+                o.early_breaks = dev[4 * q + (mode == MDRQ_MODE_BLOCKED ? 1 : 0)];
+            } else if (path == MDRQ_PATH_VAFILE) {
+                o.objects_compared = dev[4 * q + 2];
+                o.nodes_visited = dev[4 * q + 2];
+                o.columns_scanned = k;
+                o.and_chunks = s->tiles_for(path);
+            } else {
+                o.objects_compared = k ? k * s->n : 0;
+                o.columns_scanned = k;
+                o.and_chunks = k ? s->tiles_for(MDRQ_PATH_COLUMNAR) : 0;
+            }
+        }
+    });
+}
+
+// ------------------------------------------------------- prepared batches --
+int mdrq_batch_prepare(mdrq_store* s, const float* lower, const float* upper, uint32_t nq, uint32_t path,
+                       mdrq_batch** out) {
+    return guard([&] {
+        check_store(s);
+        if (!out) raise(MDRQ_EINVAL, "null out");
+        if (nq && (!lower || !upper)) raise(MDRQ_EINVAL, "null bounds");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        auto* b = new mdrq_batch();
+        try {
+            b->owner = s;
+            // the ids flavour of AUTO is resolved at run time
+            build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false), true, b);
+            upload_batch(s, b);
+        } catch (...) {
+            delete b;
+            throw;
+        }
+        *out = b;
+    });
+}
+
+int mdrq_batch_destroy(mdrq_batch* b) {
+    return guard([&] {
+        if (!b) return;
+        mdrq_store* s = b->owner;
+        if (s) {
+            std::lock_guard<std::mutex> lk(s->mu);
+            DeviceGuard dg(s->device);
+            cudaStreamSynchronize(s->stream);
+            if (s->last_batch == b) s->last_batch = nullptr;
+            delete b;
+        } else {
+            delete b;
+        }
+    });
+}
+
+int mdrq_batch_count_async(mdrq_store* s, mdrq_batch* b, uint64_t* d_counts, void* stream) {
+    return guard([&] {
+        check_store(s);
+        if (!b || b->owner != s) raise(MDRQ_EINVAL, "batch does not belong to store");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+        enqueue(s, b, false, st);
+        if (d_counts && b->nq)
+            CK(cudaMemcpyAsync(d_counts, b->d_counts.p, sizeof(uint64_t) * b->nq, cudaMemcpyDeviceToDevice, st));
+        s->last_batch = b;
+    });
+}
+
+int mdrq_batch_ids_async(mdrq_store* s, mdrq_batch* b, void* stream) {
+    return guard([&] {
+        check_store(s);
+        if (!b || b->owner != s) raise(MDRQ_EINVAL, "batch does not belong to store");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+        enqueue(s, b, true, st);
+        s->last_batch = b;
+        s->last_nq = b->nq;
+        s->last_path = b->path;
+    });
+}
+
+int mdrq_batch_reserve(mdrq_store* s, mdrq_batch* b, uint64_t* total) {
+    return guard([&] {
+        check_store(s);
+        if (!b || b->owner != s) raise(MDRQ_EINVAL, "batch does not belong to store");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        const uint64_t t = run_ids_sync(s, b);
+        if (total) *total = t;
+    });
+}
+
+int mdrq_result_device(mdrq_store* s, uint64_t* d_ids, uint64_t* d_offsets, uint64_t* total) {
+    return guard([&] {
+        check_store(s);
+        std::lock_guard<std::mutex> lk(s->mu);
+        mdrq_batch* b = s->last_batch;
+        if (!b) raise(MDRQ_EINVAL, "no ids pass has run");
+        if (d_ids) *d_ids = reinterpret_cast<uint64_t>(s->ids.p);
+        if (d_offsets) *d_offsets = reinterpret_cast<uint64_t>(b->d_offsets.p);
+        if (total) *total = s->last_total;
+    });
+}
+
+int mdrq_batch_launches(mdrq_batch* b, int ids_mode, uint32_t* launches) {
+    return guard([&] {
+        if (!b || !b->owner || !launches) raise(MDRQ_EINVAL, "null argument");
+        *launches = count_launches(b->owner, b, ids_mode != 0);
+    });
+}
+
+// --------------------------------------------------- kernel-backend level --
+namespace {
+
+bool has_nan(const float* p, uint64_t count) {
+    for (uint64_t i = 0; i < count; ++i)
+        if (std::isnan(p[i])) return true;
+    return false;
+}
+
+struct TmpStream {
+    cudaStream_t st = nullptr;
+    TmpStream() { CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); }
+    ~TmpStream() {
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+void select_device(int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        raise(MDRQ_ENODEV, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) raise(MDRQ_ENODEV, "bad device ordinal " + std::to_string(device));
+}
+
+}  // namespace
+
+int mdrq_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lower, const float* upper,
+                    int device, uint8_t* out) {
+    return guard([&] {
+        if (nrows && (!rows || !out)) raise(MDRQ_EINVAL, "null argument");
+        if (m && (!lower || !upper)) raise(MDRQ_EINVAL, "null bounds");
+        if (!nrows) return;
+        if (m == 0) {  // _kernels_cy.pyx:53-54
+            std::memset(out, 1, nrows);
+            return;
+        }
+        if (has_nan(rows, nrows * m)) raise(MDRQ_EINVAL, "NaN values are rejected at ingestion");
+        select_device(device);
+        DeviceGuard dg(device);
+        TmpStream ts;
+        DBuf<float> d_rows, d_b;
+        DBuf<uint8_t> d_out;
+        d_rows.reserve(nrows * m);
+        d_b.reserve(size_t(2) * m);
+        d_out.reserve(nrows);
+        CK(cudaMemcpyAsync(d_rows.p, rows, sizeof(float) * nrows * m, cudaMemcpyHostToDevice, ts.st));
+        CK(cudaMemcpyAsync(d_b.p, lower, sizeof(float) * m, cudaMemcpyHostToDevice, ts.st));
+        CK(cudaMemcpyAsync(d_b.p + m, upper, sizeof(float) * m, cudaMemcpyHostToDevice, ts.st));
+        launch_match_rows(d_rows.p, nrows, m, d_b.p, d_b.p + m, d_out.p, ts.st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, d_out.p, nrows, cudaMemcpyDeviceToHost, ts.st));
+        CK(cudaStreamSynchronize(ts.st));
+    });
+}
+
+int mdrq_scan_rows(const float* values, uint64_t n, uint32_t m, const float* lower, const float* upper, int mode,
+                   int device, int64_t* ids_out, uint64_t* count_out, uint64_t* early_out) {
+    return guard([&] {
+        if (!count_out) raise(MDRQ_EINVAL, "null count");
+        if (m < 1) raise(MDRQ_EINVAL, "dimensionality must be at least 1");
+        if (!lower || !upper) raise(MDRQ_EINVAL, "null bounds");
+        *count_out = 0;
+        if (early_out) *early_out = 0;
+        if (!n) return;
+        if (!values || !ids_out) raise(MDRQ_EINVAL, "null argument");
+        if (has_nan(values, n * m)) raise(MDRQ_EINVAL, "NaN values are rejected at ingestion");
+        mdrq_store* s = nullptr;
+        int rc = mdrq_store_create(values, n, m, device, MDRQ_LAYOUT_ROWWISE, 0, 0, &s);
+        if (rc != MDRQ_OK) raise(rc, g_err);
+        struct Holder {
+            mdrq_store* s;
+            ~Holder() { mdrq_store_destroy(s); }
+        } holder{s};
+        DeviceGuard dg(s->device);
+        mdrq_batch* b = &s->scratch;
+        b->owner = s;
+        build_descs(s, lower, upper, 1, MDRQ_PATH_ROWWISE, false, b);
+        upload_batch(s, b);
+        const uint64_t tot = run_ids_sync(s, b);
+        std::vector<uint32_t> tmp(tot);
+        unsigned long long st4[4] = {0, 0, 0, 0};
+        if (tot) CK(cudaMemcpyAsync(tmp.data(), s->ids.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaMemcpyAsync(st4, b->d_stats.p, sizeof(st4), cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        for (uint64_t i = 0; i < tot; ++i) ids_out[i] = int64_t(tmp[i]);
+        *count_out = tot;
+        if (early_out) *early_out = st4[mode == MDRQ_MODE_BLOCKED ? 1 : 0];
+    });
+}
+
+int mdrq_scan_column(const float* col, uint64_t n, float lo, float hi, int device, uint8_t* mask_out) {
+    return guard([&] {
+        if (!n) return;
+        if (!col || !mask_out) raise(MDRQ_EINVAL, "null argument");
+        select_device(device);
+        DeviceGuard dg(device);
+        TmpStream ts;
+        const uint64_t nwords = (n + 31) / 32;
+        DBuf<float> d_col;
+        DBuf<uint32_t> d_mask;
+        d_col.reserve(n);
+        d_mask.reserve(nwords);
+        CK(cudaMemcpyAsync(d_col.p, col, sizeof(float) * n, cudaMemcpyHostToDevice, ts.st));
+        launch_scan_column_mask(d_col.p, n, lo, hi, d_mask.p, ts.st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(mask_out, d_mask.p, (n + 7) / 8, cudaMemcpyDeviceToHost, ts.st));
+        CK(cudaStreamSynchronize(ts.st));
+    });
+}
+
+int mdrq_and_masks(const uint8_t* const* masks, uint32_t k, uint64_t nbytes, int device, uint8_t* out) {
+    return guard([&] {
+        if (k == 0) raise(MDRQ_EINVAL, "no masks to merge");
+        if (!nbytes) return;
+        if (!masks || !out) raise(MDRQ_EINVAL, "null argument");
+        select_device(device);
+        DeviceGuard dg(device);
+        TmpStream ts;
+        const uint64_t nwords = (nbytes + 3) / 4;
+        DBuf<uint32_t> d_in, d_out;
+        d_in.reserve(nwords * k);
+        d_out.reserve(nwords);
+        CK(cudaMemsetAsync(d_in.p, 0, d_in.bytes(), ts.st));
+        std::vector<const uint32_t*> ptrs(k);
+        for (uint32_t j = 0; j < k; ++j) {
+            if (!masks[j]) raise(MDRQ_EINVAL, "null mask");
+            CK(cudaMemcpyAsync(d_in.p + j * nwords, masks[j], nbytes, cudaMemcpyHostToDevice, ts.st));
+            ptrs[j] = d_in.p + j * nwords;
+        }
+        launch_and_masks(ptrs.data(), k, nwords, d_out.p, ts.st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, d_out.p, nbytes, cudaMemcpyDeviceToHost, ts.st));
+        CK(cudaStreamSynchronize(ts.st));
+    });
+}
+
+int mdrq_mask_popcount(const uint8_t* mask, uint64_t nbytes, int device, uint64_t* count_out) {
+    return guard([&] {
+        if (!count_out) raise(MDRQ_EINVAL, "null count");
+        *count_out = 0;
+        if (!nbytes) return;
+        if (!mask) raise(MDRQ_EINVAL, "null mask");
+        select_device(device);
+        DeviceGuard dg(device);
+        TmpStream ts;
+        const uint64_t nwords = (nbytes + 3) / 4;
+        DBuf<uint32_t> d_in;
+        DBuf<unsigned long long> d_c;
+        d_in.reserve(nwords);
+        d_c.reserve(1);
+        CK(cudaMemsetAsync(d_in.p, 0, d_in.bytes(), ts.st));
+        CK(cudaMemcpyAsync(d_in.p, mask, nbytes, cudaMemcpyHostToDevice, ts.st));
+        launch_popcount(d_in.p, nwords, d_c.p, ts.st);
+        CK(cudaGetLastError());
+        unsigned long long c = 0;
+        CK(cudaMemcpyAsync(&c, d_c.p, sizeof(c), cudaMemcpyDeviceToHost, ts.st));
+        CK(cudaStreamSynchronize(ts.st));
+        *count_out = c;
+    });
+}
+
+int mdrq_mask_to_ids(const uint8_t* mask, uint64_t n, int device, int64_t* ids_out, uint64_t* count_out) {
+    return guard([&] {
+        if (!count_out) raise(MDRQ_EINVAL, "null count");
+        *count_out = 0;
+        if (!n) return;
+        if (!mask || !ids_out) raise(MDRQ_EINVAL, "null argument");
+        select_device(device);
+        DeviceGuard dg(device);
+        TmpStream ts;
+        const uint64_t nbytes = (n + 7) / 8, nwords = (n + 31) / 32;
+        const uint64_t tiles = (nwords + 255) / 256;
+        DBuf<uint32_t> d_in, d_ctr;
+        DBuf<uint64_t> d_status;
+        DBuf<unsigned long long> d_c;
+        DBuf<int64_t> d_ids;
+        d_in.reserve(nwords);
+        d_ctr.reserve(1);
+        d_status.reserve(tiles);
+        d_c.reserve(1);
+        d_ids.reserve(n);
+        CK(cudaMemsetAsync(d_in.p, 0, d_in.bytes(), ts.st));
+        CK(cudaMemsetAsync(d_status.p, 0, d_status.bytes(), ts.st));
+        CK(cudaMemcpyAsync(d_in.p, mask, nbytes, cudaMemcpyHostToDevice, ts.st));
+        launch_mask_to_ids(d_in.p, n, nullptr, d_status.p, 1, d_ctr.p, d_c.p, d_ids.p, ts.st);
+        CK(cudaGetLastError());
+        unsigned long long c = 0;
+        CK(cudaMemcpyAsync(&c, d_c.p, sizeof(c), cudaMemcpyDeviceToHost, ts.st));
+        CK(cudaStreamSynchronize(ts.st));
+        if (c) CK(cudaMemcpyAsync(ids_out, d_ids.p, sizeof(int64_t) * c, cudaMemcpyDeviceToHost, ts.st));
+        CK(cudaStreamSynchronize(ts.st));
+        *count_out = c;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,361 @@
+// vafile.cu -- quantile-grid VA-file for sm_100a: builder, encoder and the
+// filter-and-refine scan.
+//
+// Replaces the reference VA-file (reference vafile.py:88-219).  The reference
+// approximates every object by a 2-bit equal-width cell per dimension
+// (VaGrid.cell_index, vafile.py:38-45), files objects into a sparse
+// code -> bucket directory (vafile.py:106-147), enumerates candidate cells
+// (vafile.py:166-199) and refines every candidate bucket exactly with
+// scan_rows (vafile.py:204-219).  On the GPU the approximation is a
+// per-dimension QUANTILE grid of 2^bits cells stored as one byte plane per
+// dimension (columnar, 1 B per tuple per dimension instead of 4 B), the
+// filter streams those planes dimension-at-a-time, and only tuples that sit
+// in an edge cell of the query box are refined against the exact float32
+// columns.  Soundness (no false negatives, no false positives):
+//   code(v) = #{ boundaries b_i : b_i <= v }            (monotone in v)
+//   code(v) <  code(lo)  =>  v < lo      code(v) > code(hi) => v > hi
+//   code(lo) < code(v) < code(hi)  =>  lo < v < hi      (no refine)
+// so only code(v) == code(lo) (finite lo) or == code(hi) (finite hi) needs an
+// exact compare.  Parity with the reference is therefore on id sets.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "launch.h"
+
+namespace mdrq {
+
+namespace {
+
+constexpr int VA_THREADS = 256;
+constexpr int VA_G = 2;                         // uint4 (16 codes) groups per thread
+constexpr int VA_WARP_TUPLES = 32 * 16 * VA_G;  // 1024
+static_assert(VA_THREADS / 32 * VA_WARP_TUPLES == kVaTile, "tile size");
+
+__global__ void sample_kernel(const float* __restrict__ col, uint64_t step, uint64_t count,
+                              float* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = col[i * step];
+}
+
+// boundary i (1 <= i < nbins) = sorted[floor(i * count / nbins)]
+__global__ void pick_kernel(const float* __restrict__ sorted, uint64_t count, uint32_t nbins,
+                            float* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (i < nbins) out[i - 1] = sorted[(uint64_t(i) * count) / nbins];
+}
+
+// code(v) = #{b <= v}, branchless binary search over nb = 2^bits - 1 sorted
+// boundaries held in shared memory; 16 codes per thread, one uint4 store.
+__global__ void __launch_bounds__(256) encode_kernel(const float* __restrict__ col, uint64_t n_pad,
+                                                     const float* __restrict__ bounds, uint32_t nb,
+                                                     uint8_t* __restrict__ codes) {
+    __shared__ float s_b[256];
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) s_b[i] = i < nb ? bounds[i] : 0.f;
+    __syncthreads();
+    const uint32_t K = nb + 1;  // power of two
+    for (uint64_t i = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) * 16; i < n_pad;
+         i += uint64_t(gridDim.x) * blockDim.x * 16) {
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const float v = col[i + j];
+            uint32_t pos = 0;
+            for (uint32_t step = K >> 1; step >= 1; step >>= 1)
+                if (s_b[pos + step - 1] <= v) pos += step;
+            w[j >> 2] |= pos << (8 * (j & 3));
+        }
+        *reinterpret_cast<uint4*>(codes + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+__global__ void minmax_kernel(const float* __restrict__ col, uint64_t n, float* __restrict__ out2) {
+    float lo = INFINITY, hi = -INFINITY;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const float v = col[i];
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        // float atomics via ordered-int trick
+        auto key = [](float f) {
+            int i = __float_as_int(f);
+            return i >= 0 ? i : (i ^ 0x7FFFFFFF);
+        };
+        atomicMin(reinterpret_cast<int*>(out2), key(lo));
+        atomicMax(reinterpret_cast<int*>(out2) + 1, key(hi));
+    }
+}
+
+__global__ void minmax_finish(float* out2) {
+    int* p = reinterpret_cast<int*>(out2);
+    for (int j = 0; j < 2; ++j) {
+        const int k = p[j];
+        p[j] = k >= 0 ? k : (k ^ 0x7FFFFFFF);
+    }
+}
+
+// SWAR range test of 4 byte-codes packed in x against [lo, hi] (0..256):
+// returns flag bits at positions 8, 9, 24, 25 for bytes 0, 1, 2, 3.
+__device__ __forceinline__ uint32_t swar_in(uint32_t x, uint32_t lo, uint32_t hi) {
+    const uint32_t e = x & 0x00FF00FFu;          // bytes 0, 2 in 16-bit lanes
+    const uint32_t o = (x >> 8) & 0x00FF00FFu;   // bytes 1, 3
+    const uint32_t klo = (0x100u - lo) * 0x00010001u;
+    const uint32_t khi = (0x100u + hi) * 0x00010001u;
+    const uint32_t ge_e = e + klo, ge_o = o + klo;   // bit 8 of lane: v >= lo
+    const uint32_t le_e = khi - e, le_o = khi - o;   // bit 8 of lane: v <= hi
+    const uint32_t ie = ge_e & le_e & 0x01000100u;
+    const uint32_t io = ge_o & le_o & 0x01000100u;
+    return ie | (io << 1);
+}
+
+// flags (bits 8, 9, 24, 25) of word w -> 4-bit tuple mask
+__device__ __forceinline__ uint32_t flags_to_nib(uint32_t f) {
+    return ((f >> 8) & 3u) | ((f >> 22) & 0xCu);
+}
+
+template <bool IDS>
+__global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_seg[32];
+    __shared__ uint32_t s_excl;
+    __shared__ uint32_t s_refined;
+
+    const QueryDesc qd = a.descs[a.q];
+    const DimPred* __restrict__ P = a.preds + qd.off;
+    const uint32_t k = qd.k;
+    if (threadIdx.x == 0) {
+        s_tile = atomicAdd(a.tile_counters + a.q, 1u);
+        s_refined = 0;
+    }
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    // tuple of (group g, word w, byte b) = base + g*512 + w*4 + b
+    const uint64_t base = uint64_t(tile) * kVaTile + warp * VA_WARP_TUPLES + lane * 16;
+
+    // alive / sure flags in SWAR layout, one word per 4 tuples
+    uint32_t al[VA_G][4], su[VA_G][4];
+#pragma unroll
+    for (int g = 0; g < VA_G; ++g)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            al[g][w] = 0x03000300u;
+            su[g][w] = 0x03000300u;
+        }
+    if (uint64_t(tile + 1) * kVaTile > a.n) {
+#pragma unroll
+        for (int g = 0; g < VA_G; ++g)
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                uint32_t f = 0;
+                const uint64_t t0 = base + g * 512 + w * 4;
+                if (t0 + 0 < a.n) f |= 1u << 8;
+                if (t0 + 1 < a.n) f |= 1u << 9;
+                if (t0 + 2 < a.n) f |= 1u << 24;
+                if (t0 + 3 < a.n) f |= 1u << 25;
+                al[g][w] = f;
+            }
+    }
+
+    for (uint32_t i = 0; i < k; ++i) {
+        uint32_t any = 0;
+#pragma unroll
+        for (int g = 0; g < VA_G; ++g) any |= al[g][0] | al[g][1] | al[g][2] | al[g][3];
+        if (!__any_sync(0xFFFFFFFFu, any)) break;
+        const DimPred p = P[i];
+        const uint32_t d = p.dim;
+        const uint32_t cl = p.cl, ch = p.ch;
+        const uint32_t sl = cl + p.edge_lo, sh = ch - p.edge_hi;  // strict interior
+        const uint4* c = reinterpret_cast<const uint4*>(a.codes + uint64_t(d) * a.stride + base);
+        uint4 x[VA_G];
+#pragma unroll
+        for (int g = 0; g < VA_G; ++g) {
+            const uint32_t ga = al[g][0] | al[g][1] | al[g][2] | al[g][3];
+            if (ga) x[g] = ld_stream_u4(c + g * 32);
+        }
+#pragma unroll
+        for (int g = 0; g < VA_G; ++g) {
+            const uint32_t ga = al[g][0] | al[g][1] | al[g][2] | al[g][3];
+            if (ga) {
+                const uint32_t xw[4] = {x[g].x, x[g].y, x[g].z, x[g].w};
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    al[g][w] &= swar_in(xw[w], cl, ch);
+                    // (sh may be "negative": 0x100 + sh wraps below 0x100 -> never <=)
+                    su[g][w] &= swar_in(xw[w], sl, sh);
+                }
+            }
+        }
+    }
+
+    // exact refinement of tuples in an edge cell: alive & ~sure
+    uint32_t hit[VA_G];
+    uint32_t refined = 0;
+#pragma unroll
+    for (int g = 0; g < VA_G; ++g) {
+        uint32_t h = 0, r = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            h |= flags_to_nib(al[g][w] & su[g][w]) << (4 * w);
+            r |= flags_to_nib(al[g][w] & ~su[g][w]) << (4 * w);
+        }
+        while (r) {
+            const int j = __ffs(r) - 1;
+            r &= r - 1;
+            ++refined;
+            const uint64_t t = base + g * 512 + j;
+            bool ok = true;
+            for (uint32_t i = 0; i < k && ok; ++i) {
+                const DimPred p = P[i];
+                const float v = __ldg(a.cols + uint64_t(p.dim) * a.stride + t);
+                ok = (p.lo <= v) & (v <= p.hi);
+            }
+            if (ok) h |= 1u << j;
+        }
+        hit[g] = h;
+    }
+    if (a.stats) {
+        refined = __reduce_add_sync(0xFFFFFFFFu, refined);
+        if (lane == 0 && refined) atomicAdd(&s_refined, refined);
+    }
+
+    if (!IDS) {
+        uint32_t c = __reduce_add_sync(0xFFFFFFFFu, __popc(hit[0]) + __popc(hit[1]));
+        if (lane == 0) s_seg[warp] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < VA_THREADS / 32; ++w) t += s_seg[w];
+            if (t) atomicAdd(a.counts + a.q, (unsigned long long)t);
+            if (a.stats && s_refined) atomicAdd(a.stats + 4 * a.q + 2, (unsigned long long)s_refined);
+        }
+        return;
+    }
+
+    // ordered compaction: order within the tile is (warp, g, lane, j)
+    const uint32_t lt = lanemask_lt();
+    uint32_t pre[VA_G];
+#pragma unroll
+    for (int g = 0; g < VA_G; ++g) {
+        const uint32_t c = __popc(hit[g]);
+        // warp exclusive scan of c
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= uint32_t(o)) incl += t;
+        }
+        pre[g] = incl - c;
+        if (lane == 31) s_seg[warp * VA_G + g] = incl;
+    }
+    (void)lt;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t nseg = (VA_THREADS / 32) * VA_G;
+        const uint32_t v = lane < nseg ? s_seg[lane] : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= uint32_t(o)) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t excl = lookback_exclusive(a.status, tile, a.epoch, total);
+        s_seg[lane] = incl - v;
+        if (lane == 0) {
+            s_excl = excl;
+            if (tile == a.num_tiles - 1) {
+                const unsigned long long qbase = a.offsets[a.q];
+                a.offsets[a.q + 1] = qbase + excl + total;
+                a.counts[a.q] = excl + total;
+            }
+            if (a.stats && s_refined) atomicAdd(a.stats + 4 * a.q + 2, (unsigned long long)s_refined);
+        }
+    }
+    __syncthreads();
+    if (hit[0] | hit[1]) {
+        const unsigned long long obase = a.offsets[a.q] + s_excl;
+#pragma unroll
+        for (int g = 0; g < VA_G; ++g) {
+            uint32_t h = hit[g];
+            unsigned long long pos = obase + s_seg[warp * VA_G + g] + pre[g];
+            while (h) {
+                const int j = __ffs(h) - 1;
+                h &= h - 1;
+                if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(base + g * 512 + j);
+                ++pos;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+void launch_va_scan(const ScanArgs& a, bool ids, cudaStream_t st) {
+    if (a.num_tiles == 0) return;
+    if (ids)
+        va_scan_kernel<true><<<a.num_tiles, VA_THREADS, 0, st>>>(a);
+    else
+        va_scan_kernel<false><<<a.num_tiles, VA_THREADS, 0, st>>>(a);
+}
+
+void launch_va_sample(const float* col, uint64_t n, uint64_t step, uint64_t count, float* out,
+                      cudaStream_t st) {
+    (void)n;
+    if (!count) return;
+    const uint64_t blocks = (count + 255) / 256;
+    sample_kernel<<<unsigned(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(col, step, count, out);
+}
+
+void launch_va_pick_boundaries(const float* sorted, uint64_t count, uint32_t nbins, float* out,
+                               cudaStream_t st) {
+    pick_kernel<<<(nbins + 255) / 256, 256, 0, st>>>(sorted, count, nbins, out);
+}
+
+void launch_va_encode(const float* col, uint64_t n_pad, const float* bounds, uint32_t nb,
+                      uint8_t* codes, cudaStream_t st) {
+    const uint64_t threads = n_pad / 16;
+    uint64_t blocks = (threads + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (!blocks) return;
+    encode_kernel<<<unsigned(blocks), 256, 0, st>>>(col, n_pad, bounds, nb, codes);
+}
+
+size_t va_sort_temp_bytes(uint64_t count) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, bytes, static_cast<const float*>(nullptr),
+                                   static_cast<float*>(nullptr), int(count));
+    return bytes;
+}
+
+void va_sort(const float* in, float* out, uint64_t count, void* temp, size_t temp_bytes,
+             cudaStream_t st) {
+    cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, int(count), 0, 32, st);
+}
+
+void launch_min_max(const float* col, uint64_t n, float* out2, cudaStream_t st) {
+    static const float init[2] = {INFINITY, -INFINITY};
+    // encode the identities as ordered ints on the host
+    int key[2];
+    for (int j = 0; j < 2; ++j) {
+        int i;
+        memcpy(&i, &init[j], 4);
+        key[j] = i >= 0 ? i : (i ^ 0x7FFFFFFF);
+    }
+    cudaMemcpyAsync(out2, key, sizeof(key), cudaMemcpyHostToDevice, st);
+    if (n) {
+        uint64_t blocks = (n + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        minmax_kernel<<<unsigned(blocks), 256, 0, st>>>(col, n, out2);
+    }
+    minmax_finish<<<1, 1, 0, st>>>(out2);
+}
+
+}  // namespace mdrq

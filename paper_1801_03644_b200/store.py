@@ -1,0 +1,217 @@
+"""Device-resident MDRQ store: the Python handle of an ``mdrq_store``.
+
+One store holds one row shard of a dataset in HBM in up to three layouts
+(DESIGN.md "Data layout"):
+
+* columnar  -- m float32 columns of n_pad entries (NaN padded);
+* row-wise  -- the row-major float32 matrix, padded to whole row tiles;
+* VA-file   -- one byte plane of quantile-grid codes per dimension, plus
+  the columns for exact refinement.
+
+Queries go in as float32 ``lower``/``upper`` matrices [nq, m] with the
+reference's +-inf sentinels; ids come back ascending (uint32 on the device,
+widened to int64 only where the reference API demands it).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, f32p, u32p, u64p
+
+DEFAULT_VA_BITS = 8
+
+
+def default_device() -> int:
+    env = os.environ.get("MDRQ_DEVICE")
+    if env:
+        return int(env)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:  # pragma: no cover - torch is optional plumbing
+        pass
+    return 0
+
+
+def _bounds(lower, upper, m: int):
+    lo = np.ascontiguousarray(lower, dtype=np.float32).reshape(-1, m)
+    hi = np.ascontiguousarray(upper, dtype=np.float32).reshape(-1, m)
+    if lo.shape != hi.shape:
+        raise ValueError("lower and upper must have the same shape")
+    return lo, hi
+
+
+class DeviceStore:
+    """Owns one ``mdrq_store`` (device arrays + result pool)."""
+
+    def __init__(self, values, *, layouts: int = _lib.LAYOUT_COLUMNAR, va_bits: int = DEFAULT_VA_BITS,
+                 device: int | None = None, id_base: int = 0):
+        lib = _lib.load()
+        values = np.ascontiguousarray(values, dtype=np.float32)
+        if values.ndim != 2:
+            raise ValueError(f"expected a 2-d value matrix, got shape {values.shape}")
+        self.n, self.m = (int(x) for x in values.shape)
+        self.device = default_device() if device is None else int(device)
+        self.id_base = int(id_base)
+        if not layouts & _lib.LAYOUT_VAFILE:
+            va_bits = 0
+        handle = ctypes.c_void_p()
+        check(lib.mdrq_store_create(values.ctypes.data_as(f32p), self.n, self.m, self.device,
+                                    layouts, va_bits, self.id_base, ctypes.byref(handle)))
+        self._h = handle
+        info = _lib.StoreInfo()
+        check(lib.mdrq_store_get_info(self._h, ctypes.byref(info)))
+        self.layouts = int(info.layouts)
+        self.va_bits = int(info.va_bits)
+        self.n_pad = int(info.n_pad)
+
+    # -- lifecycle -----------------------------------------------------------
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("store is closed")
+        return self._h
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _lib.load().mdrq_store_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- info ----------------------------------------------------------------
+    def info(self) -> dict:
+        info = _lib.StoreInfo()
+        check(_lib.load().mdrq_store_get_info(self.handle, ctypes.byref(info)))
+        return {f: getattr(info, f) for f, _ in info._fields_}
+
+    def va_boundaries(self) -> np.ndarray:
+        nb = (1 << self.va_bits) - 1
+        out = np.empty((self.m, nb), np.float32)
+        check(_lib.load().mdrq_store_va_boundaries(self.handle, out.ctypes.data_as(f32p)))
+        return out
+
+    def bounds(self) -> np.ndarray:
+        out = np.empty((self.m, 2), np.float32)
+        check(_lib.load().mdrq_store_bounds(self.handle, out.ctypes.data_as(f32p)))
+        return out
+
+    # -- one-shot queries ---------------------------------------------------
+    def count(self, lower, upper, path: str | int = "auto") -> np.ndarray:
+        lo, hi = _bounds(lower, upper, self.m)
+        nq = lo.shape[0]
+        counts = np.zeros(nq, np.uint64)
+        check(_lib.load().mdrq_query_count(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p),
+                                           nq, _path(path), counts.ctypes.data_as(u64p)))
+        return counts.astype(np.int64)
+
+    def ids(self, lower, upper, path: str | int = "auto", out: np.ndarray | None = None):
+        """-> (offsets int64[nq+1], ids uint32[total]) ascending per query.
+
+        ``out`` may be a caller-owned (e.g. pinned) uint32 buffer; the ids are
+        written into its prefix and that view is returned.
+        """
+        lib = _lib.load()
+        lo, hi = _bounds(lower, upper, self.m)
+        nq = lo.shape[0]
+        offsets = np.zeros(nq + 1, np.uint64)
+        total = ctypes.c_uint64(0)
+        buf = out if out is not None else np.empty(max(1, _guess(self.n, nq)), np.uint32)
+        rc = lib.mdrq_query_ids(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p), nq,
+                                _path(path), offsets.ctypes.data_as(u64p), buf.ctypes.data_as(u32p),
+                                buf.size, ctypes.byref(total))
+        if rc == _lib.MDRQ_ETRUNC:
+            if out is not None:
+                raise ValueError(f"ids buffer holds {out.size} ids, the batch produced {total.value}")
+            buf = np.empty(int(total.value), np.uint32)
+            check(lib.mdrq_fetch_ids(self.handle, buf.ctypes.data_as(u32p), buf.size))
+        else:
+            check(rc)
+        return offsets.astype(np.int64), buf[: int(total.value)]
+
+    def stats(self, nq: int, mode: int = _lib.MODE_SCALAR):
+        arr = (_lib.SearchStatsC * max(nq, 1))()
+        check(_lib.load().mdrq_query_stats(self.handle, mode, arr, nq))
+        return [arr[i] for i in range(nq)]
+
+    # -- prepared batches (device-resident; bench / multi-GPU) --------------
+    def prepare(self, lower, upper, path: str | int = "auto") -> "PreparedBatch":
+        return PreparedBatch(self, lower, upper, path)
+
+
+def _guess(n: int, nq: int) -> int:
+    return int(min(max(4096, n // 64 * max(nq, 1)), 1 << 26))
+
+
+def _path(path) -> int:
+    if isinstance(path, str):
+        try:
+            return _lib.PATHS[path]
+        except KeyError:
+            raise ValueError(f"unknown path {path!r} (choose from {sorted(_lib.PATHS)})") from None
+    return int(path)
+
+
+class PreparedBatch:
+    """A query batch whose descriptors live in HBM (``mdrq_batch``)."""
+
+    def __init__(self, store: DeviceStore, lower, upper, path="auto"):
+        lib = _lib.load()
+        lo, hi = _bounds(lower, upper, store.m)
+        self.store = store
+        self.nq = lo.shape[0]
+        h = ctypes.c_void_p()
+        check(lib.mdrq_batch_prepare(store.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p),
+                                     self.nq, _path(path), ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _lib.load().mdrq_batch_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def count_async(self, d_counts: int = 0, stream: int = 0) -> None:
+        check(_lib.load().mdrq_batch_count_async(self.store.handle, self._h, ctypes.c_void_p(d_counts or None),
+                                                 ctypes.c_void_p(stream or None)))
+
+    def ids_async(self, stream: int = 0) -> None:
+        check(_lib.load().mdrq_batch_ids_async(self.store.handle, self._h, ctypes.c_void_p(stream or None)))
+
+    def reserve(self) -> int:
+        t = ctypes.c_uint64(0)
+        check(_lib.load().mdrq_batch_reserve(self.store.handle, self._h, ctypes.byref(t)))
+        return int(t.value)
+
+    def result_device(self):
+        """(device ptr of ids u32, device ptr of offsets u64[nq+1], total)."""
+        a, b, t = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_uint64(0)
+        check(_lib.load().mdrq_result_device(self.store.handle, ctypes.byref(a), ctypes.byref(b),
+                                             ctypes.byref(t)))
+        return int(a.value), int(b.value), int(t.value)
+
+    def launches(self, ids: bool) -> int:
+        c = ctypes.c_uint32(0)
+        check(_lib.load().mdrq_batch_launches(self._h, int(bool(ids)), ctypes.byref(c)))
+        return int(c.value)

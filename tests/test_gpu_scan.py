@@ -1,0 +1,236 @@
+"""Access-method parity on the GPU (pkg/tests/test_scan.py, test_vafile.py
+counterparts): every GPU path returns the oracle's id set for every query."""
+
+import hashlib
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+import oracle
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+PATHS = ("columnar", "rowwise", "vafile", "columnar_batch")
+ALL_LAYOUTS = 1 | 2 | 4
+
+
+def sha1_ids(ids):
+    return hashlib.sha1(np.ascontiguousarray(ids, dtype="<u4").tobytes()).digest()
+
+
+def check_store(gpu, values, lo, hi, paths=PATHS, va_bits=8):
+    lo = np.ascontiguousarray(lo, np.float32).reshape(-1, values.shape[1])
+    hi = np.ascontiguousarray(hi, np.float32).reshape(-1, values.shape[1])
+    exp_counts = oracle.count_batch(values, lo, hi)
+    exp_offs, exp_ids = oracle.ids_batch(values, lo, hi, counts=exp_counts)
+    with gpu.DeviceStore(values, layouts=ALL_LAYOUTS, va_bits=va_bits) as st_:
+        for p in paths:
+            counts = st_.count(lo, hi, p)
+            assert np.array_equal(counts, exp_counts), p
+            offs, ids = st_.ids(lo, hi, p)
+            assert np.array_equal(offs, exp_offs), p
+            assert np.array_equal(ids.astype(np.int64), exp_ids), p
+
+
+# -- reference KATs (test_scan.py:32-45, test_core.py:83-86) -------------------
+
+def test_enumerated_example(gpu):
+    data = gpu.DataSet(np.array([[0.1], [0.5], [0.9]], dtype=np.float32))
+    for name in ("sequential", "vertical", "horizontal", "vafile"):
+        m = gpu.build_method(name, data, threads=2)
+        assert m.search(gpu.RangeQuery([0.2], [0.9])).ids.tolist() == [1, 2], name
+        m.close()
+
+
+def test_full_domain_and_empty_interval(gpu):
+    data = gpu.gen_uniform(gpu.GeneratorSpec("uniform", 50, 3, seed=1))
+    for name in ("sequential", "vertical", "horizontal", "vafile"):
+        m = gpu.build_method(name, data, threads=2)
+        assert m.search(gpu.RangeQuery.full_domain(3)).ids.tolist() == list(range(50)), name
+        assert len(m.search(gpu.RangeQuery([-5.0, 0.0, 0.0], [-1.0, 1.0, 1.0]))) == 0, name
+        m.close()
+
+
+def test_boundary_inclusive(gpu):
+    data = gpu.DataSet(np.array([[0.25], [0.9], [0.2499], [0.9001]], np.float32))
+    for name in ("sequential", "vertical", "vafile"):
+        m = gpu.build_method(name, data)
+        assert m.search(gpu.RangeQuery([0.25], [0.9])).ids.tolist() == [0, 1], name
+        m.close()
+
+
+def test_dimension_mismatch(gpu):
+    data = gpu.gen_uniform(gpu.GeneratorSpec("uniform", 10, 2, seed=1))
+    for name in ("sequential", "vertical", "vafile"):
+        m = gpu.build_method(name, data)
+        with pytest.raises(ValueError):
+            m.search(gpu.RangeQuery([0.0], [1.0]))
+        m.close()
+
+
+def test_vertical_stats_and_zero_dims(gpu):
+    # test_scan.py:105-121
+    data = gpu.gen_uniform(gpu.GeneratorSpec("uniform", 300, 19, seed=3))
+    vs = gpu.VerticalScan(data, threads=2)
+    q = gpu.RangeQuery.from_predicates(19, {2: (0.1, 0.9), 7: (0.2, 0.8), 11: (0.0, 1.0)})
+    rs, st = vs.search_with_stats(q)
+    assert st.columns_scanned == 3 and st.objects_compared == 900
+    assert rs.ids.tolist() == oracle.brute_ids(data.values, q.lower, q.upper).tolist()
+    rs, st = vs.search_with_stats(gpu.RangeQuery.full_domain(19))
+    assert rs.ids.tolist() == list(range(300)) and st.columns_scanned == 0
+    vs.close()
+
+
+def test_sequential_stats_early_breaks(gpu):
+    rng = np.random.default_rng(4)
+    v = rng.random((5000, 9), dtype=np.float32)
+    data = gpu.DataSet(v)
+    lo = np.full(9, 0.2, np.float32)
+    hi = np.full(9, 0.9, np.float32)
+    for mode, code in ((gpu.KernelMode.SCALAR, 0), (gpu.KernelMode.VECTORIZED, 1)):
+        s = gpu.SequentialScan(data, mode)
+        rs, st = s.search_with_stats(gpu.RangeQuery(lo, hi))
+        exp_ids, n, early = oracle.scan_rows(v, lo, hi, code)
+        assert np.array_equal(rs.ids, exp_ids) and st.objects_compared == n and st.early_breaks == early
+        s.close()
+
+
+# -- golden edge cases -------------------------------------------------------
+
+def test_edge_values_vs_reference_golden(gpu):
+    E = golden("edge.npz")
+    values = E["values"]
+    offs = np.concatenate([[0], np.cumsum(E["counts"])])
+    with gpu.DeviceStore(values, layouts=ALL_LAYOUTS, va_bits=2) as st_:
+        for p in PATHS:
+            o, ids = st_.ids(E["lo"], E["hi"], p)
+            assert np.array_equal(o, offs), p
+            assert np.array_equal(ids.astype(np.int64), E["ids"]), p
+    cat = E["cat_values"]
+    for bits in (1, 3, 8):
+        with gpu.DeviceStore(cat, layouts=ALL_LAYOUTS, va_bits=bits) as st_:
+            for p in PATHS:
+                o, ids = st_.ids(E["cat_lo"], E["cat_hi"], p)
+                assert np.array_equal(np.diff(o), E["cat_counts"]), (p, bits)
+                for i in range(E["cat_lo"].shape[0]):
+                    assert sha1_ids(ids[o[i]:o[i + 1]]) == E["cat_sha1"][i].tobytes(), (p, bits, i)
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 4095, 4096, 4097, 8191, 8193, 70001])
+def test_ragged_sizes(gpu, n):
+    rng = np.random.default_rng(n)
+    m = 5
+    v = rng.random((n, m), dtype=np.float32)
+    lo = (rng.random((7, m)) * 0.5).astype(np.float32)
+    hi = lo + np.float32(0.55)
+    lo[0] = -np.inf
+    hi[0] = np.inf       # full domain -> all ids
+    check_store(gpu, v, lo, hi)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 7, 8, 9, 16, 19, 33, 64, 65, 100, 256])
+def test_dimensionalities(gpu, m):
+    rng = np.random.default_rng(100 + m)
+    n = 20000
+    v = rng.random((n, m), dtype=np.float32)
+    k = min(m, 6)
+    lo = np.full((40, m), -np.inf, np.float32)
+    hi = np.full((40, m), np.inf, np.float32)
+    w = 0.05 ** (1.0 / k)
+    for q in range(40):
+        dims = rng.choice(m, size=int(rng.integers(1, k + 1)), replace=False)
+        a = rng.random(dims.size) * (1 - w)
+        lo[q, dims] = a
+        hi[q, dims] = a + w
+    check_store(gpu, v, lo, hi)
+
+
+@given(seed=st.integers(0, 2**20), n=st.integers(1, 30000), m=st.integers(1, 20), bits=st.integers(1, 8))
+@settings(max_examples=25, deadline=None)
+def test_random_partial_match_vs_oracle(gpu, seed, n, m, bits):
+    rng = np.random.default_rng(seed)
+    v = rng.random((n, m), dtype=np.float32)
+    if rng.random() < 0.3:   # low-cardinality columns -> duplicate quantile boundaries
+        v = np.floor(v * 4) / 4
+    nq = int(rng.integers(1, 40))
+    lo = np.full((nq, m), -np.inf, np.float32)
+    hi = np.full((nq, m), np.inf, np.float32)
+    for q in range(nq):
+        dims = rng.choice(m, size=int(rng.integers(0, m + 1)), replace=False)
+        a, b = np.sort(rng.random((2, dims.size)), axis=0)
+        lo[q, dims] = a
+        hi[q, dims] = b
+        if rng.random() < 0.2 and dims.size:   # point predicate on an existing value
+            j = dims[0]
+            lo[q, j] = hi[q, j] = v[int(rng.integers(0, n)), j]
+    check_store(gpu, v, lo, hi, va_bits=bits)
+
+
+def test_methods_agree_on_pair_queries(gpu):
+    # test_scan.py:199-208 / test_acceptance.py:63-92 analogue
+    data = gpu.gen_uniform(gpu.GeneratorSpec("uniform", 10_000, 5, seed=1))
+    queries = gpu.pair_query_batch(data, 200, seed=4)
+    expected = [oracle.brute_ids(data.values, q.lower, q.upper) for q in queries]
+    for name in ("sequential", "horizontal", "vertical", "vafile"):
+        m = gpu.build_method(name, data, threads=2, seed=5)
+        for q, exp in zip(queries, expected):
+            assert np.array_equal(m.search(q).ids, exp), name
+        br = m.search_batch(queries)
+        for i, exp in enumerate(expected):
+            assert np.array_equal(br[i].ids, exp), name
+        assert np.array_equal(m.count_batch(queries), [e.size for e in expected]), name
+        m.close()
+
+
+def test_selectivity_oracle_gpu(gpu):
+    data = gpu.DataSet(np.array([[0.1], [0.5], [0.9]], dtype=np.float32))
+    st = gpu.selectivity_oracle(data, gpu.RangeQuery([0.2], [0.9]))
+    assert st.joint == pytest.approx(2 / 3) and st.per_dim[0] == pytest.approx(2 / 3)
+    data = gpu.gen_uniform(gpu.GeneratorSpec("uniform", 2000, 4, seed=5))
+    q = gpu.RangeQuery.from_predicates(4, {1: (0.2, 0.7), 3: (0.1, 0.3)})
+    st = gpu.selectivity_oracle(data, q)
+    v = data.values
+    assert st.per_dim[0] == 1.0 and st.per_dim[2] == 1.0
+    assert st.per_dim[1] == np.count_nonzero((v[:, 1] >= np.float32(0.2)) & (v[:, 1] <= np.float32(0.7))) / 2000
+    assert st.joint == oracle.brute_ids(v, q.lower, q.upper).size / 2000
+
+
+def test_vafile_grid_and_soundness(gpu):
+    data = gpu.gen_uniform(gpu.GeneratorSpec("uniform", 50_000, 3, seed=16))
+    va = gpu.VaFile.from_dataset(data, bits=4)
+    b = va.grid.boundaries
+    assert b.shape == (3, 15) and np.all(np.diff(b, axis=1) >= 0)
+    # equal-frequency cells on uniform data: each holds ~1/16 of the tuples
+    cells = va.grid.approximate_all(data.values[:, :1])[:, 0]
+    frac = np.bincount(cells, minlength=16) / data.n
+    assert np.all(np.abs(frac - 1 / 16) < 0.01)
+    for q in gpu.pair_query_batch(data, 20, 17):
+        rs, stt = va.search_with_stats(q)
+        assert np.array_equal(rs.ids, oracle.brute_ids(data.values, q.lower, q.upper))
+        assert stt.columns_scanned == 3
+    va.close()
+
+
+def test_c1_all_queries_vs_reference_golden(gpu):
+    """C1: all 1000 queries, every path, ids identical to the reference's
+    SequentialScan (sha1 of each id list recorded from the reference)."""
+    from paper_1801_03644_b200 import workload
+    G = golden("c1.npz")
+    values = workload.c1_data()
+    assert hashlib.sha1(values.tobytes()).digest() == G["data_sha1"].tobytes()
+    lo, hi = workload.c1_queries()
+    with gpu.DeviceStore(values, layouts=ALL_LAYOUTS, va_bits=8) as st_:
+        for p in PATHS:
+            assert np.array_equal(st_.count(lo, hi, p), G["counts"]), p
+            offs, ids = st_.ids(lo, hi, p)
+            assert np.array_equal(np.diff(offs), G["counts"]), p
+            bad = [i for i in range(lo.shape[0]) if sha1_ids(ids[offs[i]:offs[i + 1]]) != G["sha1"][i].tobytes()]
+            assert not bad, (p, bad[:5])
+        # partial-match queries of the reference VerticalScan
+        for p in PATHS:
+            offs, ids = st_.ids(G["p_lo"], G["p_hi"], p)
+            assert np.array_equal(np.diff(offs), G["p_counts"]), p
+            for i in range(G["p_lo"].shape[0]):
+                assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G["p_sha1"][i].tobytes(), (p, i)
