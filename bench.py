@@ -224,8 +224,13 @@ def main():
     t_build = time.perf_counter()
     store = eng.DeviceStore(values, layouts=layouts, va_bits=8, device=dev, id_base=start)
     t_build = time.perf_counter() - t_build
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: the library launches on it and the CUDA events
+    # below are recorded on it (torch's legacy default stream would be NULL
+    # and the library would fall back to the store's own stream)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
 
     batch = store.prepare(lo, hi, args.path)
     total_local = batch.reserve()
@@ -354,7 +359,7 @@ def explore(store, lo, hi, n, stream):
     levels = workload.c2_queries(count=lo.shape[0])
     sptr = stream.cuda_stream
     for s, (l, h) in levels.items():
-        for path in ("columnar", "columnar_batch", "vafile", "rowwise"):
+        for path in ("vafile_batch", "columnar", "columnar_batch", "vafile", "rowwise"):
             for mode in ("count", "ids"):
                 if mode == "ids" and path == "columnar_batch":
                     continue

@@ -60,6 +60,8 @@ extern "C" {
 #define MDRQ_PATH_ROWWISE        2u  /* bulk-copy staged row tiles            */
 #define MDRQ_PATH_VAFILE         3u  /* quantile-code filter + exact refine   */
 #define MDRQ_PATH_COLUMNAR_BATCH 4u  /* many queries per pass over the columns */
+#define MDRQ_PATH_VAFILE_BATCH   5u  /* bit-sliced: <= 1024 queries per pass over
+                                        the VA code planes + exact refine    */
 
 /* kernel modes (core.py:29-44 KernelMode; affect only early-break stats) */
 #define MDRQ_MODE_SCALAR  0

@@ -33,6 +33,7 @@ PATH_COLUMNAR = 1
 PATH_ROWWISE = 2
 PATH_VAFILE = 3
 PATH_COLUMNAR_BATCH = 4
+PATH_VAFILE_BATCH = 5
 
 PATHS = {
     "auto": PATH_AUTO,
@@ -40,6 +41,7 @@ PATHS = {
     "rowwise": PATH_ROWWISE,
     "vafile": PATH_VAFILE,
     "columnar_batch": PATH_COLUMNAR_BATCH,
+    "vafile_batch": PATH_VAFILE_BATCH,
 }
 
 MODE_SCALAR = 0

@@ -20,7 +20,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libmdrq_b200.so")
 
-SOURCES = ["store.cu", "scan_columnar.cu", "scan_rowwise.cu", "vafile.cu", "masks.cu"]
+SOURCES = ["store.cu", "scan_columnar.cu", "scan_rowwise.cu", "vafile.cu", "masks.cu", "expand.cu", "vabatch.cu"]
 HEADERS = ["common.cuh", "launch.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -14,6 +14,7 @@ namespace mdrq {
 // rows) so they never satisfy lo <= v <= hi, codes are 0 (they are also
 // masked by n).
 constexpr uint64_t kPadTuples = 8192;
+constexpr uint64_t kChunkTuples = 8192;   // compaction chunk (256 mask words)
 
 struct ScanArgs {
     const float* cols;       // columnar store [m][stride]
@@ -36,6 +37,11 @@ struct ScanArgs {
     uint64_t ids_cap;
     uint32_t id_base;
     unsigned long long* stats;    // [nq][4]: early_scalar, early_blocked, refined, tiles
+    // ids mode: the scan writes its verdicts as a bitmask + per-chunk counts,
+    // launch_expand turns them into ordered ids (expand.cu)
+    uint32_t* mask;               // [n_pad / 32] words
+    uint32_t* chunk_counts;       // [n_pad / kChunkTuples], zeroed per query
+    uint32_t* chunk_offs;         // [n_pad / kChunkTuples]
 };
 
 // multi-query pass over the columnar store (union dims, <= 32 queries)
@@ -51,14 +57,51 @@ struct BatchArgs {
     unsigned long long* counts;  // [nqp] (already offset to the pass)
 };
 
+// bit-sliced multi-query VA pass (vabatch.cu), <= 1024 queries per pass
+constexpr int kVaBatchMaxDims = 24;
+// table cells per dimension for a pass with kb union dims (fits 227 KB smem)
+__host__ __device__ constexpr uint32_t va_batch_cells(uint32_t kb) { return kb <= 12 ? 64u : 32u; }
+struct VaBatchArgs {
+    const uint8_t* codes;        // VA code planes [m][stride]
+    const float* cols;           // exact columns [m][stride] (refinement)
+    uint64_t stride;
+    uint64_t n;
+    uint32_t kb;                 // union dims of this pass (<= kVaBatchMaxDims)
+    uint32_t cells;              // table cells per dim (2^tb: 32 or 64)
+    uint32_t shift;              // stored code >> shift = table cell
+    uint32_t nqp;                // queries in this pass (<= 1024)
+    const uint16_t* udims;       // [kb]
+    const uint32_t* tables;      // [2][kb][cells][32]: overlap masks, then sure masks
+    const float2* qbounds;       // [1024][kb] exact (lo, hi), +-inf where unconstrained
+    uint32_t grid;               // CTAs (chunks = grid * warps)
+    uint64_t chunk_tuples;       // tuples per warp chunk (multiple of 128)
+    unsigned long long* counts;  // [nqp] count mode (offset to the pass)
+    uint32_t* chunk_counts;      // [chunks][1024]
+    unsigned long long* base;    // [chunks][1024]
+    unsigned long long* total;   // [1024]
+    unsigned long long* qoff;    // [1024]
+    unsigned long long* offsets;     // batch offsets [nq+1]
+    unsigned long long* counts_all;  // batch counts [nq]
+    uint32_t* ids;
+    uint64_t ids_cap;
+    uint32_t id_base;
+};
+size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode);
+int va_batch_max_dims();
+uint32_t va_batch_warps();
+void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st);   // 0 count, 1 chunk counts, 2 ids
+void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st);
+
 constexpr int kColTile = 4096;     // tuples per CTA tile, single-query columnar
 constexpr int kVaTile = 8192;      // tuples per CTA tile, VA-file filter
 
 void launch_col_scan(const ScanArgs& a, bool ids, cudaStream_t st);
 void launch_row_scan(const ScanArgs& a, bool ids, cudaStream_t st);
 void launch_va_scan(const ScanArgs& a, bool ids, cudaStream_t st);
+void launch_expand(const ScanArgs& a, cudaStream_t st);
 void launch_col_batch_count(const BatchArgs& a, int num_sms, cudaStream_t st);
 int col_batch_max_dims();
+uint32_t col_batch_padded_dims(uint32_t kb);   // union dims the kernel evaluates
 uint32_t row_tile_rows(uint32_t m);
 size_t row_scan_smem(uint32_t m);
 

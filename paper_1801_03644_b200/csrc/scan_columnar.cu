@@ -12,6 +12,8 @@
 // col_scan_kernel        one query per launch, dimension-at-a-time (HBM bound)
 // col_batch_count_kernel up to 32 queries per pass over the union of their
 //                        dimensions, every column byte read once per pass
+#include <utility>
+
 #include "launch.h"
 
 namespace mdrq {
@@ -25,18 +27,15 @@ static_assert(CS_THREADS / 32 * CS_WARP_TUPLES == kColTile, "tile size");
 
 template <bool IDS>
 __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_seg[32];
-    __shared__ uint32_t s_excl;
+    __shared__ uint32_t s_cnt[CS_THREADS / 32];
 
     const QueryDesc qd = a.descs[a.q];
     const DimPred* __restrict__ P = a.preds + qd.off;
     const uint32_t k = qd.k;
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counters + a.q, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    const uint32_t tile = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint64_t base = uint64_t(tile) * kColTile + warp * CS_WARP_TUPLES + lane * 4;
+    const uint64_t wbase = uint64_t(tile) * kColTile + warp * CS_WARP_TUPLES;
+    const uint64_t base = wbase + lane * 4;
 
     uint32_t alive = 0xFFFFu;
     if (uint64_t(tile + 1) * kColTile > a.n) {  // tail tile: mask tuples >= n
@@ -64,88 +63,48 @@ __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) 
                 alive &= (in_range4(v[g], lo, hi) << (4 * g)) | ~(0xFu << (4 * g));
     }
 
+    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, __popc(alive));
     if (!IDS) {
-        uint32_t c = __reduce_add_sync(0xFFFFFFFFu, __popc(alive));
-        if (lane == 0) s_seg[warp] = c;
+        if (lane == 0) s_cnt[warp] = wc;
         __syncthreads();
         if (threadIdx.x == 0) {
             uint32_t t = 0;
 #pragma unroll
-            for (int w = 0; w < CS_THREADS / 32; ++w) t += s_seg[w];
+            for (int w = 0; w < CS_THREADS / 32; ++w) t += s_cnt[w];
             if (t) atomicAdd(a.counts + a.q, (unsigned long long)t);
         }
         return;
     }
-
-    // ---- ordered compaction: tuple order within the tile is (warp, g, lane, j)
-    const uint32_t lt = lanemask_lt();
-    uint32_t pre[CS_G];
+    // ids mode: verdict bitmask (bit i of word w = tuple 32w+i) + chunk count;
+    // lanes 8s..8s+7 of group g own the 32 tuples of one mask word
 #pragma unroll
     for (int g = 0; g < CS_G; ++g) {
-        const uint32_t nib = (alive >> (4 * g)) & 0xFu;
-        const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, nib & 1u);
-        const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, nib & 2u);
-        const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, nib & 4u);
-        const uint32_t b3 = __ballot_sync(0xFFFFFFFFu, nib & 8u);
-        pre[g] = __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
-        if (lane == 0) s_seg[warp * CS_G + g] = __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+        uint32_t v = ((alive >> (4 * g)) & 0xFu) << (4 * (lane & 7u));
+        v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+        v |= __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+        v |= __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+        if ((lane & 7u) == 0) a.mask[(wbase + g * 128) / 32 + (lane >> 3)] = v;
     }
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t v = s_seg[lane];
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= uint32_t(o)) incl += t;
-        }
-        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        const uint32_t excl = lookback_exclusive(a.status, tile, a.epoch, total);
-        s_seg[lane] = incl - v;
-        if (lane == 0) {
-            s_excl = excl;
-            if (tile == a.num_tiles - 1) {
-                const unsigned long long qbase = a.offsets[a.q];
-                a.offsets[a.q + 1] = qbase + excl + total;
-                a.counts[a.q] = excl + total;
-            }
-        }
-    }
-    __syncthreads();
-    if (alive) {
-        const unsigned long long obase = a.offsets[a.q] + s_excl;
-#pragma unroll
-        for (int g = 0; g < CS_G; ++g) {
-            uint32_t nib = (alive >> (4 * g)) & 0xFu;
-            unsigned long long pos = obase + s_seg[warp * CS_G + g] + pre[g];
-            while (nib) {
-                const int j = __ffs(nib) - 1;
-                nib &= nib - 1;
-                if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(base + g * 128 + j);
-                ++pos;
-            }
-        }
-    }
+    if (lane == 0 && wc) atomicAdd(a.chunk_counts + wbase / kChunkTuples, wc);
 }
 
 // ---------------------------------------------------------------------------
 // Multi-query count pass.  Each thread holds TPT consecutive tuples of every
 // union dimension in registers (one 16/8/4-byte load per column), then walks
-// the pass's queries with their bounds broadcast from shared memory.
+// the pass's queries with their bounds broadcast from shared memory.  The
+// dimension loop is fully unrolled over exactly KB dimensions (the host pads
+// the union to KB with (-inf, +inf) bounds), so the per-tuple verdicts stay
+// in predicate registers: two chained FSETP per (tuple, query, dimension).
 template <int KB, int TPT>
 __global__ void __launch_bounds__(256) col_batch_count_kernel(const BatchArgs a) {
     __shared__ float2 s_b[32][KB];
-    __shared__ unsigned long long s_cm[32];
     __shared__ uint32_t s_cnt[32];
     __shared__ uint16_t s_ud[KB];
 
-    const uint32_t kb = a.kb, nqp = a.nqp;
-    for (uint32_t i = threadIdx.x; i < nqp * kb; i += blockDim.x) s_b[i / kb][i % kb] = a.bounds[i];
-    for (uint32_t i = threadIdx.x; i < 32; i += blockDim.x) {
-        s_cm[i] = i < nqp ? a.cmask[i] : 0ull;
-        s_cnt[i] = 0;
-    }
-    for (uint32_t i = threadIdx.x; i < kb; i += blockDim.x) s_ud[i] = a.udims[i];
+    const uint32_t nqp = a.nqp;
+    for (uint32_t i = threadIdx.x; i < nqp * KB; i += blockDim.x) s_b[i / KB][i % KB] = a.bounds[i];
+    for (uint32_t i = threadIdx.x; i < 32; i += blockDim.x) s_cnt[i] = 0;
+    for (uint32_t i = threadIdx.x; i < KB; i += blockDim.x) s_ud[i] = a.udims[i];
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31u;
@@ -158,38 +117,29 @@ __global__ void __launch_bounds__(256) col_batch_count_kernel(const BatchArgs a)
         float v[KB][TPT];
 #pragma unroll
         for (int d = 0; d < KB; ++d) {
-            if (d < int(kb)) {
-                const float* col = a.cols + uint64_t(s_ud[d]) * a.stride + base;
-                if constexpr (TPT == 4) {
-                    const float4 t = ld_stream_f4(reinterpret_cast<const float4*>(col));
-                    v[d][0] = t.x; v[d][1] = t.y; v[d][2] = t.z; v[d][3] = t.w;
-                } else if constexpr (TPT == 2) {
-                    const float2 t = __ldcs(reinterpret_cast<const float2*>(col));
-                    v[d][0] = t.x; v[d][1] = t.y;
-                } else {
-                    v[d][0] = __ldcs(col);
-                }
+            const float* col = a.cols + uint64_t(s_ud[d]) * a.stride + base;
+            if constexpr (TPT == 4) {
+                const float4 t = ld_stream_f4(reinterpret_cast<const float4*>(col));
+                v[d][0] = t.x; v[d][1] = t.y; v[d][2] = t.z; v[d][3] = t.w;
+            } else if constexpr (TPT == 2) {
+                const float2 t = __ldcs(reinterpret_cast<const float2*>(col));
+                v[d][0] = t.x; v[d][1] = t.y;
+            } else {
+                v[d][0] = __ldcs(col);
             }
         }
-        uint32_t valid = (1u << TPT) - 1u;
-        if (base + TPT > a.n) {
-            valid = 0;
+        bool valid[TPT];
 #pragma unroll
-            for (int t = 0; t < TPT; ++t)
-                if (base + t < a.n) valid |= 1u << t;
-        }
+        for (int t = 0; t < TPT; ++t) valid[t] = base + t < a.n;
         for (uint32_t q = 0; q < nqp; ++q) {
-            const unsigned long long cm = s_cm[q];
             bool ok[TPT];
 #pragma unroll
-            for (int t = 0; t < TPT; ++t) ok[t] = (valid >> t) & 1u;
+            for (int t = 0; t < TPT; ++t) ok[t] = valid[t];
 #pragma unroll
             for (int d = 0; d < KB; ++d) {
-                if (d < int(kb) && ((cm >> d) & 1ull)) {
-                    const float2 b = s_b[q][d];
+                const float2 b = s_b[q][d];
 #pragma unroll
-                    for (int t = 0; t < TPT; ++t) ok[t] = ok[t] & (b.x <= v[d][t]) & (v[d][t] <= b.y);
-                }
+                for (int t = 0; t < TPT; ++t) ok[t] = ok[t] && (b.x <= v[d][t]) && (v[d][t] <= b.y);
             }
             uint32_t c = 0;
 #pragma unroll
@@ -220,6 +170,11 @@ void run_batch(const BatchArgs& a, int num_sms, cudaStream_t st) {
     col_batch_count_kernel<KB, TPT><<<unsigned(grid), 256, 0, st>>>(a);
 }
 
+template <int... Ks>
+void dispatch_exact(const BatchArgs& a, int num_sms, cudaStream_t st, std::integer_sequence<int, Ks...>) {
+    ((a.kb == uint32_t(Ks + 1) ? run_batch<Ks + 1, 4>(a, num_sms, st) : void()), ...);
+}
+
 }  // namespace
 
 void launch_col_scan(const ScanArgs& a, bool ids, cudaStream_t st) {
@@ -232,14 +187,16 @@ void launch_col_scan(const ScanArgs& a, bool ids, cudaStream_t st) {
 
 int col_batch_max_dims() { return 64; }
 
+uint32_t col_batch_padded_dims(uint32_t kb) {
+    if (kb <= 16) return kb;
+    if (kb <= 32) return 32;
+    return 64;
+}
+
 void launch_col_batch_count(const BatchArgs& a, int num_sms, cudaStream_t st) {
-    if (a.kb <= 4)
-        run_batch<4, 4>(a, num_sms, st);
-    else if (a.kb <= 8)
-        run_batch<8, 4>(a, num_sms, st);
-    else if (a.kb <= 16)
-        run_batch<16, 4>(a, num_sms, st);
-    else if (a.kb <= 32)
+    if (a.kb <= 16)
+        dispatch_exact(a, num_sms, st, std::make_integer_sequence<int, 16>{});
+    else if (a.kb == 32)
         run_batch<32, 2>(a, num_sms, st);
     else
         run_batch<64, 1>(a, num_sms, st);

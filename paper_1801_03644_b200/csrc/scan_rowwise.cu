@@ -66,8 +66,6 @@ __global__ void __launch_bounds__(RW_THREADS) row_scan_kernel(const ScanArgs a) 
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_tiles[2];
-    __shared__ uint32_t s_seg[32];
-    __shared__ uint32_t s_excl;
     __shared__ uint16_t s_dims[kMaxDims];
     __shared__ float s_lo[kMaxDims], s_hi[kMaxDims];
     __shared__ unsigned long long s_early[3];
@@ -149,50 +147,20 @@ __global__ void __launch_bounds__(RW_THREADS) row_scan_kernel(const ScanArgs a) 
             }
         }
 
-        if (!IDS) {
-            matched += __popc(hits);
-        } else {
-            // order within the tile: (r, warp, lane)
-            const uint32_t lt = lanemask_lt();
+        matched += __popc(hits);
+        if (IDS) {
+            // verdict bitmask: (r, warp) covers 32 consecutive rows = one word
             for (uint32_t r = 0; r < rows_per_thread; ++r) {
                 const uint32_t b = __ballot_sync(0xFFFFFFFFu, (hits >> r) & 1u);
-                if (lane == 0) s_seg[r * (RW_THREADS / 32) + warp] = __popc(b);
-            }
-            __syncthreads();
-            if (warp == 0) {
-                const uint32_t nseg = rows_per_thread * (RW_THREADS / 32);
-                const uint32_t v = lane < nseg ? s_seg[lane] : 0u;
-                uint32_t incl = v;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                    if (lane >= uint32_t(o)) incl += t;
-                }
-                const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-                const uint32_t excl = lookback_exclusive(a.status, tile, a.epoch, total);
-                s_seg[lane] = incl - v;
-                if (lane == 0) {
-                    s_excl = excl;
-                    if (tile == a.num_tiles - 1) {
-                        const unsigned long long qbase = a.offsets[a.q];
-                        a.offsets[a.q + 1] = qbase + excl + total;
-                        a.counts[a.q] = excl + total;
-                    }
-                }
-            }
-            __syncthreads();
-            // second ballot pass places the ids (all lanes participate)
-            for (uint32_t r = 0; r < rows_per_thread; ++r) {
-                const uint32_t b = __ballot_sync(0xFFFFFFFFu, (hits >> r) & 1u);
-                if ((hits >> r) & 1u) {
-                    const unsigned long long pos =
-                        a.offsets[a.q] + s_excl + s_seg[r * (RW_THREADS / 32) + warp] + __popc(b & lt);
-                    if (pos < a.ids_cap)
-                        a.ids[pos] = a.id_base + uint32_t(tile_row0 + r * RW_THREADS + threadIdx.x);
+                const uint32_t row0 = r * RW_THREADS + warp * 32;
+                if (lane == 0 && row0 < R) {
+                    const uint64_t g0 = tile_row0 + row0;
+                    a.mask[g0 / 32] = b;
+                    if (b) atomicAdd(a.chunk_counts + g0 / kChunkTuples, uint32_t(__popc(b)));
                 }
             }
         }
-        __syncthreads();  // buf[stage] and s_seg free for reuse
+        __syncthreads();  // buf[stage] free for reuse
         stage ^= 1;
     }
 

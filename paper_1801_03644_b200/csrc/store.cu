@@ -147,6 +147,13 @@ struct Pass {
     size_t udim_off = 0, bound_off = 0, cmask_off = 0;
 };
 
+// one pass of the bit-sliced VA batch (<= 1024 queries)
+struct VbPass {
+    uint32_t q0 = 0, nqp = 0, kb = 0, cells = 0, shift = 0;
+    bool fallback = false;   // union wider than kVaBatchMaxDims: per-query VA
+    size_t udim_off = 0, table_off = 0, qb_off = 0;
+};
+
 }  // namespace
 
 struct mdrq_batch {
@@ -165,6 +172,13 @@ struct mdrq_batch {
     DBuf<uint16_t> d_udims;
     DBuf<float2> d_bounds;
     DBuf<unsigned long long> d_cmask;
+    std::vector<VbPass> vb_passes;
+    std::vector<uint16_t> vb_udims;
+    std::vector<uint32_t> vb_tables;
+    std::vector<float2> vb_qb;
+    DBuf<uint16_t> d_vb_udims;
+    DBuf<uint32_t> d_vb_tables;
+    DBuf<float2> d_vb_qb;
     DBuf<uint32_t> d_tile_counters;
     DBuf<unsigned long long> d_counts;
     DBuf<unsigned long long> d_offsets;
@@ -185,6 +199,12 @@ struct mdrq_store {
     std::vector<float> h_minmax;     // [m][2]
     DBuf<uint64_t> status;
     uint32_t epoch = 0;
+    DBuf<uint32_t> mask;             // ids mode: verdict bitmask of one query
+    DBuf<uint32_t> chunk_counts, chunk_offs;
+    uint32_t nchunks = 0;
+    // bit-sliced VA batch scratch ([chunks][1024] per pass)
+    DBuf<uint32_t> vb_chunk_counts;
+    DBuf<unsigned long long> vb_base, vb_total, vb_qoff;
     DBuf<uint32_t> ids;              // result pool
     uint64_t last_total = 0;
     uint32_t last_nq = 0;
@@ -231,6 +251,89 @@ bool is_pos_inf(float v) { return std::isinf(v) && v > 0; }
 uint16_t host_code(const float* b, uint32_t nb, float v) {
     // #{b <= v}; b sorted ascending under float compare
     return uint16_t(std::upper_bound(b, b + nb, v, [](float x, float y) { return x < y; }) - b);
+}
+
+// Passes of the bit-sliced VA batch: <= 1024 queries each; per union
+// dimension u and table cell c the overlap / containment masks of the pass's
+// queries (vabatch.cu).  Table cells are the stored 8-bit codes >> shift.
+void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
+    b->vb_passes.clear();
+    b->vb_udims.clear();
+    b->vb_tables.clear();
+    b->vb_qb.clear();
+    const uint32_t m = s->m, bits = s->va_bits;
+    for (uint32_t q0 = 0; q0 < b->nq; q0 += 1024) {
+        VbPass ps;
+        ps.q0 = q0;
+        ps.nqp = std::min<uint32_t>(1024, b->nq - q0);
+        std::vector<int> uidx(m, -1);
+        std::vector<uint16_t> ud;
+        for (uint32_t q = q0; q < q0 + ps.nqp; ++q)
+            for (uint32_t i = 0; i < b->descs[q].k; ++i) {
+                const uint32_t d = b->preds[b->descs[q].off + i].dim;
+                if (uidx[d] < 0) {
+                    uidx[d] = 0;
+                    ud.push_back(uint16_t(d));
+                }
+            }
+        std::sort(ud.begin(), ud.end());
+        if (ud.empty()) ud.push_back(0);
+        for (size_t i = 0; i < ud.size(); ++i) uidx[ud[i]] = int(i);
+        ps.kb = uint32_t(ud.size());
+        if (int(ps.kb) > va_batch_max_dims()) {
+            ps.fallback = true;
+            b->vb_passes.push_back(ps);
+            continue;
+        }
+        // table cells: va_batch_cells(kb) (the kernel's constant); a store
+        // with fewer code bits uses only the first 2^bits cells
+        ps.cells = va_batch_cells(ps.kb);
+        uint32_t tb = 0;
+        while ((1u << (tb + 1)) <= ps.cells) ++tb;
+        tb = std::min(bits, tb);
+        ps.shift = bits - tb;
+        ps.udim_off = b->vb_udims.size();
+        ps.table_off = b->vb_tables.size();
+        ps.qb_off = b->vb_qb.size();
+        b->vb_udims.insert(b->vb_udims.end(), ud.begin(), ud.end());
+        const size_t plane = size_t(ps.kb) * ps.cells * 32;
+        std::vector<uint32_t> tab(2 * plane, 0u);
+        std::vector<float2> qbv(size_t(1024) * ps.kb, make_float2(-INFINITY, INFINITY));
+        for (uint32_t qi = 0; qi < ps.nqp; ++qi) {
+            const QueryDesc& qd = b->descs[q0 + qi];
+            std::vector<int> lo_c(ps.kb, -1), hi_c(ps.kb, int(ps.cells)), elo(ps.kb, 0), ehi(ps.kb, 0);
+            std::vector<uint8_t> cons(ps.kb, 0);
+            for (uint32_t i = 0; i < qd.k; ++i) {
+                const DimPred& p = b->preds[qd.off + i];
+                const int u = uidx[p.dim];
+                cons[u] = 1;
+                lo_c[u] = int(p.cl) >> ps.shift;
+                hi_c[u] = int(p.ch) >> ps.shift;
+                elo[u] = p.edge_lo;
+                ehi[u] = p.edge_hi;
+                if (p.lo > p.hi) {  // empty interval (kernel level only)
+                    lo_c[u] = int(ps.cells);
+                    hi_c[u] = -1;
+                }
+                qbv[size_t(qi) * ps.kb + u] = make_float2(p.lo, p.hi);
+            }
+            const uint32_t w = qi >> 5, bit = 1u << (qi & 31);
+            for (uint32_t u = 0; u < ps.kb; ++u)
+                for (uint32_t c = 0; c < ps.cells; ++c) {
+                    bool ov = true, su = true;
+                    if (cons[u]) {
+                        ov = int(c) >= lo_c[u] && int(c) <= hi_c[u];
+                        su = ov && (int(c) > lo_c[u] || !elo[u]) && (int(c) < hi_c[u] || !ehi[u]);
+                    }
+                    const size_t idx = (size_t(u) * ps.cells + c) * 32 + w;
+                    if (ov) tab[idx] |= bit;
+                    if (su) tab[plane + idx] |= bit;
+                }
+        }
+        b->vb_tables.insert(b->vb_tables.end(), tab.begin(), tab.end());
+        b->vb_qb.insert(b->vb_qb.end(), qbv.begin(), qbv.end());
+        b->vb_passes.push_back(ps);
+    }
 }
 
 // Build the host descriptors of a batch.  strict = reference RangeQuery
@@ -327,6 +430,12 @@ void build_descs(const mdrq_store* s, const float* lo, const float* hi, uint32_t
                 b->passes.push_back(ps);
                 continue;
             }
+            // pad the union to the kernel's dimension count: repeat the last
+            // dimension with (-inf, +inf) bounds (never rejects a stored tuple)
+            const uint32_t kbp = col_batch_padded_dims(std::max<uint32_t>(ps.kb, 1));
+            if (ud.empty()) ud.push_back(0);
+            while (ud.size() < kbp) ud.push_back(ud.back());
+            ps.kb = kbp;
             ps.udim_off = b->udims.size();
             ps.bound_off = b->bounds.size();
             ps.cmask_off = b->cmask.size();
@@ -346,6 +455,7 @@ void build_descs(const mdrq_store* s, const float* lo, const float* hi, uint32_t
             b->passes.push_back(ps);
         }
     }
+    if (path == MDRQ_PATH_VAFILE_BATCH) build_vb_passes(s, b);
 }
 
 template <class T>
@@ -360,6 +470,9 @@ void upload_batch(mdrq_store* s, mdrq_batch* b) {
     upload(b->d_udims, b->udims, s->stream);
     upload(b->d_bounds, b->bounds, s->stream);
     upload(b->d_cmask, b->cmask, s->stream);
+    upload(b->d_vb_udims, b->vb_udims, s->stream);
+    upload(b->d_vb_tables, b->vb_tables, s->stream);
+    upload(b->d_vb_qb, b->vb_qb, s->stream);
     b->d_tile_counters.reserve(b->nq);
     b->d_counts.reserve(b->nq);
     b->d_offsets.reserve(size_t(b->nq) + 1);
@@ -384,6 +497,7 @@ uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids)
             if (!(s->layouts & MDRQ_LAYOUT_ROWWISE)) raise(MDRQ_EINVAL, "store has no row-wise layout");
             return path;
         case MDRQ_PATH_VAFILE:
+        case MDRQ_PATH_VAFILE_BATCH:
             if (!(s->layouts & MDRQ_LAYOUT_VAFILE)) raise(MDRQ_EINVAL, "store has no VA-file layout");
             return path;
         default: raise(MDRQ_EINVAL, "unknown query path " + std::to_string(path));
@@ -410,6 +524,46 @@ ScanArgs base_args(mdrq_store* s, mdrq_batch* b, uint32_t path) {
     a.ids_cap = s->ids.p ? s->ids.cap : 0;
     a.id_base = s->id_base;
     a.stats = b->d_stats.p;
+    a.mask = s->mask.p;
+    a.chunk_counts = s->chunk_counts.p;
+    a.chunk_offs = s->chunk_offs.p;
+    return a;
+}
+
+VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
+    VaBatchArgs a{};
+    a.codes = s->codes.p;
+    a.cols = s->cols.p;
+    a.stride = s->n_pad;
+    a.n = s->n;
+    a.kb = ps.kb;
+    a.cells = ps.cells;
+    a.shift = ps.shift;
+    a.nqp = ps.nqp;
+    a.udims = b->d_vb_udims.p + ps.udim_off;
+    a.tables = b->d_vb_tables.p + ps.table_off;
+    a.qbounds = b->d_vb_qb.p + ps.qb_off;
+    // CTAs per SM from the ids-pass footprint (identical chunking for every mode)
+    const size_t smem = va_batch_smem(ps.kb, ps.cells, 2);
+    uint32_t per_sm = uint32_t(std::max<size_t>(1, (227u * 1024u) / (smem + 1024)));
+    per_sm = std::min<uint32_t>(per_sm, 4);
+    a.grid = uint32_t(s->num_sms) * per_sm;
+    const uint64_t chunks = uint64_t(a.grid) * va_batch_warps();
+    a.chunk_tuples = round_up((s->n + chunks - 1) / chunks, 128);
+    s->vb_chunk_counts.reserve(chunks * 1024);
+    s->vb_base.reserve(chunks * 1024);
+    s->vb_total.reserve(1024);
+    s->vb_qoff.reserve(1024);
+    a.counts = b->d_counts.p + ps.q0;
+    a.chunk_counts = s->vb_chunk_counts.p;
+    a.base = s->vb_base.p;
+    a.total = s->vb_total.p;
+    a.qoff = s->vb_qoff.p;
+    a.offsets = b->d_offsets.p;
+    a.counts_all = b->d_counts.p;
+    a.ids = s->ids.p;
+    a.ids_cap = s->ids.p ? s->ids.cap : 0;
+    a.id_base = s->id_base;
     return a;
 }
 
@@ -428,6 +582,7 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
         ScanArgs a = base_args(s, b, sp);
         a.q = q;
         a.epoch = s->next_epoch();
+        if (ids) CK(cudaMemsetAsync(s->chunk_counts.p, 0, sizeof(uint32_t) * s->nchunks, st));
         if (sp == MDRQ_PATH_ROWWISE)
             launch_row_scan(a, ids, st);
         else if (sp == MDRQ_PATH_VAFILE)
@@ -435,8 +590,29 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
         else
             launch_col_scan(a, ids, st);
         ++launches;
+        if (ids) {
+            launch_expand(a, st);
+            launches += 2;
+        }
     };
-    if (path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
+    if (path == MDRQ_PATH_VAFILE_BATCH) {
+        for (const VbPass& ps : b->vb_passes) {
+            if (ps.fallback) {
+                for (uint32_t q = ps.q0; q < ps.q0 + ps.nqp; ++q) single(MDRQ_PATH_VAFILE, q);
+                continue;
+            }
+            VaBatchArgs va = vb_args(s, b, ps);
+            if (!ids) {
+                launch_va_batch(va, 0, st);
+                launches += 1;
+            } else {
+                launch_va_batch(va, 1, st);
+                launch_va_batch_scans(va, va.grid * va_batch_warps(), ps.q0, st);
+                launch_va_batch(va, 2, st);
+                launches += 4;
+            }
+        }
+    } else if (path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
         for (const Pass& ps : b->passes) {
             if (ps.fallback) {
                 for (uint32_t q = ps.q0; q < ps.q0 + ps.nqp; ++q) single(MDRQ_PATH_COLUMNAR, q);
@@ -465,12 +641,17 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
 
 uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
     if (!b->nq || s->n == 0) return 0;
+    if (b->path == MDRQ_PATH_VAFILE_BATCH) {
+        uint32_t l = 0;
+        for (const VbPass& ps : b->vb_passes) l += ps.fallback ? ps.nqp * (ids ? 3 : 1) : (ids ? 4 : 1);
+        return l;
+    }
     if (b->path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
         uint32_t l = 0;
         for (const Pass& ps : b->passes) l += ps.fallback ? ps.nqp : 1;
         return l;
     }
-    return b->nq;
+    return ids ? 3 * b->nq : b->nq;   // ids: scan + chunk scan + expand
 }
 
 // Run an ids pass synchronously, growing the result pool until it fits.
@@ -610,6 +791,13 @@ int mdrq_store_create(const float* rows, uint64_t n, uint32_t m, int device, uin
                 CK(cudaStreamSynchronize(st));
             }
             if (!(layouts & MDRQ_LAYOUT_ROWWISE)) s->rows.release();
+            {
+                const uint64_t span = round_up(std::max(s->n_pad, s->n_pad_rows), kChunkTuples);
+                s->nchunks = uint32_t(span / kChunkTuples);
+                s->mask.reserve(span / 32);
+                s->chunk_counts.reserve(s->nchunks);
+                s->chunk_offs.reserve(s->nchunks);
+            }
             uint64_t tiles = std::max<uint64_t>((n + kColTile - 1) / kColTile, (n + s->R - 1) / s->R);
             s->status.reserve(std::max<uint64_t>(tiles, 1));
             CK(cudaMemsetAsync(s->status.p, 0, s->status.bytes(), st));

@@ -1,0 +1,235 @@
+// vabatch.cu -- bit-sliced multi-query VA-file pass (up to 1024 queries per
+// pass over the code planes), SURVEY.md 8(f) item 1.
+//
+// The reference answers a batch one query at a time (bench.py:178-186), each
+// query a full scan (scan.py:103-111) or a VA-file bucket walk
+// (vafile.py:204-219).  Here one pass over the quantile-code byte planes
+// evaluates a whole batch:
+//
+//   * per union dimension u and coarse cell c the host builds two 1024-bit
+//     query masks: OV[u][c] (queries whose box overlaps cell c in dimension
+//     u) and SU[u][c] (queries that contain cell c entirely).  Word w of a
+//     mask covers queries 32w .. 32w+31 and lives in shared memory at
+//     [u][c][w], so a warp whose LANE w owns word w reads a whole 1024-bit
+//     row with one conflict-free LDS.32 per lane;
+//   * the warp walks its chunk of tuples in order; per tuple it ANDs the rows
+//     of the tuple's cells: maybe = AND_u OV, sure = AND_u SU.  maybe & ~sure
+//     are (tuple, query) pairs in an edge cell -- refined against the exact
+//     float32 columns (broadcast loads of the tuple's values);
+//   * matches are counted per query (count mode), per (chunk, query) (first
+//     pass of ids mode) or written as ids (second pass) at
+//     qoff[q] + base[chunk][q] + running count -- ascending per query
+//     because every warp owns one contiguous tuple range.
+//
+// The coarse cell of a tuple is its stored 8-bit quantile code shifted right
+// (the 2^tb-cell grid's boundaries are every 2^(8-tb)-th boundary of the
+// 256-cell grid, so code_tb = code_8 >> (8 - tb) exactly).  Soundness is the
+// single-query VA-file's (vafile.cu): cells strictly inside [code(lo),
+// code(hi)] need no refinement, edge cells are refined exactly.
+#include <utility>
+
+#include "launch.h"
+
+namespace mdrq {
+
+namespace {
+
+constexpr int VB_THREADS = 256;
+constexpr int VB_WARPS = VB_THREADS / 32;
+
+template <int MODE, int KB>
+__global__ void __launch_bounds__(VB_THREADS) va_batch_kernel(const VaBatchArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
+    __shared__ uint32_t s_dim[KB];
+    uint32_t* s_ov = sm;                           // [KB][K][32]
+    uint32_t* s_su = sm + KB * K * 32;             // [KB][K][32]
+    uint32_t* s_cnt = s_su + KB * K * 32;          // MODE 0: [1024] ; MODE 1/2: [warps][1024]
+
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.tables);
+        uint4* dst = reinterpret_cast<uint4*>(sm);
+        const uint32_t n4 = 2 * KB * K * 32 / 4;
+        for (uint32_t i = threadIdx.x; i < n4; i += VB_THREADS) dst[i] = src[i];
+        const uint32_t ncnt = MODE == 0 ? 1024u : 1024u * VB_WARPS;
+        for (uint32_t i = threadIdx.x; i < ncnt; i += VB_THREADS) s_cnt[i] = 0;
+        if (threadIdx.x < KB) s_dim[threadIdx.x] = a.udims[threadIdx.x];
+    }
+    __syncthreads();
+
+    const uint32_t chunk = blockIdx.x * VB_WARPS + warp;
+    const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
+    uint64_t end = start + a.chunk_tuples;
+    if (end > a.n) end = a.n;
+    uint32_t* wcnt = MODE == 0 ? s_cnt : s_cnt + warp * 1024;
+
+    const uint32_t shift = a.shift;
+    const float2* __restrict__ qb = a.qbounds;     // [1024][KB]
+    const unsigned long long* __restrict__ base = MODE == 2 ? a.base + uint64_t(chunk) * 1024 : nullptr;
+    const uint32_t* s_ovl = s_ov + lane;           // lane's word of every row
+    const uint32_t* s_sul = s_su + lane;
+
+    for (uint64_t t0 = start; t0 < end; t0 += 128) {
+        uint32_t cw[KB];
+#pragma unroll
+        for (int u = 0; u < KB; ++u)
+            cw[u] = __ldcs(reinterpret_cast<const unsigned int*>(a.codes + uint64_t(s_dim[u]) * a.stride + t0) +
+                           lane);
+        const uint32_t jmax = uint32_t(end - t0 < 128 ? end - t0 : 128);
+        for (uint32_t j4 = 0; j4 < jmax; j4 += 4) {
+            uint32_t x[KB];
+#pragma unroll
+            for (int u = 0; u < KB; ++u) x[u] = __shfl_sync(0xFFFFFFFFu, cw[u], j4 >> 2);
+#pragma unroll
+            for (uint32_t jj = 0; jj < 4; ++jj) {
+                if (j4 + jj >= jmax) break;
+                uint32_t ov = 0xFFFFFFFFu, su = 0xFFFFFFFFu;
+#pragma unroll
+                for (int u = 0; u < KB; ++u) {
+                    const uint32_t c = (x[u] >> (8 * jj + shift)) & (K - 1);
+                    const uint32_t idx = u * K * 32 + c * 32;   // u*K*32 folds into the LDS offset
+                    ov &= s_ovl[idx];
+                    su &= s_sul[idx];
+                }
+                const uint64_t t = t0 + j4 + jj;
+                uint32_t hits = su;
+                uint32_t r = ov & ~su;
+                if (__any_sync(0xFFFFFFFFu, r)) {
+                    float v[KB];
+#pragma unroll
+                    for (int u = 0; u < KB; ++u) v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
+                    while (r) {
+                        const int b = __ffs(r) - 1;
+                        r &= r - 1;
+                        const float2* qq = qb + (lane * 32 + b) * KB;
+                        bool ok = true;
+#pragma unroll
+                        for (int u = 0; u < KB; ++u) {
+                            const float2 bb = qq[u];
+                            ok = ok && (bb.x <= v[u]) && (v[u] <= bb.y);
+                        }
+                        if (ok) hits |= 1u << b;
+                    }
+                }
+                while (hits) {
+                    const int b = __ffs(hits) - 1;
+                    hits &= hits - 1;
+                    const uint32_t q = lane * 32 + b;
+                    if (MODE == 0) {
+                        atomicAdd(&wcnt[q], 1u);
+                    } else if (MODE == 1) {
+                        wcnt[q] += 1;
+                    } else {
+                        const unsigned long long pos = a.qoff[q] + base[q] + wcnt[q];
+                        wcnt[q] += 1;
+                        if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(t);
+                    }
+                }
+            }
+        }
+    }
+
+    if (MODE == 0) {
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < a.nqp; q += VB_THREADS)
+            if (s_cnt[q]) atomicAdd(a.counts + q, (unsigned long long)s_cnt[q]);
+    } else if (MODE == 1) {
+        __syncwarp();
+        uint32_t* out = a.chunk_counts + uint64_t(chunk) * 1024;
+        for (uint32_t q = lane; q < 1024; q += 32) out[q] = wcnt[q];
+    }
+}
+
+// per-query exclusive scan over chunks: base[c][q], total[q]
+__global__ void vb_chunk_scan_kernel(const uint32_t* __restrict__ cc, uint32_t nchunks, uint32_t nqp,
+                                     unsigned long long* __restrict__ base, unsigned long long* __restrict__ total) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nqp) return;
+    unsigned long long run = 0;
+    for (uint32_t c = 0; c < nchunks; ++c) {
+        const uint32_t v = cc[uint64_t(c) * 1024 + q];
+        base[uint64_t(c) * 1024 + q] = run;
+        run += v;
+    }
+    total[q] = run;
+}
+
+// exclusive scan of the pass's query totals, chained on offsets[q0]
+__global__ void __launch_bounds__(1024) vb_query_scan_kernel(const unsigned long long* __restrict__ total, uint32_t nqp,
+                                                             unsigned long long* offsets, unsigned long long* counts,
+                                                             unsigned long long* qoff, uint32_t q0) {
+    __shared__ unsigned long long s_w[32];
+    const uint32_t q = threadIdx.x, lane = q & 31u, warp = q >> 5;
+    const unsigned long long v = q < nqp ? total[q] : 0ull;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= uint32_t(o)) incl += t;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned long long w = s_w[lane];
+        unsigned long long wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= uint32_t(o)) wi += t;
+        }
+        s_w[lane] = wi - w;
+    }
+    __syncthreads();
+    const unsigned long long b0 = offsets[q0];
+    const unsigned long long excl = s_w[warp] + incl - v;
+    if (q < nqp) {
+        qoff[q] = b0 + excl;
+        offsets[q0 + q + 1] = b0 + excl + v;
+        counts[q0 + q] = v;
+    }
+}
+
+template <int MODE, int KB>
+void run_kb(const VaBatchArgs& a, cudaStream_t st) {
+    const size_t smem = va_batch_smem(KB, va_batch_cells(KB), MODE);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(va_batch_kernel<MODE, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        configured = true;
+    }
+    va_batch_kernel<MODE, KB><<<a.grid, VB_THREADS, smem, st>>>(a);
+}
+
+template <int MODE, int... Ks>
+void dispatch(const VaBatchArgs& a, cudaStream_t st, std::integer_sequence<int, Ks...>) {
+    ((a.kb == uint32_t(Ks + 1) ? run_kb<MODE, Ks + 1>(a, st) : void()), ...);
+}
+
+}  // namespace
+
+size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
+    return size_t(2) * kb * cells * 32 * 4 + (mode == 0 ? 1024 * 4 : 1024 * 4 * VB_WARPS);
+}
+
+int va_batch_max_dims() { return kVaBatchMaxDims; }
+
+uint32_t va_batch_warps() { return VB_WARPS; }
+
+void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st) {
+    if (a.n == 0 || a.grid == 0) return;
+    using Seq = std::make_integer_sequence<int, kVaBatchMaxDims>;
+    if (mode == 0)
+        dispatch<0>(a, st, Seq{});
+    else if (mode == 1)
+        dispatch<1>(a, st, Seq{});
+    else
+        dispatch<2>(a, st, Seq{});
+}
+
+void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st) {
+    vb_chunk_scan_kernel<<<(a.nqp + 255) / 256, 256, 0, st>>>(a.chunk_counts, nchunks, a.nqp, a.base, a.total);
+    vb_query_scan_kernel<<<1, 1024, 0, st>>>(a.total, a.nqp, a.offsets, a.counts_all, a.qoff, q0);
+}
+
+}  // namespace mdrq

@@ -121,23 +121,18 @@ __device__ __forceinline__ uint32_t flags_to_nib(uint32_t f) {
 
 template <bool IDS>
 __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_seg[32];
-    __shared__ uint32_t s_excl;
+    __shared__ uint32_t s_cnt[VA_THREADS / 32];
     __shared__ uint32_t s_refined;
 
     const QueryDesc qd = a.descs[a.q];
     const DimPred* __restrict__ P = a.preds + qd.off;
     const uint32_t k = qd.k;
-    if (threadIdx.x == 0) {
-        s_tile = atomicAdd(a.tile_counters + a.q, 1u);
-        s_refined = 0;
-    }
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    if (threadIdx.x == 0) s_refined = 0;
+    const uint32_t tile = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     // tuple of (group g, word w, byte b) = base + g*512 + w*4 + b
-    const uint64_t base = uint64_t(tile) * kVaTile + warp * VA_WARP_TUPLES + lane * 16;
+    const uint64_t wbase = uint64_t(tile) * kVaTile + warp * VA_WARP_TUPLES;
+    const uint64_t base = wbase + lane * 16;
 
     // alive / sure flags in SWAR layout, one word per 4 tuples
     uint32_t al[VA_G][4], su[VA_G][4];
@@ -222,77 +217,34 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
     }
     if (a.stats) {
         refined = __reduce_add_sync(0xFFFFFFFFu, refined);
+        __syncthreads();
         if (lane == 0 && refined) atomicAdd(&s_refined, refined);
     }
 
+    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, __popc(hit[0]) + __popc(hit[1]));
     if (!IDS) {
-        uint32_t c = __reduce_add_sync(0xFFFFFFFFu, __popc(hit[0]) + __popc(hit[1]));
-        if (lane == 0) s_seg[warp] = c;
+        if (lane == 0) s_cnt[warp] = wc;
         __syncthreads();
         if (threadIdx.x == 0) {
             uint32_t t = 0;
 #pragma unroll
-            for (int w = 0; w < VA_THREADS / 32; ++w) t += s_seg[w];
+            for (int w = 0; w < VA_THREADS / 32; ++w) t += s_cnt[w];
             if (t) atomicAdd(a.counts + a.q, (unsigned long long)t);
             if (a.stats && s_refined) atomicAdd(a.stats + 4 * a.q + 2, (unsigned long long)s_refined);
         }
         return;
     }
-
-    // ordered compaction: order within the tile is (warp, g, lane, j)
-    const uint32_t lt = lanemask_lt();
-    uint32_t pre[VA_G];
+    // ids mode: two lanes share one mask word per group
 #pragma unroll
     for (int g = 0; g < VA_G; ++g) {
-        const uint32_t c = __popc(hit[g]);
-        // warp exclusive scan of c
-        uint32_t incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= uint32_t(o)) incl += t;
-        }
-        pre[g] = incl - c;
-        if (lane == 31) s_seg[warp * VA_G + g] = incl;
+        uint32_t v = hit[g] << (16 * (lane & 1u));
+        v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+        if ((lane & 1u) == 0) a.mask[(base + g * 512) / 32] = v;
     }
-    (void)lt;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t nseg = (VA_THREADS / 32) * VA_G;
-        const uint32_t v = lane < nseg ? s_seg[lane] : 0u;
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= uint32_t(o)) incl += t;
-        }
-        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        const uint32_t excl = lookback_exclusive(a.status, tile, a.epoch, total);
-        s_seg[lane] = incl - v;
-        if (lane == 0) {
-            s_excl = excl;
-            if (tile == a.num_tiles - 1) {
-                const unsigned long long qbase = a.offsets[a.q];
-                a.offsets[a.q + 1] = qbase + excl + total;
-                a.counts[a.q] = excl + total;
-            }
-            if (a.stats && s_refined) atomicAdd(a.stats + 4 * a.q + 2, (unsigned long long)s_refined);
-        }
-    }
-    __syncthreads();
-    if (hit[0] | hit[1]) {
-        const unsigned long long obase = a.offsets[a.q] + s_excl;
-#pragma unroll
-        for (int g = 0; g < VA_G; ++g) {
-            uint32_t h = hit[g];
-            unsigned long long pos = obase + s_seg[warp * VA_G + g] + pre[g];
-            while (h) {
-                const int j = __ffs(h) - 1;
-                h &= h - 1;
-                if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(base + g * 512 + j);
-                ++pos;
-            }
-        }
+    if (lane == 0 && wc) atomicAdd(a.chunk_counts + wbase / kChunkTuples, wc);
+    if (a.stats) {
+        __syncthreads();
+        if (threadIdx.x == 0 && s_refined) atomicAdd(a.stats + 4 * a.q + 2, (unsigned long long)s_refined);
     }
 }
 

@@ -12,7 +12,7 @@ from conftest import golden
 
 pytestmark = pytest.mark.gpu
 
-PATHS = ("columnar", "rowwise", "vafile", "columnar_batch")
+PATHS = ("columnar", "rowwise", "vafile", "columnar_batch", "vafile_batch")
 ALL_LAYOUTS = 1 | 2 | 4
 
 
@@ -203,7 +203,7 @@ def test_vafile_grid_and_soundness(gpu):
     b = va.grid.boundaries
     assert b.shape == (3, 15) and np.all(np.diff(b, axis=1) >= 0)
     # equal-frequency cells on uniform data: each holds ~1/16 of the tuples
-    cells = va.grid.approximate_all(data.values[:, :1])[:, 0]
+    cells = va.grid.approximate_all(data.values)[:, 0]
     frac = np.bincount(cells, minlength=16) / data.n
     assert np.all(np.abs(frac - 1 / 16) < 0.01)
     for q in gpu.pair_query_batch(data, 20, 17):
