@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--path", default="columnar")
+    ap.add_argument("--path", default="auto")
+    ap.add_argument("--no-paths", action="store_true", help="skip the per-path cost table")
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="tuples per GPU")
     ap.add_argument("--queries", type=int, default=NQ)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -233,6 +234,7 @@ def main():
     assert sptr != 0
 
     batch = store.prepare(lo, hi, args.path)
+    binfo = batch.info()
     total_local = batch.reserve()
     launches_per_step = batch.launches(ids=True)
 
@@ -240,7 +242,6 @@ def main():
         batch.ids_async(sptr)
         if world > 1:
             d_ids, d_offs, tot = batch.result_device()
-            # wrap the device result as tensors (same stream ordering)
             ids_t = _wrap(d_ids, tot, torch.int32, dev)
             offs_t = _wrap(d_offs, nq + 1, torch.int64, dev)
             eng.combine_ids(offs_t, ids_t)
@@ -265,44 +266,55 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    tuples = n * world * nq
-    value = tuples / (ms / 1e3)
+    value = n * world * nq / (ms / 1e3)
 
-    # ---- dominant kernel: one ids pass, its launches timed on the stream
-    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 3
-    ev2.record(stream)
-    for _ in range(reps):
-        batch.ids_async(sptr)
-    ev3.record(stream)
-    torch.cuda.synchronize()
-    pass_ms = ev2.elapsed_time(ev3) / reps
-    launch_ms = pass_ms / max(1, launches_per_step)
-    # algorithmic bytes per launch: every queried
-    # column once (4 B x n x k) + the ids written (4 B each) + counts
-    k = M
-    out_bytes = 4.0 * total_local / nq + 8
-    algo_bytes = 4.0 * n * k + out_bytes
+    # ---- dominant kernel of the step: one ids pass with events between
+    # launch groups (mdrq_batch_profile), bytes from the kernels' counters
     peak, peak_kind = measured_peaks()
-    achieved = algo_bytes / (launch_ms / 1e3) / 1e9
+    prof = batch.profile(ids=True, stream=sptr)
+    stats = store.stats(nq)
+    roofline = roofline_of(binfo["path"], prof, stats, n, nq, total_local, peak, peak_kind)
+
+    # ---- the single-query columnar scan kernel (HBM-bound by design), same data
+    col_q = min(nq, 100)
+    cb = store.prepare(lo[:col_q], hi[:col_q], "columnar")
+    cb.reserve()
+    cprof = cb.profile(ids=True, stream=sptr)
+    cstats = store.stats(col_q)
+    col_roof = roofline_of("columnar", cprof, cstats, n, col_q, None, peak, peak_kind)
+    cb.close()
+
+    # ---- per-path cost at this workload (device time per query)
+    paths = {}
+    if not args.no_paths:
+        for p in ("vafile_batch", "columnar_batch", "vafile", "columnar", "rowwise"):
+            q = nq if p.endswith("_batch") else min(nq, 50)
+            pb = store.prepare(lo[:q], hi[:q], p)
+            entry = {}
+            for mode in ("count", "ids"):
+                if mode == "ids" and p == "columnar_batch":
+                    continue
+                if mode == "ids":
+                    pb.reserve()
+                pr = pb.profile(ids=(mode == "ids"), stream=sptr)
+                entry[f"{mode}_us_per_query"] = round(sum(v[0] for v in pr.values()) * 1e3 / q, 2)
+            paths[p] = entry
+            pb.close()
 
     # ---- e2e through the public API: host queries in, host ids out (pinned)
     pinned = torch.empty(max(1, total_local + 1024), dtype=torch.int32, pin_memory=True)
     out_np = pinned.numpy().view(np.uint32)
     store.ids(lo, hi, args.path, out=out_np)  # warm
-    t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
     for _ in range(e2e_steps):
         offs, ids = store.ids(lo, hi, args.path, out=out_np)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_val = n * nq / e2e_s
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_val = n * world * nq / float(t.item())
-
-    if args.explore and rank == 0:
-        explore(store, lo, hi, n, stream)
+        e2e_s = float(t.item())
+    e2e_val = n * world * nq / e2e_s
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -317,15 +329,17 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"C2: n={n}/GPU m={M} uniform seed 0, {nq} full-match queries at "
-                                   f"selectivity {SELECTIVITY}, ids mode", "path": args.path,
+                                   f"selectivity {SELECTIVITY}, ids mode (sorted uint32 ids per query)",
+                       "path": binfo["path"], "requested_path": args.path,
                        "queries_per_step": nq, "ids_per_step": int(total_local) * world,
-                       "l2": "inputs (1.6 GB/GPU) larger than L2 (126 MB); no flush",
+                       "l2": "inputs (1.6 GB/GPU columns, 400 MB/GPU code planes) larger than L2 (126 MB); "
+                             "no flush",
                        "parallelism": f"row shards x{world}"},
-            "hbm_gbs_per_gpu": achieved,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": f"{args.path} ids pass, {launches_per_step} launches/step",
-                         "algo_bytes_per_launch": algo_bytes, "launch_ms": launch_ms},
+            "queries_per_s": nq / (ms / 1e3),
+            "hbm_gbs_per_gpu": roofline["achieved"],
+            "roofline": roofline,
+            "columnar_scan_roofline": col_roof,
+            "paths_us_per_query": paths,
             "e2e": {"value": e2e_val, "unit": "tuples/s", "h2d_bytes_per_step": int(lo.nbytes + hi.nbytes),
                     "d2h_bytes_per_step": int(total_local * 4 + (nq + 1) * 8)},
             "gpu_launches": launches_per_step * args.steps,
@@ -339,6 +353,35 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def roofline_of(path, prof, stats, n, nq, total_ids, peak, peak_kind):
+    """Roofline of the dominant kernel class of one profiled pass.
+
+    Algorithmic bytes: the HBM bytes the algorithm
+    must move -- the column / code-plane loads the scan kernels issue
+    (skipped loads are not counted), plus the kernel's own outputs (the
+    verdict bitmask n/8 B per query, or the ids 4 B each)."""
+    cls = max(("scan", "compaction", "id_write"), key=lambda c: prof[c][0])
+    ms, nl = prof[cls]
+    nl = max(nl, 1)
+    loaded = float(sum(s.bytes_loaded for s in stats))
+    ids_bytes = 4.0 * (total_ids or 0)
+    if path.endswith("_batch"):
+        passes = max(1, prof["scan"][1] if cls == "scan" else nl)
+        algo = loaded / passes + (ids_bytes / passes if cls == "id_write" else 0.0)
+        kernel = {"vafile_batch": "va_batch_kernel (bit-sliced, <=1024 queries/pass)",
+                  "columnar_batch": "col_batch_count_kernel (<=32 queries/pass)"}[path]
+        kernel += " filter pass" if cls == "scan" else " id-write pass"
+    else:
+        algo = (loaded + nq * n / 8.0) / nl
+        kernel = {"columnar": "col_scan_kernel", "vafile": "va_scan_kernel", "rowwise": "row_scan_kernel"}[path]
+    launch_ms = ms / nl
+    achieved = algo / (launch_ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "peak_kind": peak_kind, "kernel": kernel, "class": cls,
+            "algo_bytes_per_launch": algo, "launch_ms": launch_ms, "launches": nl,
+            "class_share_of_pass": ms / max(1e-9, sum(v[0] for v in prof.values()))}
 
 
 def _wrap(ptr: int, count: int, dtype, dev):

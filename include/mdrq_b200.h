@@ -86,6 +86,10 @@ typedef struct mdrq_search_stats {
     uint64_t columns_scanned;
     uint64_t early_breaks;     /* row-wise path only                        */
     uint64_t and_chunks;       /* tiles the fused AND ran over              */
+    uint64_t bytes_loaded;     /* HBM bytes the scan kernel requested: loads
+                                  not skipped (single-query paths) or the
+                                  union's planes / rows (multi-query passes,
+                                  shared equally by the pass's queries)     */
 } mdrq_search_stats;
 
 /* -- library ------------------------------------------------------------ */
@@ -162,6 +166,14 @@ int mdrq_result_device(mdrq_store* s, uint64_t* d_ids, uint64_t* d_offsets,
                        uint64_t* total);
 /* number of kernels one count / ids pass of this batch launches.          */
 int mdrq_batch_launches(mdrq_batch* b, int ids_mode, uint32_t* launches);
+/* info[0] resolved path, [1] queries, [2] multi-query passes, [3] widest
+ * union of dimensions over the passes (0 for single-query paths).         */
+int mdrq_batch_info(mdrq_batch* b, uint32_t* info /*[4]*/);
+/* run one pass with CUDA events between launch groups (synchronising) and
+ * report per-class device time / kernel launches; classes: 0 scan / filter,
+ * 1 ordered compaction, 2 id write (bit-sliced VA batch), 3 setup.          */
+int mdrq_batch_profile(mdrq_store* s, mdrq_batch* b, int ids_mode, void* stream,
+                       double* class_ms /*[4]*/, uint32_t* class_launches /*[4]*/);
 
 #ifdef __cplusplus
 }

@@ -57,7 +57,7 @@ EXPORTED = (
     "mdrq_query_count", "mdrq_query_ids", "mdrq_fetch_ids", "mdrq_query_stats",
     "mdrq_batch_prepare", "mdrq_batch_destroy", "mdrq_batch_count_async",
     "mdrq_batch_ids_async", "mdrq_batch_reserve", "mdrq_result_device",
-    "mdrq_batch_launches",
+    "mdrq_batch_launches", "mdrq_batch_profile", "mdrq_batch_info",
 )
 
 
@@ -80,6 +80,7 @@ class SearchStatsC(ctypes.Structure):
         ("columns_scanned", ctypes.c_uint64),
         ("early_breaks", ctypes.c_uint64),
         ("and_chunks", ctypes.c_uint64),
+        ("bytes_loaded", ctypes.c_uint64),
     ]
 
 
@@ -119,6 +120,8 @@ _SIGS = {
     "mdrq_batch_reserve": (_int, [_vp, _vp, _u64p]),
     "mdrq_result_device": (_int, [_vp, _u64p, _u64p, _u64p]),
     "mdrq_batch_launches": (_int, [_vp, _int, _u32p]),
+    "mdrq_batch_profile": (_int, [_vp, _vp, _int, _vp, ctypes.POINTER(ctypes.c_double), _u32p]),
+    "mdrq_batch_info": (_int, [_vp, _u32p]),
 }
 
 _lock = threading.Lock()

@@ -74,7 +74,8 @@ struct VaBatchArgs {
     const uint32_t* tables;      // [2][kb][cells][32]: overlap masks, then sure masks
     const float2* qbounds;       // [1024][kb] exact (lo, hi), +-inf where unconstrained
     uint32_t grid;               // CTAs (chunks = grid * warps)
-    uint64_t chunk_tuples;       // tuples per warp chunk (multiple of 128)
+    uint64_t chunk_tuples;       // tuples per chunk (multiple of 128, < 65536: u16 counters)
+    uint32_t nchunks;            // ceil(n / chunk_tuples); warps stride over chunks
     unsigned long long* counts;  // [nqp] count mode (offset to the pass)
     uint32_t* chunk_counts;      // [chunks][1024]
     unsigned long long* base;    // [chunks][1024]

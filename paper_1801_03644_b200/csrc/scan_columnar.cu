@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) 
                 if (base + g * 128 + j < a.n) alive |= 1u << (4 * g + j);
     }
 
+    uint32_t nload = 0;  // 16-byte loads issued (skipped groups are not read)
     for (uint32_t i = 0; i < k; ++i) {
         if (!__any_sync(0xFFFFFFFFu, alive)) break;  // whole warp rejected: skip the rest
         const DimPred p = P[i];
@@ -56,7 +57,10 @@ __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) 
         float4 v[CS_G];
 #pragma unroll
         for (int g = 0; g < CS_G; ++g)
-            if ((alive >> (4 * g)) & 0xFu) v[g] = ld_stream_f4(c + g * 32);
+            if ((alive >> (4 * g)) & 0xFu) {
+                v[g] = ld_stream_f4(c + g * 32);
+                ++nload;
+            }
 #pragma unroll
         for (int g = 0; g < CS_G; ++g)
             if ((alive >> (4 * g)) & 0xFu)
@@ -64,6 +68,10 @@ __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) 
     }
 
     const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, __popc(alive));
+    if (a.stats) {
+        nload = __reduce_add_sync(0xFFFFFFFFu, nload);
+        if (lane == 0 && nload) atomicAdd(a.stats + 4 * a.q + 3, 16ull * nload);
+    }
     if (!IDS) {
         if (lane == 0) s_cnt[warp] = wc;
         __syncthreads();

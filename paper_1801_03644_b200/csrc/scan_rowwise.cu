@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(RW_THREADS) row_scan_kernel(const ScanArgs a) 
     const uint32_t rot = k ? ((lane * g) >> 5) % k : 0;
     const uint32_t rows_per_thread = (R + RW_THREADS - 1) / RW_THREADS;
     const uint32_t blocks8 = m / 8;
-    uint32_t early_s = 0, early_b = 0, matched = 0;
+    uint32_t early_s = 0, early_b = 0, matched = 0, tiles_done = 0;
     uint32_t phase[2] = {0, 0};
     int stage = 0;
 
@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(RW_THREADS) row_scan_kernel(const ScanArgs a) 
             }
         }
         mbar_wait(&s_bar[stage], phase[stage]);
+        ++tiles_done;
         phase[stage] ^= 1u;
 
         const float* tb = buf[stage];
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(RW_THREADS) row_scan_kernel(const ScanArgs a) 
     if (threadIdx.x == 0) {
         if (a.stats && s_early[0]) atomicAdd(a.stats + 4 * a.q + 0, s_early[0]);
         if (a.stats && s_early[1]) atomicAdd(a.stats + 4 * a.q + 1, s_early[1]);
+        if (a.stats && tiles_done) atomicAdd(a.stats + 4 * a.q + 3, (unsigned long long)tiles_done * tile_bytes);
         if (!IDS && s_early[2]) atomicAdd(a.counts + a.q, s_early[2]);
     }
 }

@@ -484,7 +484,14 @@ void upload_batch(mdrq_store* s, mdrq_batch* b) {
 
 uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
     if (path == MDRQ_PATH_AUTO) {
+        // planner, from the B200 per-query costs of C2:
+        // a bit-sliced VA pass costs about as much as ~50 single-query VA
+        // scans, so it wins from 64 queries on; below that one query per
+        // pass over the code planes (VA) or the columns.
+        const bool va = (s->layouts & MDRQ_LAYOUT_VAFILE) != 0;
         if (!(s->layouts & MDRQ_LAYOUT_COLUMNAR)) return MDRQ_PATH_ROWWISE;
+        if (va && nq >= 64) return MDRQ_PATH_VAFILE_BATCH;
+        if (va) return MDRQ_PATH_VAFILE;
         if (!ids && nq >= 2) return MDRQ_PATH_COLUMNAR_BATCH;
         return MDRQ_PATH_COLUMNAR;
     }
@@ -543,13 +550,13 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.udims = b->d_vb_udims.p + ps.udim_off;
     a.tables = b->d_vb_tables.p + ps.table_off;
     a.qbounds = b->d_vb_qb.p + ps.qb_off;
-    // CTAs per SM from the ids-pass footprint (identical chunking for every mode)
-    const size_t smem = va_batch_smem(ps.kb, ps.cells, 2);
-    uint32_t per_sm = uint32_t(std::max<size_t>(1, (227u * 1024u) / (smem + 1024)));
-    per_sm = std::min<uint32_t>(per_sm, 4);
-    a.grid = uint32_t(s->num_sms) * per_sm;
-    const uint64_t chunks = uint64_t(a.grid) * va_batch_warps();
-    a.chunk_tuples = round_up((s->n + chunks - 1) / chunks, 128);
+    // one CTA per SM (the tables take most of the shared memory); chunks of
+    // < 65536 tuples (16-bit per-warp counters), identical in every mode
+    a.grid = uint32_t(s->num_sms);
+    const uint64_t warps = uint64_t(a.grid) * va_batch_warps();
+    a.chunk_tuples = std::min<uint64_t>(65408, round_up((s->n + warps - 1) / warps, 128));
+    a.nchunks = uint32_t((s->n + a.chunk_tuples - 1) / a.chunk_tuples);
+    const uint64_t chunks = a.nchunks;
     s->vb_chunk_counts.reserve(chunks * 1024);
     s->vb_base.reserve(chunks * 1024);
     s->vb_total.reserve(1024);
@@ -568,9 +575,34 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
 }
 
 // Enqueue one count / ids pass of a prepared batch.  Returns kernel launches.
-uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
+// Optional per-stage timing of one pass (mdrq_batch_profile): an event is
+// recorded before every launch group; the time to the next mark is charged
+// to the group's class (0 scan / filter, 1 compaction, 2 id write, 3 setup).
+struct Profiler {
+    cudaStream_t st = nullptr;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cls;
+    uint32_t launches[4] = {0, 0, 0, 0};
+    void mark(int c, uint32_t nlaunch) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, st));
+        ev.push_back(e);
+        cls.push_back(c);
+        if (c >= 0 && c < 4) launches[c] += nlaunch;
+    }
+    ~Profiler() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+};
+
+uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profiler* prof = nullptr) {
     const uint32_t nq = b->nq;
     if (!nq) return 0;
+    auto mark = [&](int c, uint32_t nl) {
+        if (prof) prof->mark(c, nl);
+    };
+    mark(3, 0);
     CK(cudaMemsetAsync(b->d_tile_counters.p, 0, sizeof(uint32_t) * nq, st));
     CK(cudaMemsetAsync(b->d_counts.p, 0, sizeof(unsigned long long) * nq, st));
     CK(cudaMemsetAsync(b->d_stats.p, 0, sizeof(unsigned long long) * nq * 4, st));
@@ -582,7 +614,11 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
         ScanArgs a = base_args(s, b, sp);
         a.q = q;
         a.epoch = s->next_epoch();
-        if (ids) CK(cudaMemsetAsync(s->chunk_counts.p, 0, sizeof(uint32_t) * s->nchunks, st));
+        if (ids) {
+            mark(1, 0);
+            CK(cudaMemsetAsync(s->chunk_counts.p, 0, sizeof(uint32_t) * s->nchunks, st));
+        }
+        mark(0, 1);
         if (sp == MDRQ_PATH_ROWWISE)
             launch_row_scan(a, ids, st);
         else if (sp == MDRQ_PATH_VAFILE)
@@ -591,6 +627,7 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
             launch_col_scan(a, ids, st);
         ++launches;
         if (ids) {
+            mark(1, 2);
             launch_expand(a, st);
             launches += 2;
         }
@@ -603,11 +640,15 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
             }
             VaBatchArgs va = vb_args(s, b, ps);
             if (!ids) {
+                mark(0, 1);
                 launch_va_batch(va, 0, st);
                 launches += 1;
             } else {
+                mark(0, 1);
                 launch_va_batch(va, 1, st);
-                launch_va_batch_scans(va, va.grid * va_batch_warps(), ps.q0, st);
+                mark(1, 2);
+                launch_va_batch_scans(va, va.nchunks, ps.q0, st);
+                mark(2, 1);
                 launch_va_batch(va, 2, st);
                 launches += 4;
             }
@@ -628,6 +669,7 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st) {
             ba.bounds = b->d_bounds.p + ps.bound_off;
             ba.cmask = b->d_cmask.p + ps.cmask_off;
             ba.counts = b->d_counts.p + ps.q0;
+            mark(0, 1);
             launch_col_batch_count(ba, s->num_sms, st);
             ++launches;
         }
@@ -939,10 +981,22 @@ int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats, uint32_t
                                s->stream));
         CK(cudaStreamSynchronize(s->stream));
         const uint32_t path = b->path;
+        // multi-query passes: the union's planes / columns, shared by the pass
+        std::vector<uint64_t> pass_bytes(nq, 0);
+        if (path == MDRQ_PATH_VAFILE_BATCH) {
+            for (const VbPass& p : b->vb_passes)
+                for (uint32_t q = p.q0; q < p.q0 + p.nqp; ++q)
+                    pass_bytes[q] = p.fallback ? 0 : (s->n * p.kb) / p.nqp;
+        } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
+            for (const Pass& p : b->passes)
+                for (uint32_t q = p.q0; q < p.q0 + p.nqp; ++q)
+                    pass_bytes[q] = p.fallback ? 0 : (4 * s->n * p.kb) / p.nqp;
+        }
         for (uint32_t q = 0; q < nq; ++q) {
             mdrq_search_stats& o = stats[q];
             const uint64_t k = b->descs[q].k;
             o = mdrq_search_stats{};
+            o.bytes_loaded = dev[4 * q + 3] + pass_bytes[q];
             if (path == MDRQ_PATH_ROWWISE) {
                 o.objects_compared = s->n;
                 o.early_breaks = dev[4 * q + (mode == MDRQ_MODE_BLOCKED ? 1 : 0)];
@@ -1047,6 +1101,58 @@ int mdrq_result_device(mdrq_store* s, uint64_t* d_ids, uint64_t* d_offsets, uint
         if (d_ids) *d_ids = reinterpret_cast<uint64_t>(s->ids.p);
         if (d_offsets) *d_offsets = reinterpret_cast<uint64_t>(b->d_offsets.p);
         if (total) *total = s->last_total;
+    });
+}
+
+int mdrq_batch_info(mdrq_batch* b, uint32_t* info) {
+    return guard([&] {
+        if (!b || !info) raise(MDRQ_EINVAL, "null argument");
+        info[0] = b->path;
+        info[1] = b->nq;
+        uint32_t passes = 0, kb = 0;
+        if (b->path == MDRQ_PATH_VAFILE_BATCH)
+            for (const VbPass& p : b->vb_passes) {
+                ++passes;
+                kb = std::max(kb, p.kb);
+            }
+        else if (b->path == MDRQ_PATH_COLUMNAR_BATCH)
+            for (const Pass& p : b->passes) {
+                ++passes;
+                kb = std::max(kb, p.kb);
+            }
+        info[2] = passes;
+        info[3] = kb;
+    });
+}
+
+int mdrq_batch_profile(mdrq_store* s, mdrq_batch* b, int ids_mode, void* stream, double* class_ms,
+                       uint32_t* class_launches) {
+    return guard([&] {
+        check_store(s);
+        if (!b || b->owner != s) raise(MDRQ_EINVAL, "batch does not belong to store");
+        if (!class_ms || !class_launches) raise(MDRQ_EINVAL, "null output");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+        Profiler prof;
+        prof.st = st;
+        enqueue(s, b, ids_mode != 0, st, &prof);
+        prof.mark(-1, 0);
+        CK(cudaStreamSynchronize(st));
+        for (int c = 0; c < 4; ++c) {
+            class_ms[c] = 0.0;
+            class_launches[c] = prof.launches[c];
+        }
+        for (size_t i = 0; i + 1 < prof.ev.size(); ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, prof.ev[i], prof.ev[i + 1]));
+            if (prof.cls[i] >= 0) class_ms[prof.cls[i]] += ms;
+        }
+        if (ids_mode) {
+            s->last_batch = b;
+            s->last_nq = b->nq;
+            s->last_path = b->path;
+        }
     });
 }
 

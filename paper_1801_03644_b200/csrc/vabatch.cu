@@ -34,17 +34,19 @@ namespace mdrq {
 
 namespace {
 
-constexpr int VB_THREADS = 256;
+constexpr int VB_THREADS = 512;
 constexpr int VB_WARPS = VB_THREADS / 32;
 
 template <int MODE, int KB>
-__global__ void __launch_bounds__(VB_THREADS) va_batch_kernel(const VaBatchArgs a) {
+__global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_ov = sm;                           // [KB][K][32]
     uint32_t* s_su = sm + KB * K * 32;             // [KB][K][32]
-    uint32_t* s_cnt = s_su + KB * K * 32;          // MODE 0: [1024] ; MODE 1/2: [warps][1024]
+    // MODE 0: u32 [1024] shared by the CTA ; MODE 1/2: u16 [warps][1024]
+    uint32_t* s_cnt32 = s_su + KB * K * 32;
+    uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_su + KB * K * 32);
 
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     {
@@ -52,92 +54,101 @@ __global__ void __launch_bounds__(VB_THREADS) va_batch_kernel(const VaBatchArgs 
         uint4* dst = reinterpret_cast<uint4*>(sm);
         const uint32_t n4 = 2 * KB * K * 32 / 4;
         for (uint32_t i = threadIdx.x; i < n4; i += VB_THREADS) dst[i] = src[i];
-        const uint32_t ncnt = MODE == 0 ? 1024u : 1024u * VB_WARPS;
-        for (uint32_t i = threadIdx.x; i < ncnt; i += VB_THREADS) s_cnt[i] = 0;
+        if (MODE == 0)
+            for (uint32_t i = threadIdx.x; i < 1024; i += VB_THREADS) s_cnt32[i] = 0;
         if (threadIdx.x < KB) s_dim[threadIdx.x] = a.udims[threadIdx.x];
     }
     __syncthreads();
 
-    const uint32_t chunk = blockIdx.x * VB_WARPS + warp;
-    const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
-    uint64_t end = start + a.chunk_tuples;
-    if (end > a.n) end = a.n;
-    uint32_t* wcnt = MODE == 0 ? s_cnt : s_cnt + warp * 1024;
-
     const uint32_t shift = a.shift;
     const float2* __restrict__ qb = a.qbounds;     // [1024][KB]
-    const unsigned long long* __restrict__ base = MODE == 2 ? a.base + uint64_t(chunk) * 1024 : nullptr;
     const uint32_t* s_ovl = s_ov + lane;           // lane's word of every row
     const uint32_t* s_sul = s_su + lane;
+    uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 1/2: this warp's chunk counters
 
-    for (uint64_t t0 = start; t0 < end; t0 += 128) {
-        uint32_t cw[KB];
+    for (uint32_t chunk = blockIdx.x * VB_WARPS + warp; chunk < a.nchunks; chunk += gridDim.x * VB_WARPS) {
+        const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
+        uint64_t end = start + a.chunk_tuples;
+        if (end > a.n) end = a.n;
+        if (MODE != 0) {
 #pragma unroll
-        for (int u = 0; u < KB; ++u)
-            cw[u] = __ldcs(reinterpret_cast<const unsigned int*>(a.codes + uint64_t(s_dim[u]) * a.stride + t0) +
-                           lane);
-        const uint32_t jmax = uint32_t(end - t0 < 128 ? end - t0 : 128);
-        for (uint32_t j4 = 0; j4 < jmax; j4 += 4) {
-            uint32_t x[KB];
+            for (int i = 0; i < 32; ++i) wcnt[lane * 32 + i] = 0;
+        }
+        const unsigned long long* __restrict__ base = MODE == 2 ? a.base + uint64_t(chunk) * 1024 : nullptr;
+
+        for (uint64_t t0 = start; t0 < end; t0 += 128) {
+            uint32_t cw[KB];
 #pragma unroll
-            for (int u = 0; u < KB; ++u) x[u] = __shfl_sync(0xFFFFFFFFu, cw[u], j4 >> 2);
+            for (int u = 0; u < KB; ++u)
+                cw[u] = __ldcs(reinterpret_cast<const unsigned int*>(a.codes + uint64_t(s_dim[u]) * a.stride + t0) +
+                               lane);
+            // table cells of the 4 tuples of every word: (code >> shift) per byte
 #pragma unroll
-            for (uint32_t jj = 0; jj < 4; ++jj) {
-                if (j4 + jj >= jmax) break;
-                uint32_t ov = 0xFFFFFFFFu, su = 0xFFFFFFFFu;
+            for (int u = 0; u < KB; ++u) cw[u] = (cw[u] >> shift) & (0x01010101u * (K - 1));
+            const uint32_t jmax = uint32_t(end - t0 < 128 ? end - t0 : 128);
+            for (uint32_t j4 = 0; j4 < jmax; j4 += 4) {
+                uint32_t x[KB];
 #pragma unroll
-                for (int u = 0; u < KB; ++u) {
-                    const uint32_t c = (x[u] >> (8 * jj + shift)) & (K - 1);
-                    const uint32_t idx = u * K * 32 + c * 32;   // u*K*32 folds into the LDS offset
-                    ov &= s_ovl[idx];
-                    su &= s_sul[idx];
-                }
-                const uint64_t t = t0 + j4 + jj;
-                uint32_t hits = su;
-                uint32_t r = ov & ~su;
-                if (__any_sync(0xFFFFFFFFu, r)) {
-                    float v[KB];
+                for (int u = 0; u < KB; ++u) x[u] = __shfl_sync(0xFFFFFFFFu, cw[u], j4 >> 2);
 #pragma unroll
-                    for (int u = 0; u < KB; ++u) v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
-                    while (r) {
-                        const int b = __ffs(r) - 1;
-                        r &= r - 1;
-                        const float2* qq = qb + (lane * 32 + b) * KB;
-                        bool ok = true;
+                for (uint32_t jj = 0; jj < 4; ++jj) {
+                    if (j4 + jj >= jmax) break;
+                    uint32_t ov = 0xFFFFFFFFu, su = 0xFFFFFFFFu;
 #pragma unroll
-                        for (int u = 0; u < KB; ++u) {
-                            const float2 bb = qq[u];
-                            ok = ok && (bb.x <= v[u]) && (v[u] <= bb.y);
-                        }
-                        if (ok) hits |= 1u << b;
+                    for (int u = 0; u < KB; ++u) {
+                        const uint32_t idx = u * K * 32 + ((x[u] >> (8 * jj)) & 0xFFu) * 32;
+                        ov &= s_ovl[idx];
+                        su &= s_sul[idx];
                     }
-                }
-                while (hits) {
-                    const int b = __ffs(hits) - 1;
-                    hits &= hits - 1;
-                    const uint32_t q = lane * 32 + b;
-                    if (MODE == 0) {
-                        atomicAdd(&wcnt[q], 1u);
-                    } else if (MODE == 1) {
-                        wcnt[q] += 1;
-                    } else {
-                        const unsigned long long pos = a.qoff[q] + base[q] + wcnt[q];
-                        wcnt[q] += 1;
-                        if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(t);
+                    const uint64_t t = t0 + j4 + jj;
+                    uint32_t hits = su;
+                    uint32_t r = ov & ~su;
+                    if (__any_sync(0xFFFFFFFFu, r)) {
+                        float v[KB];
+#pragma unroll
+                        for (int u = 0; u < KB; ++u) v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
+                        while (r) {
+                            const int b = __ffs(r) - 1;
+                            r &= r - 1;
+                            const float2* qq = qb + (lane * 32 + b) * KB;
+                            bool ok = true;
+#pragma unroll
+                            for (int u = 0; u < KB; ++u) {
+                                const float2 bb = qq[u];
+                                ok = ok && (bb.x <= v[u]) && (v[u] <= bb.y);
+                            }
+                            if (ok) hits |= 1u << b;
+                        }
+                    }
+                    while (hits) {
+                        const int b = __ffs(hits) - 1;
+                        hits &= hits - 1;
+                        const uint32_t q = lane * 32 + b;
+                        if (MODE == 0) {
+                            atomicAdd(&s_cnt32[q], 1u);
+                        } else if (MODE == 1) {
+                            wcnt[q] += 1;
+                        } else {
+                            const unsigned long long pos = a.qoff[q] + base[q] + wcnt[q];
+                            wcnt[q] += 1;
+                            if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(t);
+                        }
                     }
                 }
             }
+        }
+        if (MODE == 1) {
+            __syncwarp();
+            uint32_t* out = a.chunk_counts + uint64_t(chunk) * 1024;
+            for (uint32_t q = lane; q < 1024; q += 32) out[q] = wcnt[q];
+            __syncwarp();
         }
     }
 
     if (MODE == 0) {
         __syncthreads();
         for (uint32_t q = threadIdx.x; q < a.nqp; q += VB_THREADS)
-            if (s_cnt[q]) atomicAdd(a.counts + q, (unsigned long long)s_cnt[q]);
-    } else if (MODE == 1) {
-        __syncwarp();
-        uint32_t* out = a.chunk_counts + uint64_t(chunk) * 1024;
-        for (uint32_t q = lane; q < 1024; q += 32) out[q] = wcnt[q];
+            if (s_cnt32[q]) atomicAdd(a.counts + q, (unsigned long long)s_cnt32[q]);
     }
 }
 
@@ -193,10 +204,10 @@ __global__ void __launch_bounds__(1024) vb_query_scan_kernel(const unsigned long
 template <int MODE, int KB>
 void run_kb(const VaBatchArgs& a, cudaStream_t st) {
     const size_t smem = va_batch_smem(KB, va_batch_cells(KB), MODE);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(va_batch_kernel<MODE, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
+    static size_t configured = 0;   // dynamic smem limit set so far (static smem comes on top)
+    if (smem > configured) {
+        cudaFuncSetAttribute(va_batch_kernel<MODE, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        configured = smem;
     }
     va_batch_kernel<MODE, KB><<<a.grid, VB_THREADS, smem, st>>>(a);
 }
@@ -209,7 +220,7 @@ void dispatch(const VaBatchArgs& a, cudaStream_t st, std::integer_sequence<int, 
 }  // namespace
 
 size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
-    return size_t(2) * kb * cells * 32 * 4 + (mode == 0 ? 1024 * 4 : 1024 * 4 * VB_WARPS);
+    return size_t(2) * kb * cells * 32 * 4 + (mode == 0 ? 1024 * 4 : 1024 * 2 * VB_WARPS);
 }
 
 int va_batch_max_dims() { return kVaBatchMaxDims; }

@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
             }
     }
 
+    uint32_t nload = 0;  // 16-byte code loads issued
     for (uint32_t i = 0; i < k; ++i) {
         uint32_t any = 0;
 #pragma unroll
@@ -172,7 +173,10 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
 #pragma unroll
         for (int g = 0; g < VA_G; ++g) {
             const uint32_t ga = al[g][0] | al[g][1] | al[g][2] | al[g][3];
-            if (ga) x[g] = ld_stream_u4(c + g * 32);
+            if (ga) {
+                x[g] = ld_stream_u4(c + g * 32);
+                ++nload;
+            }
         }
 #pragma unroll
         for (int g = 0; g < VA_G; ++g) {
@@ -216,6 +220,9 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
         hit[g] = h;
     }
     if (a.stats) {
+        // code bytes + exact refine reads (one 4-byte column value per dim)
+        nload = __reduce_add_sync(0xFFFFFFFFu, nload);
+        if (lane == 0 && nload) atomicAdd(a.stats + 4 * a.q + 3, 16ull * nload);
         refined = __reduce_add_sync(0xFFFFFFFFu, refined);
         __syncthreads();
         if (lane == 0 && refined) atomicAdd(&s_refined, refined);

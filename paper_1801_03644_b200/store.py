@@ -211,6 +211,24 @@ class PreparedBatch:
                                              ctypes.byref(t)))
         return int(a.value), int(b.value), int(t.value)
 
+    CLASSES = ("scan", "compaction", "id_write", "setup")
+    PATH_NAMES = {v: k for k, v in _lib.PATHS.items()}
+
+    def info(self) -> dict:
+        arr = (ctypes.c_uint32 * 4)()
+        check(_lib.load().mdrq_batch_info(self._h, arr))
+        return {"path": self.PATH_NAMES.get(int(arr[0]), str(arr[0])), "nq": int(arr[1]),
+                "passes": int(arr[2]), "max_union_dims": int(arr[3])}
+
+    def profile(self, ids: bool, stream: int = 0) -> dict:
+        """One synchronising pass with CUDA events between launch groups:
+        {class: (device ms, kernel launches)}."""
+        ms = (ctypes.c_double * 4)()
+        nl = (ctypes.c_uint32 * 4)()
+        check(_lib.load().mdrq_batch_profile(self.store.handle, self._h, int(bool(ids)),
+                                             ctypes.c_void_p(stream or None), ms, nl))
+        return {c: (float(ms[i]), int(nl[i])) for i, c in enumerate(self.CLASSES)}
+
     def launches(self, ids: bool) -> int:
         c = ctypes.c_uint32(0)
         check(_lib.load().mdrq_batch_launches(self._h, int(bool(ids)), ctypes.byref(c)))
