@@ -3,11 +3,11 @@
 // The scan kernels of ids mode write the verdicts of a query as a packed
 // bitmask over the store's tuples (bit i of 32-bit word w = tuple 32w+i, the
 // reference's little-endian mask layout, scan.py:85-88) plus one count per
-// 8192-tuple chunk.  Two light kernels then turn the mask into ascending ids:
+// 65536-tuple chunk.  Two light kernels then turn the mask into ascending ids:
 //
 //   chunk_scan_kernel  exclusive prefix of the chunk counts (one CTA), chains
 //                      the query's output base: offsets[q+1] = offsets[q] + total
-//   expand_kernel      one CTA per chunk, one mask word per thread: block scan
+//   expand_kernel      one CTA per chunk, 8 mask words per thread: block scan
 //                      of popcounts, then every set bit is written as
 //                      id_base + tuple at offsets[q] + chunk_offset + rank
 //
@@ -66,17 +66,34 @@ __global__ void __launch_bounds__(SCAN_THREADS) chunk_scan_kernel(const uint32_t
     }
 }
 
+// one CTA per 65536-tuple chunk: 256 threads x 8 consecutive mask words
 __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict__ mask, uint64_t n,
                                                      const uint32_t* __restrict__ chunk_offs,
                                                      const unsigned long long* __restrict__ offsets, uint32_t q,
                                                      uint32_t* __restrict__ ids, uint64_t cap, uint32_t id_base) {
+    constexpr int WPT = kChunkTuples / 32 / 256;   // words per thread
     __shared__ uint32_t s_warp[8];
     const uint32_t chunk = blockIdx.x;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint64_t w = uint64_t(chunk) * 256 + threadIdx.x;
-    uint32_t bits = (w * 32 < n) ? mask[w] : 0u;
-    if ((w + 1) * 32 > n && w * 32 < n) bits &= (n % 32) ? ((1u << (n % 32)) - 1u) : 0xFFFFFFFFu;
-    const uint32_t c = __popc(bits);
+    const uint64_t w0 = uint64_t(chunk) * (kChunkTuples / 32) + uint64_t(threadIdx.x) * WPT;
+    const uint64_t nwords = (n + 31) / 32;
+    uint32_t bits[WPT];
+    if (w0 + WPT <= nwords) {
+        const uint4* p = reinterpret_cast<const uint4*>(mask + w0);
+#pragma unroll
+        for (int i = 0; i < WPT / 4; ++i) {
+            const uint4 v = p[i];
+            bits[4 * i] = v.x; bits[4 * i + 1] = v.y; bits[4 * i + 2] = v.z; bits[4 * i + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < WPT; ++i) bits[i] = w0 + i < nwords ? mask[w0 + i] : 0u;
+    }
+    if ((n % 32) && w0 <= nwords - 1 && nwords - 1 < w0 + WPT)
+        bits[nwords - 1 - w0] &= (1u << (n % 32)) - 1u;
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < WPT; ++i) c += __popc(bits[i]);
     uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -96,18 +113,44 @@ __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict_
         if (lane < 8) s_warp[lane] = wi - v;
     }
     __syncthreads();
-    if (!bits) return;
+    if (!c) return;
     unsigned long long pos = offsets[q] + chunk_offs[chunk] + s_warp[warp] + (incl - c);
-    const uint32_t t0 = id_base + uint32_t(w * 32);
-    while (bits) {
-        const int j = __ffs(bits) - 1;
-        bits &= bits - 1;
-        if (pos < cap) ids[pos] = t0 + uint32_t(j);
-        ++pos;
+#pragma unroll
+    for (int i = 0; i < WPT; ++i) {
+        uint32_t b = bits[i];
+        const uint32_t t0 = id_base + uint32_t((w0 + i) * 32);
+        while (b) {
+            const int j = __ffs(b) - 1;
+            b &= b - 1;
+            if (pos < cap) ids[pos] = t0 + uint32_t(j);
+            ++pos;
+        }
     }
 }
 
+__global__ void reduce_partials_kernel(const unsigned long long* __restrict__ partials, uint32_t nq, bool add_counts,
+                                       unsigned long long* counts, unsigned long long* stats) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    unsigned long long c = 0, bytes = 0, refined = 0;
+    const unsigned long long* p = partials + uint64_t(q) * kPartialSlots * 4;
+    for (int s = 0; s < kPartialSlots; ++s) {
+        c += p[4 * s + 0];
+        bytes += p[4 * s + 1];
+        refined += p[4 * s + 2];
+    }
+    if (add_counts) counts[q] += c;
+    stats[4 * q + 2] += refined;
+    stats[4 * q + 3] += bytes;
+}
+
 }  // namespace
+
+void launch_reduce_partials(const unsigned long long* partials, uint32_t nq, bool add_counts,
+                            unsigned long long* counts, unsigned long long* stats, cudaStream_t st) {
+    if (!nq) return;
+    reduce_partials_kernel<<<(nq + 255) / 256, 256, 0, st>>>(partials, nq, add_counts, counts, stats);
+}
 
 void launch_expand(const ScanArgs& a, cudaStream_t st) {
     const uint32_t nchunks = uint32_t((a.n + kChunkTuples - 1) / kChunkTuples);

@@ -14,7 +14,7 @@ namespace mdrq {
 // rows) so they never satisfy lo <= v <= hi, codes are 0 (they are also
 // masked by n).
 constexpr uint64_t kPadTuples = 8192;
-constexpr uint64_t kChunkTuples = 8192;   // compaction chunk (256 mask words)
+constexpr uint64_t kChunkTuples = 65536;  // compaction chunk (2048 mask words)
 
 struct ScanArgs {
     const float* cols;       // columnar store [m][stride]
@@ -42,7 +42,22 @@ struct ScanArgs {
     uint32_t* mask;               // [n_pad / 32] words
     uint32_t* chunk_counts;       // [n_pad / kChunkTuples], zeroed per query
     uint32_t* chunk_offs;         // [n_pad / kChunkTuples]
+    // per-query accumulators spread over 32 slots (one CTA per tile would
+    // otherwise serialise thousands of atomics on one address):
+    // [nq][32][4] = count, bytes loaded, tuples refined, spare
+    unsigned long long* partials;
 };
+
+constexpr int kPartialSlots = 32;
+
+// add v to accumulator `field` of the launch's query (slot by CTA index)
+__device__ __forceinline__ void partial_add(const ScanArgs& a, int field, unsigned long long v) {
+    atomicAdd(a.partials + (uint64_t(a.q) * kPartialSlots + (blockIdx.x & (kPartialSlots - 1))) * 4 + field, v);
+}
+
+// fold the partial slots into counts (count mode) and stats[q][2..3]
+void launch_reduce_partials(const unsigned long long* partials, uint32_t nq, bool add_counts,
+                            unsigned long long* counts, unsigned long long* stats, cudaStream_t st);
 
 // multi-query pass over the columnar store (union dims, <= 32 queries)
 struct BatchArgs {

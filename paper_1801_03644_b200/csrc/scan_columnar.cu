@@ -6,8 +6,8 @@
 // unpacks the ids (scan.py:85-88).  Here the three steps are fused into one
 // pass: the candidate mask of a tile lives in registers across dimensions,
 // a lane skips its 128-bit load of the next column once its four tuples are
-// all rejected, and surviving tuples are compacted into ascending ids with a
-// warp ballot + block scan + decoupled look-back (single pass, ordered).
+// all rejected, and in ids mode the verdicts leave as a bitmask + per-chunk
+// counts that expand.cu turns into ascending ids.
 //
 // col_scan_kernel        one query per launch, dimension-at-a-time (HBM bound)
 // col_batch_count_kernel up to 32 queries per pass over the union of their
@@ -28,6 +28,7 @@ static_assert(CS_THREADS / 32 * CS_WARP_TUPLES == kColTile, "tile size");
 template <bool IDS>
 __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) {
     __shared__ uint32_t s_cnt[CS_THREADS / 32];
+    __shared__ uint32_t s_ld[CS_THREADS / 32];
 
     const QueryDesc qd = a.descs[a.q];
     const DimPred* __restrict__ P = a.preds + qd.off;
@@ -56,11 +57,10 @@ __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) 
         const float4* c = reinterpret_cast<const float4*>(a.cols + uint64_t(d) * a.stride + base);
         float4 v[CS_G];
 #pragma unroll
+        for (int g = 0; g < CS_G; ++g) nload += ((alive >> (4 * g)) & 0xFu) ? 1u : 0u;
+#pragma unroll
         for (int g = 0; g < CS_G; ++g)
-            if ((alive >> (4 * g)) & 0xFu) {
-                v[g] = ld_stream_f4(c + g * 32);
-                ++nload;
-            }
+            if ((alive >> (4 * g)) & 0xFu) v[g] = ld_stream_f4(c + g * 32);
 #pragma unroll
         for (int g = 0; g < CS_G; ++g)
             if ((alive >> (4 * g)) & 0xFu)
@@ -68,21 +68,23 @@ __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) 
     }
 
     const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, __popc(alive));
-    if (a.stats) {
-        nload = __reduce_add_sync(0xFFFFFFFFu, nload);
-        if (lane == 0 && nload) atomicAdd(a.stats + 4 * a.q + 3, 16ull * nload);
+    nload = __reduce_add_sync(0xFFFFFFFFu, nload);
+    if (lane == 0) {
+        s_cnt[warp] = wc;
+        s_ld[warp] = nload;
     }
-    if (!IDS) {
-        if (lane == 0) s_cnt[warp] = wc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t t = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0, ld = 0;
 #pragma unroll
-            for (int w = 0; w < CS_THREADS / 32; ++w) t += s_cnt[w];
-            if (t) atomicAdd(a.counts + a.q, (unsigned long long)t);
+        for (int w = 0; w < CS_THREADS / 32; ++w) {
+            t += s_cnt[w];
+            ld += s_ld[w];
         }
-        return;
+        if (!IDS && t) partial_add(a, 0, t);
+        if (ld) partial_add(a, 1, 16ull * ld);
     }
+    if (!IDS) return;
     // ids mode: verdict bitmask (bit i of word w = tuple 32w+i) + chunk count;
     // lanes 8s..8s+7 of group g own the 32 tuples of one mask word
 #pragma unroll

@@ -183,6 +183,7 @@ struct mdrq_batch {
     DBuf<unsigned long long> d_counts;
     DBuf<unsigned long long> d_offsets;
     DBuf<unsigned long long> d_stats;
+    DBuf<unsigned long long> d_partials;   // [nq][kPartialSlots][4]
 };
 
 struct mdrq_store {
@@ -477,6 +478,7 @@ void upload_batch(mdrq_store* s, mdrq_batch* b) {
     b->d_counts.reserve(b->nq);
     b->d_offsets.reserve(size_t(b->nq) + 1);
     b->d_stats.reserve(size_t(b->nq) * 4);
+    b->d_partials.reserve(size_t(b->nq) * kPartialSlots * 4);
     // H2D copies above may read pageable host vectors that a later rebuild
     // mutates: make them complete before returning.
     CK(cudaStreamSynchronize(s->stream));
@@ -534,6 +536,7 @@ ScanArgs base_args(mdrq_store* s, mdrq_batch* b, uint32_t path) {
     a.mask = s->mask.p;
     a.chunk_counts = s->chunk_counts.p;
     a.chunk_offs = s->chunk_offs.p;
+    a.partials = b->d_partials.p;
     return a;
 }
 
@@ -580,19 +583,31 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
 // to the group's class (0 scan / filter, 1 compaction, 2 id write, 3 setup).
 struct Profiler {
     cudaStream_t st = nullptr;
-    std::vector<cudaEvent_t> ev;
+    bool counting = true;            // first run only counts the marks
+    size_t used = 0;
+    std::vector<cudaEvent_t> ev;     // created up front: no API cost between launches
     std::vector<int> cls;
     uint32_t launches[4] = {0, 0, 0, 0};
     void mark(int c, uint32_t nlaunch) {
-        cudaEvent_t e;
-        CK(cudaEventCreate(&e));
-        CK(cudaEventRecord(e, st));
-        ev.push_back(e);
+        if (counting) {
+            ++used;
+            return;
+        }
+        if (used >= ev.size()) raise(MDRQ_ECUDA, "profiler event pool exhausted");
+        CK(cudaEventRecord(ev[used], st));
         cls.push_back(c);
+        ++used;
         if (c >= 0 && c < 4) launches[c] += nlaunch;
     }
+    void arm() {
+        ev.resize(used + 1);
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        counting = false;
+        used = 0;
+    }
     ~Profiler() {
-        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
     }
 };
 
@@ -606,9 +621,11 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profil
     CK(cudaMemsetAsync(b->d_tile_counters.p, 0, sizeof(uint32_t) * nq, st));
     CK(cudaMemsetAsync(b->d_counts.p, 0, sizeof(unsigned long long) * nq, st));
     CK(cudaMemsetAsync(b->d_stats.p, 0, sizeof(unsigned long long) * nq * 4, st));
+    CK(cudaMemsetAsync(b->d_partials.p, 0, sizeof(unsigned long long) * nq * kPartialSlots * 4, st));
     if (ids) CK(cudaMemsetAsync(b->d_offsets.p, 0, sizeof(unsigned long long) * (nq + 1), st));
     if (s->n == 0) return 0;
     uint32_t launches = 0;
+    bool used_partials = false;   // single-query column / VA kernels accumulate into partials
     const uint32_t path = b->path;
     auto single = [&](uint32_t sp, uint32_t q) {
         ScanArgs a = base_args(s, b, sp);
@@ -619,12 +636,15 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profil
             CK(cudaMemsetAsync(s->chunk_counts.p, 0, sizeof(uint32_t) * s->nchunks, st));
         }
         mark(0, 1);
-        if (sp == MDRQ_PATH_ROWWISE)
+        if (sp == MDRQ_PATH_ROWWISE) {
             launch_row_scan(a, ids, st);
-        else if (sp == MDRQ_PATH_VAFILE)
+        } else if (sp == MDRQ_PATH_VAFILE) {
             launch_va_scan(a, ids, st);
-        else
+            used_partials = true;
+        } else {
             launch_col_scan(a, ids, st);
+            used_partials = true;
+        }
         ++launches;
         if (ids) {
             mark(1, 2);
@@ -677,23 +697,39 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profil
         const uint32_t sp = path == MDRQ_PATH_COLUMNAR_BATCH ? MDRQ_PATH_COLUMNAR : path;
         for (uint32_t q = 0; q < nq; ++q) single(sp, q);
     }
+    if (used_partials) {
+        mark(3, 1);
+        launch_reduce_partials(b->d_partials.p, nq, !ids, b->d_counts.p, b->d_stats.p, st);
+        ++launches;
+    }
     CK(cudaGetLastError());
     return launches;
 }
 
 uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
     if (!b->nq || s->n == 0) return 0;
+    // mirrors enqueue(): + 1 partial-reduction launch whenever a single-query
+    // column / VA scan ran (it is not launched for row-wise scans)
     if (b->path == MDRQ_PATH_VAFILE_BATCH) {
         uint32_t l = 0;
-        for (const VbPass& ps : b->vb_passes) l += ps.fallback ? ps.nqp * (ids ? 3 : 1) : (ids ? 4 : 1);
-        return l;
+        bool single = false;
+        for (const VbPass& ps : b->vb_passes) {
+            l += ps.fallback ? ps.nqp * (ids ? 3 : 1) : (ids ? 4 : 1);
+            single |= ps.fallback;
+        }
+        return l + (single ? 1 : 0);
     }
     if (b->path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
         uint32_t l = 0;
-        for (const Pass& ps : b->passes) l += ps.fallback ? ps.nqp : 1;
-        return l;
+        bool single = false;
+        for (const Pass& ps : b->passes) {
+            l += ps.fallback ? ps.nqp : 1;
+            single |= ps.fallback;
+        }
+        return l + (single ? 1 : 0);
     }
-    return ids ? 3 * b->nq : b->nq;   // ids: scan + chunk scan + expand
+    const uint32_t per_query = ids ? 3 : 1;   // ids: scan + chunk scan + expand
+    return per_query * b->nq + (b->path == MDRQ_PATH_ROWWISE ? 0 : 1);
 }
 
 // Run an ids pass synchronously, growing the result pool until it fits.
@@ -1136,6 +1172,9 @@ int mdrq_batch_profile(mdrq_store* s, mdrq_batch* b, int ids_mode, void* stream,
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
         Profiler prof;
         prof.st = st;
+        enqueue(s, b, ids_mode != 0, st, &prof);   // counting run (also a warm-up pass)
+        CK(cudaStreamSynchronize(st));
+        prof.arm();
         enqueue(s, b, ids_mode != 0, st, &prof);
         prof.mark(-1, 0);
         CK(cudaStreamSynchronize(st));

@@ -41,6 +41,7 @@ template <int MODE, int KB>
 __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
+    constexpr bool PV = KB <= 8;                   // exact values prefetched into registers
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_ov = sm;                           // [KB][K][32]
     uint32_t* s_su = sm + KB * K * 32;             // [KB][K][32]
@@ -76,15 +77,30 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
         }
         const unsigned long long* __restrict__ base = MODE == 2 ? a.base + uint64_t(chunk) * 1024 : nullptr;
 
+        // software pipeline: the codes (and, for narrow unions, the exact
+        // values) of the next 128-tuple block are loaded while this block is
+        // evaluated; lane l holds tuples t0+4l .. t0+4l+3 of every union dim
+        uint32_t cw_n[KB];
+        float4 vv_n[PV ? KB : 1];
+        auto load_block = [&](uint64_t tb) {
+#pragma unroll
+            for (int u = 0; u < KB; ++u) {
+                const uint64_t off = uint64_t(s_dim[u]) * a.stride + tb;
+                cw_n[u] = __ldcs(reinterpret_cast<const unsigned int*>(a.codes + off) + lane);
+                if constexpr (PV) vv_n[u] = __ldcs(reinterpret_cast<const float4*>(a.cols + off) + lane);
+            }
+        };
+        if (start < end) load_block(start);
         for (uint64_t t0 = start; t0 < end; t0 += 128) {
             uint32_t cw[KB];
+            float4 vv[PV ? KB : 1];
 #pragma unroll
-            for (int u = 0; u < KB; ++u)
-                cw[u] = __ldcs(reinterpret_cast<const unsigned int*>(a.codes + uint64_t(s_dim[u]) * a.stride + t0) +
-                               lane);
-            // table cells of the 4 tuples of every word: (code >> shift) per byte
-#pragma unroll
-            for (int u = 0; u < KB; ++u) cw[u] = (cw[u] >> shift) & (0x01010101u * (K - 1));
+            for (int u = 0; u < KB; ++u) {
+                // table cells of the 4 tuples of every word: (code >> shift) per byte
+                cw[u] = (cw_n[u] >> shift) & (0x01010101u * (K - 1));
+                if constexpr (PV) vv[u] = vv_n[u];
+            }
+            if (t0 + 128 < end) load_block(t0 + 128);
             const uint32_t jmax = uint32_t(end - t0 < 128 ? end - t0 : 128);
             for (uint32_t j4 = 0; j4 < jmax; j4 += 4) {
                 uint32_t x[KB];
@@ -104,9 +120,18 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     uint32_t hits = su;
                     uint32_t r = ov & ~su;
                     if (__any_sync(0xFFFFFFFFu, r)) {
+                        // exact refinement of (tuple, query) pairs in an edge cell
                         float v[KB];
 #pragma unroll
-                        for (int u = 0; u < KB; ++u) v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
+                        for (int u = 0; u < KB; ++u) {
+                            if constexpr (PV) {
+                                const float4 w = vv[u];
+                                const float c = jj == 0 ? w.x : jj == 1 ? w.y : jj == 2 ? w.z : w.w;
+                                v[u] = __shfl_sync(0xFFFFFFFFu, c, j4 >> 2);
+                            } else {
+                                v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
+                            }
+                        }
                         while (r) {
                             const int b = __ffs(r) - 1;
                             r &= r - 1;

@@ -122,12 +122,12 @@ __device__ __forceinline__ uint32_t flags_to_nib(uint32_t f) {
 template <bool IDS>
 __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
     __shared__ uint32_t s_cnt[VA_THREADS / 32];
-    __shared__ uint32_t s_refined;
+    __shared__ uint32_t s_ld[VA_THREADS / 32];
+    __shared__ uint32_t s_rf[VA_THREADS / 32];
 
     const QueryDesc qd = a.descs[a.q];
     const DimPred* __restrict__ P = a.preds + qd.off;
     const uint32_t k = qd.k;
-    if (threadIdx.x == 0) s_refined = 0;
     const uint32_t tile = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     // tuple of (group g, word w, byte b) = base + g*512 + w*4 + b
@@ -171,12 +171,11 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
         const uint4* c = reinterpret_cast<const uint4*>(a.codes + uint64_t(d) * a.stride + base);
         uint4 x[VA_G];
 #pragma unroll
+        for (int g = 0; g < VA_G; ++g) nload += (al[g][0] | al[g][1] | al[g][2] | al[g][3]) ? 1u : 0u;
+#pragma unroll
         for (int g = 0; g < VA_G; ++g) {
             const uint32_t ga = al[g][0] | al[g][1] | al[g][2] | al[g][3];
-            if (ga) {
-                x[g] = ld_stream_u4(c + g * 32);
-                ++nload;
-            }
+            if (ga) x[g] = ld_stream_u4(c + g * 32);
         }
 #pragma unroll
         for (int g = 0; g < VA_G; ++g) {
@@ -219,28 +218,30 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
         }
         hit[g] = h;
     }
-    if (a.stats) {
-        // code bytes + exact refine reads (one 4-byte column value per dim)
-        nload = __reduce_add_sync(0xFFFFFFFFu, nload);
-        if (lane == 0 && nload) atomicAdd(a.stats + 4 * a.q + 3, 16ull * nload);
-        refined = __reduce_add_sync(0xFFFFFFFFu, refined);
-        __syncthreads();
-        if (lane == 0 && refined) atomicAdd(&s_refined, refined);
-    }
-
     const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, __popc(hit[0]) + __popc(hit[1]));
-    if (!IDS) {
-        if (lane == 0) s_cnt[warp] = wc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int w = 0; w < VA_THREADS / 32; ++w) t += s_cnt[w];
-            if (t) atomicAdd(a.counts + a.q, (unsigned long long)t);
-            if (a.stats && s_refined) atomicAdd(a.stats + 4 * a.q + 2, (unsigned long long)s_refined);
-        }
-        return;
+    nload = __reduce_add_sync(0xFFFFFFFFu, nload);
+    refined = __reduce_add_sync(0xFFFFFFFFu, refined);
+    if (lane == 0) {
+        s_cnt[warp] = wc;
+        s_ld[warp] = nload;
+        s_rf[warp] = refined;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0, ld = 0, rf = 0;
+#pragma unroll
+        for (int w = 0; w < VA_THREADS / 32; ++w) {
+            t += s_cnt[w];
+            ld += s_ld[w];
+            rf += s_rf[w];
+        }
+        if (!IDS && t) partial_add(a, 0, t);
+        // code bytes + one 4-byte column value per queried dim per refined tuple
+        const unsigned long long bytes = 16ull * ld + 4ull * k * rf;
+        if (bytes) partial_add(a, 1, bytes);
+        if (rf) partial_add(a, 2, rf);
+    }
+    if (!IDS) return;
     // ids mode: two lanes share one mask word per group
 #pragma unroll
     for (int g = 0; g < VA_G; ++g) {
@@ -249,10 +250,6 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
         if ((lane & 1u) == 0) a.mask[(base + g * 512) / 32] = v;
     }
     if (lane == 0 && wc) atomicAdd(a.chunk_counts + wbase / kChunkTuples, wc);
-    if (a.stats) {
-        __syncthreads();
-        if (threadIdx.x == 0 && s_refined) atomicAdd(a.stats + 4 * a.q + 2, (unsigned long long)s_refined);
-    }
 }
 
 }  // namespace

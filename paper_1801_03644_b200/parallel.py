@@ -136,10 +136,17 @@ def combine_counts(local_counts, group=None):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    local_counts = local_counts.to(torch.int64).contiguous()
-    gathered = torch.empty((world,) + tuple(local_counts.shape), dtype=torch.int64, device=local_counts.device)
-    dist.all_gather_into_tensor(gathered, local_counts, group=group)
-    return gathered.sum(0)
+    local_counts = local_counts.to(torch.int64).contiguous().reshape(-1)
+    return _all_gather(local_counts, world, group).sum(0)
+
+
+def _all_gather(t, world: int, group):
+    """[numel] -> [world, numel] (flat output: works on NCCL and gloo)."""
+    import torch
+    import torch.distributed as dist
+    out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out.view(world, t.numel())
 
 
 def combine_ids(local_offsets, local_ids, group=None):
@@ -158,8 +165,7 @@ def combine_ids(local_offsets, local_ids, group=None):
     local_offsets = local_offsets.to(device=dev, dtype=torch.int64)
     counts = local_offsets[1:] - local_offsets[:-1]
     nq = counts.numel()
-    all_counts = torch.empty((world, nq), dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(all_counts, counts.contiguous(), group=group)
+    all_counts = _all_gather(counts.contiguous(), world, group)
     totals = all_counts.sum(1)                      # ids per rank
     per_query = all_counts.sum(0)                   # ids per query
     out_offsets = torch.zeros(nq + 1, dtype=torch.int64, device=dev)
@@ -172,8 +178,7 @@ def combine_ids(local_offsets, local_ids, group=None):
     nloc = local_ids.numel()
     if nloc:
         padded[:nloc] = local_ids
-    gathered = torch.empty((world, padded.numel()), dtype=ids_dtype, device=dev)
-    dist.all_gather_into_tensor(gathered, padded, group=group)
+    gathered = _all_gather(padded, world, group)
     total = int(out_offsets[-1].item())
     out = torch.empty(total, dtype=ids_dtype, device=dev)
     for r in range(world):

@@ -142,6 +142,191 @@ def c5_queries(count: int = C5["queries"]):
     return box_queries(np.random.default_rng(1), count, C5["m"], C5["selectivity"])
 
 
+C3 = dict(n=100_000_000, m=16, queries=2000, centres=20, sigma=0.03, zipf=1.1, sel=(1e-3, 5e-2))
+C4 = dict(n=10_000_000, m=19, queries=5000)
+CHUNK_ROWS = 1 << 20  # generation chunk of the clustered / mixed configs
+
+
+def _chunks(start: int, stop: int):
+    """(chunk index, row range within the chunk) covering rows [start, stop)."""
+    c = start // CHUNK_ROWS
+    while c * CHUNK_ROWS < stop:
+        a = max(start, c * CHUNK_ROWS) - c * CHUNK_ROWS
+        b = min(stop, (c + 1) * CHUNK_ROWS) - c * CHUNK_ROWS
+        yield c, a, b
+        c += 1
+
+
+def c3_model():
+    """Gaussian-mixture model of C3: 20 centres U[0,1)^16 (default_rng(3)),
+    Zipf(1.1) weights, per-dimension sigma 0.03."""
+    centres = np.random.default_rng(3).random((C3["centres"], C3["m"]))
+    w = 1.0 / np.arange(1, C3["centres"] + 1) ** C3["zipf"]
+    return centres, w / w.sum()
+
+
+def c3_chunk(c: int, rows: int | None = None) -> np.ndarray:
+    """Chunk c (CHUNK_ROWS rows) of C3: default_rng([3, c]) draws the cluster
+    of every row (choice) then the N(0, sigma) noise; values are clipped to
+    [0, nextafter(1, 0)] in float32."""
+    rows = CHUNK_ROWS if rows is None else rows
+    centres, p = c3_model()
+    rng = np.random.default_rng([3, c])
+    assign = rng.choice(C3["centres"], size=rows, p=p)
+    noise = rng.normal(0.0, C3["sigma"], (rows, C3["m"]))
+    v = (centres[assign] + noise).astype(np.float32)
+    np.clip(v, np.float32(0.0), np.nextafter(np.float32(1.0), np.float32(0.0)), out=v)
+    return v
+
+
+def _chunked(chunk_fn, m: int, start: int, stop: int, n: int, workers: int | None) -> np.ndarray:
+    """Rows [start, stop) of a chunk-generated table; chunks are independent
+    (seeded by their index), so they are generated in parallel worker
+    processes writing straight into shared memory."""
+    import os
+    out_shape = (stop - start, m)
+    jobs = list(_chunks(start, stop))
+    workers = workers or min(len(jobs), os.cpu_count() or 1)
+    if workers <= 1 or len(jobs) <= 1:
+        out = np.empty(out_shape, np.float32)
+        o = 0
+        for c, a, b in jobs:
+            out[o:o + b - a] = chunk_fn(c, min(CHUNK_ROWS, n - c * CHUNK_ROWS))[a:b]
+            o += b - a
+        return out
+    import multiprocessing as mp
+    from multiprocessing import shared_memory
+    shm = shared_memory.SharedMemory(create=True, size=max(1, out_shape[0] * m * 4))
+    try:
+        offs = []
+        o = 0
+        for c, a, b in jobs:
+            offs.append(o)
+            o += b - a
+        ctx = mp.get_context("fork")
+        with ctx.Pool(workers) as pool:
+            pool.starmap(_fill_chunk, [(chunk_fn, shm.name, out_shape, off, c, a, b, n, m)
+                                       for off, (c, a, b) in zip(offs, jobs)])
+        out = np.ndarray(out_shape, np.float32, buffer=shm.buf).copy()
+    finally:
+        shm.close()
+        shm.unlink()
+    return out
+
+
+def _fill_chunk(chunk_fn, name, shape, off, c, a, b, n, m):
+    from multiprocessing import shared_memory
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        dst = np.ndarray(shape, np.float32, buffer=shm.buf)
+        dst[off:off + b - a] = chunk_fn(c, min(CHUNK_ROWS, n - c * CHUNK_ROWS))[a:b]
+    finally:
+        shm.close()
+
+
+def c3_data(start: int = 0, stop: int | None = None, n: int = C3["n"], workers: int | None = None) -> np.ndarray:
+    stop = n if stop is None else stop
+    return _chunked(c3_chunk, C3["m"], start, stop, n, workers)
+
+
+def _tune_halfwidth(sample: np.ndarray, centre: np.ndarray, dims: np.ndarray, target: float) -> float:
+    """Bisection on the common half-width so the box around `centre` on
+    `dims` selects ~target of `sample` (mirrors the reference's
+    selectivity-bucket tuning, bench.py:215-252)."""
+    cols = sample[:, dims]
+    c = centre[dims]
+    lo_h, hi_h = 0.0, 1.0
+    for _ in range(22):
+        h = 0.5 * (lo_h + hi_h)
+        sel = np.count_nonzero((np.abs(cols - c) <= h).all(axis=1)) / sample.shape[0]
+        if sel < target:
+            lo_h = h
+        else:
+            hi_h = h
+    return hi_h
+
+
+def c3_queries(count: int = C3["queries"], sample_rows: int = 1 << 18):
+    """C3 partial-match queries: k ~ U{2..8} of the 16 dims, centred on a
+    random tuple of chunk 0, half-width tuned by bisection on a sample of
+    chunk 0 for a log-uniform target selectivity in [1e-3, 5e-2]."""
+    rng = np.random.default_rng(4)
+    chunk0 = c3_chunk(0)
+    sample = chunk0[:sample_rows]
+    m = C3["m"]
+    lo = np.full((count, m), -np.inf, np.float32)
+    hi = np.full((count, m), np.inf, np.float32)
+    a, b = np.log(C3["sel"][0]), np.log(C3["sel"][1])
+    for q in range(count):
+        k = int(rng.integers(2, 9))
+        dims = np.sort(rng.choice(m, size=k, replace=False))
+        centre = chunk0[int(rng.integers(0, CHUNK_ROWS))]
+        target = float(np.exp(rng.uniform(a, b)))
+        h = _tune_halfwidth(sample, centre, dims, target)
+        lo[q, dims] = (centre[dims] - h).astype(np.float32)
+        hi[q, dims] = (centre[dims] + h).astype(np.float32)
+    return lo, hi
+
+
+_C4_CARDS = (2, 3, 5, 10, 25, 50)
+_C4_NORMAL = ((45.0, 15.0), (70.0, 15.0), (120.0, 20.0), (25.0, 5.0), (60.0, 10.0))
+
+
+def _zipf_p(k: int, s: float) -> np.ndarray:
+    w = 1.0 / np.arange(1, k + 1) ** s
+    return w / w.sum()
+
+
+def c4_chunk(c: int, rows: int | None = None) -> np.ndarray:
+    """Chunk c of C4 (genomics-shaped, 19 float32 columns, default_rng([4, c])):
+    d0 chromosome 1..25 Zipf(1.0); d1 position U{0..2.5e8-1} (float32, exact
+    only to multiples of 16 above 2^24); d2-d7 categoricals of cardinality
+    2, 3, 5, 10, 25, 50 with Zipf(1.2) frequencies; d8-d12 normal values
+    rounded to integers and clipped to [0, 250]; d13-d18 U[0, 1)."""
+    rows = CHUNK_ROWS if rows is None else rows
+    rng = np.random.default_rng([4, c])
+    v = np.empty((rows, 19), np.float32)
+    v[:, 0] = rng.choice(np.arange(1, 26), size=rows, p=_zipf_p(25, 1.0))
+    v[:, 1] = rng.integers(0, 250_000_000, size=rows).astype(np.float32)
+    for j, card in enumerate(_C4_CARDS):
+        v[:, 2 + j] = rng.choice(card, size=rows, p=_zipf_p(card, 1.2))
+    for j, (mu, sd) in enumerate(_C4_NORMAL):
+        v[:, 8 + j] = np.clip(np.rint(rng.normal(mu, sd, rows)), 0, 250)
+    v[:, 13:] = rng.random((rows, 6), dtype=np.float32)
+    return v
+
+
+def c4_data(start: int = 0, stop: int | None = None, n: int = C4["n"], workers: int | None = None) -> np.ndarray:
+    stop = n if stop is None else stop
+    return _chunked(c4_chunk, 19, start, stop, n, workers)
+
+
+def c4_queries(count: int = C4["queries"]):
+    """C4 partial-match queries on 3-5 dims around a random tuple of chunk 0:
+    equality (lo == hi) on categorical / integer dims (d0, d2-d12), an
+    interval of log-uniform relative width on d1 and d13-d18 -- selectivities
+    spread over ~1e-7..1e-2 (exact values from the oracle)."""
+    rng = np.random.default_rng(5)
+    chunk0 = c4_chunk(0)
+    lo = np.full((count, 19), -np.inf, np.float32)
+    hi = np.full((count, 19), np.inf, np.float32)
+    for q in range(count):
+        k = int(rng.integers(3, 6))
+        dims = np.sort(rng.choice(19, size=k, replace=False))
+        row = chunk0[int(rng.integers(0, CHUNK_ROWS))]
+        for j in dims:
+            v = row[j]
+            if j == 1:
+                w = np.float32(2.5e8 * np.exp(rng.uniform(np.log(1e-4), np.log(0.3))))
+                lo[q, j], hi[q, j] = v - w / 2, v + w / 2
+            elif j >= 13:
+                w = np.float32(np.exp(rng.uniform(np.log(1e-3), np.log(0.5))))
+                lo[q, j], hi[q, j] = v - w / 2, v + w / 2
+            else:
+                lo[q, j] = hi[q, j] = v
+    return lo, hi
+
+
 def queries_from_arrays(lo: np.ndarray, hi: np.ndarray) -> list[RangeQuery]:
     return [RangeQuery(lo[i], hi[i]) for i in range(lo.shape[0])]
 

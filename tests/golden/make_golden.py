@@ -276,12 +276,51 @@ def make_c2(mdrq, per_level: int = 20):
     np.savez_compressed(os.path.join(HERE, "c2.npz"), **out)
 
 
+def _make_generated(mdrq, name, data_fn, query_fn, ref_queries: int = 20):
+    """C3 / C4: the queries themselves (slow to tune, committed), the
+    reference's id lists (counts + sha1) for the first `ref_queries`, and --
+    from the C oracle, which the other fixtures pin to the reference -- the
+    counts of every query."""
+    import oracle
+    values = data_fn()
+    lo, hi = query_fn()
+    data = mdrq.DataSet(values)
+    scan = mdrq.build_method("horizontal", data, threads=os.cpu_count() or 8, seed=0,
+                             mode=mdrq.KernelMode.SCALAR)
+    counts, shas = [], []
+    for i in range(ref_queries):
+        ids = scan.search(mdrq.RangeQuery(lo[i], hi[i])).ids
+        counts.append(ids.size)
+        shas.append(np.frombuffer(sha1_ids(ids), np.uint8))
+    scan.close()
+    all_counts = oracle.count_batch(values, lo, hi)
+    assert np.array_equal(all_counts[:ref_queries], counts), "oracle disagrees with the reference"
+    np.savez_compressed(
+        os.path.join(HERE, f"{name}.npz"),
+        data_sha1=np.frombuffer(hashlib.sha1(values.tobytes()).digest(), np.uint8),
+        lo=lo, hi=hi, ref_counts=np.array(counts, np.int64), ref_sha1=np.stack(shas),
+        oracle_counts=all_counts)
+    print(f"  {name}: mean selectivity {all_counts.mean() / values.shape[0]:.3g}, "
+          f"range {all_counts.min() / values.shape[0]:.2g}..{all_counts.max() / values.shape[0]:.2g}", flush=True)
+
+
+def make_c3(mdrq):
+    from paper_1801_03644_b200 import workload
+    _make_generated(mdrq, "c3", workload.c3_data, workload.c3_queries)
+
+
+def make_c4(mdrq):
+    from paper_1801_03644_b200 import workload
+    _make_generated(mdrq, "c4", workload.c4_data, workload.c4_queries)
+
+
 def main():
     mdrq = load_reference()
-    what = sys.argv[1:] or ["kernels", "edge", "c1", "c2"]
+    what = sys.argv[1:] or ["kernels", "edge", "c1", "c2", "c3", "c4"]
     for w in what:
         print(f"generating {w} ...", flush=True)
-        {"kernels": make_kernels, "edge": make_edge, "c1": make_c1, "c2": make_c2}[w](mdrq)
+        {"kernels": make_kernels, "edge": make_edge, "c1": make_c1, "c2": make_c2,
+         "c3": make_c3, "c4": make_c4}[w](mdrq)
     print("done")
 
 

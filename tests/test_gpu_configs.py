@@ -1,0 +1,73 @@
+"""Full-size configuration parity on the GPU (BASELINE.json configs).
+
+C2 (5e7 x 8): the first 20 queries of every selectivity level against the
+reference's own id lists (sha1, tests/golden/c2.npz, recorded with the
+reference's HorizontalScan), and all 5000 queries through every path with
+size-independent properties: count == len(ids), ids strictly ascending and
+< n, and the paths agree with each other id for id.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def sha1_ids(ids):
+    return hashlib.sha1(np.ascontiguousarray(ids, dtype="<u4").tobytes()).digest()
+
+
+@pytest.fixture(scope="module")
+def c2_store(gpu):
+    from paper_1801_03644_b200 import workload
+    values = workload.c2_data()
+    G = golden("c2.npz")
+    assert hashlib.sha1(values.tobytes()).digest() == G["data_sha1"].tobytes()
+    st = gpu.DeviceStore(values, layouts=1 | 2 | 4, va_bits=8)
+    yield st, values
+    st.close()
+
+
+def test_c2_vs_reference_golden(c2_store):
+    from paper_1801_03644_b200 import workload
+    st, _ = c2_store
+    G = golden("c2.npz")
+    levels = workload.c2_queries()
+    for li, (s, (lo, hi)) in enumerate(levels.items()):
+        assert G[f"level{li}_s"][0] == s
+        k = G[f"level{li}_counts"].size
+        for path in ("columnar", "vafile", "vafile_batch", "rowwise"):
+            offs, ids = st.ids(lo[:k], hi[:k], path)
+            assert np.array_equal(np.diff(offs), G[f"level{li}_counts"]), (s, path)
+            for i in range(k):
+                assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G[f"level{li}_sha1"][i].tobytes(), (s, path, i)
+
+
+def test_c2_all_queries_paths_agree(c2_store):
+    from paper_1801_03644_b200 import workload
+    st, values = c2_store
+    n = values.shape[0]
+    for s, (lo, hi) in workload.c2_queries().items():
+        ref_offs, ref_ids = st.ids(lo, hi, "vafile_batch")
+        counts = np.diff(ref_offs)
+        assert np.array_equal(st.count(lo, hi, "vafile_batch"), counts), s
+        assert np.array_equal(st.count(lo, hi, "columnar_batch"), counts), s
+        # strictly ascending within every query, all < n
+        d = np.diff(ref_ids.astype(np.int64))
+        starts = ref_offs[1:-1]
+        d[starts[(starts > 0) & (starts < ref_ids.size)] - 1] = 1
+        assert (d > 0).all() and (ref_ids.size == 0 or ref_ids.max() < n)
+        sub = slice(0, 100) if s < 0.1 else slice(0, 20)   # keep the single-query paths quick
+        for path in ("columnar", "vafile"):
+            offs, ids = st.ids(lo[sub], hi[sub], path)
+            m = offs[-1]
+            assert np.array_equal(offs, ref_offs[: offs.size]), (s, path)
+            assert np.array_equal(ids, ref_ids[:m]), (s, path)
+        # a few queries against the OpenMP oracle on the full table
+        exp = oracle.count_batch(values, lo[:4], hi[:4])
+        assert np.array_equal(counts[:4], exp), s
