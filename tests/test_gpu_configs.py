@@ -48,6 +48,39 @@ def test_c2_vs_reference_golden(c2_store):
                 assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G[f"level{li}_sha1"][i].tobytes(), (s, path, i)
 
 
+def _check_generated(gpu, name, values):
+    """C3 / C4: the reference's id lists for the first queries (sha1) and the
+    pinned oracle's counts for every query, on the full table."""
+    G = golden(f"{name}.npz")
+    assert hashlib.sha1(values.tobytes()).digest() == G["data_sha1"].tobytes(), "generator drifted"
+    lo, hi = G["lo"], G["hi"]
+    k = G["ref_counts"].size
+    with gpu.DeviceStore(values, layouts=1 | 4, va_bits=8) as st:
+        for path in ("vafile_batch", "columnar_batch", "vafile", "columnar"):
+            q = lo.shape[0] if path.endswith("_batch") else 200
+            assert np.array_equal(st.count(lo[:q], hi[:q], path), G["oracle_counts"][:q]), (name, path)
+        for path in ("vafile_batch", "vafile", "columnar"):
+            offs, ids = st.ids(lo[:k], hi[:k], path)
+            assert np.array_equal(np.diff(offs), G["ref_counts"]), (name, path)
+            for i in range(k):
+                assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G["ref_sha1"][i].tobytes(), (name, path, i)
+        # every query in ids mode: counts and cross-path id equality
+        offs, ids = st.ids(lo, hi, "vafile_batch")
+        assert np.array_equal(np.diff(offs), G["oracle_counts"]), name
+        o2, i2 = st.ids(lo[:200], hi[:200], "columnar")
+        assert np.array_equal(o2, offs[:201]) and np.array_equal(i2, ids[:o2[-1]]), name
+
+
+def test_c3_vs_reference_golden(gpu):
+    from paper_1801_03644_b200 import workload
+    _check_generated(gpu, "c3", workload.c3_data())
+
+
+def test_c4_vs_reference_golden(gpu):
+    from paper_1801_03644_b200 import workload
+    _check_generated(gpu, "c4", workload.c4_data())
+
+
 def test_c2_all_queries_paths_agree(c2_store):
     from paper_1801_03644_b200 import workload
     st, values = c2_store
