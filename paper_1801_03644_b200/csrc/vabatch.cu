@@ -45,9 +45,11 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_ov = sm;                           // [KB][K][32]
     uint32_t* s_su = sm + KB * K * 32;             // [KB][K][32]
+    // narrow unions also keep the exact query bounds [1024][KB] in smem
+    float2* s_qb = reinterpret_cast<float2*>(s_su + KB * K * 32);
     // MODE 0: u32 [1024] shared by the CTA ; MODE 1/2: u16 [warps][1024]
-    uint32_t* s_cnt32 = s_su + KB * K * 32;
-    uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_su + KB * K * 32);
+    uint32_t* s_cnt32 = s_su + KB * K * 32 + (PV ? KB * 1024 * 2 : 0);
+    uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_cnt32);
 
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     {
@@ -55,6 +57,11 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
         uint4* dst = reinterpret_cast<uint4*>(sm);
         const uint32_t n4 = 2 * KB * K * 32 / 4;
         for (uint32_t i = threadIdx.x; i < n4; i += VB_THREADS) dst[i] = src[i];
+        if constexpr (PV) {
+            const uint4* qsrc = reinterpret_cast<const uint4*>(a.qbounds);
+            uint4* qdst = reinterpret_cast<uint4*>(s_qb);
+            for (uint32_t i = threadIdx.x; i < KB * 1024 / 2; i += VB_THREADS) qdst[i] = qsrc[i];
+        }
         if (MODE == 0)
             for (uint32_t i = threadIdx.x; i < 1024; i += VB_THREADS) s_cnt32[i] = 0;
         if (threadIdx.x < KB) s_dim[threadIdx.x] = a.udims[threadIdx.x];
@@ -62,7 +69,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     __syncthreads();
 
     const uint32_t shift = a.shift;
-    const float2* __restrict__ qb = a.qbounds;     // [1024][KB]
+    const float2* __restrict__ qb = PV ? s_qb : a.qbounds;     // [1024][KB]
     const uint32_t* s_ovl = s_ov + lane;           // lane's word of every row
     const uint32_t* s_sul = s_su + lane;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 1/2: this warp's chunk counters
@@ -106,19 +113,25 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 uint32_t x[KB];
 #pragma unroll
                 for (int u = 0; u < KB; ++u) x[u] = __shfl_sync(0xFFFFFFFFu, cw[u], j4 >> 2);
+                // filter the 4 tuples of this step first (4 x 2 x KB independent
+                // LDS in flight), then refine / emit them in order
+                uint32_t ov4[4], su4[4];
+#pragma unroll
+                for (uint32_t jj = 0; jj < 4; ++jj) ov4[jj] = su4[jj] = 0xFFFFFFFFu;
+#pragma unroll
+                for (int u = 0; u < KB; ++u)
+#pragma unroll
+                    for (uint32_t jj = 0; jj < 4; ++jj) {
+                        const uint32_t idx = u * K * 32 + ((x[u] >> (8 * jj)) & 0xFFu) * 32;
+                        ov4[jj] &= s_ovl[idx];
+                        su4[jj] &= s_sul[idx];
+                    }
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) {
                     if (j4 + jj >= jmax) break;
-                    uint32_t ov = 0xFFFFFFFFu, su = 0xFFFFFFFFu;
-#pragma unroll
-                    for (int u = 0; u < KB; ++u) {
-                        const uint32_t idx = u * K * 32 + ((x[u] >> (8 * jj)) & 0xFFu) * 32;
-                        ov &= s_ovl[idx];
-                        su &= s_sul[idx];
-                    }
                     const uint64_t t = t0 + j4 + jj;
-                    uint32_t hits = su;
-                    uint32_t r = ov & ~su;
+                    uint32_t hits = su4[jj];
+                    uint32_t r = ov4[jj] & ~su4[jj];
                     if (__any_sync(0xFFFFFFFFu, r)) {
                         // exact refinement of (tuple, query) pairs in an edge cell
                         float v[KB];
@@ -245,7 +258,8 @@ void dispatch(const VaBatchArgs& a, cudaStream_t st, std::integer_sequence<int, 
 }  // namespace
 
 size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
-    return size_t(2) * kb * cells * 32 * 4 + (mode == 0 ? 1024 * 4 : 1024 * 2 * VB_WARPS);
+    const size_t qbounds = kb <= 8 ? size_t(kb) * 1024 * 8 : 0;   // PV kernels keep the bounds in smem
+    return size_t(2) * kb * cells * 32 * 4 + qbounds + (mode == 0 ? 1024 * 4 : 1024 * 2 * VB_WARPS);
 }
 
 int va_batch_max_dims() { return kVaBatchMaxDims; }

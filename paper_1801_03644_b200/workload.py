@@ -133,9 +133,25 @@ def c2_queries(count: int = C2["queries"], levels=C2["levels"]):
     return {s: box_queries(rng, count, C2["m"], s) for s in levels}
 
 
-def c5_data(start: int = 0, stop: int | None = None, n: int = C5["n"]) -> np.ndarray:
+def _uniform_chunk_fn(seed: int, m: int):
+    return _UniformChunk(seed, m)
+
+
+class _UniformChunk:
+    """Picklable chunk generator of default_rng(seed).random((n, m), f32)."""
+
+    def __init__(self, seed: int, m: int):
+        self.seed, self.m = seed, m
+
+    def __call__(self, c: int, rows: int) -> np.ndarray:
+        return uniform_rows(self.seed, self.m, c * CHUNK_ROWS, c * CHUNK_ROWS + rows)
+
+
+def c5_data(start: int = 0, stop: int | None = None, n: int = C5["n"], workers: int | None = None) -> np.ndarray:
+    """Rows [start, stop) of C5 (= default_rng(0).random((5e8, 10), float32)),
+    generated chunk-parallel with the PCG64 stream advanced per chunk."""
     stop = n if stop is None else stop
-    return uniform_rows(0, C5["m"], start, stop)
+    return _chunked(_uniform_chunk_fn(0, C5["m"]), C5["m"], start, stop, n, workers)
 
 
 def c5_queries(count: int = C5["queries"]):
@@ -196,6 +212,7 @@ def _chunked(chunk_fn, m: int, start: int, stop: int, n: int, workers: int | Non
         return out
     import multiprocessing as mp
     from multiprocessing import shared_memory
+    import weakref
     shm = shared_memory.SharedMemory(create=True, size=max(1, out_shape[0] * m * 4))
     try:
         offs = []
@@ -203,14 +220,15 @@ def _chunked(chunk_fn, m: int, start: int, stop: int, n: int, workers: int | Non
         for c, a, b in jobs:
             offs.append(o)
             o += b - a
-        ctx = mp.get_context("fork")
+        # spawn, not fork: the caller may already run CUDA / torch threads
+        ctx = mp.get_context("spawn")
         with ctx.Pool(workers) as pool:
             pool.starmap(_fill_chunk, [(chunk_fn, shm.name, out_shape, off, c, a, b, n, m)
                                        for off, (c, a, b) in zip(offs, jobs)])
-        out = np.ndarray(out_shape, np.float32, buffer=shm.buf).copy()
     finally:
-        shm.close()
-        shm.unlink()
+        shm.unlink()   # the mapping stays valid until the array below is freed
+    out = np.ndarray(out_shape, np.float32, buffer=shm.buf)
+    weakref.finalize(out, shm.close)
     return out
 
 

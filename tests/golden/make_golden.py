@@ -21,6 +21,10 @@ Every expected value below comes from a reference API call:
                plus 200 partial-match queries through VerticalScan
   c2.npz       C2 (5e7 x 8, seed 0): HorizontalScan (8 threads) counts +
                sha1 for the first 20 queries of each selectivity level
+  c3.npz/c4.npz  C3 / C4 (our generators, workload.py): the queries, the
+               reference's id lists for the first 20, oracle counts for all
+  c5.npz       C5 (5e8 x 10): SequentialScan(SCALAR) id lists for the first 8
+               queries, oracle counts for the first 200, table slice hashes
 """
 
 from __future__ import annotations
@@ -314,13 +318,40 @@ def make_c4(mdrq):
     _make_generated(mdrq, "c4", workload.c4_data, workload.c4_queries)
 
 
+def make_c5(mdrq, ref_queries: int = 8, oracle_queries: int = 200):
+    """C5 (5e8 x 10, 20 GB): the reference's SequentialScan(SCALAR) -- the
+    ground truth its own `verify` uses (cli.py:222) -- on the first
+    `ref_queries` queries, the pinned C oracle's counts on the first
+    `oracle_queries`, and the sha1 of 1M-row slices of the table."""
+    import oracle
+    from paper_1801_03644_b200 import workload
+    values = workload.c5_data()
+    lo, hi = workload.c5_queries()
+    slices = [0, 123_456_789, 499_000_000]
+    out = {"slice_starts": np.array(slices, np.int64),
+           "slice_sha1": np.stack([np.frombuffer(hashlib.sha1(values[s:s + 1_000_000].tobytes()).digest(),
+                                                 np.uint8) for s in slices])}
+    data = mdrq.DataSet(values)
+    scan = mdrq.SequentialScan(data, mdrq.KernelMode.SCALAR)
+    counts, shas = [], []
+    for i in range(ref_queries):
+        ids = scan.search(mdrq.RangeQuery(lo[i], hi[i])).ids
+        counts.append(ids.size)
+        shas.append(np.frombuffer(sha1_ids(ids), np.uint8))
+        print(f"  C5 query {i}: {ids.size} ids", flush=True)
+    oc = oracle.count_batch(values, lo[:oracle_queries], hi[:oracle_queries])
+    assert np.array_equal(oc[:ref_queries], counts), "oracle disagrees with the reference"
+    out.update(ref_counts=np.array(counts, np.int64), ref_sha1=np.stack(shas), oracle_counts=oc)
+    np.savez_compressed(os.path.join(HERE, "c5.npz"), **out)
+
+
 def main():
     mdrq = load_reference()
     what = sys.argv[1:] or ["kernels", "edge", "c1", "c2", "c3", "c4"]
     for w in what:
         print(f"generating {w} ...", flush=True)
         {"kernels": make_kernels, "edge": make_edge, "c1": make_c1, "c2": make_c2,
-         "c3": make_c3, "c4": make_c4}[w](mdrq)
+         "c3": make_c3, "c4": make_c4, "c5": make_c5}[w](mdrq)
     print("done")
 
 

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Profiling recipe of one round (run under gpurun, 1 GPU).  Every ncu command
+# is preceded by the same command line exiting 0 without ncu.
+set -u
+OUT=gpurun_out
+B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-paths"
+$B > $OUT/plain.log 2>&1
+echo "plain=$?" >> $OUT/rc.txt
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/launches.csv $B > $OUT/ncu_launches.log 2>&1
+echo "launches=$?" >> $OUT/rc.txt
+timeout 1200 ncu --set full --clock-control none --import-source on \
+    -k regex:va_batch_kernel -c 2 -o $OUT/prof_vab $B > $OUT/ncu_vab.log 2>&1
+echo "vab=$?" >> $OUT/rc.txt
+timeout 1200 ncu --set full --clock-control none --import-source on \
+    -k regex:col_scan_kernel -s 10 -c 1 -o $OUT/prof_col $B > $OUT/ncu_col.log 2>&1
+echo "col=$?" >> $OUT/rc.txt
