@@ -81,6 +81,38 @@ def test_c4_vs_reference_golden(gpu):
     _check_generated(gpu, "c4", workload.c4_data())
 
 
+def test_c5_full_size_vs_reference_golden(gpu):
+    """C5: 5e8 x 10 (20 GB) on one GPU.  The table is generated chunk-parallel
+    (PCG64 advanced per chunk) and checked against slice hashes of the
+    one-shot generator; the first 8 queries against the reference's
+    SequentialScan id lists, the first 200 counts against the oracle, 1024
+    queries in ids mode for size-independent properties."""
+    from paper_1801_03644_b200 import workload
+    G = golden("c5.npz")
+    values = workload.c5_data()
+    for s, h in zip(G["slice_starts"], G["slice_sha1"]):
+        assert hashlib.sha1(values[s:s + 1_000_000].tobytes()).digest() == h.tobytes(), s
+    lo, hi = workload.c5_queries()
+    k = G["ref_counts"].size
+    n = values.shape[0]
+    with gpu.DeviceStore(values, layouts=1 | 4, va_bits=8) as st:
+        del values
+        nq = G["oracle_counts"].size
+        assert np.array_equal(st.count(lo[:nq], hi[:nq], "vafile_batch"), G["oracle_counts"])
+        assert np.array_equal(st.count(lo[:32], hi[:32], "columnar_batch"), G["oracle_counts"][:32])
+        for path in ("vafile_batch", "vafile", "columnar"):
+            offs, ids = st.ids(lo[:k], hi[:k], path)
+            assert np.array_equal(np.diff(offs), G["ref_counts"]), path
+            for i in range(k):
+                assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G["ref_sha1"][i].tobytes(), (path, i)
+        offs, ids = st.ids(lo[:1024], hi[:1024], "vafile_batch")
+        assert np.array_equal(np.diff(offs), st.count(lo[:1024], hi[:1024], "vafile_batch"))
+        d = np.diff(ids.astype(np.int64))
+        starts = offs[1:-1]
+        d[starts[(starts > 0) & (starts < ids.size)] - 1] = 1
+        assert (d > 0).all() and ids.max() < n
+
+
 def test_c2_all_queries_paths_agree(c2_store):
     from paper_1801_03644_b200 import workload
     st, values = c2_store
