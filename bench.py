@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-paths", action="store_true", help="skip the per-path cost table")
+    ap.add_argument("--force-merge", action="store_true",
+                    help="run the NCCL id merge even with one rank (torchrun --nproc-per-node 1)")
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="tuples per GPU")
     ap.add_argument("--queries", type=int, default=NQ)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -208,7 +210,10 @@ def main():
     from paper_1801_03644_b200 import _lib, workload
 
     world, rank, local = dist_env()
-    if world > 1:
+    # the NCCL merge runs whenever there is more than one rank; --force-merge
+    # exercises it with a single torchrun rank (the only GPU count here)
+    merge = world > 1 or args.force_merge
+    if merge:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -240,7 +245,7 @@ def main():
 
     def step():
         batch.ids_async(sptr)
-        if world > 1:
+        if merge:
             d_ids, d_offs, tot = batch.result_device()
             ids_t = _wrap(d_ids, tot, torch.int32, dev)
             offs_t = _wrap(d_offs, nq + 1, torch.int64, dev)
@@ -350,7 +355,7 @@ def main():
         print(json.dumps(line), flush=True)
     batch.close()
     store.close()
-    if world > 1:
+    if merge:
         dist.destroy_process_group()
     return 0
 
