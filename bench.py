@@ -373,11 +373,16 @@ def roofline_of(path, prof, stats, n, nq, total_ids, peak, peak_kind):
     loaded = float(sum(s.bytes_loaded for s in stats))
     ids_bytes = 4.0 * (total_ids or 0)
     if path.endswith("_batch"):
-        passes = max(1, prof["scan"][1] if cls == "scan" else nl)
-        algo = loaded / passes + (ids_bytes / passes if cls == "id_write" else 0.0)
+        passes = max(1, prof["scan"][1])
+        if cls == "scan":
+            # filter pass: the union's code planes + (ids mode) one 4-byte
+            # staged (tuple, query) record per match
+            algo = (loaded + ids_bytes) / passes
+        else:
+            algo = (2 * ids_bytes) / max(nl, 1)   # records read + ids written
         kernel = {"vafile_batch": "va_batch_kernel (bit-sliced, <=1024 queries/pass)",
                   "columnar_batch": "col_batch_count_kernel (<=32 queries/pass)"}[path]
-        kernel += " filter pass" if cls == "scan" else " id-write pass"
+        kernel += " filter pass" if cls == "scan" else " scatter"
     else:
         algo = (loaded + nq * n / 8.0) / nl
         kernel = {"columnar": "col_scan_kernel", "vafile": "va_scan_kernel", "rowwise": "row_scan_kernel"}[path]

@@ -101,11 +101,24 @@ struct VaBatchArgs {
     uint32_t* ids;
     uint64_t ids_cap;
     uint32_t id_base;
+    // single-pass ids (mode 3): (tuple offset << 10 | query) records staged in
+    // linked 1024-record blocks per chunk, scattered into place afterwards
+    uint32_t* rec;               // [max_blocks][kRecBlock]
+    uint32_t* blk_next;          // [max_blocks]
+    uint32_t* blk_count;         // [max_blocks]
+    uint32_t* chunk_head;        // [chunks], 0xFFFFFFFF = no records
+    uint32_t* cursor;            // block allocator
+    uint32_t* overflow;          // set when the staging pool ran out (mode 2 then runs)
+    uint32_t max_blocks;
 };
+constexpr uint32_t kRecBlock = 1024;
+constexpr uint32_t kNoBlock = 0xFFFFFFFFu;
 size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode);
 int va_batch_max_dims();
 uint32_t va_batch_warps();
-void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st);   // 0 count, 1 chunk counts, 2 ids
+// mode 0 count, 1 chunk counts, 2 ids (recount pass), 3 chunk counts + staged records
+void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st);
+void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st);
 void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st);
 
 constexpr int kColTile = 4096;     // tuples per CTA tile, single-query columnar

@@ -51,6 +51,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     uint32_t* s_cnt32 = s_su + KB * K * 32 + (PV ? KB * 1024 * 2 : 0);
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_cnt32);
 
+    // the recount pass only runs when the single-pass staging overflowed
+    if (MODE == 2 && a.overflow && *reinterpret_cast<volatile const uint32_t*>(a.overflow) == 0) return;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.tables);
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             for (int i = 0; i < 32; ++i) wcnt[lane * 32 + i] = 0;
         }
         const unsigned long long* __restrict__ base = MODE == 2 ? a.base + uint64_t(chunk) * 1024 : nullptr;
+        uint32_t blk = kNoBlock, fill = 0;   // MODE 3: current staging block of this chunk
 
         // software pipeline: the codes (and, for narrow unions, the exact
         // values) of the next 128-tuple block are loaded while this block is
@@ -158,13 +161,56 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             if (ok) hits |= 1u << b;
                         }
                     }
+                    if (MODE == 3) {
+                        // stage (tuple offset, query) records in tuple order:
+                        // warp prefix of the per-lane hit counts
+                        const uint32_t cnt = __popc(hits);
+                        const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, cnt);
+                        if (tot) {
+                            uint32_t incl = cnt;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const uint32_t x2 = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                                if (lane >= uint32_t(o)) incl += x2;
+                            }
+                            if (blk != kNoBlock - 1 && (blk == kNoBlock || fill + tot > kRecBlock)) {
+                                uint32_t nb = 0;
+                                if (lane == 0) {
+                                    nb = atomicAdd(a.cursor, 1u);
+                                    if (nb >= a.max_blocks) {
+                                        atomicExch(a.overflow, 1u);
+                                        nb = kNoBlock - 1;   // stop staging this chunk
+                                    }
+                                    if (blk == kNoBlock)
+                                        a.chunk_head[chunk] = nb;
+                                    else {
+                                        a.blk_count[blk] = fill;
+                                        a.blk_next[blk] = nb;
+                                    }
+                                }
+                                blk = __shfl_sync(0xFFFFFFFFu, nb, 0);
+                                fill = 0;
+                            }
+                            if (blk != kNoBlock - 1) {
+                                uint32_t* dst = a.rec + uint64_t(blk) * kRecBlock + fill + (incl - cnt);
+                                const uint32_t trel = uint32_t(t - start) << 10;
+                                uint32_t h = hits;
+                                while (h) {
+                                    const int b = __ffs(h) - 1;
+                                    h &= h - 1;
+                                    *dst++ = trel | (lane * 32 + b);
+                                }
+                            }
+                            fill += tot;
+                        }
+                    }
                     while (hits) {
                         const int b = __ffs(hits) - 1;
                         hits &= hits - 1;
                         const uint32_t q = lane * 32 + b;
                         if (MODE == 0) {
                             atomicAdd(&s_cnt32[q], 1u);
-                        } else if (MODE == 1) {
+                        } else if (MODE == 1 || MODE == 3) {
                             wcnt[q] += 1;
                         } else {
                             const unsigned long long pos = a.qoff[q] + base[q] + wcnt[q];
@@ -175,7 +221,11 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 }
             }
         }
-        if (MODE == 1) {
+        if (MODE == 3 && lane == 0 && blk < kNoBlock - 1) {
+            a.blk_count[blk] = fill;
+            a.blk_next[blk] = kNoBlock;
+        }
+        if (MODE == 1 || MODE == 3) {
             __syncwarp();
             uint32_t* out = a.chunk_counts + uint64_t(chunk) * 1024;
             for (uint32_t q = lane; q < 1024; q += 32) out[q] = wcnt[q];
@@ -239,6 +289,44 @@ __global__ void __launch_bounds__(1024) vb_query_scan_kernel(const unsigned long
     }
 }
 
+// Scatter the staged records of mode 3 into place: one warp per chunk walks
+// the chunk's block list in order; records with equal queries inside a
+// 32-record group are ranked by lane (match_any), so every query's ids stay
+// ascending.  Position = qoff[q] + base[chunk][q] + running count.
+__global__ void __launch_bounds__(256) vb_scatter_kernel(const VaBatchArgs a) {
+    __shared__ uint32_t s_run[8][1024];
+    if (*reinterpret_cast<volatile const uint32_t*>(a.overflow)) return;   // mode 2 recounts instead
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t* run = s_run[warp];
+    for (uint32_t chunk = blockIdx.x * 8 + warp; chunk < a.nchunks; chunk += gridDim.x * 8) {
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) run[lane * 32 + i] = 0;
+        __syncwarp();
+        const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
+        const unsigned long long* base = a.base + uint64_t(chunk) * 1024;
+        for (uint32_t b = a.chunk_head[chunk]; b != kNoBlock; b = a.blk_next[b]) {
+            const uint32_t cnt = a.blk_count[b];
+            const uint32_t* rec = a.rec + uint64_t(b) * kRecBlock;
+            for (uint32_t i = 0; i < cnt; i += 32) {
+                const bool active = i + lane < cnt;
+                const uint32_t r = active ? rec[i + lane] : 0u;
+                const uint32_t q = active ? (r & 1023u) : 0xFFFFFFFFu;
+                const uint32_t same = __match_any_sync(0xFFFFFFFFu, q);
+                const uint32_t rank = __popc(same & lanemask_lt());
+                uint32_t prev = 0;
+                if (active) {
+                    prev = run[q];
+                    const unsigned long long pos = a.qoff[q] + base[q] + prev + rank;
+                    if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(start + (r >> 10));
+                }
+                __syncwarp();
+                if (active && rank == 0) run[q] = prev + __popc(same);
+                __syncwarp();
+            }
+        }
+    }
+}
+
 template <int MODE, int KB>
 void run_kb(const VaBatchArgs& a, cudaStream_t st) {
     const size_t smem = va_batch_smem(KB, va_batch_cells(KB), MODE);
@@ -273,8 +361,16 @@ void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st) {
         dispatch<0>(a, st, Seq{});
     else if (mode == 1)
         dispatch<1>(a, st, Seq{});
-    else
+    else if (mode == 2)
         dispatch<2>(a, st, Seq{});
+    else
+        dispatch<3>(a, st, Seq{});
+}
+
+void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st) {
+    if (a.n == 0 || a.nchunks == 0) return;
+    const uint32_t blocks = (a.nchunks + 7) / 8;
+    vb_scatter_kernel<<<blocks, 256, 0, st>>>(a);
 }
 
 void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st) {
