@@ -86,7 +86,7 @@ struct VaBatchArgs {
     uint32_t shift;              // stored code >> shift = table cell
     uint32_t nqp;                // queries in this pass (<= 1024)
     const uint16_t* udims;       // [kb]
-    const uint32_t* tables;      // [2][kb][cells][32]: overlap masks, then sure masks
+    const uint32_t* tables;      // [kb][cells][32][2]: (overlap, containment) query-mask words
     const float2* qbounds;       // [1024][kb] exact (lo, hi), +-inf where unconstrained
     uint32_t grid;               // CTAs (chunks = grid * warps)
     uint64_t chunk_tuples;       // tuples per chunk (multiple of 128, < 65536: u16 counters)

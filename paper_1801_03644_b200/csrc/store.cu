@@ -329,9 +329,10 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
                         ov = int(c) >= lo_c[u] && int(c) <= hi_c[u];
                         su = ov && (int(c) > lo_c[u] || !elo[u]) && (int(c) < hi_c[u] || !ehi[u]);
                     }
-                    const size_t idx = (size_t(u) * ps.cells + c) * 32 + w;
+                    // interleaved (overlap, containment) words: [u][c][w][2]
+                    const size_t idx = ((size_t(u) * ps.cells + c) * 32 + w) * 2;
                     if (ov) tab[idx] |= bit;
-                    if (su) tab[plane + idx] |= bit;
+                    if (su) tab[idx + 1] |= bit;
                 }
         }
         b->vb_tables.insert(b->vb_tables.end(), tab.begin(), tab.end());

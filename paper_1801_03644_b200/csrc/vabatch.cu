@@ -43,12 +43,11 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
     constexpr bool PV = KB <= 8;                   // exact values prefetched into registers
     __shared__ uint32_t s_dim[KB];
-    uint32_t* s_ov = sm;                           // [KB][K][32]
-    uint32_t* s_su = sm + KB * K * 32;             // [KB][K][32]
+    uint32_t* s_end = sm + 2 * KB * K * 32;        // end of the [KB][K][32] x (ov, su) table
     // narrow unions also keep the exact query bounds [1024][KB] in smem
-    float2* s_qb = reinterpret_cast<float2*>(s_su + KB * K * 32);
-    // MODE 0: u32 [1024] shared by the CTA ; MODE 1/2: u16 [warps][1024]
-    uint32_t* s_cnt32 = s_su + KB * K * 32 + (PV ? KB * 1024 * 2 : 0);
+    float2* s_qb = reinterpret_cast<float2*>(s_end);
+    // MODE 0: u32 [1024] shared by the CTA ; MODE 1/2/3: u16 [warps][1024]
+    uint32_t* s_cnt32 = s_end + (PV ? KB * 1024 * 2 : 0);
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_cnt32);
 
     // the recount pass only runs when the single-pass staging overflowed
@@ -72,8 +71,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
 
     const uint32_t shift = a.shift;
     const float2* __restrict__ qb = PV ? s_qb : a.qbounds;     // [1024][KB]
-    const uint32_t* s_ovl = s_ov + lane;           // lane's word of every row
-    const uint32_t* s_sul = s_su + lane;
+    // rows interleave (overlap, containment) words: entry (u, c, w) is the
+    // uint2 at byte (u*K + c)*256 + w*8; lane w reads its entry of a row
+    const char* s_tabl = reinterpret_cast<const char*>(sm) + lane * 8;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 1/2: this warp's chunk counters
 
     for (uint32_t chunk = blockIdx.x * VB_WARPS + warp; chunk < a.nchunks; chunk += gridDim.x * VB_WARPS) {
@@ -125,9 +125,15 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 for (int u = 0; u < KB; ++u)
 #pragma unroll
                     for (uint32_t jj = 0; jj < 4; ++jj) {
-                        const uint32_t idx = u * K * 32 + ((x[u] >> (8 * jj)) & 0xFFu) * 32;
-                        ov4[jj] &= s_ovl[idx];
-                        su4[jj] &= s_sul[idx];
+                        // byte offset of row (u, cell) = cell * 256 (+ u*K*256 as immediate):
+                        // the cell byte of tuple jj masked in place at bits 8..13
+                        const uint32_t xb = x[u];
+                        const uint32_t cb = jj == 0 ? (xb << 8) & ((K - 1) << 8)
+                                          : jj == 1 ? xb & ((K - 1) << 8)
+                                                    : (xb >> (8 * (jj - 1))) & ((K - 1) << 8);
+                        const uint2 e = *reinterpret_cast<const uint2*>(s_tabl + cb + u * K * 256);
+                        ov4[jj] &= e.x;
+                        su4[jj] &= e.y;
                     }
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) {
