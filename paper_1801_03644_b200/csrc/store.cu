@@ -517,6 +517,29 @@ uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids)
     }
 }
 
+// Ids mode of an AUTO batch planned as a bit-sliced pass: when the queries
+// are expected to return many ids (estimated from the VA code ranges under
+// independence), the per-query path's bitmask compaction beats staging one
+// record per match (C3 in profiles/r01_configs.json), so switch to it.
+void refine_auto_ids(const mdrq_store* s, mdrq_batch* b) {
+    if (b->path != MDRQ_PATH_VAFILE_BATCH || !b->nq) return;
+    const double cells = double(s->nb() + 1);
+    double est = 0.0;
+    for (uint32_t q = 0; q < b->nq; ++q) {
+        double sel = 1.0;
+        for (uint32_t i = 0; i < b->descs[q].k; ++i) {
+            const DimPred& p = b->preds[b->descs[q].off + i];
+            sel *= p.ch >= p.cl ? double(p.ch - p.cl + 1) / cells : 0.0;
+        }
+        est += sel;
+    }
+    // narrow unions (<= 8 dims) keep values and bounds on chip and stay
+    // ahead even at 1e-2 (C2); wide unions lose from ~5e-3 on (C3)
+    uint32_t kb = 0;
+    for (const VbPass& p : b->vb_passes) kb = std::max(kb, p.kb);
+    if (kb > 8 && est / b->nq > 5e-3) b->path = MDRQ_PATH_VAFILE;
+}
+
 ScanArgs base_args(mdrq_store* s, mdrq_batch* b, uint32_t path) {
     ScanArgs a{};
     a.cols = s->cols.p;
@@ -1000,6 +1023,7 @@ int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper, uint32
         mdrq_batch* b = &s->scratch;
         b->owner = s;
         build_descs(s, lower, upper, nq, resolve_path(s, path, nq, true), true, b);
+        if (path == MDRQ_PATH_AUTO) refine_auto_ids(s, b);
         upload_batch(s, b);
         const uint64_t tot = run_ids_sync(s, b);
         *total = tot;
