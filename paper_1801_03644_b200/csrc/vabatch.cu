@@ -197,20 +197,21 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                                 blk = __shfl_sync(0xFFFFFFFFu, nb, 0);
                                 fill = 0;
                             }
-                            if (blk != kNoBlock - 1) {
-                                uint32_t* dst = a.rec + uint64_t(blk) * kRecBlock + fill + (incl - cnt);
-                                const uint32_t trel = uint32_t(t - start) << 10;
-                                uint32_t h = hits;
-                                while (h) {
-                                    const int b = __ffs(h) - 1;
-                                    h &= h - 1;
-                                    *dst++ = trel | (lane * 32 + b);
-                                }
+                            // one loop writes the records and counts them per (chunk, query)
+                            const bool stage_on = blk != kNoBlock - 1;
+                            uint32_t* dst = a.rec + uint64_t(stage_on ? blk : 0) * kRecBlock + fill + (incl - cnt);
+                            const uint32_t trel = uint32_t(t - start) << 10;
+                            while (hits) {
+                                const int b = __ffs(hits) - 1;
+                                hits &= hits - 1;
+                                const uint32_t q = lane * 32 + b;
+                                if (stage_on) *dst++ = trel | q;
+                                wcnt[q] += 1;
                             }
                             fill += tot;
                         }
                     }
-                    while (hits) {
+                    while (MODE != 3 && hits) {
                         const int b = __ffs(hits) - 1;
                         hits &= hits - 1;
                         const uint32_t q = lane * 32 + b;
