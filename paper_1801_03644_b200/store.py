@@ -71,6 +71,34 @@ class DeviceStore:
         self.va_bits = int(info.va_bits)
         self.n_pad = int(info.n_pad)
 
+    @classmethod
+    def from_file(cls, path, *, shard: tuple[int, int] | None = None, layouts: int = _lib.LAYOUT_COLUMNAR,
+                  va_bits: int = DEFAULT_VA_BITS, device: int | None = None) -> "DeviceStore":
+        """Stream a dataset file in the reference's binary format (magic
+        'MDRQ' v1, core.py:295-320) into a device store.  With
+        ``shard=(rank, world)`` only this rank's contiguous row range is
+        read (memory-mapped, so a 20 GB file never sits in host RAM twice)
+        and the store's ids start at the shard's first row (SURVEY.md 8f
+        item 2)."""
+        import os
+
+        from .core import read_header
+        from .parallel import shard_range
+        n, m, off = read_header(path)
+        payload = os.path.getsize(path) - off
+        if payload != n * m * 4:
+            raise ValueError(f"{path}: payload is {payload} bytes, expected {n * m * 4} for n={n} m={m}")
+        start, stop = (0, n) if shard is None else shard_range(n, shard[1], shard[0])
+        if n == 0:
+            rows = np.empty((0, m), np.float32)
+        else:
+            mm = np.memmap(path, dtype="<f4", mode="r", offset=off, shape=(n, m))
+            rows = np.asarray(mm[start:stop], dtype=np.float32)
+        for s in range(0, rows.shape[0], 1 << 22):
+            if np.isnan(rows[s:s + (1 << 22)]).any():
+                raise ValueError("NaN values are rejected at ingestion")
+        return cls(rows, layouts=layouts, va_bits=va_bits, device=device, id_base=start)
+
     # -- lifecycle -----------------------------------------------------------
     @property
     def handle(self):

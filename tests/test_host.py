@@ -172,3 +172,12 @@ def test_methods_registry_rejects_trees_and_unknown():
     for name in ("kdtree", "rstar", "nope"):
         with pytest.raises(ValueError):
             build_method(name, data)
+
+
+def test_cli_parser_and_report_columns():
+    from paper_1801_03644_b200.cli import REPORT_COLUMNS, build_parser
+    # the reference's CSV header (bench.py:34-38)
+    assert REPORT_COLUMNS[:3] == ("method", "n", "m") and REPORT_COLUMNS[-2:] == ("objects_compared",
+                                                                                   "nodes_visited")
+    a = build_parser().parse_args(["bench", "--n", "10", "--queries", "3", "--out", "x.csv"])
+    assert (a.cmd, a.n, a.count, a.out) == ("bench", 10, 3, "x.csv")
