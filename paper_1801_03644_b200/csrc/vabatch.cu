@@ -34,6 +34,12 @@ namespace mdrq {
 
 namespace {
 
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 r;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr));
+    return r;
+}
+
 constexpr int VB_THREADS = 512;
 constexpr int VB_WARPS = VB_THREADS / 32;
 
@@ -72,8 +78,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     const uint32_t shift = a.shift;
     const float2* __restrict__ qb = PV ? s_qb : a.qbounds;     // [1024][KB]
     // rows interleave (overlap, containment) words: entry (u, c, w) is the
-    // uint2 at byte (u*K + c)*256 + w*8; lane w reads its entry of a row
-    const char* s_tabl = reinterpret_cast<const char*>(sm) + lane * 8;
+    // uint2 at byte (u*K + c)*256 + w*8; lane w reads its entry of a row.
+    // 32-bit shared-window address of the lane's column of the table.
+    const uint32_t s_tab32 = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) + lane * 8;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 1/2: this warp's chunk counters
 
     for (uint32_t chunk = blockIdx.x * VB_WARPS + warp; chunk < a.nchunks; chunk += gridDim.x * VB_WARPS) {
@@ -122,18 +129,23 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) ov4[jj] = su4[jj] = 0xFFFFFFFFu;
 #pragma unroll
-                for (int u = 0; u < KB; ++u)
+                for (int u = 0; u < KB; u += 2)
 #pragma unroll
                     for (uint32_t jj = 0; jj < 4; ++jj) {
-                        // byte offset of row (u, cell) = cell * 256 (+ u*K*256 as immediate):
-                        // the cell byte of tuple jj masked in place at bits 8..13
-                        const uint32_t xb = x[u];
-                        const uint32_t cb = jj == 0 ? (xb << 8) & ((K - 1) << 8)
-                                          : jj == 1 ? xb & ((K - 1) << 8)
-                                                    : (xb >> (8 * (jj - 1))) & ((K - 1) << 8);
-                        const uint2 e = *reinterpret_cast<const uint2*>(s_tabl + cb + u * K * 256);
-                        ov4[jj] &= e.x;
-                        su4[jj] &= e.y;
+                        // byte offset of row (u, cell) = cell * 256 (+ u*K*256 as an
+                        // immediate): one PRMT moves the cell byte of tuple jj to bits
+                        // 8..15 (cells are pre-masked to < K); two dims per 3-input AND
+                        const uint32_t ca = __byte_perm(x[u], 0u, 0x4404u | (jj << 4));
+                        const uint2 ea = lds64(s_tab32 + ca + u * K * 256);
+                        if (u + 1 < KB) {
+                            const uint32_t cb = __byte_perm(x[u + 1], 0u, 0x4404u | (jj << 4));
+                            const uint2 eb = lds64(s_tab32 + cb + (u + 1) * K * 256);
+                            ov4[jj] = ov4[jj] & ea.x & eb.x;
+                            su4[jj] = su4[jj] & ea.y & eb.y;
+                        } else {
+                            ov4[jj] &= ea.x;
+                            su4[jj] &= ea.y;
+                        }
                     }
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) {
