@@ -344,6 +344,7 @@ def main():
             "hbm_gbs_per_gpu": roofline["achieved"],
             "roofline": roofline,
             "columnar_scan_roofline": col_roof,
+            "pass_profile": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in prof.items()},
             "paths_us_per_query": paths,
             "e2e": {"value": e2e_val, "unit": "tuples/s", "h2d_bytes_per_step": int(lo.nbytes + hi.nbytes),
                     "d2h_bytes_per_step": int(total_local * 4 + (nq + 1) * 8)},

@@ -260,17 +260,39 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
 }
 
 // per-query exclusive scan over chunks: base[c][q], total[q]
-__global__ void vb_chunk_scan_kernel(const uint32_t* __restrict__ cc, uint32_t nchunks, uint32_t nqp,
-                                     unsigned long long* __restrict__ base, unsigned long long* __restrict__ total) {
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nqp) return;
+// per-query exclusive scan over chunks: base[c][q], total[q].  One CTA per
+// 32 queries: thread (s, ql) sums slice s of the chunks for query ql, a scan
+// over the 32 slice sums in smem, then every thread writes its slice's bases.
+__global__ void __launch_bounds__(1024) vb_chunk_scan_kernel(const uint32_t* __restrict__ cc, uint32_t nchunks,
+                                                             uint32_t nqp, unsigned long long* __restrict__ base,
+                                                             unsigned long long* __restrict__ total) {
+    __shared__ unsigned long long s_sum[32][33];
+    const uint32_t ql = threadIdx.x & 31u, sl = threadIdx.x >> 5;
+    const uint32_t q = blockIdx.x * 32 + ql;
+    const uint32_t per = (nchunks + 31) / 32;
+    const uint32_t c0 = min(nchunks, sl * per), c1 = min(nchunks, c0 + per);
     unsigned long long run = 0;
-    for (uint32_t c = 0; c < nchunks; ++c) {
+    if (q < nqp)
+        for (uint32_t c = c0; c < c1; ++c) run += cc[uint64_t(c) * 1024 + q];
+    s_sum[sl][ql] = run;
+    __syncthreads();
+    if (sl == 0) {
+        unsigned long long acc = 0;
+        for (uint32_t i = 0; i < 32; ++i) {
+            const unsigned long long v = s_sum[i][ql];
+            s_sum[i][ql] = acc;
+            acc += v;
+        }
+        if (q < nqp) total[q] = acc;
+    }
+    __syncthreads();
+    if (q >= nqp) return;
+    run = s_sum[sl][ql];
+    for (uint32_t c = c0; c < c1; ++c) {
         const uint32_t v = cc[uint64_t(c) * 1024 + q];
         base[uint64_t(c) * 1024 + q] = run;
         run += v;
     }
-    total[q] = run;
 }
 
 // exclusive scan of the pass's query totals, chained on offsets[q0]
@@ -313,34 +335,44 @@ __global__ void __launch_bounds__(1024) vb_query_scan_kernel(const unsigned long
 // 32-record group are ranked by lane (match_any), so every query's ids stay
 // ascending.  Position = qoff[q] + base[chunk][q] + running count.
 __global__ void __launch_bounds__(256) vb_scatter_kernel(const VaBatchArgs a) {
-    __shared__ uint32_t s_run[8][1024];
+    extern __shared__ unsigned long long s_pos[];   // [8 warps][1024] next output position
     if (*reinterpret_cast<volatile const uint32_t*>(a.overflow)) return;   // mode 2 recounts instead
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    uint32_t* run = s_run[warp];
+    unsigned long long* pos = s_pos + warp * 1024;
+    const uint32_t lt = lanemask_lt();
     for (uint32_t chunk = blockIdx.x * 8 + warp; chunk < a.nchunks; chunk += gridDim.x * 8) {
-#pragma unroll 8
-        for (int i = 0; i < 32; ++i) run[lane * 32 + i] = 0;
+        const unsigned long long* base = a.base + uint64_t(chunk) * 1024;
+        for (uint32_t q = lane; q < 1024; q += 32) pos[q] = a.qoff[q] + base[q];
         __syncwarp();
         const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
-        const unsigned long long* base = a.base + uint64_t(chunk) * 1024;
         for (uint32_t b = a.chunk_head[chunk]; b != kNoBlock; b = a.blk_next[b]) {
             const uint32_t cnt = a.blk_count[b];
             const uint32_t* rec = a.rec + uint64_t(b) * kRecBlock;
-            for (uint32_t i = 0; i < cnt; i += 32) {
-                const bool active = i + lane < cnt;
-                const uint32_t r = active ? rec[i + lane] : 0u;
-                const uint32_t q = active ? (r & 1023u) : 0xFFFFFFFFu;
-                const uint32_t same = __match_any_sync(0xFFFFFFFFu, q);
-                const uint32_t rank = __popc(same & lanemask_lt());
-                uint32_t prev = 0;
-                if (active) {
-                    prev = run[q];
-                    const unsigned long long pos = a.qoff[q] + base[q] + prev + rank;
-                    if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(start + (r >> 10));
+            for (uint32_t i = 0; i < cnt; i += 128) {
+                // 4 groups of 32 records loaded together, then placed in order
+                uint32_t r[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const uint32_t j = i + 32 * g + lane;
+                    r[g] = j < cnt ? __ldcs(rec + j) : 0u;
                 }
-                __syncwarp();
-                if (active && rank == 0) run[q] = prev + __popc(same);
-                __syncwarp();
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    if (i + 32 * g >= cnt) break;
+                    const bool active = i + 32 * g + lane < cnt;
+                    const uint32_t q = active ? (r[g] & 1023u) : 0xFFFFFFFFu;
+                    const uint32_t same = __match_any_sync(0xFFFFFFFFu, q);
+                    const uint32_t rank = __popc(same & lt);
+                    unsigned long long p = 0;
+                    if (active) {
+                        p = pos[q];
+                        const unsigned long long at = p + rank;
+                        if (at < a.ids_cap) a.ids[at] = a.id_base + uint32_t(start + (r[g] >> 10));
+                    }
+                    __syncwarp();
+                    if (active && rank == 0) pos[q] = p + __popc(same);
+                    __syncwarp();
+                }
             }
         }
     }
@@ -389,11 +421,17 @@ void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st) {
 void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st) {
     if (a.n == 0 || a.nchunks == 0) return;
     const uint32_t blocks = (a.nchunks + 7) / 8;
-    vb_scatter_kernel<<<blocks, 256, 0, st>>>(a);
+    const int smem = 8 * 1024 * sizeof(unsigned long long);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(vb_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        configured = true;
+    }
+    vb_scatter_kernel<<<blocks, 256, smem, st>>>(a);
 }
 
 void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st) {
-    vb_chunk_scan_kernel<<<(a.nqp + 255) / 256, 256, 0, st>>>(a.chunk_counts, nchunks, a.nqp, a.base, a.total);
+    vb_chunk_scan_kernel<<<(a.nqp + 31) / 32, 1024, 0, st>>>(a.chunk_counts, nchunks, a.nqp, a.base, a.total);
     vb_query_scan_kernel<<<1, 1024, 0, st>>>(a.total, a.nqp, a.offsets, a.counts_all, a.qoff, q0);
 }
 
