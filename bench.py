@@ -343,6 +343,7 @@ def main():
             "queries_per_s": nq / (ms / 1e3),
             "hbm_gbs_per_gpu": roofline["achieved"],
             "roofline": roofline,
+            "smem_roofline": smem_roofline(binfo, prof, n, clocks.summary()),
             "columnar_scan_roofline": col_roof,
             "pass_profile": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in prof.items()},
             "paths_us_per_query": paths,
@@ -359,6 +360,25 @@ def main():
     if merge:
         dist.destroy_process_group()
     return 0
+
+
+def smem_roofline(binfo, prof, n, clocks):
+    """The resource that bounds the bit-sliced filter pass: shared-memory
+    wavefronts.  Algorithmic count per pass: one LDS.64 (2 wavefronts) per
+    tuple per union dimension (the (overlap, containment) table row word of
+    every lane); peak: 1 wavefront per cycle per SM at the SM clock measured
+    during the timed region (148 SMs)."""
+    if binfo["path"] != "vafile_batch" or not prof["scan"][1]:
+        return None
+    kb = binfo["max_union_dims"]
+    wavefronts = 2.0 * n * kb
+    launch_s = prof["scan"][0] / prof["scan"][1] / 1e3
+    mhz = clocks.get("sm_mhz") or 1965.0
+    peak = 148 * mhz * 1e6
+    achieved = wavefronts / launch_s
+    return {"resource": "shared-memory wavefronts (table rows)", "achieved": achieved, "peak": peak,
+            "unit": "wavefronts/s", "frac": achieved / peak, "algo_wavefronts_per_launch": wavefronts,
+            "sm_mhz": mhz}
 
 
 def roofline_of(path, prof, stats, n, nq, total_ids, peak, peak_kind):
