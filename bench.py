@@ -46,8 +46,8 @@ NQ = 1000
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-paths", action="store_true", help="skip the per-path cost table")
@@ -163,7 +163,9 @@ def run_reference(args):
         t0 = time.perf_counter()
         scan.search(lo[0], hi[0])
         per_q = time.perf_counter() - t0
-        q_per_step = max(1, min(args.queries, int(2.0 / max(per_q, 1e-6))))
+        # each step a bounded sample: <= 2 s, and the whole run <= ~2 minutes
+        step_budget = min(2.0, 120.0 / max(1, args.steps + args.warmup))
+        q_per_step = max(1, min(args.queries, int(step_budget / max(per_q, 1e-6))))
         # warmup
         qi = 0
         for _ in range(args.warmup):
