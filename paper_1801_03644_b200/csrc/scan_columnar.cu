@@ -21,10 +21,14 @@ namespace mdrq {
 namespace {
 
 constexpr int CS_THREADS = 256;
-constexpr int CS_G = 4;                            // float4 groups per thread
-constexpr int CS_WARP_TUPLES = 32 * 4 * CS_G;      // 512
+constexpr int CS_LANE_TUPLES = 16;                 // 64 contiguous bytes per lane and column
+constexpr int CS_WARP_TUPLES = 32 * CS_LANE_TUPLES;  // 512
 static_assert(CS_THREADS / 32 * CS_WARP_TUPLES == kColTile, "tile size");
 
+// Lane l of a warp owns tuples wbase + 16l .. +15: one 64-byte block per
+// column -- the HBM access granularity -- read as 4 x 16 B when any of its
+// 16 tuples is still alive and skipped otherwise, so the bytes requested
+// are exactly the blocks the dimension-at-a-time algorithm must touch.
 template <bool IDS>
 __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) {
     __shared__ uint32_t s_cnt[CS_THREADS / 32];
@@ -36,35 +40,27 @@ __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) 
     const uint32_t tile = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t wbase = uint64_t(tile) * kColTile + warp * CS_WARP_TUPLES;
-    const uint64_t base = wbase + lane * 4;
+    const uint64_t base = wbase + lane * CS_LANE_TUPLES;
 
-    uint32_t alive = 0xFFFFu;
-    if (uint64_t(tile + 1) * kColTile > a.n) {  // tail tile: mask tuples >= n
-        alive = 0;
-#pragma unroll
-        for (int g = 0; g < CS_G; ++g)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (base + g * 128 + j < a.n) alive |= 1u << (4 * g + j);
-    }
+    uint32_t alive = 0xFFFFu;   // bit j: tuple base + j
+    if (base + CS_LANE_TUPLES > a.n) alive = base >= a.n ? 0u : (1u << (a.n - base)) - 1u;
 
-    uint32_t nload = 0;  // 16-byte loads issued (skipped groups are not read)
+    uint32_t nload = 0;  // 64-byte blocks read (skipped blocks are not)
     for (uint32_t i = 0; i < k; ++i) {
         if (!__any_sync(0xFFFFFFFFu, alive)) break;  // whole warp rejected: skip the rest
         const DimPred p = P[i];
-        const uint32_t d = p.dim;
         const float lo = p.lo, hi = p.hi;
-        const float4* c = reinterpret_cast<const float4*>(a.cols + uint64_t(d) * a.stride + base);
-        float4 v[CS_G];
+        if (alive) {
+            const float4* c = reinterpret_cast<const float4*>(a.cols + uint64_t(p.dim) * a.stride + base);
+            float4 v[4];
 #pragma unroll
-        for (int g = 0; g < CS_G; ++g) nload += ((alive >> (4 * g)) & 0xFu) ? 1u : 0u;
+            for (int g = 0; g < 4; ++g) v[g] = ld_stream_f4(c + g);
+            uint32_t in = 0;
 #pragma unroll
-        for (int g = 0; g < CS_G; ++g)
-            if ((alive >> (4 * g)) & 0xFu) v[g] = ld_stream_f4(c + g * 32);
-#pragma unroll
-        for (int g = 0; g < CS_G; ++g)
-            if ((alive >> (4 * g)) & 0xFu)
-                alive &= (in_range4(v[g], lo, hi) << (4 * g)) | ~(0xFu << (4 * g));
+            for (int g = 0; g < 4; ++g) in |= in_range4(v[g], lo, hi) << (4 * g);
+            alive &= in;
+            ++nload;
+        }
     }
 
     const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, __popc(alive));
@@ -82,19 +78,14 @@ __global__ void __launch_bounds__(CS_THREADS) col_scan_kernel(const ScanArgs a) 
             ld += s_ld[w];
         }
         if (!IDS && t) partial_add(a, 0, t);
-        if (ld) partial_add(a, 1, 16ull * ld);
+        if (ld) partial_add(a, 1, 64ull * ld);
     }
     if (!IDS) return;
-    // ids mode: verdict bitmask (bit i of word w = tuple 32w+i) + chunk count;
-    // lanes 8s..8s+7 of group g own the 32 tuples of one mask word
-#pragma unroll
-    for (int g = 0; g < CS_G; ++g) {
-        uint32_t v = ((alive >> (4 * g)) & 0xFu) << (4 * (lane & 7u));
-        v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
-        v |= __shfl_xor_sync(0xFFFFFFFFu, v, 2);
-        v |= __shfl_xor_sync(0xFFFFFFFFu, v, 4);
-        if ((lane & 7u) == 0) a.mask[(wbase + g * 128) / 32 + (lane >> 3)] = v;
-    }
+    // ids mode: verdict bitmask (bit i of word w = tuple 32w+i) + chunk
+    // count; lanes 2s, 2s+1 hold the two halves of one mask word
+    uint32_t v = alive << (16 * (lane & 1u));
+    v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+    if ((lane & 1u) == 0) a.mask[base / 32] = v;
     if (lane == 0 && wc) atomicAdd(a.chunk_counts + wbase / kChunkTuples, wc);
 }
 
