@@ -76,6 +76,19 @@ struct BatchArgs {
 constexpr int kVaBatchMaxDims = 24;
 // table cells per dimension for a pass with kb union dims (fits 227 KB smem)
 __host__ __device__ constexpr uint32_t va_batch_cells(uint32_t kb) { return kb <= 12 ? 64u : 32u; }
+// Narrow unions (kb <= kVbPvDims) keep the exact values and query bounds in
+// shared memory and refine every overlap candidate exactly, so their table is
+// overlap-only: rows of dims (2p, 2p+1) at cell c are adjacent,
+// word (u, c, w) at ((u/2 * cells + c) * 2 + u%2) * 32 + w.  Their exact
+// bounds are [1024][va_batch_vdims(kb)] float2, padded with (-inf, +inf).
+// Wider unions use (overlap, containment) pairs [kb][cells][32][2] and refine
+// only the edge-cell candidates from global memory.
+constexpr uint32_t kVbPvDims = 8;
+__host__ __device__ constexpr bool va_batch_pv(uint32_t kb) { return kb <= kVbPvDims; }
+__host__ __device__ constexpr uint32_t va_batch_vdims(uint32_t kb) { return kb <= 4 ? 4u : 8u; }
+__host__ __device__ constexpr uint32_t va_batch_table_words(uint32_t kb, uint32_t cells) {
+    return va_batch_pv(kb) ? (kb + 1) / 2 * cells * 64 : kb * cells * 64;
+}
 struct VaBatchArgs {
     const uint8_t* codes;        // VA code planes [m][stride]
     const float* cols;           // exact columns [m][stride] (refinement)
@@ -86,8 +99,8 @@ struct VaBatchArgs {
     uint32_t shift;              // stored code >> shift = table cell
     uint32_t nqp;                // queries in this pass (<= 1024)
     const uint16_t* udims;       // [kb]
-    const uint32_t* tables;      // [kb][cells][32][2]: (overlap, containment) query-mask words
-    const float2* qbounds;       // [1024][kb] exact (lo, hi), +-inf where unconstrained
+    const uint32_t* tables;      // query-mask words, layout per va_batch_pv(kb) (above)
+    const float2* qbounds;       // [1024][kb or vdims] exact (lo, hi), +-inf where unconstrained
     uint32_t grid;               // CTAs (chunks = grid * warps)
     uint64_t chunk_tuples;       // tuples per chunk (multiple of 128, < 65536: u16 counters)
     uint32_t nchunks;            // ceil(n / chunk_tuples); warps stride over chunks

@@ -300,9 +300,10 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
         ps.table_off = b->vb_tables.size();
         ps.qb_off = b->vb_qb.size();
         b->vb_udims.insert(b->vb_udims.end(), ud.begin(), ud.end());
-        const size_t plane = size_t(ps.kb) * ps.cells * 32;
-        std::vector<uint32_t> tab(2 * plane, 0u);
-        std::vector<float2> qbv(size_t(1024) * ps.kb, make_float2(-INFINITY, INFINITY));
+        const bool pv = va_batch_pv(ps.kb);
+        const uint32_t qstride = pv ? va_batch_vdims(ps.kb) : ps.kb;
+        std::vector<uint32_t> tab(va_batch_table_words(ps.kb, ps.cells), 0u);
+        std::vector<float2> qbv(size_t(1024) * qstride, make_float2(-INFINITY, INFINITY));
         for (uint32_t qi = 0; qi < ps.nqp; ++qi) {
             const QueryDesc& qd = b->descs[q0 + qi];
             std::vector<int> lo_c(ps.kb, -1), hi_c(ps.kb, int(ps.cells)), elo(ps.kb, 0), ehi(ps.kb, 0);
@@ -319,7 +320,7 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
                     lo_c[u] = int(ps.cells);
                     hi_c[u] = -1;
                 }
-                qbv[size_t(qi) * ps.kb + u] = make_float2(p.lo, p.hi);
+                qbv[size_t(qi) * qstride + u] = make_float2(p.lo, p.hi);
             }
             const uint32_t w = qi >> 5, bit = 1u << (qi & 31);
             for (uint32_t u = 0; u < ps.kb; ++u)
@@ -328,6 +329,11 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
                     if (cons[u]) {
                         ov = int(c) >= lo_c[u] && int(c) <= hi_c[u];
                         su = ov && (int(c) > lo_c[u] || !elo[u]) && (int(c) < hi_c[u] || !ehi[u]);
+                    }
+                    if (pv) {
+                        // overlap only, rows of dim pairs adjacent (launch.h)
+                        if (ov) tab[((size_t(u / 2) * ps.cells + c) * 2 + u % 2) * 32 + w] |= bit;
+                        continue;
                     }
                     // interleaved (overlap, containment) words: [u][c][w][2]
                     const size_t idx = ((size_t(u) * ps.cells + c) * 32 + w) * 2;

@@ -6,26 +6,32 @@
 // (vafile.py:204-219).  Here one pass over the quantile-code byte planes
 // evaluates a whole batch:
 //
-//   * per union dimension u and coarse cell c the host builds two 1024-bit
-//     query masks: OV[u][c] (queries whose box overlaps cell c in dimension
-//     u) and SU[u][c] (queries that contain cell c entirely).  Word w of a
-//     mask covers queries 32w .. 32w+31 and lives in shared memory at
-//     [u][c][w], so a warp whose LANE w owns word w reads a whole 1024-bit
-//     row with one conflict-free LDS.32 per lane;
+//   * per union dimension u and coarse cell c the host builds a 1024-bit
+//     query mask OV[u][c] (queries whose box overlaps cell c in dimension u)
+//     and, for unions wider than 8 dims, SU[u][c] (queries that contain cell
+//     c entirely).  Word w of a mask covers queries 32w .. 32w+31 and lives
+//     in shared memory, so a warp whose LANE w owns word w reads a whole
+//     1024-bit row with one conflict-free LDS per lane;
 //   * the warp walks its chunk of tuples in order; per tuple it ANDs the rows
-//     of the tuple's cells: maybe = AND_u OV, sure = AND_u SU.  maybe & ~sure
-//     are (tuple, query) pairs in an edge cell -- refined against the exact
-//     float32 columns (broadcast loads of the tuple's values);
-//   * matches are counted per query (count mode), per (chunk, query) (first
-//     pass of ids mode) or written as ids (second pass) at
-//     qoff[q] + base[chunk][q] + running count -- ascending per query
-//     because every warp owns one contiguous tuple range.
+//     of the tuple's cells: maybe = AND_u OV.  Narrow unions (<= 8 dims)
+//     refine every candidate in maybe exactly -- the block's float32 values
+//     are staged tuple-major in shared memory and the query bounds live
+//     there too, so a refinement is a few LDS.128; wider unions AND the SU
+//     rows as well and refine only maybe & ~sure (edge cells) from global;
+//   * matches are counted per query (mode 0), per (chunk, query) (mode 1),
+//     or, in ids mode, counted per (chunk, query) while (tuple, query)
+//     records are staged in tuple order (mode 3); a scan over the chunk
+//     counts then places every record at qoff[q] + base[chunk][q] + rank
+//     (vb_scatter_kernel) -- ascending per query because every warp owns one
+//     contiguous tuple range.  If the staging pool overflows, mode 2
+//     recomputes the pass writing the ids directly.
 //
 // The coarse cell of a tuple is its stored 8-bit quantile code shifted right
 // (the 2^tb-cell grid's boundaries are every 2^(8-tb)-th boundary of the
 // 256-cell grid, so code_tb = code_8 >> (8 - tb) exactly).  Soundness is the
-// single-query VA-file's (vafile.cu): cells strictly inside [code(lo),
-// code(hi)] need no refinement, edge cells are refined exactly.
+// single-query VA-file's (vafile.cu): a tuple outside a query's box in some
+// dimension has a cell outside [code(lo), code(hi)] there, so OV never drops
+// a match; cells strictly inside need no refinement, edge cells are refined.
 #include <utility>
 
 #include "launch.h"
@@ -43,17 +49,36 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 constexpr int VB_THREADS = 512;
 constexpr int VB_WARPS = VB_THREADS / 32;
 
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t r;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
+    return r;
+}
+
+__device__ __forceinline__ float f4_get(const float4& w, uint32_t i) {
+    return i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w;
+}
+
+// staged-value slot of float4 s in a warp's buffer: a bijection that only
+// permutes the low 3 bits, so the 8 lanes of a quarter-warp storing the same
+// (tuple-in-lane, half) land on 8 distinct 16-byte bank groups
+__device__ __forceinline__ uint32_t val_slot(uint32_t s) { return s ^ ((s >> 3) & 7u); }
+
 template <int MODE, int KB>
 __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
-    constexpr bool PV = KB <= 8;                   // exact values prefetched into registers
+    constexpr bool PV = va_batch_pv(KB);           // values + bounds in smem, overlap-only table
+    constexpr int KBV = PV ? int(va_batch_vdims(KB)) : KB;
+    constexpr int H = PV ? KBV / 4 : 1;            // float4 slots per staged tuple
     __shared__ uint32_t s_dim[KB];
-    uint32_t* s_end = sm + 2 * KB * K * 32;        // end of the [KB][K][32] x (ov, su) table
-    // narrow unions also keep the exact query bounds [1024][KB] in smem
-    float2* s_qb = reinterpret_cast<float2*>(s_end);
+    uint32_t* s_end = sm + va_batch_table_words(KB, K);
+    // PV: exact query bounds [1024][KBV/2] float4 (lo_u, hi_u, lo_u+1, hi_u+1)
+    // and every warp's staged block values [128 * H] float4
+    float4* s_qb = reinterpret_cast<float4*>(s_end);
+    float4* s_val = s_qb + (PV ? 1024 * KBV / 2 : 0);
     // MODE 0: u32 [1024] shared by the CTA ; MODE 1/2/3: u16 [warps][1024]
-    uint32_t* s_cnt32 = s_end + (PV ? KB * 1024 * 2 : 0);
+    uint32_t* s_cnt32 = reinterpret_cast<uint32_t*>(s_val + (PV ? VB_WARPS * 128 * H : 0));
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_cnt32);
 
     // the recount pass only runs when the single-pass staging overflowed
@@ -62,12 +87,12 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.tables);
         uint4* dst = reinterpret_cast<uint4*>(sm);
-        const uint32_t n4 = 2 * KB * K * 32 / 4;
+        const uint32_t n4 = va_batch_table_words(KB, K) / 4;
         for (uint32_t i = threadIdx.x; i < n4; i += VB_THREADS) dst[i] = src[i];
         if constexpr (PV) {
             const uint4* qsrc = reinterpret_cast<const uint4*>(a.qbounds);
             uint4* qdst = reinterpret_cast<uint4*>(s_qb);
-            for (uint32_t i = threadIdx.x; i < KB * 1024 / 2; i += VB_THREADS) qdst[i] = qsrc[i];
+            for (uint32_t i = threadIdx.x; i < 1024 * KBV / 2; i += VB_THREADS) qdst[i] = qsrc[i];
         }
         if (MODE == 0)
             for (uint32_t i = threadIdx.x; i < 1024; i += VB_THREADS) s_cnt32[i] = 0;
@@ -76,12 +101,14 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     __syncthreads();
 
     const uint32_t shift = a.shift;
-    const float2* __restrict__ qb = PV ? s_qb : a.qbounds;     // [1024][KB]
-    // rows interleave (overlap, containment) words: entry (u, c, w) is the
-    // uint2 at byte (u*K + c)*256 + w*8; lane w reads its entry of a row.
-    // 32-bit shared-window address of the lane's column of the table.
-    const uint32_t s_tab32 = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) + lane * 8;
-    uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 1/2: this warp's chunk counters
+    // 32-bit shared-window address of the lane's column of the table:
+    //   PV: overlap word (u, c, w) at byte (u/2*K + c)*256 + (u%2)*128 + w*4
+    //   else (overlap, containment) uint2 (u, c, w) at byte (u*K + c)*256 + w*8
+    // so the cell byte moved to bits 8..15 by one PRMT is the row offset.
+    const uint32_t s_tab32 = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) + lane * (PV ? 4 : 8);
+    uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 1/2/3: this warp's chunk counters
+    float4* wval = s_val + warp * 128 * H;         // PV: this warp's staged values
+    const uint32_t lt = lanemask_lt();
 
     for (uint32_t chunk = blockIdx.x * VB_WARPS + warp; chunk < a.nchunks; chunk += gridDim.x * VB_WARPS) {
         const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
@@ -110,12 +137,28 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
         if (start < end) load_block(start);
         for (uint64_t t0 = start; t0 < end; t0 += 128) {
             uint32_t cw[KB];
-            float4 vv[PV ? KB : 1];
 #pragma unroll
-            for (int u = 0; u < KB; ++u) {
+            for (int u = 0; u < KB; ++u)
                 // table cells of the 4 tuples of every word: (code >> shift) per byte
                 cw[u] = (cw_n[u] >> shift) & (0x01010101u * (K - 1));
-                if constexpr (PV) vv[u] = vv_n[u];
+            if constexpr (PV) {
+                // stage the block's exact values tuple-major (tuple t, dims
+                // 4h..4h+3 in float4 slot t*H + h, zero-padded dims) so a
+                // refinement reads a tuple with H broadcast LDS.128
+                __syncwarp();
+#pragma unroll
+                for (uint32_t jj = 0; jj < 4; ++jj)
+#pragma unroll
+                    for (int h = 0; h < H; ++h) {
+                        float c[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int u = 4 * h + e;
+                            c[e] = u < KB ? f4_get(vv_n[u < KB ? u : 0], jj) : 0.0f;
+                        }
+                        wval[val_slot((4 * lane + jj) * H + h)] = make_float4(c[0], c[1], c[2], c[3]);
+                    }
+                __syncwarp();
             }
             if (t0 + 128 < end) load_block(t0 + 128);
             const uint32_t jmax = uint32_t(end - t0 < 128 ? end - t0 : 128);
@@ -123,8 +166,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 uint32_t x[KB];
 #pragma unroll
                 for (int u = 0; u < KB; ++u) x[u] = __shfl_sync(0xFFFFFFFFu, cw[u], j4 >> 2);
-                // filter the 4 tuples of this step first (4 x 2 x KB independent
-                // LDS in flight), then refine / emit them in order
+                // filter the 4 tuples of this step first (independent LDS in
+                // flight), then refine / emit them in order
                 uint32_t ov4[4], su4[4];
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) ov4[jj] = su4[jj] = 0xFFFFFFFFu;
@@ -132,64 +175,108 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 for (int u = 0; u < KB; u += 2)
 #pragma unroll
                     for (uint32_t jj = 0; jj < 4; ++jj) {
-                        // byte offset of row (u, cell) = cell * 256 (+ u*K*256 as an
-                        // immediate): one PRMT moves the cell byte of tuple jj to bits
-                        // 8..15 (cells are pre-masked to < K); two dims per 3-input AND
+                        // one PRMT moves the cell byte of tuple jj to bits 8..15
+                        // (cells are pre-masked to < K); two dims per 3-input AND
                         const uint32_t ca = __byte_perm(x[u], 0u, 0x4404u | (jj << 4));
-                        const uint2 ea = lds64(s_tab32 + ca + u * K * 256);
-                        if (u + 1 < KB) {
-                            const uint32_t cb = __byte_perm(x[u + 1], 0u, 0x4404u | (jj << 4));
-                            const uint2 eb = lds64(s_tab32 + cb + (u + 1) * K * 256);
-                            ov4[jj] = ov4[jj] & ea.x & eb.x;
-                            su4[jj] = su4[jj] & ea.y & eb.y;
+                        if constexpr (PV) {
+                            const uint32_t ea = lds32(s_tab32 + ca + (u / 2) * K * 256);
+                            if (u + 1 < KB) {
+                                const uint32_t cb = __byte_perm(x[u + 1], 0u, 0x4404u | (jj << 4));
+                                const uint32_t eb = lds32(s_tab32 + cb + (u / 2) * K * 256 + 128);
+                                ov4[jj] = ov4[jj] & ea & eb;
+                            } else {
+                                ov4[jj] &= ea;
+                            }
                         } else {
-                            ov4[jj] &= ea.x;
-                            su4[jj] &= ea.y;
+                            const uint2 ea = lds64(s_tab32 + ca + u * K * 256);
+                            if (u + 1 < KB) {
+                                const uint32_t cb = __byte_perm(x[u + 1], 0u, 0x4404u | (jj << 4));
+                                const uint2 eb = lds64(s_tab32 + cb + (u + 1) * K * 256);
+                                ov4[jj] = ov4[jj] & ea.x & eb.x;
+                                su4[jj] = su4[jj] & ea.y & eb.y;
+                            } else {
+                                ov4[jj] &= ea.x;
+                                su4[jj] &= ea.y;
+                            }
                         }
                     }
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) {
                     if (j4 + jj >= jmax) break;
                     const uint64_t t = t0 + j4 + jj;
-                    uint32_t hits = su4[jj];
-                    uint32_t r = ov4[jj] & ~su4[jj];
-                    if (__any_sync(0xFFFFFFFFu, r)) {
-                        // exact refinement of (tuple, query) pairs in an edge cell
-                        float v[KB];
+                    uint32_t hits;
+                    if constexpr (PV) {
+                        // every overlap candidate is refined exactly
+                        hits = 0;
+                        uint32_t r = ov4[jj];
+                        if (__any_sync(0xFFFFFFFFu, r)) {
+                            float v[4 * H];
+                            const uint32_t s0 = (j4 + jj) * H;
 #pragma unroll
-                        for (int u = 0; u < KB; ++u) {
-                            if constexpr (PV) {
-                                const float4 w = vv[u];
-                                const float c = jj == 0 ? w.x : jj == 1 ? w.y : jj == 2 ? w.z : w.w;
-                                v[u] = __shfl_sync(0xFFFFFFFFu, c, j4 >> 2);
-                            } else {
-                                v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
+                            for (int h = 0; h < H; ++h) {
+                                const float4 w = wval[val_slot(s0 + h)];
+                                v[4 * h] = w.x;
+                                v[4 * h + 1] = w.y;
+                                v[4 * h + 2] = w.z;
+                                v[4 * h + 3] = w.w;
+                            }
+                            while (r) {
+                                const int b = __ffs(r) - 1;
+                                r &= r - 1;
+                                const float4* qq = s_qb + (lane * 32 + b) * (KBV / 2);
+                                bool ok = true;
+#pragma unroll
+                                for (int u2 = 0; u2 < KBV / 2; ++u2) {
+                                    const float4 bb = qq[u2];
+                                    ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
+                                         (v[2 * u2 + 1] <= bb.w);
+                                }
+                                hits |= uint32_t(ok) << b;
                             }
                         }
-                        while (r) {
-                            const int b = __ffs(r) - 1;
-                            r &= r - 1;
-                            const float2* qq = qb + (lane * 32 + b) * KB;
-                            bool ok = true;
+                    } else {
+                        // cells strictly inside are sure; edge-cell pairs are
+                        // refined against the exact columns
+                        hits = su4[jj];
+                        uint32_t r = ov4[jj] & ~su4[jj];
+                        if (__any_sync(0xFFFFFFFFu, r)) {
+                            float v[KB];
 #pragma unroll
-                            for (int u = 0; u < KB; ++u) {
-                                const float2 bb = qq[u];
-                                ok = ok && (bb.x <= v[u]) && (v[u] <= bb.y);
+                            for (int u = 0; u < KB; ++u) v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
+                            while (r) {
+                                const int b = __ffs(r) - 1;
+                                r &= r - 1;
+                                const float2* qq = a.qbounds + (lane * 32 + b) * KB;
+                                bool ok = true;
+#pragma unroll
+                                for (int u = 0; u < KB; ++u) {
+                                    const float2 bb = qq[u];
+                                    ok = ok && (bb.x <= v[u]) && (v[u] <= bb.y);
+                                }
+                                if (ok) hits |= 1u << b;
                             }
-                            if (ok) hits |= 1u << b;
                         }
                     }
                     if (MODE == 3) {
                         // stage (tuple offset, query) records in tuple order:
-                        // warp prefix of the per-lane hit counts
+                        // warp prefix of the per-lane hit counts (a ballot when
+                        // no lane has more than one hit, the common case)
                         const uint32_t cnt = __popc(hits);
-                        const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, cnt);
-                        if (tot) {
-                            uint32_t incl = cnt;
+                        const uint32_t anyb = __ballot_sync(0xFFFFFFFFu, cnt != 0);
+                        if (anyb) {
+                            uint32_t excl, tot;
+                            if (__ballot_sync(0xFFFFFFFFu, cnt > 1) == 0) {
+                                excl = __popc(anyb & lt);
+                                tot = __popc(anyb);
+                            } else {
+                                uint32_t incl = cnt;
 #pragma unroll
-                            for (int o = 1; o < 32; o <<= 1) {
-                                const uint32_t x2 = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                                if (lane >= uint32_t(o)) incl += x2;
+                                for (int o = 1; o < 32; o <<= 1) {
+                                    const uint32_t x2 = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                                    if (lane >= uint32_t(o)) incl += x2;
+                                }
+                                excl = incl - cnt;
+                                tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
                             }
                             if (blk != kNoBlock - 1 && (blk == kNoBlock || fill + tot > kRecBlock)) {
                                 uint32_t nb = 0;
@@ -211,7 +298,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             }
                             // one loop writes the records and counts them per (chunk, query)
                             const bool stage_on = blk != kNoBlock - 1;
-                            uint32_t* dst = a.rec + uint64_t(stage_on ? blk : 0) * kRecBlock + fill + (incl - cnt);
+                            uint32_t* dst = a.rec + uint64_t(stage_on ? blk : 0) * kRecBlock + fill + excl;
                             const uint32_t trel = uint32_t(t - start) << 10;
                             while (hits) {
                                 const int b = __ffs(hits) - 1;
@@ -229,7 +316,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         const uint32_t q = lane * 32 + b;
                         if (MODE == 0) {
                             atomicAdd(&s_cnt32[q], 1u);
-                        } else if (MODE == 1 || MODE == 3) {
+                        } else if (MODE == 1) {
                             wcnt[q] += 1;
                         } else {
                             const unsigned long long pos = a.qoff[q] + base[q] + wcnt[q];
@@ -259,7 +346,6 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     }
 }
 
-// per-query exclusive scan over chunks: base[c][q], total[q]
 // per-query exclusive scan over chunks: base[c][q], total[q].  One CTA per
 // 32 queries: thread (s, ql) sums slice s of the chunks for query ql, a scan
 // over the 32 slice sums in smem, then every thread writes its slice's bases.
@@ -397,8 +483,10 @@ void dispatch(const VaBatchArgs& a, cudaStream_t st, std::integer_sequence<int, 
 }  // namespace
 
 size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
-    const size_t qbounds = kb <= 8 ? size_t(kb) * 1024 * 8 : 0;   // PV kernels keep the bounds in smem
-    return size_t(2) * kb * cells * 32 * 4 + qbounds + (mode == 0 ? 1024 * 4 : 1024 * 2 * VB_WARPS);
+    // PV kernels keep the bounds [1024][vdims] float2 and the staged values
+    // [warps][128][vdims] float in smem
+    const size_t pv = va_batch_pv(kb) ? size_t(va_batch_vdims(kb)) * (1024 * 8 + VB_WARPS * 128 * 4) : 0;
+    return size_t(va_batch_table_words(kb, cells)) * 4 + pv + (mode == 0 ? 1024 * 4 : 1024 * 2 * VB_WARPS);
 }
 
 int va_batch_max_dims() { return kVaBatchMaxDims; }

@@ -3,6 +3,8 @@
 # is preceded by the same command line exiting 0 without ncu.
 set -u
 OUT=gpurun_out
+python bench.py > $OUT/bench_default.log 2> $OUT/bench_default.err
+echo "bench=$?" >> $OUT/rc.txt
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-paths"
 $B > $OUT/plain.log 2>&1
 echo "plain=$?" >> $OUT/rc.txt
@@ -10,8 +12,12 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches.csv $B > $OUT/ncu_launches.log 2>&1
 echo "launches=$?" >> $OUT/rc.txt
 timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:va_batch_kernel -c 2 -o $OUT/prof_vab $B > $OUT/ncu_vab.log 2>&1
+    -k regex:"va_batch_kernel|vb_scatter" -c 3 -o $OUT/prof_vab $B > $OUT/ncu_vab.log 2>&1
 echo "vab=$?" >> $OUT/rc.txt
 timeout 1200 ncu --set full --clock-control none --import-source on \
     -k regex:col_scan_kernel -s 10 -c 1 -o $OUT/prof_col $B > $OUT/ncu_col.log 2>&1
 echo "col=$?" >> $OUT/rc.txt
+P="python tools/probe_path.py rowwise count 3"
+$P > $OUT/probe_row.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on \
+    -k regex:row_scan_kernel -s 1 -c 1 -o $OUT/prof_row $P > $OUT/ncu_row.log 2>&1
+echo "row=$?" >> $OUT/rc.txt
