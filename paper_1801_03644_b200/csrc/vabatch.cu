@@ -40,20 +40,8 @@ namespace mdrq {
 
 namespace {
 
-__device__ __forceinline__ uint2 lds64(uint32_t addr) {
-    uint2 r;
-    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr));
-    return r;
-}
-
 constexpr int VB_THREADS = 512;
 constexpr int VB_WARPS = VB_THREADS / 32;
-
-__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
-    uint32_t r;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
-    return r;
-}
 
 __device__ __forceinline__ float f4_get(const float4& w, uint32_t i) {
     return i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w;
@@ -101,11 +89,13 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     __syncthreads();
 
     const uint32_t shift = a.shift;
-    // 32-bit shared-window address of the lane's column of the table:
+    // byte offset of the lane's word in a table row:
     //   PV: overlap word (u, c, w) at byte (u/2*K + c)*256 + (u%2)*128 + w*4
     //   else (overlap, containment) uint2 (u, c, w) at byte (u*K + c)*256 + w*8
-    // so the cell byte moved to bits 8..15 by one PRMT is the row offset.
-    const uint32_t s_tab32 = static_cast<uint32_t>(__cvta_generic_to_shared(sm)) + lane * (PV ? 4 : 8);
+    // One PRMT builds (cell << 8) | lane offset from the code word; the rest
+    // is an immediate.
+    const uint32_t lane_off = lane * (PV ? 4 : 8);
+    const char* s_tab = reinterpret_cast<const char*>(sm);
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 1/2/3: this warp's chunk counters
     float4* wval = s_val + warp * 128 * H;         // PV: this warp's staged values
     const uint32_t lt = lanemask_lt();
@@ -175,23 +165,25 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 for (int u = 0; u < KB; u += 2)
 #pragma unroll
                     for (uint32_t jj = 0; jj < 4; ++jj) {
-                        // one PRMT moves the cell byte of tuple jj to bits 8..15
-                        // (cells are pre-masked to < K); two dims per 3-input AND
-                        const uint32_t ca = __byte_perm(x[u], 0u, 0x4404u | (jj << 4));
+                        // byte 0 = lane offset, byte 1 = cell of tuple jj (cells
+                        // are pre-masked to < K); two dims per 3-input AND
+                        const uint32_t sel = 0x5504u | (jj << 4);
+                        const uint32_t ca = __byte_perm(x[u], lane_off, sel);
                         if constexpr (PV) {
-                            const uint32_t ea = lds32(s_tab32 + ca + (u / 2) * K * 256);
+                            const uint32_t ea = *reinterpret_cast<const uint32_t*>(s_tab + ca + (u / 2) * K * 256);
                             if (u + 1 < KB) {
-                                const uint32_t cb = __byte_perm(x[u + 1], 0u, 0x4404u | (jj << 4));
-                                const uint32_t eb = lds32(s_tab32 + cb + (u / 2) * K * 256 + 128);
+                                const uint32_t cb = __byte_perm(x[u + 1], lane_off, sel);
+                                const uint32_t eb =
+                                    *reinterpret_cast<const uint32_t*>(s_tab + cb + (u / 2) * K * 256 + 128);
                                 ov4[jj] = ov4[jj] & ea & eb;
                             } else {
                                 ov4[jj] &= ea;
                             }
                         } else {
-                            const uint2 ea = lds64(s_tab32 + ca + u * K * 256);
+                            const uint2 ea = *reinterpret_cast<const uint2*>(s_tab + ca + u * K * 256);
                             if (u + 1 < KB) {
-                                const uint32_t cb = __byte_perm(x[u + 1], 0u, 0x4404u | (jj << 4));
-                                const uint2 eb = lds64(s_tab32 + cb + (u + 1) * K * 256);
+                                const uint32_t cb = __byte_perm(x[u + 1], lane_off, sel);
+                                const uint2 eb = *reinterpret_cast<const uint2*>(s_tab + cb + (u + 1) * K * 256);
                                 ov4[jj] = ov4[jj] & ea.x & eb.x;
                                 su4[jj] = su4[jj] & ea.y & eb.y;
                             } else {
@@ -200,45 +192,53 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             }
                         }
                     }
+                // warp-uniform mask of the step's tuples with any candidate
+                // (overlap covers the sure matches); only those are refined
+                // and emitted, in tuple order
+                uint32_t nib = 0;
 #pragma unroll
-                for (uint32_t jj = 0; jj < 4; ++jj) {
-                    if (j4 + jj >= jmax) break;
+                for (uint32_t jj = 0; jj < 4; ++jj) nib |= uint32_t(ov4[jj] != 0u) << jj;
+                uint32_t tm = __reduce_or_sync(0xFFFFFFFFu, nib);
+                if (j4 + 4 > jmax) tm &= (1u << (jmax - j4)) - 1u;
+                while (tm) {
+                    const uint32_t jj = __ffs(tm) - 1;
+                    tm &= tm - 1;
+                    const uint32_t ovw = jj == 0 ? ov4[0] : jj == 1 ? ov4[1] : jj == 2 ? ov4[2] : ov4[3];
                     const uint64_t t = t0 + j4 + jj;
                     uint32_t hits;
                     if constexpr (PV) {
                         // every overlap candidate is refined exactly
                         hits = 0;
-                        uint32_t r = ov4[jj];
-                        if (__any_sync(0xFFFFFFFFu, r)) {
-                            float v[4 * H];
-                            const uint32_t s0 = (j4 + jj) * H;
+                        uint32_t r = ovw;
+                        float v[4 * H];
+                        const uint32_t s0 = (j4 + jj) * H;
 #pragma unroll
-                            for (int h = 0; h < H; ++h) {
-                                const float4 w = wval[val_slot(s0 + h)];
-                                v[4 * h] = w.x;
-                                v[4 * h + 1] = w.y;
-                                v[4 * h + 2] = w.z;
-                                v[4 * h + 3] = w.w;
-                            }
-                            while (r) {
-                                const int b = __ffs(r) - 1;
-                                r &= r - 1;
-                                const float4* qq = s_qb + (lane * 32 + b) * (KBV / 2);
-                                bool ok = true;
+                        for (int h = 0; h < H; ++h) {
+                            const float4 w = wval[val_slot(s0 + h)];
+                            v[4 * h] = w.x;
+                            v[4 * h + 1] = w.y;
+                            v[4 * h + 2] = w.z;
+                            v[4 * h + 3] = w.w;
+                        }
+                        while (r) {
+                            const int b = __ffs(r) - 1;
+                            r &= r - 1;
+                            const float4* qq = s_qb + (lane * 32 + b) * (KBV / 2);
+                            bool ok = true;
 #pragma unroll
-                                for (int u2 = 0; u2 < KBV / 2; ++u2) {
-                                    const float4 bb = qq[u2];
-                                    ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
-                                         (v[2 * u2 + 1] <= bb.w);
-                                }
-                                hits |= uint32_t(ok) << b;
+                            for (int u2 = 0; u2 < KBV / 2; ++u2) {
+                                const float4 bb = qq[u2];
+                                ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
+                                     (v[2 * u2 + 1] <= bb.w);
                             }
+                            hits |= uint32_t(ok) << b;
                         }
                     } else {
                         // cells strictly inside are sure; edge-cell pairs are
                         // refined against the exact columns
-                        hits = su4[jj];
-                        uint32_t r = ov4[jj] & ~su4[jj];
+                        const uint32_t suw = jj == 0 ? su4[0] : jj == 1 ? su4[1] : jj == 2 ? su4[2] : su4[3];
+                        hits = suw;
+                        uint32_t r = ovw & ~suw;
                         if (__any_sync(0xFFFFFFFFu, r)) {
                             float v[KB];
 #pragma unroll
