@@ -115,11 +115,16 @@ struct VaBatchArgs {
     uint64_t ids_cap;
     uint32_t id_base;
     // single-pass ids (mode 3): (tuple offset << 10 | query) records staged in
-    // linked 1024-record blocks per chunk, scattered into place afterwards
+    // 1024-record blocks allocated from a pool; each block is tagged with its
+    // chunk and its ordinal in the chunk, and a block-list kernel puts the
+    // pool in chunk order before the scatter
     uint32_t* rec;               // [max_blocks][kRecBlock]
-    uint32_t* blk_next;          // [max_blocks]
-    uint32_t* blk_count;         // [max_blocks]
-    uint32_t* chunk_head;        // [chunks], 0xFFFFFFFF = no records
+    uint32_t* blk_count;         // [max_blocks] records in the block
+    uint32_t* blk_chunk;         // [max_blocks] chunk of the block
+    uint32_t* blk_seq;           // [max_blocks] ordinal of the block within its chunk
+    uint32_t* chunk_nblk;        // [chunks] staged blocks of the chunk
+    uint32_t* chunk_first;       // [chunks] exclusive scan of chunk_nblk
+    uint32_t* blk_list;          // [max_blocks] block ids in (chunk, ordinal) order
     uint32_t* cursor;            // block allocator
     uint32_t* overflow;          // set when the staging pool ran out (mode 2 then runs)
     uint32_t max_blocks;
@@ -133,6 +138,7 @@ uint32_t va_batch_warps();
 void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st);
 void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st);
 void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st);
+void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st);
 
 constexpr int kColTile = 4096;     // tuples per CTA tile, single-query columnar
 constexpr int kVaTile = 8192;      // tuples per CTA tile, VA-file filter

@@ -207,7 +207,8 @@ struct mdrq_store {
     DBuf<uint32_t> vb_chunk_counts;
     DBuf<unsigned long long> vb_base, vb_total, vb_qoff;
     // single-pass ids staging (linked record blocks), grown when a pass overflows
-    DBuf<uint32_t> vb_rec, vb_blk_next, vb_blk_count, vb_chunk_head, vb_flags;  // flags: cursor, overflow
+    DBuf<uint32_t> vb_rec, vb_blk_count, vb_blk_chunk, vb_blk_seq, vb_blk_list;
+    DBuf<uint32_t> vb_chunk_nblk, vb_chunk_first, vb_flags;  // flags: cursor, overflow
     uint32_t vb_max_blocks = 1u << 16;   // 64K blocks x 1024 records x 4 B = 256 MB
     DBuf<uint32_t> ids;              // result pool
     uint64_t last_total = 0;
@@ -608,14 +609,20 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.ids_cap = s->ids.p ? s->ids.cap : 0;
     a.id_base = s->id_base;
     s->vb_rec.reserve(size_t(s->vb_max_blocks) * kRecBlock);
-    s->vb_blk_next.reserve(s->vb_max_blocks);
     s->vb_blk_count.reserve(s->vb_max_blocks);
-    s->vb_chunk_head.reserve(chunks);
+    s->vb_blk_chunk.reserve(s->vb_max_blocks);
+    s->vb_blk_seq.reserve(s->vb_max_blocks);
+    s->vb_blk_list.reserve(s->vb_max_blocks);
+    s->vb_chunk_nblk.reserve(chunks);
+    s->vb_chunk_first.reserve(chunks);
     s->vb_flags.reserve(2);
     a.rec = s->vb_rec.p;
-    a.blk_next = s->vb_blk_next.p;
     a.blk_count = s->vb_blk_count.p;
-    a.chunk_head = s->vb_chunk_head.p;
+    a.blk_chunk = s->vb_blk_chunk.p;
+    a.blk_seq = s->vb_blk_seq.p;
+    a.blk_list = s->vb_blk_list.p;
+    a.chunk_nblk = s->vb_chunk_nblk.p;
+    a.chunk_first = s->vb_chunk_first.p;
     a.cursor = s->vb_flags.p;
     a.overflow = s->vb_flags.p + 1;
     a.max_blocks = s->vb_max_blocks;
@@ -710,19 +717,20 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profil
                 launches += 1;
             } else {
                 // single pass: filter + per-chunk counts + staged records,
-                // scans, scatter; the recount pass (mode 2) only works when
-                // the staging pool overflowed (it checks the flag on device)
+                // scans, block list, scatter; the recount pass (mode 2) only
+                // works when the staging pool overflowed (it checks the flag
+                // on device)
                 mark(3, 0);
-                CK(cudaMemsetAsync(va.chunk_head, 0xFF, sizeof(uint32_t) * va.nchunks, st));
                 CK(cudaMemsetAsync(va.cursor, 0, 2 * sizeof(uint32_t), st));
                 mark(0, 1);
                 launch_va_batch(va, 3, st);
-                mark(1, 2);
+                mark(1, 3);
                 launch_va_batch_scans(va, va.nchunks, ps.q0, st);
+                launch_va_batch_block_list(va, st);
                 mark(2, 2);
                 launch_va_batch_scatter(va, st);
                 launch_va_batch(va, 2, st);
-                launches += 5;
+                launches += 6;
             }
         }
     } else if (path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
@@ -766,7 +774,7 @@ uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
         uint32_t l = 0;
         bool single = false;
         for (const VbPass& ps : b->vb_passes) {
-            l += ps.fallback ? ps.nqp * (ids ? 3 : 1) : (ids ? 5 : 1);
+            l += ps.fallback ? ps.nqp * (ids ? 3 : 1) : (ids ? 6 : 1);
             single |= ps.fallback;
         }
         return l + (single ? 1 : 0);
@@ -801,8 +809,10 @@ uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
             // correct): give the next passes twice the pool
             s->vb_max_blocks *= 2;
             s->vb_rec.release();
-            s->vb_blk_next.release();
             s->vb_blk_count.release();
+            s->vb_blk_chunk.release();
+            s->vb_blk_seq.release();
+            s->vb_blk_list.release();
         }
         if (total <= (s->ids.p ? s->ids.cap : 0)) {
             s->last_total = total;

@@ -32,6 +32,7 @@
 // single-query VA-file's (vafile.cu): a tuple outside a query's box in some
 // dimension has a cell outside [code(lo), code(hi)] there, so OV never drops
 // a match; cells strictly inside need no refinement, edge cells are refined.
+#include <algorithm>
 #include <utility>
 
 #include "launch.h"
@@ -109,7 +110,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             for (int i = 0; i < 32; ++i) wcnt[lane * 32 + i] = 0;
         }
         const unsigned long long* __restrict__ base = MODE == 2 ? a.base + uint64_t(chunk) * 1024 : nullptr;
-        uint32_t blk = kNoBlock, fill = 0;   // MODE 3: current staging block of this chunk
+        // MODE 3: current staging block of this chunk, its fill, blocks so far
+        uint32_t blk = kNoBlock, fill = 0, nblk = 0;
 
         // software pipeline: the codes (and, for narrow unions, the exact
         // values) of the next 128-tuple block are loaded while this block is
@@ -285,15 +287,14 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                                     if (nb >= a.max_blocks) {
                                         atomicExch(a.overflow, 1u);
                                         nb = kNoBlock - 1;   // stop staging this chunk
+                                    } else {
+                                        a.blk_chunk[nb] = chunk;
+                                        a.blk_seq[nb] = nblk;
                                     }
-                                    if (blk == kNoBlock)
-                                        a.chunk_head[chunk] = nb;
-                                    else {
-                                        a.blk_count[blk] = fill;
-                                        a.blk_next[blk] = nb;
-                                    }
+                                    if (blk != kNoBlock) a.blk_count[blk] = fill;
                                 }
                                 blk = __shfl_sync(0xFFFFFFFFu, nb, 0);
+                                nblk += blk != kNoBlock - 1;
                                 fill = 0;
                             }
                             // one loop writes the records and counts them per (chunk, query)
@@ -327,9 +328,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 }
             }
         }
-        if (MODE == 3 && lane == 0 && blk < kNoBlock - 1) {
-            a.blk_count[blk] = fill;
-            a.blk_next[blk] = kNoBlock;
+        if (MODE == 3 && lane == 0) {
+            if (blk < kNoBlock - 1) a.blk_count[blk] = fill;
+            a.chunk_nblk[chunk] = nblk;
         }
         if (MODE == 1 || MODE == 3) {
             __syncwarp();
@@ -381,19 +382,16 @@ __global__ void __launch_bounds__(1024) vb_chunk_scan_kernel(const uint32_t* __r
     }
 }
 
-// exclusive scan of the pass's query totals, chained on offsets[q0]
-__global__ void __launch_bounds__(1024) vb_query_scan_kernel(const unsigned long long* __restrict__ total, uint32_t nqp,
-                                                             unsigned long long* offsets, unsigned long long* counts,
-                                                             unsigned long long* qoff, uint32_t q0) {
-    __shared__ unsigned long long s_w[32];
-    const uint32_t q = threadIdx.x, lane = q & 31u, warp = q >> 5;
-    const unsigned long long v = q < nqp ? total[q] : 0ull;
+// exclusive prefix of v over a 1024-thread CTA (s_w: 32 scratch words)
+__device__ __forceinline__ unsigned long long cta_scan_excl(unsigned long long v, unsigned long long* s_w) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     unsigned long long incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= uint32_t(o)) incl += t;
     }
+    __syncthreads();
     if (lane == 31) s_w[warp] = incl;
     __syncthreads();
     if (warp == 0) {
@@ -407,59 +405,211 @@ __global__ void __launch_bounds__(1024) vb_query_scan_kernel(const unsigned long
         s_w[lane] = wi - w;
     }
     __syncthreads();
+    return s_w[warp] + incl - v;
+}
+
+// exclusive scan of the pass's query totals, chained on offsets[q0]; in ids
+// mode also the exclusive scan of the chunks' staged block counts (the
+// chunk offsets of the block list)
+__global__ void __launch_bounds__(1024) vb_query_scan_kernel(const unsigned long long* __restrict__ total, uint32_t nqp,
+                                                             unsigned long long* offsets, unsigned long long* counts,
+                                                             unsigned long long* qoff, uint32_t q0,
+                                                             const uint32_t* __restrict__ chunk_nblk,
+                                                             uint32_t* chunk_first, uint32_t nchunks) {
+    __shared__ unsigned long long s_w[32];
+    const uint32_t q = threadIdx.x;
+    const unsigned long long v = q < nqp ? total[q] : 0ull;
+    const unsigned long long excl = cta_scan_excl(v, s_w);
     const unsigned long long b0 = offsets[q0];
-    const unsigned long long excl = s_w[warp] + incl - v;
     if (q < nqp) {
         qoff[q] = b0 + excl;
         offsets[q0 + q + 1] = b0 + excl + v;
         counts[q0 + q] = v;
     }
+    if (!chunk_nblk) return;
+    const uint32_t per = (nchunks + 1023) / 1024;
+    const uint32_t c0 = min(nchunks, q * per), c1 = min(nchunks, c0 + per);
+    unsigned long long sum = 0;
+    for (uint32_t c = c0; c < c1; ++c) sum += chunk_nblk[c];
+    unsigned long long ex = cta_scan_excl(sum, s_w);
+    for (uint32_t c = c0; c < c1; ++c) {
+        chunk_first[c] = uint32_t(ex);
+        ex += chunk_nblk[c];
+    }
 }
 
-// Scatter the staged records of mode 3 into place: one warp per chunk walks
-// the chunk's block list in order; records with equal queries inside a
-// 32-record group are ranked by lane (match_any), so every query's ids stay
-// ascending.  Position = qoff[q] + base[chunk][q] + running count.
-__global__ void __launch_bounds__(256) vb_scatter_kernel(const VaBatchArgs a) {
-    extern __shared__ unsigned long long s_pos[];   // [8 warps][1024] next output position
+// Put the staged blocks in (chunk, ordinal) order: blk_list[first[chunk] +
+// seq] = block.  Skipped when the pool overflowed (the scatter is too).
+__global__ void __launch_bounds__(256) vb_block_list_kernel(const VaBatchArgs a) {
+    if (*reinterpret_cast<volatile const uint32_t*>(a.overflow)) return;
+    const uint32_t used = min(*reinterpret_cast<volatile const uint32_t*>(a.cursor), a.max_blocks);
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < used; b += gridDim.x * blockDim.x)
+        a.blk_list[a.chunk_first[a.blk_chunk[b]] + a.blk_seq[b]] = b;
+}
+
+// lanes of the warp whose (active) 10-bit query equals this lane's: ten
+// ballots, cheaper than MATCH.ANY on this part
+__device__ __forceinline__ uint32_t match_q10(uint32_t q, bool act) {
+    uint32_t m = __ballot_sync(0xFFFFFFFFu, act);
+#pragma unroll
+    for (int b = 0; b < 10; ++b) {
+        const uint32_t bit = (q >> b) & 1u;
+        const uint32_t bb = __ballot_sync(0xFFFFFFFFu, bit);
+        m &= bit ? bb : ~bb;
+    }
+    return m;
+}
+
+// Scatter the staged records of mode 3 into place.  One CTA per chunk (grid-
+// strided) takes the chunk's records in windows of up to 16 blocks, sorts a
+// window by query in shared memory (stable counting sort: per-warp segment
+// counts, a prefix over warps and queries, then ballot-match ranking inside
+// each 32-record group) and writes every query's run of ids contiguously at
+// pos[q] = qoff[q] + base[chunk][q] + ids of earlier windows.  Runs of
+// adjacent chunks abut in the output, so the L2 assembles full sectors
+// instead of read-modify-writing scattered 4-byte stores.
+constexpr int SC_THREADS = 512;
+constexpr int SC_WARPS = SC_THREADS / 32;
+constexpr uint32_t SC_WIN_BLOCKS = 16;
+constexpr uint32_t SC_WIN = SC_WIN_BLOCKS * kRecBlock;   // records per window
+constexpr size_t SC_SMEM = size_t(SC_WIN) * (4 + 4 + 2) + size_t(SC_WARPS) * 1024 * (2 + 1) + 1025 * 4 + 1024 * 8;
+
+__global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatchArgs a) {
+    extern __shared__ __align__(16) uint32_t ss[];
+    unsigned long long* s_pos = reinterpret_cast<unsigned long long*>(ss);   // [1024] next output position
+    uint32_t* s_rec = ss + 2 * 1024;                   // [SC_WIN] the window's records, in order
+    uint32_t* s_out = s_rec + SC_WIN;                  // [SC_WIN] tuple offsets, sorted by query
+    uint32_t* s_off = s_out + SC_WIN;                  // [1025] window offsets by query
+    uint16_t* s_q = reinterpret_cast<uint16_t*>(s_off + 1025);   // [SC_WIN] query of each sorted slot
+    uint16_t* s_wc = s_q + SC_WIN;                     // [warps][1024] segment counts -> offsets
+    uint8_t* s_tag = reinterpret_cast<uint8_t*>(s_wc + SC_WARPS * 1024);   // [warps][1024] duplicate probe
+    __shared__ uint32_t s_blk[SC_WIN_BLOCKS], s_bcnt[SC_WIN_BLOCKS], s_boff[SC_WIN_BLOCKS + 1];
+    __shared__ uint32_t s_wsum[SC_WARPS];
     if (*reinterpret_cast<volatile const uint32_t*>(a.overflow)) return;   // mode 2 recounts instead
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    unsigned long long* pos = s_pos + warp * 1024;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
-    for (uint32_t chunk = blockIdx.x * 8 + warp; chunk < a.nchunks; chunk += gridDim.x * 8) {
+    for (uint32_t chunk = blockIdx.x; chunk < a.nchunks; chunk += gridDim.x) {
         const unsigned long long* base = a.base + uint64_t(chunk) * 1024;
-        for (uint32_t q = lane; q < 1024; q += 32) pos[q] = a.qoff[q] + base[q];
-        __syncwarp();
+        for (uint32_t q = tid; q < 1024; q += SC_THREADS) s_pos[q] = a.qoff[q] + base[q];
         const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
-        for (uint32_t b = a.chunk_head[chunk]; b != kNoBlock; b = a.blk_next[b]) {
-            const uint32_t cnt = a.blk_count[b];
-            const uint32_t* rec = a.rec + uint64_t(b) * kRecBlock;
-            for (uint32_t i = 0; i < cnt; i += 128) {
-                // 4 groups of 32 records loaded together, then placed in order
-                uint32_t r[4];
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const uint32_t j = i + 32 * g + lane;
-                    r[g] = j < cnt ? __ldcs(rec + j) : 0u;
+        const uint32_t first = a.chunk_first[chunk], nblk = a.chunk_nblk[chunk];
+        for (uint32_t k0 = 0; k0 < nblk; k0 += SC_WIN_BLOCKS) {
+            // the window: blocks k0 .. k0+15 of the chunk's list
+            if (tid < SC_WIN_BLOCKS) {
+                const uint32_t k = k0 + tid;
+                const uint32_t blk = k < nblk ? a.blk_list[first + k] : 0u;
+                s_blk[tid] = blk;
+                s_bcnt[tid] = k < nblk ? a.blk_count[blk] : 0u;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t acc = 0;
+                for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k) {
+                    s_boff[k] = acc;
+                    acc += s_bcnt[k];
                 }
+                s_boff[SC_WIN_BLOCKS] = acc;
+            }
+            for (uint32_t i = tid; i < SC_WARPS * 1024 / 2; i += SC_THREADS) reinterpret_cast<uint32_t*>(s_wc)[i] = 0;
+            __syncthreads();
+            const uint32_t n = s_boff[SC_WIN_BLOCKS];
+            {
+                // every load of the window in flight at once: 2 records per
+                // thread per block
+                uint32_t v[SC_WIN_BLOCKS][2];
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    if (i + 32 * g >= cnt) break;
-                    const bool active = i + 32 * g + lane < cnt;
-                    const uint32_t q = active ? (r[g] & 1023u) : 0xFFFFFFFFu;
-                    const uint32_t same = __match_any_sync(0xFFFFFFFFu, q);
-                    const uint32_t rank = __popc(same & lt);
-                    unsigned long long p = 0;
-                    if (active) {
-                        p = pos[q];
-                        const unsigned long long at = p + rank;
-                        if (at < a.ids_cap) a.ids[at] = a.id_base + uint32_t(start + (r[g] >> 10));
+                for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k)
+#pragma unroll
+                    for (uint32_t h = 0; h < 2; ++h) {
+                        const uint32_t i = tid + h * SC_THREADS;
+                        v[k][h] = i < s_bcnt[k] ? __ldcs(a.rec + uint64_t(s_blk[k]) * kRecBlock + i) : 0u;
                     }
-                    __syncwarp();
-                    if (active && rank == 0) pos[q] = p + __popc(same);
-                    __syncwarp();
+#pragma unroll
+                for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k)
+#pragma unroll
+                    for (uint32_t h = 0; h < 2; ++h) {
+                        const uint32_t i = tid + h * SC_THREADS;
+                        if (i < s_bcnt[k]) s_rec[s_boff[k] + i] = v[k][h];
+                    }
+            }
+            __syncthreads();
+            // warp w owns the contiguous segment [s0, s1) of the window
+            const uint32_t seg = (n + SC_WARPS * 32 - 1) / (SC_WARPS * 32) * 32;
+            const uint32_t s0 = min(n, warp * seg), s1 = min(n, s0 + seg);
+            uint16_t* wc = s_wc + warp * 1024;
+            {
+                // segment counts: two 16-bit counters per word (a segment
+                // holds <= SC_WIN / SC_WARPS records, no carry between halves)
+                uint32_t* wc32 = reinterpret_cast<uint32_t*>(wc);
+                for (uint32_t j = s0 + lane; j < s1; j += 32) {
+                    const uint32_t q = s_rec[j] & 1023u;
+                    atomicAdd(wc32 + (q >> 1), 1u << ((q & 1u) * 16));
                 }
             }
+            __syncthreads();
+            // per query: exclusive prefix over the warps' segments, window total
+            uint32_t tot[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t q = tid * 2 + h;
+                uint32_t run = 0;
+#pragma unroll
+                for (int w = 0; w < SC_WARPS; ++w) {
+                    const uint32_t c = s_wc[w * 1024 + q];
+                    s_wc[w * 1024 + q] = uint16_t(run);
+                    run += c;
+                }
+                tot[h] = run;
+            }
+            // exclusive scan of the totals over the 1024 queries
+            const uint32_t pair = tot[0] + tot[1];
+            uint32_t incl = pair;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= uint32_t(o)) incl += x;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            uint32_t wbase = 0;
+            for (uint32_t w = 0; w < warp; ++w) wbase += s_wsum[w];
+            const uint32_t ex = wbase + incl - pair;
+            s_off[tid * 2] = ex;
+            s_off[tid * 2 + 1] = ex + tot[0];
+            if (tid == 0) s_off[1024] = n;
+            __syncthreads();
+            // stable placement: rank = earlier warps' segments + earlier
+            // groups of this segment + lanes below with the same query
+            uint8_t* tag = s_tag + warp * 1024;
+            for (uint32_t j = s0; j < s1; j += 32) {
+                const bool act = j + lane < s1;
+                const uint32_t r = act ? s_rec[j + lane] : 0u;
+                const uint32_t q = act ? (r & 1023u) : 0xFFFFFFFFu;
+                // duplicate queries inside a group are rare: probe with a
+                // last-writer tag, rank with the ballot match only if needed
+                if (act) tag[q] = uint8_t(lane);
+                __syncwarp();
+                const bool dup = act && tag[q] != lane;
+                const uint32_t same = __any_sync(0xFFFFFFFFu, dup) ? match_q10(q, act) : (1u << lane);
+                if (act) {
+                    const uint32_t p = s_off[q] + wc[q] + __popc(same & lt);
+                    s_out[p] = r >> 10;
+                    s_q[p] = uint16_t(q);
+                }
+                __syncwarp();
+                if (act && (same & lt) == 0) wc[q] += __popc(same);
+                __syncwarp();
+            }
+            __syncthreads();
+            // write the runs: consecutive slots of one query are consecutive ids
+            for (uint32_t j = tid; j < n; j += SC_THREADS) {
+                const uint32_t q = s_q[j];
+                const unsigned long long at = s_pos[q] + (j - s_off[q]);
+                if (at < a.ids_cap) __stcs(a.ids + at, a.id_base + uint32_t(start + s_out[j]));
+            }
+            __syncthreads();
+            for (uint32_t q = tid; q < 1024; q += SC_THREADS) s_pos[q] += s_off[q + 1] - s_off[q];
+            __syncthreads();
         }
     }
 }
@@ -508,19 +658,23 @@ void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st) {
 
 void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st) {
     if (a.n == 0 || a.nchunks == 0) return;
-    const uint32_t blocks = (a.nchunks + 7) / 8;
-    const int smem = 8 * 1024 * sizeof(unsigned long long);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(vb_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(vb_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SC_SMEM));
         configured = true;
     }
-    vb_scatter_kernel<<<blocks, 256, smem, st>>>(a);
+    const uint32_t blocks = std::min<uint32_t>(a.nchunks, a.grid);   // one CTA per SM
+    vb_scatter_kernel<<<blocks, SC_THREADS, SC_SMEM, st>>>(a);
 }
 
 void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st) {
     vb_chunk_scan_kernel<<<(a.nqp + 31) / 32, 1024, 0, st>>>(a.chunk_counts, nchunks, a.nqp, a.base, a.total);
-    vb_query_scan_kernel<<<1, 1024, 0, st>>>(a.total, a.nqp, a.offsets, a.counts_all, a.qoff, q0);
+    vb_query_scan_kernel<<<1, 1024, 0, st>>>(a.total, a.nqp, a.offsets, a.counts_all, a.qoff, q0, a.chunk_nblk,
+                                             a.chunk_first, nchunks);
+}
+
+void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st) {
+    vb_block_list_kernel<<<a.grid * 4, 256, 0, st>>>(a);
 }
 
 }  // namespace mdrq

@@ -234,3 +234,29 @@ def test_c1_all_queries_vs_reference_golden(gpu):
             assert np.array_equal(np.diff(offs), G["p_counts"]), p
             for i in range(G["p_lo"].shape[0]):
                 assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G["p_sha1"][i].tobytes(), (p, i)
+
+
+def test_vafile_batch_staging_overflow_and_dense_groups(gpu):
+    """Single-pass ids of the bit-sliced VA batch (vabatch.cu mode 3) beyond
+    its default staging pool (64K blocks x 1024 records): the pass falls back
+    to the recount kernel and the pool grows, so the second call stages
+    everything -- same ids both times.  Dense queries also put equal queries
+    into one 32-record group of the scatter's stable ranking."""
+    rng = np.random.default_rng(5)
+    n, m, nfull = 1_200_000, 3, 60
+    values = rng.random((n, m), dtype=np.float32)
+    lo = np.full((nfull + 4, m), -np.inf, np.float32)
+    hi = np.full((nfull + 4, m), np.inf, np.float32)
+    lo[nfull:] = rng.uniform(0, 0.7, (4, m)).astype(np.float32)
+    hi[nfull:] = lo[nfull:] + np.float32(0.3)
+    exp_counts = oracle.count_batch(values, lo[nfull:], hi[nfull:])
+    exp_offs, exp_ids = oracle.ids_batch(values, lo[nfull:], hi[nfull:], counts=exp_counts)
+    every = np.arange(n, dtype=np.uint32)
+    with gpu.DeviceStore(values, layouts=1 | 4) as st_:
+        for _ in range(2):
+            offs, ids = st_.ids(lo, hi, "vafile_batch")
+            assert offs[nfull] == nfull * n
+            for q in (0, 1, nfull // 2, nfull - 1):
+                assert np.array_equal(ids[offs[q]:offs[q + 1]], every), q
+            assert np.array_equal(offs[nfull:] - offs[nfull], exp_offs)
+            assert np.array_equal(ids[offs[nfull]:].astype(np.int64), exp_ids)
