@@ -103,10 +103,11 @@ struct VaBatchArgs {
     const float2* qbounds;       // [1024][kb or vdims] exact (lo, hi), +-inf where unconstrained
     uint32_t grid;               // CTAs (chunks = grid * warps)
     uint64_t chunk_tuples;       // tuples per chunk (multiple of 128, < 65536: u16 counters)
-    uint32_t nchunks;            // ceil(n / chunk_tuples); warps stride over chunks
+    uint32_t nchunks;            // subchunks: ceil(n / chunk_tuples), one warp each
+    uint32_t ngroups;            // groups of kVbWarps consecutive subchunks, one CTA each
     unsigned long long* counts;  // [nqp] count mode (offset to the pass)
-    uint32_t* chunk_counts;      // [chunks][1024]
-    unsigned long long* base;    // [chunks][1024]
+    uint32_t* chunk_counts;      // [groups][1024] (mode 2: [subchunks][1024] prefix scratch)
+    unsigned long long* base;    // [groups][1024]
     unsigned long long* total;   // [1024]
     unsigned long long* qoff;    // [1024]
     unsigned long long* offsets;     // batch offsets [nq+1]
@@ -134,10 +135,10 @@ constexpr uint32_t kNoBlock = 0xFFFFFFFFu;
 size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode);
 int va_batch_max_dims();
 uint32_t va_batch_warps();
-// mode 0 count, 1 chunk counts, 2 ids (recount pass), 3 chunk counts + staged records
+// mode 0 count, 2 ids (recount pass after a staging overflow), 3 group counts + staged records
 void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st);
 void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st);
-void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st);
+void launch_va_batch_scans(const VaBatchArgs& a, uint32_t q0, cudaStream_t st);
 void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st);
 
 constexpr int kColTile = 4096;     // tuples per CTA tile, single-query columnar

@@ -593,6 +593,7 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     const uint64_t warps = uint64_t(a.grid) * va_batch_warps();
     a.chunk_tuples = std::min<uint64_t>(65408, round_up((s->n + warps - 1) / warps, 128));
     a.nchunks = uint32_t((s->n + a.chunk_tuples - 1) / a.chunk_tuples);
+    a.ngroups = (a.nchunks + va_batch_warps() - 1) / va_batch_warps();
     const uint64_t chunks = a.nchunks;
     s->vb_chunk_counts.reserve(chunks * 1024);
     s->vb_base.reserve(chunks * 1024);
@@ -626,6 +627,9 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.cursor = s->vb_flags.p;
     a.overflow = s->vb_flags.p + 1;
     a.max_blocks = s->vb_max_blocks;
+    // test hook: cap the staging pool so small batches take the recount path
+    static const char* cap = getenv("MDRQ_VB_STAGING_BLOCKS");
+    if (cap) a.max_blocks = std::min<uint32_t>(a.max_blocks, uint32_t(strtoul(cap, nullptr, 10)));
     return a;
 }
 
@@ -722,14 +726,23 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profil
                 // on device)
                 mark(3, 0);
                 CK(cudaMemsetAsync(va.cursor, 0, 2 * sizeof(uint32_t), st));
+                static const bool dbg = getenv("MDRQ_DEBUG_SYNC") != nullptr;
+                auto dsync = [&](const char* what) {
+                    if (dbg) ck(cudaStreamSynchronize(st), what);
+                };
                 mark(0, 1);
                 launch_va_batch(va, 3, st);
+                dsync("mode3");
                 mark(1, 3);
-                launch_va_batch_scans(va, va.nchunks, ps.q0, st);
+                launch_va_batch_scans(va, ps.q0, st);
+                dsync("scans");
                 launch_va_batch_block_list(va, st);
+                dsync("list");
                 mark(2, 2);
                 launch_va_batch_scatter(va, st);
+                dsync("scatter");
                 launch_va_batch(va, 2, st);
+                dsync("mode2");
                 launches += 6;
             }
         }

@@ -43,6 +43,7 @@ namespace {
 
 constexpr int VB_THREADS = 512;
 constexpr int VB_WARPS = VB_THREADS / 32;
+constexpr uint32_t VB_QCAP = 160;   // candidate queue per warp: < 32 left over + 4 steps x 32 lanes
 
 __device__ __forceinline__ float f4_get(const float4& w, uint32_t i) {
     return i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w;
@@ -60,32 +61,40 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     constexpr bool PV = va_batch_pv(KB);           // values + bounds in smem, overlap-only table
     constexpr int KBV = PV ? int(va_batch_vdims(KB)) : KB;
     constexpr int H = PV ? KBV / 4 : 1;            // float4 slots per staged tuple
+    constexpr bool DENSE = MODE != 2;              // candidates refined lane-parallel from a queue
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_end = sm + va_batch_table_words(KB, K);
     // PV: exact query bounds [1024][KBV/2] float4 (lo_u, hi_u, lo_u+1, hi_u+1)
     // and every warp's staged block values [128 * H] float4
     float4* s_qb = reinterpret_cast<float4*>(s_end);
     float4* s_val = s_qb + (PV ? 1024 * KBV / 2 : 0);
-    // MODE 0: u32 [1024] shared by the CTA ; MODE 1/2/3: u16 [warps][1024]
-    uint32_t* s_cnt32 = reinterpret_cast<uint32_t*>(s_val + (PV ? VB_WARPS * 128 * H : 0));
-    uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_cnt32);
+    uint32_t* s_rest = reinterpret_cast<uint32_t*>(s_val + (PV ? VB_WARPS * 128 * H : 0));
+    // DENSE (modes 0, 3): CTA counters u32 [1024], then every warp's candidate
+    // queue: overlap words [QCAP], (wide unions) containment words [QCAP],
+    // meta u16 [QCAP] = tuple-in-block << 5 | query word.
+    // MODE 2: per-warp counters u16 [warps][1024].
+    uint32_t* s_cnt32 = s_rest;
+    uint32_t* s_qw = s_rest + 1024;
+    uint32_t* s_qs = s_qw + VB_WARPS * VB_QCAP;
+    uint16_t* s_qm = reinterpret_cast<uint16_t*>(s_qs + (PV ? 0 : VB_WARPS * VB_QCAP));
+    uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_rest);
 
     // the recount pass only runs when the single-pass staging overflowed
-    if (MODE == 2 && a.overflow && *reinterpret_cast<volatile const uint32_t*>(a.overflow) == 0) return;
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (MODE == 2 && *reinterpret_cast<volatile const uint32_t*>(a.overflow) == 0) return;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.tables);
         uint4* dst = reinterpret_cast<uint4*>(sm);
         const uint32_t n4 = va_batch_table_words(KB, K) / 4;
-        for (uint32_t i = threadIdx.x; i < n4; i += VB_THREADS) dst[i] = src[i];
+        for (uint32_t i = tid; i < n4; i += VB_THREADS) dst[i] = src[i];
         if constexpr (PV) {
             const uint4* qsrc = reinterpret_cast<const uint4*>(a.qbounds);
             uint4* qdst = reinterpret_cast<uint4*>(s_qb);
-            for (uint32_t i = threadIdx.x; i < 1024 * KBV / 2; i += VB_THREADS) qdst[i] = qsrc[i];
+            for (uint32_t i = tid; i < 1024 * KBV / 2; i += VB_THREADS) qdst[i] = qsrc[i];
         }
         if (MODE == 0)
-            for (uint32_t i = threadIdx.x; i < 1024; i += VB_THREADS) s_cnt32[i] = 0;
-        if (threadIdx.x < KB) s_dim[threadIdx.x] = a.udims[threadIdx.x];
+            for (uint32_t i = tid; i < 1024; i += VB_THREADS) s_cnt32[i] = 0;
+        if (tid < KB) s_dim[tid] = a.udims[tid];
     }
     __syncthreads();
 
@@ -97,25 +106,67 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     // is an immediate.
     const uint32_t lane_off = lane * (PV ? 4 : 8);
     const char* s_tab = reinterpret_cast<const char*>(sm);
-    uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 1/2/3: this warp's chunk counters
     float4* wval = s_val + warp * 128 * H;         // PV: this warp's staged values
+    uint32_t* qw = s_qw + warp * VB_QCAP;
+    uint32_t* qs = s_qs + warp * VB_QCAP;
+    uint16_t* qm = s_qm + warp * VB_QCAP;
+    uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 2
     const uint32_t lt = lanemask_lt();
 
-    for (uint32_t chunk = blockIdx.x * VB_WARPS + warp; chunk < a.nchunks; chunk += gridDim.x * VB_WARPS) {
-        const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
-        uint64_t end = start + a.chunk_tuples;
-        if (end > a.n) end = a.n;
-        if (MODE != 0) {
+    // Exact refinement of one query word for one tuple: bit b of the result
+    // is set iff query wq + b (a candidate in `word`) contains the tuple.
+    // tl = tuple within the staged block (PV), t = tuple index (wide unions).
+    auto refine_word = [&](uint32_t word, uint32_t su, uint32_t tl, uint64_t t, uint32_t wq) -> uint32_t {
+        uint32_t hits = PV ? 0u : su;
+        uint32_t r = PV ? word : (word & ~su);
+        if (r) {
+            float v[PV ? 4 * H : KB];
+            if constexpr (PV) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) wcnt[lane * 32 + i] = 0;
+                for (int h = 0; h < H; ++h) {
+                    const float4 w4 = wval[val_slot(tl * H + h)];
+                    v[4 * h] = w4.x;
+                    v[4 * h + 1] = w4.y;
+                    v[4 * h + 2] = w4.z;
+                    v[4 * h + 3] = w4.w;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < KB; ++u) v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
+            }
+            while (r) {
+                const int b = __ffs(r) - 1;
+                r &= r - 1;
+                bool ok = true;
+                if constexpr (PV) {
+                    const float4* qq = s_qb + (wq + b) * (KBV / 2);
+#pragma unroll
+                    for (int u2 = 0; u2 < KBV / 2; ++u2) {
+                        const float4 bb = qq[u2];
+                        ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
+                             (v[2 * u2 + 1] <= bb.w);
+                    }
+                } else {
+                    const float2* qq = a.qbounds + (wq + b) * KB;
+#pragma unroll
+                    for (int u = 0; u < KB; ++u) {
+                        const float2 bb = qq[u];
+                        ok = ok & (bb.x <= v[u]) & (v[u] <= bb.y);
+                    }
+                }
+                hits |= uint32_t(ok) << b;
+            }
         }
-        const unsigned long long* __restrict__ base = MODE == 2 ? a.base + uint64_t(chunk) * 1024 : nullptr;
-        // MODE 3: current staging block of this chunk, its fill, blocks so far
-        uint32_t blk = kNoBlock, fill = 0, nblk = 0;
+        return hits;
+    };
 
-        // software pipeline: the codes (and, for narrow unions, the exact
-        // values) of the next 128-tuple block are loaded while this block is
-        // evaluated; lane l holds tuples t0+4l .. t0+4l+3 of every union dim
+    // Walk the tuples [start, end) of a subchunk in 128-tuple blocks (lane l
+    // holds tuples t0+4l .. t0+4l+3 of every union dim; the next block's codes
+    // and values are loaded while this one is evaluated).  Per block:
+    // before_block(t0), the block's values staged (PV), then per 4-tuple step
+    // the overlap (and containment) words of the lane's query word for the 4
+    // tuples: step(t0, j4, jmax, ov4, su4).
+    auto for_each_step = [&](uint64_t start, uint64_t end, auto&& before_block, auto&& step) {
         uint32_t cw_n[KB];
         float4 vv_n[PV ? KB : 1];
         auto load_block = [&](uint64_t tb) {
@@ -133,10 +184,11 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             for (int u = 0; u < KB; ++u)
                 // table cells of the 4 tuples of every word: (code >> shift) per byte
                 cw[u] = (cw_n[u] >> shift) & (0x01010101u * (K - 1));
+            before_block(t0);
             if constexpr (PV) {
                 // stage the block's exact values tuple-major (tuple t, dims
                 // 4h..4h+3 in float4 slot t*H + h, zero-padded dims) so a
-                // refinement reads a tuple with H broadcast LDS.128
+                // refinement reads a tuple with H LDS.128
                 __syncwarp();
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj)
@@ -158,8 +210,6 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 uint32_t x[KB];
 #pragma unroll
                 for (int u = 0; u < KB; ++u) x[u] = __shfl_sync(0xFFFFFFFFu, cw[u], j4 >> 2);
-                // filter the 4 tuples of this step first (independent LDS in
-                // flight), then refine / emit them in order
                 uint32_t ov4[4], su4[4];
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) ov4[jj] = su4[jj] = 0xFFFFFFFFu;
@@ -194,9 +244,162 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             }
                         }
                     }
-                // warp-uniform mask of the step's tuples with any candidate
-                // (overlap covers the sure matches); only those are refined
-                // and emitted, in tuple order
+                step(t0, j4, jmax, ov4, su4);
+            }
+        }
+    };
+
+    for (uint32_t g = blockIdx.x; uint64_t(g) * VB_WARPS < a.nchunks; g += gridDim.x) {
+        // group g = subchunks 16g .. 16g+15 (one per warp, consecutive tuple
+        // ranges); counts / bases are per group, staged blocks per subchunk
+        const uint32_t chunk = g * VB_WARPS + warp;
+        const bool has_chunk = chunk < a.nchunks;
+        const uint64_t gstart = uint64_t(g) * VB_WARPS * a.chunk_tuples;
+        const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
+        const uint64_t end = has_chunk ? (start + a.chunk_tuples < a.n ? start + a.chunk_tuples : a.n) : start;
+        if constexpr (MODE == 3) {
+            for (uint32_t q = tid; q < 1024; q += VB_THREADS) s_cnt32[q] = 0;
+            __syncthreads();
+        }
+        if constexpr (DENSE) {
+            // Candidate words (tuple, query word, overlap bits) go to the
+            // warp's queue in tuple order; every 32 entries are refined with
+            // one entry per lane, so the refinement and the emission run on
+            // full warps instead of the one or two lanes a tuple's candidates
+            // touch.
+            uint32_t qn = 0;
+            uint64_t blk_t0 = start;
+            uint32_t blk = kNoBlock, fill = 0, nblk = 0;   // MODE 3 staging state of the subchunk
+            auto process = [&](uint32_t e0, uint32_t cnt) {
+                const bool act = lane < cnt;
+                const uint32_t word = act ? qw[e0 + lane] : 0u;
+                const uint32_t su = (!PV && act) ? qs[e0 + lane] : 0u;
+                const uint32_t meta = act ? qm[e0 + lane] : 0u;
+                const uint32_t tl = meta >> 5, wq = (meta & 31u) * 32;
+                const uint64_t t = blk_t0 + tl;
+                uint32_t hits = refine_word(word, su, tl, t, wq);
+                if constexpr (MODE == 0) {
+                    while (hits) {
+                        const int b = __ffs(hits) - 1;
+                        hits &= hits - 1;
+                        atomicAdd(&s_cnt32[wq + b], 1u);
+                    }
+                } else {
+                    // stage (tuple offset in the group, query) records in
+                    // entry order = tuple order: warp prefix of the per-lane
+                    // hit counts (a ballot when no lane has two hits)
+                    const uint32_t cnt_h = __popc(hits);
+                    const uint32_t anyb = __ballot_sync(0xFFFFFFFFu, cnt_h != 0);
+                    if (anyb) {
+                        uint32_t excl, tot;
+                        if (__ballot_sync(0xFFFFFFFFu, cnt_h > 1) == 0) {
+                            excl = __popc(anyb & lt);
+                            tot = __popc(anyb);
+                        } else {
+                            uint32_t incl = cnt_h;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const uint32_t x2 = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                                if (lane >= uint32_t(o)) incl += x2;
+                            }
+                            excl = incl - cnt_h;
+                            tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                        }
+                        if (blk != kNoBlock - 1 && (blk == kNoBlock || fill + tot > kRecBlock)) {
+                            uint32_t nb = 0;
+                            if (lane == 0) {
+                                nb = atomicAdd(a.cursor, 1u);
+                                if (nb >= a.max_blocks) {
+                                    atomicExch(a.overflow, 1u);
+                                    nb = kNoBlock - 1;   // stop staging this subchunk
+                                } else {
+                                    a.blk_chunk[nb] = chunk;
+                                    a.blk_seq[nb] = nblk;
+                                }
+                                if (blk != kNoBlock) a.blk_count[blk] = fill;
+                            }
+                            blk = __shfl_sync(0xFFFFFFFFu, nb, 0);
+                            nblk += blk != kNoBlock - 1;
+                            fill = 0;
+                        }
+                        const bool stage_on = blk != kNoBlock - 1;
+                        uint32_t* dst = a.rec + uint64_t(stage_on ? blk : 0) * kRecBlock + fill + excl;
+                        const uint32_t trel = uint32_t(t - gstart) << 10;
+                        while (hits) {
+                            const int b = __ffs(hits) - 1;
+                            hits &= hits - 1;
+                            const uint32_t q = wq + b;
+                            if (stage_on) *dst++ = trel | q;
+                            atomicAdd(&s_cnt32[q], 1u);
+                        }
+                        fill += tot;
+                    }
+                }
+            };
+            auto flush = [&]() {
+                if (qn) {
+                    __syncwarp();
+                    process(0, qn);
+                    qn = 0;
+                }
+            };
+            for_each_step(
+                start, end,
+                [&](uint64_t t0) {
+                    flush();   // the queued entries need the previous block's staged values
+                    blk_t0 = t0;
+                },
+                [&](uint64_t, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[4], const uint32_t(&su4)[4]) {
+#pragma unroll
+                    for (uint32_t jj = 0; jj < 4; ++jj) {
+                        const bool nz = ov4[jj] != 0u && j4 + jj < jmax;
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, nz);
+                        if (nz) {
+                            const uint32_t slot = qn + __popc(bal & lt);
+                            qw[slot] = ov4[jj];
+                            if constexpr (!PV) qs[slot] = su4[jj];
+                            qm[slot] = uint16_t(((j4 + jj) << 5) | lane);
+                        }
+                        qn += __popc(bal);
+                    }
+                    if (qn >= 32) {
+                        __syncwarp();
+                        uint32_t e0 = 0;
+                        for (; e0 + 32 <= qn; e0 += 32) process(e0, 32);
+                        // move the < 32 remaining entries to the front
+                        const uint32_t rem = qn - e0;
+                        uint32_t mw = 0, ms = 0, mm = 0;
+                        if (lane < rem) {
+                            mw = qw[e0 + lane];
+                            if constexpr (!PV) ms = qs[e0 + lane];
+                            mm = qm[e0 + lane];
+                        }
+                        __syncwarp();
+                        if (lane < rem) {
+                            qw[lane] = mw;
+                            if constexpr (!PV) qs[lane] = ms;
+                            qm[lane] = uint16_t(mm);
+                        }
+                        __syncwarp();
+                        qn = rem;
+                    }
+                });
+            flush();
+            if (MODE == 3 && has_chunk && lane == 0) {
+                if (blk < kNoBlock - 1) a.blk_count[blk] = fill;
+                a.chunk_nblk[chunk] = nblk;
+            }
+        } else {
+            // MODE 2, the fallback when the staging pool overflowed: count the
+            // subchunk per query, prefix the warps' counts within the group,
+            // then walk the subchunk again writing ids in place (chunk_counts
+            // is sized for subchunks, so its rows hold the prefixes)
+            const unsigned long long* __restrict__ base = a.base + uint64_t(g) * 1024;
+            uint32_t* pre = a.chunk_counts;
+            const uint32_t* wpre = pre + uint64_t(chunk) * 1024;
+            bool write_ids = false;
+            auto per_tuple = [&](uint64_t t0, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[4],
+                                 const uint32_t(&su4)[4]) {
                 uint32_t nib = 0;
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) nib |= uint32_t(ov4[jj] != 0u) << jj;
@@ -206,143 +409,56 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     const uint32_t jj = __ffs(tm) - 1;
                     tm &= tm - 1;
                     const uint32_t ovw = jj == 0 ? ov4[0] : jj == 1 ? ov4[1] : jj == 2 ? ov4[2] : ov4[3];
+                    const uint32_t suw = jj == 0 ? su4[0] : jj == 1 ? su4[1] : jj == 2 ? su4[2] : su4[3];
                     const uint64_t t = t0 + j4 + jj;
-                    uint32_t hits;
-                    if constexpr (PV) {
-                        // every overlap candidate is refined exactly
-                        hits = 0;
-                        uint32_t r = ovw;
-                        float v[4 * H];
-                        const uint32_t s0 = (j4 + jj) * H;
-#pragma unroll
-                        for (int h = 0; h < H; ++h) {
-                            const float4 w = wval[val_slot(s0 + h)];
-                            v[4 * h] = w.x;
-                            v[4 * h + 1] = w.y;
-                            v[4 * h + 2] = w.z;
-                            v[4 * h + 3] = w.w;
-                        }
-                        while (r) {
-                            const int b = __ffs(r) - 1;
-                            r &= r - 1;
-                            const float4* qq = s_qb + (lane * 32 + b) * (KBV / 2);
-                            bool ok = true;
-#pragma unroll
-                            for (int u2 = 0; u2 < KBV / 2; ++u2) {
-                                const float4 bb = qq[u2];
-                                ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
-                                     (v[2 * u2 + 1] <= bb.w);
-                            }
-                            hits |= uint32_t(ok) << b;
-                        }
-                    } else {
-                        // cells strictly inside are sure; edge-cell pairs are
-                        // refined against the exact columns
-                        const uint32_t suw = jj == 0 ? su4[0] : jj == 1 ? su4[1] : jj == 2 ? su4[2] : su4[3];
-                        hits = suw;
-                        uint32_t r = ovw & ~suw;
-                        if (__any_sync(0xFFFFFFFFu, r)) {
-                            float v[KB];
-#pragma unroll
-                            for (int u = 0; u < KB; ++u) v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
-                            while (r) {
-                                const int b = __ffs(r) - 1;
-                                r &= r - 1;
-                                const float2* qq = a.qbounds + (lane * 32 + b) * KB;
-                                bool ok = true;
-#pragma unroll
-                                for (int u = 0; u < KB; ++u) {
-                                    const float2 bb = qq[u];
-                                    ok = ok && (bb.x <= v[u]) && (v[u] <= bb.y);
-                                }
-                                if (ok) hits |= 1u << b;
-                            }
-                        }
-                    }
-                    if (MODE == 3) {
-                        // stage (tuple offset, query) records in tuple order:
-                        // warp prefix of the per-lane hit counts (a ballot when
-                        // no lane has more than one hit, the common case)
-                        const uint32_t cnt = __popc(hits);
-                        const uint32_t anyb = __ballot_sync(0xFFFFFFFFu, cnt != 0);
-                        if (anyb) {
-                            uint32_t excl, tot;
-                            if (__ballot_sync(0xFFFFFFFFu, cnt > 1) == 0) {
-                                excl = __popc(anyb & lt);
-                                tot = __popc(anyb);
-                            } else {
-                                uint32_t incl = cnt;
-#pragma unroll
-                                for (int o = 1; o < 32; o <<= 1) {
-                                    const uint32_t x2 = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                                    if (lane >= uint32_t(o)) incl += x2;
-                                }
-                                excl = incl - cnt;
-                                tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-                            }
-                            if (blk != kNoBlock - 1 && (blk == kNoBlock || fill + tot > kRecBlock)) {
-                                uint32_t nb = 0;
-                                if (lane == 0) {
-                                    nb = atomicAdd(a.cursor, 1u);
-                                    if (nb >= a.max_blocks) {
-                                        atomicExch(a.overflow, 1u);
-                                        nb = kNoBlock - 1;   // stop staging this chunk
-                                    } else {
-                                        a.blk_chunk[nb] = chunk;
-                                        a.blk_seq[nb] = nblk;
-                                    }
-                                    if (blk != kNoBlock) a.blk_count[blk] = fill;
-                                }
-                                blk = __shfl_sync(0xFFFFFFFFu, nb, 0);
-                                nblk += blk != kNoBlock - 1;
-                                fill = 0;
-                            }
-                            // one loop writes the records and counts them per (chunk, query)
-                            const bool stage_on = blk != kNoBlock - 1;
-                            uint32_t* dst = a.rec + uint64_t(stage_on ? blk : 0) * kRecBlock + fill + excl;
-                            const uint32_t trel = uint32_t(t - start) << 10;
-                            while (hits) {
-                                const int b = __ffs(hits) - 1;
-                                hits &= hits - 1;
-                                const uint32_t q = lane * 32 + b;
-                                if (stage_on) *dst++ = trel | q;
-                                wcnt[q] += 1;
-                            }
-                            fill += tot;
-                        }
-                    }
-                    while (MODE != 3 && hits) {
+                    uint32_t hits = refine_word(ovw, suw, j4 + jj, t, lane * 32);
+                    while (hits) {
                         const int b = __ffs(hits) - 1;
                         hits &= hits - 1;
                         const uint32_t q = lane * 32 + b;
-                        if (MODE == 0) {
-                            atomicAdd(&s_cnt32[q], 1u);
-                        } else if (MODE == 1) {
-                            wcnt[q] += 1;
-                        } else {
-                            const unsigned long long pos = a.qoff[q] + base[q] + wcnt[q];
-                            wcnt[q] += 1;
+                        if (write_ids) {
+                            const unsigned long long pos = a.qoff[q] + base[q] + wpre[q] + wcnt[q];
                             if (pos < a.ids_cap) a.ids[pos] = a.id_base + uint32_t(t);
                         }
+                        wcnt[q] += 1;
                     }
                 }
+            };
+            auto nothing = [](uint64_t) {};
+#pragma unroll
+            for (int i = 0; i < 32; ++i) wcnt[lane * 32 + i] = 0;
+            __syncwarp();
+            for_each_step(start, end, nothing, per_tuple);
+            __syncthreads();
+            // exclusive prefix over the group's warps per query (u32, kept in
+            // the per-subchunk scratch rows of chunk_counts, free after the
+            // scans), the u16 counters restart as running counts
+            for (uint32_t q = tid; q < 1024; q += VB_THREADS) {
+                uint32_t run = 0;
+#pragma unroll
+                for (int w = 0; w < VB_WARPS; ++w) {
+                    if (g * VB_WARPS + w < a.nchunks) pre[uint64_t(g * VB_WARPS + w) * 1024 + q] = run;
+                    run += s_cnt16[w * 1024 + q];
+                    s_cnt16[w * 1024 + q] = 0;
+                }
             }
+            __threadfence_block();
+            __syncthreads();
+            write_ids = true;
+            for_each_step(start, end, nothing, per_tuple);
+            __syncthreads();
         }
-        if (MODE == 3 && lane == 0) {
-            if (blk < kNoBlock - 1) a.blk_count[blk] = fill;
-            a.chunk_nblk[chunk] = nblk;
-        }
-        if (MODE == 1 || MODE == 3) {
-            __syncwarp();
-            uint32_t* out = a.chunk_counts + uint64_t(chunk) * 1024;
-            for (uint32_t q = lane; q < 1024; q += 32) out[q] = wcnt[q];
-            __syncwarp();
+        if constexpr (MODE == 3) {
+            __syncthreads();
+            uint32_t* out = a.chunk_counts + uint64_t(g) * 1024;
+            for (uint32_t q = tid; q < 1024; q += VB_THREADS) out[q] = s_cnt32[q];
+            __syncthreads();
         }
     }
 
     if (MODE == 0) {
         __syncthreads();
-        for (uint32_t q = threadIdx.x; q < a.nqp; q += VB_THREADS)
+        for (uint32_t q = tid; q < a.nqp; q += VB_THREADS)
             if (s_cnt32[q]) atomicAdd(a.counts + q, (unsigned long long)s_cnt32[q]);
     }
 }
@@ -460,13 +576,13 @@ __device__ __forceinline__ uint32_t match_q10(uint32_t q, bool act) {
     return m;
 }
 
-// Scatter the staged records of mode 3 into place.  One CTA per chunk (grid-
-// strided) takes the chunk's records in windows of up to 16 blocks, sorts a
+// Scatter the staged records of mode 3 into place.  One CTA per group (grid-
+// strided) takes the group's records in windows of up to 16 blocks, sorts a
 // window by query in shared memory (stable counting sort: per-warp segment
 // counts, a prefix over warps and queries, then ballot-match ranking inside
 // each 32-record group) and writes every query's run of ids contiguously at
-// pos[q] = qoff[q] + base[chunk][q] + ids of earlier windows.  Runs of
-// adjacent chunks abut in the output, so the L2 assembles full sectors
+// pos[q] = qoff[q] + base[group][q] + ids of earlier windows.  Runs of
+// adjacent groups abut in the output, so the L2 assembles full sectors
 // instead of read-modify-writing scattered 4-byte stores.
 constexpr int SC_THREADS = 512;
 constexpr int SC_WARPS = SC_THREADS / 32;
@@ -488,13 +604,17 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
     if (*reinterpret_cast<volatile const uint32_t*>(a.overflow)) return;   // mode 2 recounts instead
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
-    for (uint32_t chunk = blockIdx.x; chunk < a.nchunks; chunk += gridDim.x) {
-        const unsigned long long* base = a.base + uint64_t(chunk) * 1024;
+    for (uint32_t g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
+        // group g: the blocks of subchunks 16g .. 16g+15, consecutive in the
+        // block list; record tuple offsets are relative to the group start
+        const unsigned long long* base = a.base + uint64_t(g) * 1024;
         for (uint32_t q = tid; q < 1024; q += SC_THREADS) s_pos[q] = a.qoff[q] + base[q];
-        const uint64_t start = uint64_t(chunk) * a.chunk_tuples;
-        const uint32_t first = a.chunk_first[chunk], nblk = a.chunk_nblk[chunk];
+        const uint64_t start = uint64_t(g) * VB_WARPS * a.chunk_tuples;
+        const uint32_t c0 = g * VB_WARPS, c1 = min(a.nchunks, c0 + VB_WARPS) - 1;
+        const uint32_t first = a.chunk_first[c0];
+        const uint32_t nblk = a.chunk_first[c1] + a.chunk_nblk[c1] - first;
         for (uint32_t k0 = 0; k0 < nblk; k0 += SC_WIN_BLOCKS) {
-            // the window: blocks k0 .. k0+15 of the chunk's list
+            // the window: blocks k0 .. k0+15 of the group's list
             if (tid < SC_WIN_BLOCKS) {
                 const uint32_t k = k0 + tid;
                 const uint32_t blk = k < nblk ? a.blk_list[first + k] : 0u;
@@ -633,10 +753,16 @@ void dispatch(const VaBatchArgs& a, cudaStream_t st, std::integer_sequence<int, 
 }  // namespace
 
 size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
-    // PV kernels keep the bounds [1024][vdims] float2 and the staged values
-    // [warps][128][vdims] float in smem
-    const size_t pv = va_batch_pv(kb) ? size_t(va_batch_vdims(kb)) * (1024 * 8 + VB_WARPS * 128 * 4) : 0;
-    return size_t(va_batch_table_words(kb, cells)) * 4 + pv + (mode == 0 ? 1024 * 4 : 1024 * 2 * VB_WARPS);
+    // mirrors the layout at the top of va_batch_kernel
+    const bool pv = va_batch_pv(kb);
+    const size_t vd = va_batch_vdims(kb);
+    size_t bytes = size_t(va_batch_table_words(kb, cells)) * 4;
+    if (pv) bytes += vd * 1024 * 8 + size_t(VB_WARPS) * 128 * vd * 4;   // bounds + staged values
+    if (mode == 2)
+        bytes += size_t(VB_WARPS) * 1024 * 2;
+    else
+        bytes += 1024 * 4 + size_t(VB_WARPS) * VB_QCAP * (4 + (pv ? 0 : 4) + 2);
+    return bytes;
 }
 
 int va_batch_max_dims() { return kVaBatchMaxDims; }
@@ -648,8 +774,6 @@ void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st) {
     using Seq = std::make_integer_sequence<int, kVaBatchMaxDims>;
     if (mode == 0)
         dispatch<0>(a, st, Seq{});
-    else if (mode == 1)
-        dispatch<1>(a, st, Seq{});
     else if (mode == 2)
         dispatch<2>(a, st, Seq{});
     else
@@ -663,14 +787,14 @@ void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st) {
         cudaFuncSetAttribute(vb_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SC_SMEM));
         configured = true;
     }
-    const uint32_t blocks = std::min<uint32_t>(a.nchunks, a.grid);   // one CTA per SM
+    const uint32_t blocks = std::min<uint32_t>(a.ngroups, a.grid);   // one CTA per SM
     vb_scatter_kernel<<<blocks, SC_THREADS, SC_SMEM, st>>>(a);
 }
 
-void launch_va_batch_scans(const VaBatchArgs& a, uint32_t nchunks, uint32_t q0, cudaStream_t st) {
-    vb_chunk_scan_kernel<<<(a.nqp + 31) / 32, 1024, 0, st>>>(a.chunk_counts, nchunks, a.nqp, a.base, a.total);
+void launch_va_batch_scans(const VaBatchArgs& a, uint32_t q0, cudaStream_t st) {
+    vb_chunk_scan_kernel<<<(a.nqp + 31) / 32, 1024, 0, st>>>(a.chunk_counts, a.ngroups, a.nqp, a.base, a.total);
     vb_query_scan_kernel<<<1, 1024, 0, st>>>(a.total, a.nqp, a.offsets, a.counts_all, a.qoff, q0, a.chunk_nblk,
-                                             a.chunk_first, nchunks);
+                                             a.chunk_first, a.nchunks);
 }
 
 void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st) {

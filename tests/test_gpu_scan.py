@@ -260,3 +260,42 @@ def test_vafile_batch_staging_overflow_and_dense_groups(gpu):
                 assert np.array_equal(ids[offs[q]:offs[q + 1]], every), q
             assert np.array_equal(offs[nfull:] - offs[nfull], exp_offs)
             assert np.array_equal(ids[offs[nfull]:].astype(np.int64), exp_ids)
+
+
+_RECOUNT_SCRIPT = r"""
+import sys
+import numpy as np
+import oracle
+import paper_1801_03644_b200 as eng
+rng = np.random.default_rng(3)
+for n, m, nq, s in ((20000, 3, 5, 0.1), (300000, 8, 40, 0.01), (300000, 12, 50, 0.01)):
+    v = rng.random((n, m), dtype=np.float32)
+    w = s ** (1 / m)
+    lo = rng.uniform(0, 1 - w, (nq, m)).astype(np.float32)
+    hi = (lo + w).astype(np.float32)
+    lo[0, 1:] = -np.inf
+    hi[0, 1:] = np.inf
+    ec = oracle.count_batch(v, lo, hi)
+    eo, ei = oracle.ids_batch(v, lo, hi, counts=ec)
+    with eng.DeviceStore(v, layouts=1 | 4) as st:
+        o, i = st.ids(lo, hi, "vafile_batch")
+        assert np.array_equal(o, eo) and np.array_equal(i.astype(np.int64), ei), (n, m, nq, s)
+print("recount ok")
+"""
+
+
+@pytest.mark.parametrize("cap", ["0", "3"])
+def test_vafile_batch_recount_fallback(gpu, cap):
+    """The recount kernel (vabatch.cu mode 2) that replaces the staged
+    single pass when the staging pool overflows: the pool is capped through
+    the MDRQ_VB_STAGING_BLOCKS test hook (read once per process, hence the
+    subprocess), so every pass takes the fallback; ids equal the oracle's for
+    narrow (staged values) and wide (global refinement) unions."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MDRQ_VB_STAGING_BLOCKS=cap, PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _RECOUNT_SCRIPT], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "recount ok" in r.stdout, r.stdout + r.stderr
