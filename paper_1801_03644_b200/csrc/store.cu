@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
 #include <mutex>
 #include <new>
 #include <stdexcept>
@@ -254,8 +256,16 @@ bool is_neg_inf(float v) { return std::isinf(v) && v < 0; }
 bool is_pos_inf(float v) { return std::isinf(v) && v > 0; }
 
 uint16_t host_code(const float* b, uint32_t nb, float v) {
-    // #{b <= v}; b sorted ascending under float compare
-    return uint16_t(std::upper_bound(b, b + nb, v, [](float x, float y) { return x < y; }) - b);
+    // #{b <= v}; b sorted ascending under float compare.  Branch-free binary
+    // search (the prefix b[0..pos) is <= v; grow it by halving steps).
+    uint32_t step = 1;
+    while (step * 2 <= nb) step *= 2;
+    uint32_t pos = 0;
+    for (; step; step >>= 1) {
+        const uint32_t cand = pos + step;
+        pos = (cand <= nb && b[cand - 1] <= v) ? cand : pos;
+    }
+    return uint16_t(pos);
 }
 
 // Passes of the bit-sliced VA batch: <= 1024 queries each; per union
@@ -303,45 +313,47 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
         b->vb_udims.insert(b->vb_udims.end(), ud.begin(), ud.end());
         const bool pv = va_batch_pv(ps.kb);
         const uint32_t qstride = pv ? va_batch_vdims(ps.kb) : ps.kb;
-        std::vector<uint32_t> tab(va_batch_table_words(ps.kb, ps.cells), 0u);
+        const uint32_t cells = ps.cells;
+        std::vector<uint32_t> tab(va_batch_table_words(ps.kb, cells), 0u);
         std::vector<float2> qbv(size_t(1024) * qstride, make_float2(-INFINITY, INFINITY));
+        // word index of (u, c, w): overlap word, and (wide unions) the
+        // containment word right after it
+        auto ov_idx = [&](uint32_t u, uint32_t c, uint32_t w) -> size_t {
+            return pv ? ((size_t(u / 2) * cells + c) * 2 + u % 2) * 32 + w : ((size_t(u) * cells + c) * 32 + w) * 2;
+        };
+        // queries unconstrained in dimension u: every cell, set once per word below
+        std::vector<uint32_t> free_mask(size_t(ps.kb) * 32, 0u);
         for (uint32_t qi = 0; qi < ps.nqp; ++qi) {
             const QueryDesc& qd = b->descs[q0 + qi];
-            std::vector<int> lo_c(ps.kb, -1), hi_c(ps.kb, int(ps.cells)), elo(ps.kb, 0), ehi(ps.kb, 0);
-            std::vector<uint8_t> cons(ps.kb, 0);
+            const uint32_t w = qi >> 5, bit = 1u << (qi & 31);
+            uint32_t constrained = 0;   // bit per union dim (kb <= 24)
             for (uint32_t i = 0; i < qd.k; ++i) {
                 const DimPred& p = b->preds[qd.off + i];
-                const int u = uidx[p.dim];
-                cons[u] = 1;
-                lo_c[u] = int(p.cl) >> ps.shift;
-                hi_c[u] = int(p.ch) >> ps.shift;
-                elo[u] = p.edge_lo;
-                ehi[u] = p.edge_hi;
-                if (p.lo > p.hi) {  // empty interval (kernel level only)
-                    lo_c[u] = int(ps.cells);
-                    hi_c[u] = -1;
-                }
+                const uint32_t u = uint32_t(uidx[p.dim]);
+                constrained |= 1u << u;
                 qbv[size_t(qi) * qstride + u] = make_float2(p.lo, p.hi);
-            }
-            const uint32_t w = qi >> 5, bit = 1u << (qi & 31);
-            for (uint32_t u = 0; u < ps.kb; ++u)
-                for (uint32_t c = 0; c < ps.cells; ++c) {
-                    bool ov = true, su = true;
-                    if (cons[u]) {
-                        ov = int(c) >= lo_c[u] && int(c) <= hi_c[u];
-                        su = ov && (int(c) > lo_c[u] || !elo[u]) && (int(c) < hi_c[u] || !ehi[u]);
-                    }
-                    if (pv) {
-                        // overlap only, rows of dim pairs adjacent (launch.h)
-                        if (ov) tab[((size_t(u / 2) * ps.cells + c) * 2 + u % 2) * 32 + w] |= bit;
-                        continue;
-                    }
-                    // interleaved (overlap, containment) words: [u][c][w][2]
-                    const size_t idx = ((size_t(u) * ps.cells + c) * 32 + w) * 2;
-                    if (ov) tab[idx] |= bit;
-                    if (su) tab[idx + 1] |= bit;
+                if (p.lo > p.hi) continue;   // empty interval (kernel level only): no cell overlaps
+                // overlap cells [lo_c, hi_c]; containment drops the edge cells
+                const int lo_c = int(p.cl) >> ps.shift, hi_c = int(p.ch) >> ps.shift, top = int(cells) - 1;
+                for (int c = std::max(lo_c, 0); c <= std::min(hi_c, top); ++c) tab[ov_idx(u, uint32_t(c), w)] |= bit;
+                if (!pv) {
+                    const int s_lo = lo_c + (p.edge_lo ? 1 : 0), s_hi = hi_c - (p.edge_hi ? 1 : 0);
+                    for (int c = std::max(s_lo, 0); c <= std::min(s_hi, top); ++c)
+                        tab[ov_idx(u, uint32_t(c), w) + 1] |= bit;
                 }
+            }
+            for (uint32_t u = 0; u < ps.kb; ++u)
+                if (!(constrained >> u & 1u)) free_mask[size_t(u) * 32 + w] |= bit;
         }
+        for (uint32_t u = 0; u < ps.kb; ++u)
+            for (uint32_t w = 0; w < 32; ++w) {
+                const uint32_t f = free_mask[size_t(u) * 32 + w];
+                if (!f) continue;
+                for (uint32_t c = 0; c < cells; ++c) {
+                    tab[ov_idx(u, c, w)] |= f;
+                    if (!pv) tab[ov_idx(u, c, w) + 1] |= f;
+                }
+            }
         b->vb_tables.insert(b->vb_tables.end(), tab.begin(), tab.end());
         b->vb_qb.insert(b->vb_qb.end(), qbv.begin(), qbv.end());
         b->vb_passes.push_back(ps);
@@ -364,6 +376,7 @@ void build_descs(const mdrq_store* s, const float* lo, const float* hi, uint32_t
     b->cmask.clear();
     const uint32_t nb = s->nb();
     std::vector<std::pair<float, uint32_t>> order;
+    std::vector<uint32_t> codes(m, 0);   // per dim of the query: code(lo) | code(hi) << 16
     for (uint32_t q = 0; q < nq; ++q) {
         const float* ql = lo + uint64_t(q) * m;
         const float* qh = hi + uint64_t(q) * m;
@@ -383,7 +396,9 @@ void build_descs(const mdrq_store* s, const float* lo, const float* hi, uint32_t
             float est = 1.0f;
             if (nb && !s->h_va_bounds.empty()) {
                 const float* bd = s->h_va_bounds.data() + size_t(j) * nb;
-                est = float(int(host_code(bd, nb, h)) - int(host_code(bd, nb, l)) + 1) / float(nb + 1);
+                const uint16_t cl = host_code(bd, nb, l), ch = host_code(bd, nb, h);
+                codes[j] = uint32_t(cl) | uint32_t(ch) << 16;
+                est = float(int(ch) - int(cl) + 1) / float(nb + 1);
             } else if (!s->h_minmax.empty()) {
                 const float mn = s->h_minmax[2 * j], mx = s->h_minmax[2 * j + 1];
                 const double w = double(mx) - double(mn);
@@ -394,10 +409,13 @@ void build_descs(const mdrq_store* s, const float* lo, const float* hi, uint32_t
             }
             order.emplace_back(path == MDRQ_PATH_ROWWISE ? float(j) : est, j);
         }
-        std::stable_sort(order.begin(), order.end(),
-                         [](const std::pair<float, uint32_t>& x, const std::pair<float, uint32_t>& y) {
-                             return x.first < y.first;
-                         });
+        // stable insertion sort by estimate (a handful of dims; no allocation)
+        for (size_t i = 1; i < order.size(); ++i) {
+            const auto e = order[i];
+            size_t k = i;
+            for (; k > 0 && e.first < order[k - 1].first; --k) order[k] = order[k - 1];
+            order[k] = e;
+        }
         b->descs[q].k = uint32_t(order.size());
         b->descs[q].off = uint32_t(b->preds.size());
         for (auto& e : order) {
@@ -407,9 +425,8 @@ void build_descs(const mdrq_store* s, const float* lo, const float* hi, uint32_t
             p.hi = qh[j];
             p.dim = uint16_t(j);
             if (nb) {
-                const float* bd = s->h_va_bounds.data() + size_t(j) * nb;
-                p.cl = host_code(bd, nb, p.lo);
-                p.ch = host_code(bd, nb, p.hi);
+                p.cl = uint16_t(codes[j] & 0xFFFFu);
+                p.ch = uint16_t(codes[j] >> 16);
                 p.edge_lo = is_neg_inf(p.lo) ? 0 : 1;
                 p.edge_hi = is_pos_inf(p.hi) ? 0 : 1;
                 if (p.lo > p.hi) {  // kernel-level only: empty interval, reject every code
@@ -1051,10 +1068,16 @@ int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper, uint32
         DeviceGuard dg(s->device);
         mdrq_batch* b = &s->scratch;
         b->owner = s;
+        static const bool tdbg = getenv("MDRQ_DEBUG_TIMING") != nullptr;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        const auto t0 = now();
         build_descs(s, lower, upper, nq, resolve_path(s, path, nq, true), true, b);
         if (path == MDRQ_PATH_AUTO) refine_auto_ids(s, b);
+        const auto t1 = now();
         upload_batch(s, b);
+        const auto t2 = now();
         const uint64_t tot = run_ids_sync(s, b);
+        const auto t3 = now();
         *total = tot;
         if (nq && s->n) {
             CK(cudaMemcpyAsync(offsets, b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
@@ -1069,6 +1092,12 @@ int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper, uint32
             CK(cudaMemcpyAsync(ids, s->ids.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost, s->stream));
         }
         CK(cudaStreamSynchronize(s->stream));
+        if (tdbg) {
+            const auto t4 = now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            fprintf(stderr, "query_ids: prepare %.3f upload %.3f run %.3f copy %.3f ms\n", ms(t0, t1), ms(t1, t2),
+                    ms(t2, t3), ms(t3, t4));
+        }
     });
     if (rc == MDRQ_OK && trunc) {
         g_err = "ids buffer too small";
