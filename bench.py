@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto")
-    ap.add_argument("--no-paths", action="store_true", help="skip the per-path cost table")
+    ap.add_argument("--no-paths", action="store_true",
+                    help="skip the per-path cost table and the columnar roofline probe")
     ap.add_argument("--force-merge", action="store_true",
                     help="run the NCCL id merge even with one rank (torchrun --nproc-per-node 1)")
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="tuples per GPU")
@@ -282,14 +283,17 @@ def main():
     stats = store.stats(nq)
     roofline = roofline_of(binfo["path"], prof, stats, n, nq, total_local, peak, peak_kind)
 
-    # ---- the single-query columnar scan kernel (HBM-bound by design), same data
-    col_q = min(nq, 100)
-    cb = store.prepare(lo[:col_q], hi[:col_q], "columnar")
-    cb.reserve()
-    cprof = cb.profile(ids=True, stream=sptr)
-    cstats = store.stats(col_q)
-    col_roof = roofline_of("columnar", cprof, cstats, n, col_q, None, peak, peak_kind)
-    cb.close()
+    # ---- the single-query columnar scan kernel (HBM-bound by design), same
+    # data; skipped with --no-paths so a profiled run holds only the step
+    col_roof = None
+    if not args.no_paths:
+        col_q = min(nq, 100)
+        cb = store.prepare(lo[:col_q], hi[:col_q], "columnar")
+        cb.reserve()
+        cprof = cb.profile(ids=True, stream=sptr)
+        cstats = store.stats(col_q)
+        col_roof = roofline_of("columnar", cprof, cstats, n, col_q, None, peak, peak_kind)
+        cb.close()
 
     # ---- per-path cost at this workload (device time per query)
     paths = {}
@@ -400,8 +404,9 @@ def roofline_of(path, prof, stats, n, nq, total_ids, peak, peak_kind):
     if path.endswith("_batch"):
         passes = max(1, prof["scan"][1])
         if cls == "scan":
-            # filter pass: the union's code planes + (ids mode) one 4-byte
-            # staged (tuple, query) record per match
+            # filter pass: the union's code planes (and, for unions of <= 8
+            # dims, their exact columns, refined on chip) + (ids mode) one
+            # 4-byte staged (tuple, query) record per match
             algo = (loaded + ids_bytes) / passes
         else:
             algo = (2 * ids_bytes) / max(nl, 1)   # records read + ids written

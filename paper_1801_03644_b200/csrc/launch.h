@@ -80,7 +80,8 @@ __host__ __device__ constexpr uint32_t va_batch_cells(uint32_t kb) { return kb <
 // shared memory and refine every overlap candidate exactly, so their table is
 // overlap-only: rows of dims (2p, 2p+1) at cell c are adjacent,
 // word (u, c, w) at ((u/2 * cells + c) * 2 + u%2) * 32 + w.  Their exact
-// bounds are [1024][va_batch_vdims(kb)] float2, padded with (-inf, +inf).
+// bounds are [vdims/2][1024][2] float2 -- float4 (lo, hi of dims 2p, 2p+1)
+// per dim pair p and query -- padded with (-inf, +inf).
 // Wider unions use (overlap, containment) pairs [kb][cells][32][2] and refine
 // only the edge-cell candidates from global memory.
 constexpr uint32_t kVbPvDims = 8;
@@ -100,7 +101,7 @@ struct VaBatchArgs {
     uint32_t nqp;                // queries in this pass (<= 1024)
     const uint16_t* udims;       // [kb]
     const uint32_t* tables;      // query-mask words, layout per va_batch_pv(kb) (above)
-    const float2* qbounds;       // [1024][kb or vdims] exact (lo, hi), +-inf where unconstrained
+    const float2* qbounds;       // exact (lo, hi), +-inf where unconstrained; layout per va_batch_pv(kb)
     uint32_t grid;               // CTAs (chunks = grid * warps)
     uint64_t chunk_tuples;       // tuples per chunk (multiple of 128, < 65536: u16 counters)
     uint32_t nchunks;            // subchunks: ceil(n / chunk_tuples), one warp each

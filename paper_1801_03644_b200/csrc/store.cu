@@ -331,7 +331,10 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
                 const DimPred& p = b->preds[qd.off + i];
                 const uint32_t u = uint32_t(uidx[p.dim]);
                 constrained |= 1u << u;
-                qbv[size_t(qi) * qstride + u] = make_float2(p.lo, p.hi);
+                // narrow unions: dim-pair-major [u/2][1024 queries][2] (lanes
+                // refining different queries hit different banks); wide
+                // unions: query-major [1024][kb]
+                qbv[pv ? (size_t(u / 2) * 1024 + qi) * 2 + u % 2 : size_t(qi) * qstride + u] = make_float2(p.lo, p.hi);
                 if (p.lo > p.hi) continue;   // empty interval (kernel level only): no cell overlaps
                 // overlap cells [lo_c, hi_c]; containment drops the edge cells
                 const int lo_c = int(p.cl) >> ps.shift, hi_c = int(p.ch) >> ps.shift, top = int(cells) - 1;
@@ -1135,11 +1138,13 @@ int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats, uint32_t
         CK(cudaStreamSynchronize(s->stream));
         const uint32_t path = b->path;
         // multi-query passes: the union's planes / columns, shared by the pass
+        // (narrow VA unions also stream the union's exact columns for the
+        // on-chip refinement: 1 + 4 bytes per tuple and dimension)
         std::vector<uint64_t> pass_bytes(nq, 0);
         if (path == MDRQ_PATH_VAFILE_BATCH) {
             for (const VbPass& p : b->vb_passes)
                 for (uint32_t q = p.q0; q < p.q0 + p.nqp; ++q)
-                    pass_bytes[q] = p.fallback ? 0 : (s->n * p.kb) / p.nqp;
+                    pass_bytes[q] = p.fallback ? 0 : (s->n * p.kb * (va_batch_pv(p.kb) ? 5 : 1)) / p.nqp;
         } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
             for (const Pass& p : b->passes)
                 for (uint32_t q = p.q0; q < p.q0 + p.nqp; ++q)

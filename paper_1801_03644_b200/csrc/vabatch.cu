@@ -64,19 +64,18 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     constexpr bool DENSE = MODE != 2;              // candidates refined lane-parallel from a queue
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_end = sm + va_batch_table_words(KB, K);
-    // PV: exact query bounds [1024][KBV/2] float4 (lo_u, hi_u, lo_u+1, hi_u+1)
-    // and every warp's staged block values [128 * H] float4
+    // PV: exact query bounds [KBV/2][1024] float4 (lo_u, hi_u, lo_u+1, hi_u+1
+    // of dim pair u/2) and every warp's staged block values [128 * H] float4
     float4* s_qb = reinterpret_cast<float4*>(s_end);
     float4* s_val = s_qb + (PV ? 1024 * KBV / 2 : 0);
     uint32_t* s_rest = reinterpret_cast<uint32_t*>(s_val + (PV ? VB_WARPS * 128 * H : 0));
     // DENSE (modes 0, 3): CTA counters u32 [1024], then every warp's candidate
-    // queue: overlap words [QCAP], (wide unions) containment words [QCAP],
-    // meta u16 [QCAP] = tuple-in-block << 5 | query word.
+    // queue: entries uint2 [QCAP] = (overlap word, tuple-in-block << 5 | query
+    // word), (wide unions) containment words u32 [QCAP].
     // MODE 2: per-warp counters u16 [warps][1024].
     uint32_t* s_cnt32 = s_rest;
-    uint32_t* s_qw = s_rest + 1024;
-    uint32_t* s_qs = s_qw + VB_WARPS * VB_QCAP;
-    uint16_t* s_qm = reinterpret_cast<uint16_t*>(s_qs + (PV ? 0 : VB_WARPS * VB_QCAP));
+    uint2* s_qe = reinterpret_cast<uint2*>(s_rest + 1024);
+    uint32_t* s_qs = reinterpret_cast<uint32_t*>(s_qe + VB_WARPS * VB_QCAP);
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_rest);
 
     // the recount pass only runs when the single-pass staging overflowed
@@ -107,9 +106,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     const uint32_t lane_off = lane * (PV ? 4 : 8);
     const char* s_tab = reinterpret_cast<const char*>(sm);
     float4* wval = s_val + warp * 128 * H;         // PV: this warp's staged values
-    uint32_t* qw = s_qw + warp * VB_QCAP;
+    uint2* qe = s_qe + warp * VB_QCAP;
     uint32_t* qs = s_qs + warp * VB_QCAP;
-    uint16_t* qm = s_qm + warp * VB_QCAP;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 2
     const uint32_t lt = lanemask_lt();
 
@@ -139,10 +137,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 r &= r - 1;
                 bool ok = true;
                 if constexpr (PV) {
-                    const float4* qq = s_qb + (wq + b) * (KBV / 2);
+                    const float4* qq = s_qb + (wq + b);
 #pragma unroll
                     for (int u2 = 0; u2 < KBV / 2; ++u2) {
-                        const float4 bb = qq[u2];
+                        const float4 bb = qq[u2 * 1024];
                         ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
                              (v[2 * u2 + 1] <= bb.w);
                     }
@@ -272,9 +270,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             uint32_t blk = kNoBlock, fill = 0, nblk = 0;   // MODE 3 staging state of the subchunk
             auto process = [&](uint32_t e0, uint32_t cnt) {
                 const bool act = lane < cnt;
-                const uint32_t word = act ? qw[e0 + lane] : 0u;
+                const uint2 ent = act ? qe[e0 + lane] : make_uint2(0u, 0u);
+                const uint32_t word = ent.x, meta = ent.y;
                 const uint32_t su = (!PV && act) ? qs[e0 + lane] : 0u;
-                const uint32_t meta = act ? qm[e0 + lane] : 0u;
                 const uint32_t tl = meta >> 5, wq = (meta & 31u) * 32;
                 const uint64_t t = blk_t0 + tl;
                 uint32_t hits = refine_word(word, su, tl, t, wq);
@@ -356,9 +354,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, nz);
                         if (nz) {
                             const uint32_t slot = qn + __popc(bal & lt);
-                            qw[slot] = ov4[jj];
+                            qe[slot] = make_uint2(ov4[jj], ((j4 + jj) << 5) | lane);
                             if constexpr (!PV) qs[slot] = su4[jj];
-                            qm[slot] = uint16_t(((j4 + jj) << 5) | lane);
                         }
                         qn += __popc(bal);
                     }
@@ -368,17 +365,16 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         for (; e0 + 32 <= qn; e0 += 32) process(e0, 32);
                         // move the < 32 remaining entries to the front
                         const uint32_t rem = qn - e0;
-                        uint32_t mw = 0, ms = 0, mm = 0;
+                        uint2 me = make_uint2(0u, 0u);
+                        uint32_t ms = 0;
                         if (lane < rem) {
-                            mw = qw[e0 + lane];
+                            me = qe[e0 + lane];
                             if constexpr (!PV) ms = qs[e0 + lane];
-                            mm = qm[e0 + lane];
                         }
                         __syncwarp();
                         if (lane < rem) {
-                            qw[lane] = mw;
+                            qe[lane] = me;
                             if constexpr (!PV) qs[lane] = ms;
-                            qm[lane] = uint16_t(mm);
                         }
                         __syncwarp();
                         qn = rem;
@@ -761,7 +757,7 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
     if (mode == 2)
         bytes += size_t(VB_WARPS) * 1024 * 2;
     else
-        bytes += 1024 * 4 + size_t(VB_WARPS) * VB_QCAP * (4 + (pv ? 0 : 4) + 2);
+        bytes += 1024 * 4 + size_t(VB_WARPS) * VB_QCAP * (8 + (pv ? 0 : 4));
     return bytes;
 }
 

@@ -11,11 +11,14 @@ echo "plain=$?" >> $OUT/rc.txt
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches.csv $B > $OUT/ncu_launches.log 2>&1
 echo "launches=$?" >> $OUT/rc.txt
+# the second ids pass of the batch (the first one sizes the result pool):
+# launches 4..5 of the filter / scatter kernels = mode 3 filter + scatter
 timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"va_batch_kernel|vb_scatter" -c 3 -o $OUT/prof_vab $B > $OUT/ncu_vab.log 2>&1
+    -k regex:"va_batch_kernel|vb_scatter" -s 3 -c 2 -o $OUT/prof_vab $B > $OUT/ncu_vab.log 2>&1
 echo "vab=$?" >> $OUT/rc.txt
-timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:col_scan_kernel -s 10 -c 1 -o $OUT/prof_col $B > $OUT/ncu_col.log 2>&1
+C="python tools/probe_path.py columnar ids 20"
+$C > $OUT/probe_col.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on \
+    -k regex:col_scan_kernel -s 10 -c 1 -o $OUT/prof_col $C > $OUT/ncu_col.log 2>&1
 echo "col=$?" >> $OUT/rc.txt
 P="python tools/probe_path.py rowwise count 3"
 $P > $OUT/probe_row.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on \
