@@ -282,6 +282,9 @@ def main():
     prof = batch.profile(ids=True, stream=sptr)
     stats = store.stats(nq)
     roofline = roofline_of(binfo["path"], prof, stats, n, nq, total_local, peak, peak_kind)
+    if binfo["path"] == "vafile_batch":
+        key = f"va_batch_kernel<3, {binfo['max_union_dims']}>" if roofline["class"] == "scan" else "vb_scatter_kernel"
+        roofline.update(ncu_traffic(key))
 
     # ---- the single-query columnar scan kernel (HBM-bound by design), same
     # data; skipped with --no-paths so a profiled run holds only the step
@@ -293,6 +296,7 @@ def main():
         cprof = cb.profile(ids=True, stream=sptr)
         cstats = store.stats(col_q)
         col_roof = roofline_of("columnar", cprof, cstats, n, col_q, None, peak, peak_kind)
+        col_roof.update(ncu_traffic("col_scan_kernel<1>"))
         cb.close()
 
     # ---- per-path cost at this workload (device time per query)
@@ -387,6 +391,20 @@ def smem_roofline(binfo, prof, n, clocks):
     return {"resource": "shared-memory wavefronts (table rows)", "achieved": achieved, "peak": peak,
             "unit": "wavefronts/s", "frac": achieved / peak, "algo_wavefronts_per_launch": wavefronts,
             "sm_mhz": mhz}
+
+
+def ncu_traffic(kernel: str) -> dict:
+    """DRAM read + write bytes per launch of `kernel` from the newest committed
+    ncu --set full capture (profiles/rNN_traffic.json, written from the
+    round's tools/profile_round.sh captures); null when not captured."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        with open(f) as fh:
+            d = json.load(fh)
+        if kernel in d:
+            return {"traffic": float(d[kernel]), "traffic_source": f"{os.path.relpath(f, ROOT)}: {kernel}"}
+    return {"traffic": None}
 
 
 def roofline_of(path, prof, stats, n, nq, total_ids, peak, peak_kind):
