@@ -143,6 +143,20 @@ int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper,
                    uint32_t nq, uint32_t path, uint64_t* offsets,
                    uint32_t* ids, uint64_t ids_cap, uint64_t* total);
 int mdrq_fetch_ids(mdrq_store* s, uint32_t* ids, uint64_t ids_cap);
+/* A stream of nbatches ids batches (replaces the reference's loop of
+ * search_batch / search calls over successive query batches, bench.py:178-186,
+ * methods.py search_batch): batch k holds nqs[k] queries, its bounds follow
+ * batch k-1's in lower/upper.  Results go to offsets_out[k] (nqs[k]+1) and
+ * ids_out[k] (capacity ids_caps[k]); totals[k] = its id count.  Batches are
+ * pipelined: batch k's device->host copies overlap batch k+1's scan (three
+ * slots with their own result pools, a copy stream).  Returns MDRQ_ETRUNC
+ * when some totals[k] > ids_caps[k] (that batch's ids are not copied; the
+ * rest are).  *h2d_bytes (optional) = query descriptor bytes uploaded.     */
+int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
+                          const uint32_t* nqs, uint32_t nbatches, uint32_t path,
+                          uint64_t* const* offsets_out, uint32_t* const* ids_out,
+                          const uint64_t* ids_caps, uint64_t* totals,
+                          uint64_t* h2d_bytes);
 /* SearchStats of the last count/ids call, one entry per query.            */
 int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats,
                      uint32_t nq);

@@ -186,7 +186,21 @@ struct mdrq_batch {
     DBuf<unsigned long long> d_offsets;
     DBuf<unsigned long long> d_stats;
     DBuf<unsigned long long> d_partials;   // [nq][kPartialSlots][4]
+    // result pool of its own (stream slots); otherwise the store's pool
+    bool own_pool = false;
+    DBuf<uint32_t> own_ids;
 };
+
+// One slot of the pipelined ids stream (mdrq_query_ids_stream): a batch with
+// its own result pool, the events that order it, and a pinned mirror of its
+// total / staging-overflow flag.
+struct StreamSlot {
+    mdrq_batch b;
+    cudaEvent_t comp = nullptr, copy = nullptr;
+    unsigned long long* h_flags = nullptr;   // pinned [2]: total, overflow
+    bool busy = false;                       // a D2H of this slot is in flight
+};
+constexpr int kStreamSlots = 3;
 
 struct mdrq_store {
     int device = 0;
@@ -219,6 +233,23 @@ struct mdrq_store {
     mdrq_batch* last_batch = nullptr;
     mdrq_batch scratch;
     std::mutex mu;
+    // pipelined ids stream: a copy stream + slots, created on first use
+    cudaStream_t copy_stream = nullptr;
+    StreamSlot* slots = nullptr;
+    ~mdrq_store() {
+        if (slots) {
+            for (int i = 0; i < kStreamSlots; ++i) {
+                if (slots[i].comp) cudaEventDestroy(slots[i].comp);
+                if (slots[i].copy) cudaEventDestroy(slots[i].copy);
+                if (slots[i].h_flags) cudaFreeHost(slots[i].h_flags);
+            }
+            delete[] slots;
+        }
+        if (copy_stream) {
+            cudaStreamSynchronize(copy_stream);
+            cudaStreamDestroy(copy_stream);
+        }
+    }
 
     uint32_t nb() const { return va_bits ? ((1u << va_bits) - 1u) : 0u; }
     uint32_t tiles_for(uint32_t path) const {
@@ -496,7 +527,7 @@ void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
     if (!h.empty()) CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
 }
 
-void upload_batch(mdrq_store* s, mdrq_batch* b) {
+void upload_batch(mdrq_store* s, mdrq_batch* b, bool sync = true) {
     upload(b->d_descs, b->descs, s->stream);
     upload(b->d_preds, b->preds, s->stream);
     upload(b->d_udims, b->udims, s->stream);
@@ -511,8 +542,16 @@ void upload_batch(mdrq_store* s, mdrq_batch* b) {
     b->d_stats.reserve(size_t(b->nq) * 4);
     b->d_partials.reserve(size_t(b->nq) * kPartialSlots * 4);
     // H2D copies above may read pageable host vectors that a later rebuild
-    // mutates: make them complete before returning.
-    CK(cudaStreamSynchronize(s->stream));
+    // mutates: make them complete before returning (the ids stream rebuilds
+    // a slot only after its previous pass and copies completed).
+    if (sync) CK(cudaStreamSynchronize(s->stream));
+}
+
+uint64_t upload_bytes(const mdrq_batch* b) {
+    return b->descs.size() * sizeof(QueryDesc) + b->preds.size() * sizeof(DimPred) +
+           b->udims.size() * sizeof(uint16_t) + b->bounds.size() * sizeof(float2) +
+           b->cmask.size() * sizeof(unsigned long long) + b->vb_udims.size() * sizeof(uint16_t) +
+           b->vb_tables.size() * sizeof(uint32_t) + b->vb_qb.size() * sizeof(float2);
 }
 
 uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
@@ -567,6 +606,9 @@ void refine_auto_ids(const mdrq_store* s, mdrq_batch* b) {
     if (kb > 8 && est / b->nq > 5e-3) b->path = MDRQ_PATH_VAFILE;
 }
 
+// the result pool a batch writes: its own (stream slots) or the store's
+DBuf<uint32_t>& pool_of(mdrq_store* s, mdrq_batch* b) { return b->own_pool ? b->own_ids : s->ids; }
+
 ScanArgs base_args(mdrq_store* s, mdrq_batch* b, uint32_t path) {
     ScanArgs a{};
     a.cols = s->cols.p;
@@ -583,8 +625,8 @@ ScanArgs base_args(mdrq_store* s, mdrq_batch* b, uint32_t path) {
     a.status = s->status.p;
     a.counts = b->d_counts.p;
     a.offsets = b->d_offsets.p;
-    a.ids = s->ids.p;
-    a.ids_cap = s->ids.p ? s->ids.cap : 0;
+    a.ids = pool_of(s, b).p;
+    a.ids_cap = pool_of(s, b).p ? pool_of(s, b).cap : 0;
     a.id_base = s->id_base;
     a.stats = b->d_stats.p;
     a.mask = s->mask.p;
@@ -626,8 +668,8 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.qoff = s->vb_qoff.p;
     a.offsets = b->d_offsets.p;
     a.counts_all = b->d_counts.p;
-    a.ids = s->ids.p;
-    a.ids_cap = s->ids.p ? s->ids.cap : 0;
+    a.ids = pool_of(s, b).p;
+    a.ids_cap = pool_of(s, b).p ? pool_of(s, b).cap : 0;
     a.id_base = s->id_base;
     s->vb_rec.reserve(size_t(s->vb_max_blocks) * kRecBlock);
     s->vb_blk_count.reserve(s->vb_max_blocks);
@@ -826,6 +868,18 @@ uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
 }
 
 // Run an ids pass synchronously, growing the result pool until it fits.
+// The single-pass VA staging ran out (the recount pass kept the result
+// correct): give the next passes twice the pool.
+void grow_vb_staging(mdrq_store* s) {
+    if (s->vb_max_blocks >= (1u << 22)) return;
+    s->vb_max_blocks *= 2;
+    s->vb_rec.release();
+    s->vb_blk_count.release();
+    s->vb_blk_chunk.release();
+    s->vb_blk_seq.release();
+    s->vb_blk_list.release();
+}
+
 uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
     for (int attempt = 0; attempt < 2; ++attempt) {
         enqueue(s, b, true, s->stream);
@@ -837,24 +891,16 @@ uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
             CK(cudaMemcpyAsync(&overflowed, s->vb_flags.p + 1, sizeof(overflowed), cudaMemcpyDeviceToHost,
                                s->stream));
         CK(cudaStreamSynchronize(s->stream));
-        if (overflowed && s->vb_max_blocks < (1u << 22)) {
-            // the single-pass staging ran out (the recount pass kept the result
-            // correct): give the next passes twice the pool
-            s->vb_max_blocks *= 2;
-            s->vb_rec.release();
-            s->vb_blk_count.release();
-            s->vb_blk_chunk.release();
-            s->vb_blk_seq.release();
-            s->vb_blk_list.release();
-        }
-        if (total <= (s->ids.p ? s->ids.cap : 0)) {
+        if (overflowed) grow_vb_staging(s);
+        DBuf<uint32_t>& pool = pool_of(s, b);
+        if (total <= (pool.p ? pool.cap : 0)) {
             s->last_total = total;
             s->last_nq = b->nq;
             s->last_path = b->path;
             s->last_batch = b;
             return total;
         }
-        s->ids.reserve(size_t(total + total / 8 + 4096));
+        pool.reserve(size_t(total + total / 8 + 4096));
     }
     raise(MDRQ_ECUDA, "result pool did not converge");
 }
@@ -1104,6 +1150,104 @@ int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper, uint32
     });
     if (rc == MDRQ_OK && trunc) {
         g_err = "ids buffer too small";
+        return MDRQ_ETRUNC;
+    }
+    return rc;
+}
+
+int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper, const uint32_t* nqs,
+                          uint32_t nbatches, uint32_t path, uint64_t* const* offsets_out, uint32_t* const* ids_out,
+                          const uint64_t* ids_caps, uint64_t* totals, uint64_t* h2d_bytes) {
+    int trunc = 0;
+    int rc = guard([&] {
+        check_store(s);
+        if (nbatches && (!nqs || !offsets_out || !ids_out || !ids_caps || !totals)) raise(MDRQ_EINVAL, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        std::vector<uint64_t> q0(size_t(nbatches) + 1, 0);
+        for (uint32_t k = 0; k < nbatches; ++k) {
+            q0[k + 1] = q0[k] + nqs[k];
+            if (nqs[k] && (!lower || !upper)) raise(MDRQ_EINVAL, "null bounds");
+        }
+        if (!s->slots) {
+            CK(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+            s->slots = new StreamSlot[kStreamSlots];
+            for (int i = 0; i < kStreamSlots; ++i) {
+                CK(cudaEventCreateWithFlags(&s->slots[i].comp, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&s->slots[i].copy, cudaEventDisableTiming));
+                CK(cudaMallocHost(reinterpret_cast<void**>(&s->slots[i].h_flags), 2 * sizeof(unsigned long long)));
+                s->slots[i].b.owner = s;
+                s->slots[i].b.own_pool = true;
+            }
+        }
+        uint64_t up = 0;
+        // batch k: host build + H2D + filter/scatter on the store stream,
+        // total and overflow flag mirrored to pinned memory
+        auto launch = [&](uint32_t k) {
+            StreamSlot& sl = s->slots[k % kStreamSlots];
+            if (sl.busy) {
+                CK(cudaEventSynchronize(sl.copy));   // batch k-3's results have left the slot
+                sl.busy = false;
+            }
+            mdrq_batch* b = &sl.b;
+            const uint32_t nq = nqs[k];
+            build_descs(s, lower + q0[k] * s->m, upper + q0[k] * s->m, nq, resolve_path(s, path, nq, true), true, b);
+            if (path == MDRQ_PATH_AUTO) refine_auto_ids(s, b);
+            upload_batch(s, b, false);
+            up += upload_bytes(b);
+            enqueue(s, b, true, s->stream);
+            sl.h_flags[0] = sl.h_flags[1] = 0;
+            if (nq && s->n) {
+                CK(cudaMemcpyAsync(sl.h_flags, b->d_offsets.p + nq, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   s->stream));
+                if (b->path == MDRQ_PATH_VAFILE_BATCH && s->vb_flags.p)
+                    CK(cudaMemcpyAsync(sl.h_flags + 1, s->vb_flags.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                       s->stream));
+            }
+            CK(cudaEventRecord(sl.comp, s->stream));
+        };
+        // batch k's results to the caller on the copy stream, while batch
+        // k+1 runs on the store stream
+        auto finish = [&](uint32_t k) {
+            StreamSlot& sl = s->slots[k % kStreamSlots];
+            mdrq_batch* b = &sl.b;
+            const uint32_t nq = nqs[k];
+            CK(cudaEventSynchronize(sl.comp));
+            const uint64_t total = sl.h_flags[0];
+            if (sl.h_flags[1]) grow_vb_staging(s);
+            DBuf<uint32_t>& pool = b->own_ids;
+            if (total > (pool.p ? pool.cap : 0)) {
+                // the slot's pool was too small: grow it and run the batch again
+                pool.reserve(size_t(total + total / 8 + 4096));
+                enqueue(s, b, true, s->stream);
+                CK(cudaEventRecord(sl.comp, s->stream));
+            }
+            totals[k] = total;
+            CK(cudaStreamWaitEvent(s->copy_stream, sl.comp, 0));
+            if (nq && s->n)
+                CK(cudaMemcpyAsync(offsets_out[k], b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
+                                   s->copy_stream));
+            else
+                std::memset(offsets_out[k], 0, sizeof(uint64_t) * (size_t(nq) + 1));
+            if (total > ids_caps[k])
+                trunc = 1;
+            else if (total)
+                CK(cudaMemcpyAsync(ids_out[k], pool.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost,
+                                   s->copy_stream));
+            CK(cudaEventRecord(sl.copy, s->copy_stream));
+            sl.busy = true;
+        };
+        for (uint32_t k = 0; k < nbatches; ++k) {
+            launch(k);
+            if (k) finish(k - 1);
+        }
+        if (nbatches) finish(nbatches - 1);
+        CK(cudaStreamSynchronize(s->copy_stream));
+        for (int i = 0; i < kStreamSlots; ++i) s->slots[i].busy = false;
+        if (h2d_bytes) *h2d_bytes = up;
+    });
+    if (rc == MDRQ_OK && trunc) {
+        g_err = "ids buffer too small for at least one batch (see totals)";
         return MDRQ_ETRUNC;
     }
     return rc;

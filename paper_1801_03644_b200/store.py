@@ -173,6 +173,54 @@ class DeviceStore:
             check(rc)
         return offsets.astype(np.int64), buf[: int(total.value)]
 
+    def ids_stream(self, batches, path: str | int = "auto", outs=None, info: dict | None = None):
+        """Pipelined ids for a sequence of query batches ``[(lower, upper),
+        ...]`` -> list of ``(offsets int64[nq+1], ids uint32[total])``, one per
+        batch, each exactly what :meth:`ids` returns for it.  Batch k's
+        device->host copies overlap batch k+1's scan (mdrq_query_ids_stream).
+
+        ``outs`` optionally gives one caller-owned (e.g. pinned) uint32 buffer
+        per batch; a batch that does not fit its buffer raises ValueError.
+        ``info``, when a dict, receives ``h2d_bytes`` (descriptor bytes
+        uploaded) and ``totals``.
+        """
+        lib = _lib.load()
+        pairs = [_bounds(lo, hi, self.m) for lo, hi in batches]
+        nb = len(pairs)
+        if nb == 0:
+            return []
+        if outs is not None and len(outs) != nb:
+            raise ValueError(f"{len(outs)} output buffers for {nb} batches")
+        nqs = np.array([p[0].shape[0] for p in pairs], np.uint32)
+        lo_all = np.ascontiguousarray(np.concatenate([p[0] for p in pairs]), np.float32)
+        hi_all = np.ascontiguousarray(np.concatenate([p[1] for p in pairs]), np.float32)
+        offs = [np.zeros(int(q) + 1, np.uint64) for q in nqs]
+        bufs = list(outs) if outs is not None else [np.empty(max(1, _guess(self.n, int(q))), np.uint32)
+                                                    for q in nqs]
+        caps = np.array([b.size for b in bufs], np.uint64)
+        totals = np.zeros(nb, np.uint64)
+        h2d = ctypes.c_uint64(0)
+        offs_p = (u64p * nb)(*[o.ctypes.data_as(u64p) for o in offs])
+        ids_p = (u32p * nb)(*[b.ctypes.data_as(u32p) for b in bufs])
+        rc = lib.mdrq_query_ids_stream(self.handle, lo_all.ctypes.data_as(f32p), hi_all.ctypes.data_as(f32p),
+                                       nqs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), nb, _path(path),
+                                       offs_p, ids_p, caps.ctypes.data_as(u64p), totals.ctypes.data_as(u64p),
+                                       ctypes.byref(h2d))
+        if rc != _lib.MDRQ_ETRUNC:
+            check(rc)
+        out = []
+        for k in range(nb):
+            if totals[k] > caps[k]:
+                if outs is not None:
+                    raise ValueError(f"ids buffer {k} holds {caps[k]} ids, the batch produced {totals[k]}")
+                out.append(self.ids(pairs[k][0], pairs[k][1], path))   # rare: the size guess was short
+            else:
+                out.append((offs[k].astype(np.int64), bufs[k][: int(totals[k])]))
+        if info is not None:
+            info["h2d_bytes"] = int(h2d.value)
+            info["totals"] = [int(t) for t in totals]
+        return out
+
     def stats(self, nq: int, mode: int = _lib.MODE_SCALAR):
         arr = (_lib.SearchStatsC * max(nq, 1))()
         check(_lib.load().mdrq_query_stats(self.handle, mode, arr, nq))

@@ -299,3 +299,36 @@ def test_vafile_batch_recount_fallback(gpu, cap):
     r = subprocess.run([sys.executable, "-c", _RECOUNT_SCRIPT], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "recount ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_ids_stream_pipelined_batches(gpu):
+    """DeviceStore.ids_stream (mdrq_query_ids_stream): several batches of
+    different sizes and paths through the three pipelined slots (slot reuse,
+    first-use pool growth, an empty batch) equal the oracle batch by batch;
+    a caller buffer that is too small raises."""
+    rng = np.random.default_rng(11)
+    n, m = 300_000, 6
+    values = rng.random((n, m), dtype=np.float32)
+    batches = []
+    for nq, s in ((70, 1e-2), (5, 1e-1), (0, 1e-3), (130, 1e-3), (64, 1e-2), (1, 0.5), (200, 1e-3)):
+        w = s ** (1 / m)
+        lo = rng.uniform(0, 1 - w, (nq, m)).astype(np.float32)
+        hi = (lo + w).astype(np.float32)
+        if nq > 2:
+            lo[1, 2:] = -np.inf
+            hi[1, 2:] = np.inf
+        batches.append((lo, hi))
+    with gpu.DeviceStore(values, layouts=1 | 2 | 4) as st:
+        for path in ("auto", "vafile_batch", "columnar"):
+            info = {}
+            res = st.ids_stream(batches, path, info=info)
+            assert len(res) == len(batches) and info["h2d_bytes"] > 0
+            for (lo, hi), (offs, ids) in zip(batches, res):
+                if lo.shape[0] == 0:
+                    assert offs.tolist() == [0] and ids.size == 0
+                    continue
+                ec = oracle.count_batch(values, lo, hi)
+                eo, ei = oracle.ids_batch(values, lo, hi, counts=ec)
+                assert np.array_equal(offs, eo) and np.array_equal(ids.astype(np.int64), ei), path
+        with pytest.raises(ValueError, match="ids buffer"):
+            st.ids_stream(batches[:2], "vafile_batch", outs=[np.empty(10, np.uint32)] * 2)
