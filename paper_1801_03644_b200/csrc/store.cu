@@ -869,10 +869,25 @@ uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
 
 // Run an ids pass synchronously, growing the result pool until it fits.
 // The single-pass VA staging ran out (the recount pass kept the result
-// correct): give the next passes twice the pool.
-void grow_vb_staging(mdrq_store* s) {
-    if (s->vb_max_blocks >= (1u << 22)) return;
-    s->vb_max_blocks *= 2;
+// correct): size the pool for the pass's `total` records (one per match,
+// + ~10 % for partly filled blocks, + one partial block per subchunk), at
+// least twice the current pool, within 2^24 blocks (64 GB) and what the
+// device has free beyond a 2 GB reserve.
+void grow_vb_staging(mdrq_store* s, uint64_t total) {
+    constexpr uint64_t kMaxBlocks = 1ull << 24;
+    const uint64_t per_block = uint64_t(kRecBlock) * 4 + 4 * sizeof(uint32_t);
+    uint64_t want = std::max<uint64_t>(2ull * s->vb_max_blocks,
+                                       total / kRecBlock + total / (10 * kRecBlock) + 2ull * 16 * s->num_sms + 64);
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        // the current pool is released first, so its bytes count as free
+        const uint64_t avail = free_b + uint64_t(s->vb_max_blocks) * per_block;
+        const uint64_t reserve = 2ull << 30;
+        want = std::min<uint64_t>(want, avail > reserve ? (avail - reserve) / per_block : 0);
+    }
+    want = std::min<uint64_t>(want, kMaxBlocks);
+    if (want <= s->vb_max_blocks) return;
+    s->vb_max_blocks = uint32_t(want);
     s->vb_rec.release();
     s->vb_blk_count.release();
     s->vb_blk_chunk.release();
@@ -891,7 +906,7 @@ uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
             CK(cudaMemcpyAsync(&overflowed, s->vb_flags.p + 1, sizeof(overflowed), cudaMemcpyDeviceToHost,
                                s->stream));
         CK(cudaStreamSynchronize(s->stream));
-        if (overflowed) grow_vb_staging(s);
+        if (overflowed) grow_vb_staging(s, total);
         DBuf<uint32_t>& pool = pool_of(s, b);
         if (total <= (pool.p ? pool.cap : 0)) {
             s->last_total = total;
@@ -1214,7 +1229,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             const uint32_t nq = nqs[k];
             CK(cudaEventSynchronize(sl.comp));
             const uint64_t total = sl.h_flags[0];
-            if (sl.h_flags[1]) grow_vb_staging(s);
+            if (sl.h_flags[1]) grow_vb_staging(s, total);
             DBuf<uint32_t>& pool = b->own_ids;
             if (total > (pool.p ? pool.cap : 0)) {
                 // the slot's pool was too small: grow it and run the batch again

@@ -7,6 +7,12 @@ from collections import Counter
 
 rows = list(csv.reader(open(sys.argv[1])))
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+which = int(sys.argv[3]) if len(sys.argv) > 3 else 0   # kernel index in a multi-kernel export
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+a = starts[which]
+b = starts[which + 1] if which + 1 < len(starts) else len(rows)
+print("kernel:", rows[a][1][:100])
+rows = rows[a:b]
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
 body = [r for r in rows[2:] if len(r) == len(hdr)]
