@@ -332,3 +332,25 @@ def test_ids_stream_pipelined_batches(gpu):
                 assert np.array_equal(offs, eo) and np.array_equal(ids.astype(np.int64), ei), path
         with pytest.raises(ValueError, match="ids buffer"):
             st.ids_stream(batches[:2], "vafile_batch", outs=[np.empty(10, np.uint32)] * 2)
+
+
+@pytest.mark.parametrize("m", [3, 8, 11])
+def test_vafile_batch_multi_pass_vs_oracle(gpu, m):
+    """More queries than one bit-sliced pass holds (1 024): three passes, the
+    last one partial, narrow (on-chip refinement) and wide (containment
+    rows) unions, selectivities from 1e-4 to 5e-2, partial-match and point
+    predicates; counts and ids equal the oracle's."""
+    rng = np.random.default_rng(40 + m)
+    n, nq = 200_000, 2100
+    v = rng.random((n, m), dtype=np.float32)
+    v[::97] = v[1::97][: v[::97].shape[0]]   # duplicate rows
+    s = 10 ** rng.uniform(-4, np.log10(5e-2), nq)
+    w = (s ** (1.0 / m)).astype(np.float32)[:, None]
+    lo = (rng.random((nq, m)) * (1 - w)).astype(np.float32)
+    hi = (lo + w).astype(np.float32)
+    free = rng.random((nq, m)) < 0.25
+    lo[free] = -np.inf
+    hi[free] = np.inf
+    pts = rng.integers(0, n, nq // 10)
+    lo[: nq // 10, 0] = hi[: nq // 10, 0] = v[pts, 0]
+    check_store(gpu, v, lo, hi, paths=("vafile_batch",))
