@@ -557,12 +557,13 @@ uint64_t upload_bytes(const mdrq_batch* b) {
 uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
     if (path == MDRQ_PATH_AUTO) {
         // planner, from the B200 per-query costs of C2:
-        // a bit-sliced VA pass costs about as much as ~50 single-query VA
-        // scans, so it wins from 64 queries on; below that one query per
-        // pass over the code planes (VA) or the columns.
+        // a bit-sliced VA pass costs about as much as ~18 single-query VA
+        // scans (2.2 ms vs 119-143 us at 8..32 queries), so it wins from 20
+        // queries on; below that one query per pass over the code planes
+        // (VA) or the columns.
         const bool va = (s->layouts & MDRQ_LAYOUT_VAFILE) != 0;
         if (!(s->layouts & MDRQ_LAYOUT_COLUMNAR)) return MDRQ_PATH_ROWWISE;
-        if (va && nq >= 64) return MDRQ_PATH_VAFILE_BATCH;
+        if (va && nq >= 20) return MDRQ_PATH_VAFILE_BATCH;
         if (va) return MDRQ_PATH_VAFILE;
         if (!ids && nq >= 2) return MDRQ_PATH_COLUMNAR_BATCH;
         return MDRQ_PATH_COLUMNAR;
@@ -581,29 +582,6 @@ uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids)
             return path;
         default: raise(MDRQ_EINVAL, "unknown query path " + std::to_string(path));
     }
-}
-
-// Ids mode of an AUTO batch planned as a bit-sliced pass: when the queries
-// are expected to return many ids (estimated from the VA code ranges under
-// independence), the per-query path's bitmask compaction beats staging one
-// record per match (C3 in profiles/r01_configs.json), so switch to it.
-void refine_auto_ids(const mdrq_store* s, mdrq_batch* b) {
-    if (b->path != MDRQ_PATH_VAFILE_BATCH || !b->nq) return;
-    const double cells = double(s->nb() + 1);
-    double est = 0.0;
-    for (uint32_t q = 0; q < b->nq; ++q) {
-        double sel = 1.0;
-        for (uint32_t i = 0; i < b->descs[q].k; ++i) {
-            const DimPred& p = b->preds[b->descs[q].off + i];
-            sel *= p.ch >= p.cl ? double(p.ch - p.cl + 1) / cells : 0.0;
-        }
-        est += sel;
-    }
-    // narrow unions (<= 8 dims) keep values and bounds on chip and stay
-    // ahead even at 1e-2 (C2); wide unions lose from ~5e-3 on (C3)
-    uint32_t kb = 0;
-    for (const VbPass& p : b->vb_passes) kb = std::max(kb, p.kb);
-    if (kb > 8 && est / b->nq > 5e-3) b->path = MDRQ_PATH_VAFILE;
 }
 
 // the result pool a batch writes: its own (stream slots) or the store's
@@ -1136,7 +1114,6 @@ int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper, uint32
         auto now = [] { return std::chrono::steady_clock::now(); };
         const auto t0 = now();
         build_descs(s, lower, upper, nq, resolve_path(s, path, nq, true), true, b);
-        if (path == MDRQ_PATH_AUTO) refine_auto_ids(s, b);
         const auto t1 = now();
         upload_batch(s, b);
         const auto t2 = now();
@@ -1207,8 +1184,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             mdrq_batch* b = &sl.b;
             const uint32_t nq = nqs[k];
             build_descs(s, lower + q0[k] * s->m, upper + q0[k] * s->m, nq, resolve_path(s, path, nq, true), true, b);
-            if (path == MDRQ_PATH_AUTO) refine_auto_ids(s, b);
-            upload_batch(s, b, false);
+                upload_batch(s, b, false);
             up += upload_bytes(b);
             enqueue(s, b, true, s->stream);
             sl.h_flags[0] = sl.h_flags[1] = 0;
