@@ -102,6 +102,7 @@ struct VaBatchArgs {
     const uint16_t* udims;       // [kb]
     const uint32_t* tables;      // query-mask words, layout per va_batch_pv(kb) (above)
     const float2* qbounds;       // exact (lo, hi), +-inf where unconstrained; layout per va_batch_pv(kb)
+    const uint32_t* qcmask;      // [1024] constrained union dims per query (bit u)
     uint32_t grid;               // CTAs (chunks = grid * warps)
     uint64_t chunk_tuples;       // tuples per chunk (multiple of 128, < 65536: u16 counters)
     uint32_t nchunks;            // subchunks: ceil(n / chunk_tuples), one warp each

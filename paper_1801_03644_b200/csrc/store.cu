@@ -153,7 +153,7 @@ struct Pass {
 struct VbPass {
     uint32_t q0 = 0, nqp = 0, kb = 0, cells = 0, shift = 0;
     bool fallback = false;   // union wider than kVaBatchMaxDims: per-query VA
-    size_t udim_off = 0, table_off = 0, qb_off = 0;
+    size_t udim_off = 0, table_off = 0, qb_off = 0, cm_off = 0;
 };
 
 }  // namespace
@@ -178,9 +178,11 @@ struct mdrq_batch {
     std::vector<uint16_t> vb_udims;
     std::vector<uint32_t> vb_tables;
     std::vector<float2> vb_qb;
+    std::vector<uint32_t> vb_cm;   // per query of a pass: constrained union dims
     DBuf<uint16_t> d_vb_udims;
     DBuf<uint32_t> d_vb_tables;
     DBuf<float2> d_vb_qb;
+    DBuf<uint32_t> d_vb_cm;
     DBuf<uint32_t> d_tile_counters;
     DBuf<unsigned long long> d_counts;
     DBuf<unsigned long long> d_offsets;
@@ -307,6 +309,7 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
     b->vb_udims.clear();
     b->vb_tables.clear();
     b->vb_qb.clear();
+    b->vb_cm.clear();
     const uint32_t m = s->m, bits = s->va_bits;
     for (uint32_t q0 = 0; q0 < b->nq; q0 += 1024) {
         VbPass ps;
@@ -341,6 +344,7 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
         ps.udim_off = b->vb_udims.size();
         ps.table_off = b->vb_tables.size();
         ps.qb_off = b->vb_qb.size();
+        ps.cm_off = b->vb_cm.size();
         b->vb_udims.insert(b->vb_udims.end(), ud.begin(), ud.end());
         const bool pv = va_batch_pv(ps.kb);
         const uint32_t qstride = pv ? va_batch_vdims(ps.kb) : ps.kb;
@@ -354,6 +358,7 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
         };
         // queries unconstrained in dimension u: every cell, set once per word below
         std::vector<uint32_t> free_mask(size_t(ps.kb) * 32, 0u);
+        std::vector<uint32_t> cmv(1024, 0u);
         for (uint32_t qi = 0; qi < ps.nqp; ++qi) {
             const QueryDesc& qd = b->descs[q0 + qi];
             const uint32_t w = qi >> 5, bit = 1u << (qi & 31);
@@ -378,6 +383,7 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
             }
             for (uint32_t u = 0; u < ps.kb; ++u)
                 if (!(constrained >> u & 1u)) free_mask[size_t(u) * 32 + w] |= bit;
+            cmv[qi] = constrained;
         }
         for (uint32_t u = 0; u < ps.kb; ++u)
             for (uint32_t w = 0; w < 32; ++w) {
@@ -390,6 +396,7 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
             }
         b->vb_tables.insert(b->vb_tables.end(), tab.begin(), tab.end());
         b->vb_qb.insert(b->vb_qb.end(), qbv.begin(), qbv.end());
+        b->vb_cm.insert(b->vb_cm.end(), cmv.begin(), cmv.end());
         b->vb_passes.push_back(ps);
     }
 }
@@ -536,6 +543,7 @@ void upload_batch(mdrq_store* s, mdrq_batch* b, bool sync = true) {
     upload(b->d_vb_udims, b->vb_udims, s->stream);
     upload(b->d_vb_tables, b->vb_tables, s->stream);
     upload(b->d_vb_qb, b->vb_qb, s->stream);
+    upload(b->d_vb_cm, b->vb_cm, s->stream);
     b->d_tile_counters.reserve(b->nq);
     b->d_counts.reserve(b->nq);
     b->d_offsets.reserve(size_t(b->nq) + 1);
@@ -551,7 +559,8 @@ uint64_t upload_bytes(const mdrq_batch* b) {
     return b->descs.size() * sizeof(QueryDesc) + b->preds.size() * sizeof(DimPred) +
            b->udims.size() * sizeof(uint16_t) + b->bounds.size() * sizeof(float2) +
            b->cmask.size() * sizeof(unsigned long long) + b->vb_udims.size() * sizeof(uint16_t) +
-           b->vb_tables.size() * sizeof(uint32_t) + b->vb_qb.size() * sizeof(float2);
+           b->vb_tables.size() * sizeof(uint32_t) + b->vb_qb.size() * sizeof(float2) +
+           b->vb_cm.size() * sizeof(uint32_t);
 }
 
 uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
@@ -627,6 +636,7 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.udims = b->d_vb_udims.p + ps.udim_off;
     a.tables = b->d_vb_tables.p + ps.table_off;
     a.qbounds = b->d_vb_qb.p + ps.qb_off;
+    a.qcmask = b->d_vb_cm.p + ps.cm_off;
     // one CTA per SM (the tables take most of the shared memory); chunks of
     // < 65536 tuples (16-bit per-warp counters), identical in every mode
     a.grid = uint32_t(s->num_sms);

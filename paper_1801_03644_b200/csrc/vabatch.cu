@@ -129,8 +129,13 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     v[4 * h + 3] = w4.w;
                 }
             } else {
+                // the values of the dims some candidate of the word constrains
+                // (partial-match queries leave most of a wide union free)
+                uint32_t need = 0;
+                for (uint32_t rr = r; rr; rr &= rr - 1) need |= __ldg(a.qcmask + wq + __ffs(rr) - 1);
 #pragma unroll
-                for (int u = 0; u < KB; ++u) v[u] = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
+                for (int u = 0; u < KB; ++u)
+                    v[u] = (need >> u & 1u) ? __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t) : 0.0f;
             }
             while (r) {
                 const int b = __ffs(r) - 1;
@@ -145,12 +150,16 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                              (v[2 * u2 + 1] <= bb.w);
                     }
                 } else {
-                    const float2* qq = a.qbounds + (wq + b) * KB;
+                    // only the query's constrained dims
+                    const uint32_t q = wq + b;
+                    const float2* qq = a.qbounds + q * KB;
+                    const uint32_t cm = __ldg(a.qcmask + q);
 #pragma unroll
-                    for (int u = 0; u < KB; ++u) {
-                        const float2 bb = qq[u];
-                        ok = ok & (bb.x <= v[u]) & (v[u] <= bb.y);
-                    }
+                    for (int u = 0; u < KB; ++u)
+                        if (cm >> u & 1u) {
+                            const float2 bb = __ldg(qq + u);
+                            ok = ok & (bb.x <= v[u]) & (v[u] <= bb.y);
+                        }
                 }
                 hits |= uint32_t(ok) << b;
             }
