@@ -64,3 +64,16 @@ def test_shared_object_is_sm100a():
     assert r.returncode == 0, r.stderr
     archs = set(re.findall(r"sm_(\d+a?)", r.stdout))
     assert archs == {"100a"}, archs
+
+
+def test_null_store_and_arguments_are_einval():
+    """Every store entry point rejects a null store / null outputs with
+    MDRQ_EINVAL instead of crashing (no device needed)."""
+    from paper_1801_03644_b200 import _lib
+    lib = _lib.load()
+    total = ctypes.c_uint64(0)
+    assert lib.mdrq_query_ids(None, None, None, 0, 0, None, None, 0, ctypes.byref(total)) == _lib.MDRQ_EINVAL
+    assert lib.mdrq_query_count(None, None, None, 0, 0, None) == _lib.MDRQ_EINVAL
+    assert lib.mdrq_query_ids_stream(None, None, None, None, 1, 0, None, None, None, None, None) == _lib.MDRQ_EINVAL
+    assert lib.mdrq_fetch_ids(None, None, 0) == _lib.MDRQ_EINVAL
+    assert lib.mdrq_last_error()

@@ -280,6 +280,8 @@ for n, m, nq, s in ((20000, 3, 5, 0.1), (300000, 8, 40, 0.01), (300000, 12, 50, 
     with eng.DeviceStore(v, layouts=1 | 4) as st:
         o, i = st.ids(lo, hi, "vafile_batch")
         assert np.array_equal(o, eo) and np.array_equal(i.astype(np.int64), ei), (n, m, nq, s)
+        for o, i in st.ids_stream([(lo, hi)] * 4, "vafile_batch"):   # the pipelined slots too
+            assert np.array_equal(o, eo) and np.array_equal(i.astype(np.int64), ei), (n, m, nq, s)
 print("recount ok")
 """
 
