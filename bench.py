@@ -286,6 +286,9 @@ def main():
         key = f"va_batch_kernel<3, {binfo['max_union_dims']}>" if roofline["class"] == "scan" else "vb_scatter_kernel"
         roofline.update(ncu_traffic(key))
 
+    rpeak = read_peak(dev)
+    add_peaks(roofline, rpeak)
+
     # ---- the single-query columnar scan kernel (HBM-bound by design), same
     # data; skipped with --no-paths so a profiled run holds only the step
     col_roof = None
@@ -297,6 +300,7 @@ def main():
         cstats = store.stats(col_q)
         col_roof = roofline_of("columnar", cprof, cstats, n, col_q, None, peak, peak_kind)
         col_roof.update(ncu_traffic("col_scan_kernel<1>"))
+        add_peaks(col_roof, rpeak)
         cb.close()
 
     # ---- per-path cost at this workload (device time per query)
@@ -412,6 +416,28 @@ def smem_roofline(binfo, prof, n, clocks):
     return {"resource": "shared-memory wavefronts (table rows)", "achieved": achieved, "peak": peak,
             "unit": "wavefronts/s", "frac": achieved / peak, "algo_wavefronts_per_launch": wavefronts,
             "sm_mhz": mhz}
+
+
+SPEC_HBM_GBS = 8000.0   # B200 HBM3e spec, the BASELINE roofline denominator
+
+
+def read_peak(device: int) -> float | None:
+    """Measured read-stream bandwidth (mdrq_measure_read_bw: 4 GB, best of
+    5), SURVEY.md 8(d)'s second denominator beside the copy peak."""
+    import ctypes
+    from paper_1801_03644_b200 import _lib
+    g = ctypes.c_double(0)
+    rc = _lib.load().mdrq_measure_read_bw(device, 4 << 30, 5, ctypes.byref(g))
+    return g.value if rc == 0 else None
+
+
+def add_peaks(roof: dict | None, rpeak: float | None) -> None:
+    if not roof:
+        return
+    roof["peak_spec"] = SPEC_HBM_GBS
+    roof["frac_spec"] = roof["achieved"] / SPEC_HBM_GBS
+    roof["peak_read_measured"] = rpeak
+    roof["frac_read_measured"] = roof["achieved"] / rpeak if rpeak else None
 
 
 def ncu_traffic(kernel: str) -> dict:

@@ -96,6 +96,10 @@ typedef struct mdrq_search_stats {
 const char* mdrq_last_error(void);
 int mdrq_abi_version(void);
 int mdrq_device_count(int* count);
+/* Read-stream bandwidth probe (GB/s, best of iters) over a `bytes` buffer:
+ * the roofline denominator beside MEASURED_PEAKS' copy figure (SURVEY.md
+ * 8(d)).  Measurement utility, not part of the reference interface.       */
+int mdrq_measure_read_bw(int device, uint64_t bytes, int iters, double* gbs);
 
 /* -- kernel-backend level: host buffers in and out (parity / tests) ------ */
 /* match_row for `nrows` rows against one query: out[r] = 1 match / 0 not.  */

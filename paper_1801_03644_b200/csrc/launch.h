@@ -182,6 +182,7 @@ void launch_popcount(const uint32_t* words, uint64_t nwords, unsigned long long*
 void launch_mask_to_ids(const uint32_t* words, uint64_t n, uint32_t* status_scratch,
                         uint64_t* status, uint32_t epoch, uint32_t* tile_counter,
                         unsigned long long* count, int64_t* ids, cudaStream_t st);
+void launch_read_stream(const void* p, uint64_t bytes, uint32_t* sink, int num_sms, cudaStream_t st);
 void launch_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lo,
                        const float* hi, uint8_t* out, cudaStream_t st);
 

@@ -921,6 +921,40 @@ const char* mdrq_last_error(void) { return g_err.c_str(); }
 
 int mdrq_abi_version(void) { return MDRQ_ABI_VERSION; }
 
+int mdrq_measure_read_bw(int device, uint64_t bytes, int iters, double* gbs) {
+    return guard([&] {
+        if (!gbs || bytes < 16 || iters < 1) raise(MDRQ_EINVAL, "bad argument");
+        DeviceGuard dg(device);
+        int sms = 148;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        bytes &= ~uint64_t(15);
+        DBuf<uint8_t> buf;
+        DBuf<uint32_t> sink;
+        buf.reserve(bytes);
+        sink.reserve(1);
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CK(cudaMemsetAsync(buf.p, 1, bytes, st));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        float best = 1e30f;
+        for (int i = 0; i < iters + 1; ++i) {   // first launch warms up
+            CK(cudaEventRecord(e0, st));
+            launch_read_stream(buf.p, bytes, sink.p, sms, st);
+            CK(cudaEventRecord(e1, st));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            if (i) best = std::min(best, ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
+        *gbs = double(bytes) / (double(best) * 1e-3) / 1e9;
+    });
+}
+
 int mdrq_device_count(int* count) {
     return guard([&] {
         if (!count) raise(MDRQ_EINVAL, "null count");
