@@ -329,7 +329,7 @@ def main():
     # synchronous DeviceStore.ids for reference.
     pinned = [torch.empty(max(1, total_local + 1024), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
               for _ in range(3)]
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e_steps = max(3, min(args.steps, 20))
     store.ids_stream([(lo, hi)] * 3, args.path, outs=pinned)   # warm: slots and their result pools
     info = {}
     if world > 1:
