@@ -134,15 +134,15 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
     const uint64_t wbase = uint64_t(tile) * kVaTile + warp * VA_WARP_TUPLES;
     const uint64_t base = wbase + lane * 16;
 
-    // alive / sure flags in SWAR layout, one word per 4 tuples
-    uint32_t al[VA_G][4], su[VA_G][4];
+    // alive flags in SWAR layout, one word per 4 tuples (every tuple still
+    // alive after the last dimension is refined exactly: at 256 cells per
+    // dimension the alive set is barely larger than the answer, and dropping
+    // a second "strictly inside" test halves the per-code work)
+    uint32_t al[VA_G][4];
 #pragma unroll
     for (int g = 0; g < VA_G; ++g)
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            al[g][w] = 0x03000300u;
-            su[g][w] = 0x03000300u;
-        }
+        for (int w = 0; w < 4; ++w) al[g][w] = 0x03000300u;
     if (uint64_t(tile + 1) * kVaTile > a.n) {
 #pragma unroll
         for (int g = 0; g < VA_G; ++g)
@@ -167,7 +167,6 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
         const DimPred p = P[i];
         const uint32_t d = p.dim;
         const uint32_t cl = p.cl, ch = p.ch;
-        const uint32_t sl = cl + p.edge_lo, sh = ch - p.edge_hi;  // strict interior
         const uint4* c = reinterpret_cast<const uint4*>(a.codes + uint64_t(d) * a.stride + base);
         uint4 x[VA_G];
 #pragma unroll
@@ -183,26 +182,19 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
             if (ga) {
                 const uint32_t xw[4] = {x[g].x, x[g].y, x[g].z, x[g].w};
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    al[g][w] &= swar_in(xw[w], cl, ch);
-                    // (sh may be "negative": 0x100 + sh wraps below 0x100 -> never <=)
-                    su[g][w] &= swar_in(xw[w], sl, sh);
-                }
+                for (int w = 0; w < 4; ++w) al[g][w] &= swar_in(xw[w], cl, ch);
             }
         }
     }
 
-    // exact refinement of tuples in an edge cell: alive & ~sure
+    // exact refinement of every alive tuple
     uint32_t hit[VA_G];
     uint32_t refined = 0;
 #pragma unroll
     for (int g = 0; g < VA_G; ++g) {
         uint32_t h = 0, r = 0;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            h |= flags_to_nib(al[g][w] & su[g][w]) << (4 * w);
-            r |= flags_to_nib(al[g][w] & ~su[g][w]) << (4 * w);
-        }
+        for (int w = 0; w < 4; ++w) r |= flags_to_nib(al[g][w]) << (4 * w);
         while (r) {
             const int j = __ffs(r) - 1;
             r &= r - 1;
