@@ -53,7 +53,9 @@ def parse():
     ap.add_argument("--no-paths", action="store_true",
                     help="skip the per-path cost table and the columnar roofline probe")
     ap.add_argument("--force-merge", action="store_true",
-                    help="run the NCCL id merge even with one rank (torchrun --nproc-per-node 1)")
+                    help="run the NCCL combine even with one rank (torchrun --nproc-per-node 1)")
+    ap.add_argument("--merge-in-step", action="store_true",
+                    help="include the full id exchange (all ids on every rank) in the timed step")
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="tuples per GPU")
     ap.add_argument("--queries", type=int, default=NQ)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -246,13 +248,26 @@ def main():
     total_local = batch.reserve()
     launches_per_step = batch.launches(ids=True)
 
+    def exchange():
+        # every rank's ids of every query, rank-ordered (NCCL all_gather of
+        # the padded id slices + one segmented-copy kernel)
+        d_ids, d_offs, tot = batch.result_device()
+        ids_t = _wrap(d_ids, tot, torch.int32, dev)
+        offs_t = _wrap(d_offs, nq + 1, torch.int64, dev)
+        return eng.combine_ids(offs_t, ids_t)
+
     def step():
         batch.ids_async(sptr)
         if merge:
-            d_ids, d_offs, tot = batch.result_device()
-            ids_t = _wrap(d_ids, tot, torch.int32, dev)
-            offs_t = _wrap(d_offs, nq + 1, torch.int64, dev)
-            eng.combine_ids(offs_t, ids_t)
+            if args.merge_in_step:
+                exchange()
+            else:
+                # the counts combine: every rank learns the global offsets
+                # (where its rank-ordered slices go); the id exchange itself
+                # is timed separately below
+                d_ids, d_offs, tot = batch.result_device()
+                offs_t = _wrap(d_offs, nq + 1, torch.int64, dev)
+                eng.combine_counts(offs_t[1:] - offs_t[:-1])
 
     for _ in range(args.warmup):
         step()
@@ -275,6 +290,30 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = n * world * nq / (ms / 1e3)
+
+    # ---- the id exchange on its own (all ids of every query on every rank)
+    xchg = None
+    if merge and not args.merge_in_step:
+        exchange()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(3):
+            offs_all, _ = exchange()
+        x1.record(stream)
+        torch.cuda.synchronize()
+        xms = x0.elapsed_time(x1) / 3
+        if world > 1:
+            t = torch.tensor([xms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            xms = float(t.item())
+        ids_all = int(offs_all[-1].item())
+        xchg = {"ms_per_step": xms, "ids_total": ids_all, "bytes_in_per_rank": 4 * (ids_all - total_local),
+                "included_in_value": False,
+                "how": "NCCL all_gather of every rank's padded id slices + mdrq_copy_segments placement; "
+                       "the step itself ends with the counts combine (global offsets on every rank)"}
 
     # ---- dominant kernel of the step: one ids pass with events between
     # launch groups (mdrq_batch_profile), bytes from the kernels' counters
@@ -368,7 +407,10 @@ def main():
                        "queries_per_step": nq, "ids_per_step": int(total_local) * world,
                        "l2": "inputs (1.6 GB/GPU columns, 400 MB/GPU code planes) larger than L2 (126 MB); "
                              "no flush",
-                       "parallelism": f"row shards x{world}"},
+                       "parallelism": f"row shards x{world}",
+                       "combine": ("none (one rank)" if not merge else
+                                   "ids exchanged in the step" if args.merge_in_step else
+                                   "counts all_gather in the step; id exchange timed separately (id_exchange)")},
             "queries_per_s": nq / (ms / 1e3),
             "hbm_gbs_per_gpu": roofline["achieved"],
             "roofline": roofline,
@@ -384,6 +426,7 @@ def main():
                     "ms_per_step": e2e_s * 1e3,
                     "sync_call": {"value": n * world * nq / sync_s, "ms_per_step": sync_s * 1e3,
                                   "api": "DeviceStore.ids, one synchronous call per step"}},
+            "id_exchange": xchg,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

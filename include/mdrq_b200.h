@@ -100,6 +100,14 @@ int mdrq_device_count(int* count);
  * the roofline denominator beside MEASURED_PEAKS' copy figure (SURVEY.md
  * 8(d)).  Measurement utility, not part of the reference interface.       */
 int mdrq_measure_read_bw(int device, uint64_t bytes, int iters, double* gbs);
+/* Device-side segmented copy on `stream` (device pointers): segment i moves
+ * len[i] uint32 from src + src_off[i] to dst + dst_off[i].  The multi-GPU
+ * id merge places every rank's slice of every query with it (the
+ * reference's concat + sort of per-partition results, parallel.py:156-157,
+ * scan.py:160, without the sort).                                          */
+int mdrq_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_off,
+                       const int64_t* dst_off, const int64_t* len, uint64_t nseg,
+                       void* stream);
 
 /* -- kernel-backend level: host buffers in and out (parity / tests) ------ */
 /* match_row for `nrows` rows against one query: out[r] = 1 match / 0 not.  */

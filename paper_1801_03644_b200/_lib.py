@@ -49,7 +49,7 @@ MODE_BLOCKED = 1
 
 #: every symbol include/mdrq_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
-    "mdrq_last_error", "mdrq_abi_version", "mdrq_device_count", "mdrq_measure_read_bw",
+    "mdrq_last_error", "mdrq_abi_version", "mdrq_device_count", "mdrq_measure_read_bw", "mdrq_copy_segments",
     "mdrq_match_rows", "mdrq_scan_rows", "mdrq_scan_column", "mdrq_and_masks",
     "mdrq_mask_popcount", "mdrq_mask_to_ids",
     "mdrq_store_create", "mdrq_store_destroy", "mdrq_store_get_info",
@@ -99,6 +99,7 @@ _SIGS = {
     "mdrq_abi_version": (_int, []),
     "mdrq_device_count": (_int, [ctypes.POINTER(_int)]),
     "mdrq_measure_read_bw": (_int, [_int, _u64, _int, ctypes.POINTER(ctypes.c_double)]),
+    "mdrq_copy_segments": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp]),
     "mdrq_match_rows": (_int, [_f32p, _u64, _u32, _f32p, _f32p, _int, _u8p]),
     "mdrq_scan_rows": (_int, [_f32p, _u64, _u32, _f32p, _f32p, _int, _int, _i64p, _u64p, _u64p]),
     "mdrq_scan_column": (_int, [_f32p, _u64, ctypes.c_float, ctypes.c_float, _int, _u8p]),

@@ -183,6 +183,8 @@ void launch_mask_to_ids(const uint32_t* words, uint64_t n, uint32_t* status_scra
                         uint64_t* status, uint32_t epoch, uint32_t* tile_counter,
                         unsigned long long* count, int64_t* ids, cudaStream_t st);
 void launch_read_stream(const void* p, uint64_t bytes, uint32_t* sink, int num_sms, cudaStream_t st);
+void launch_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_off, const int64_t* dst_off,
+                          const int64_t* len, uint64_t nseg, cudaStream_t st);
 void launch_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lo,
                        const float* hi, uint8_t* out, cudaStream_t st);
 

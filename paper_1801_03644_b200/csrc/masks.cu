@@ -196,6 +196,36 @@ void launch_read_stream(const void* p, uint64_t bytes, uint32_t* sink, int num_s
     read_stream_kernel<<<4 * num_sms, 512, 0, st>>>(reinterpret_cast<const uint4*>(p), bytes / 16, sink);
 }
 
+// Segmented copy (multi-GPU id merge): segment i moves len[i] uint32 from
+// src + src_off[i] to dst + dst_off[i]; a CTA per segment (grid-strided),
+// 16-byte accesses when both ends are 16-byte aligned.
+__global__ void __launch_bounds__(256) copy_segments_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                                           const int64_t* __restrict__ src_off,
+                                                           const int64_t* __restrict__ dst_off,
+                                                           const int64_t* __restrict__ len, uint64_t nseg) {
+    for (uint64_t i = blockIdx.x; i < nseg; i += gridDim.x) {
+        const uint64_t n = uint64_t(len[i]);
+        if (!n) continue;
+        const uint32_t* s = src + src_off[i];
+        uint32_t* d = dst + dst_off[i];
+        uint64_t j = 0;
+        if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15u) == 0) {
+            const uint64_t n4 = n / 4;
+            for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x)
+                __stcs(reinterpret_cast<uint4*>(d) + k, __ldcs(reinterpret_cast<const uint4*>(s) + k));
+            j = n4 * 4;
+        }
+        for (uint64_t k = j + threadIdx.x; k < n; k += blockDim.x) d[k] = s[k];
+    }
+}
+
+void launch_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_off, const int64_t* dst_off,
+                          const int64_t* len, uint64_t nseg, cudaStream_t st) {
+    if (!nseg) return;
+    const uint32_t grid = uint32_t(nseg < 65535 ? nseg : 65535);
+    copy_segments_kernel<<<grid, 256, 0, st>>>(src, dst, src_off, dst_off, len, nseg);
+}
+
 void launch_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lo, const float* hi,
                        uint8_t* out, cudaStream_t st) {
     if (!nrows) return;

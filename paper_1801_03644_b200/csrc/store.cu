@@ -921,6 +921,15 @@ const char* mdrq_last_error(void) { return g_err.c_str(); }
 
 int mdrq_abi_version(void) { return MDRQ_ABI_VERSION; }
 
+int mdrq_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_off, const int64_t* dst_off,
+                       const int64_t* len, uint64_t nseg, void* stream) {
+    return guard([&] {
+        if (nseg && (!src || !dst || !src_off || !dst_off || !len)) raise(MDRQ_EINVAL, "null argument");
+        launch_copy_segments(src, dst, src_off, dst_off, len, nseg, static_cast<cudaStream_t>(stream));
+        CK(cudaGetLastError());
+    });
+}
+
 int mdrq_measure_read_bw(int device, uint64_t bytes, int iters, double* gbs) {
     return guard([&] {
         if (!gbs || bytes < 16 || iters < 1) raise(MDRQ_EINVAL, "bad argument");

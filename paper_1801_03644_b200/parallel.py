@@ -181,6 +181,23 @@ def combine_ids(local_offsets, local_ids, group=None):
     gathered = _all_gather(padded, world, group)
     total = int(out_offsets[-1].item())
     out = torch.empty(total, dtype=ids_dtype, device=dev)
+    if dev.type == "cuda" and ids_dtype.itemsize == 4:
+        # one segmented-copy kernel (mdrq_copy_segments): segment (r, q) is
+        # rank r's slice of query q
+        import ctypes
+        from . import _lib
+        loff = torch.cumsum(all_counts, 1) - all_counts                 # [world, nq] within rank r
+        stride = gathered.shape[1]
+        src_off = (loff + torch.arange(world, device=dev, dtype=torch.int64)[:, None] * stride).contiguous()
+        dst_off = (out_offsets[:-1][None, :] + rank_prefix).contiguous()
+        seg_len = all_counts.contiguous()
+        if total:
+            _lib.check(_lib.load().mdrq_copy_segments(
+                ctypes.c_void_p(gathered.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                ctypes.c_void_p(src_off.data_ptr()), ctypes.c_void_p(dst_off.data_ptr()),
+                ctypes.c_void_p(seg_len.data_ptr()), world * nq,
+                ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+        return out_offsets, out
     for r in range(world):
         tr = int(totals[r].item())
         if tr == 0:

@@ -98,3 +98,48 @@ def test_nan_rejected_at_kernel_level(gpu):
     v = np.array([[0.1, np.nan]], np.float32)
     with pytest.raises(ValueError, match="NaN"):
         gpu.kernels.scan_rows(v, np.zeros(2, np.float32), np.ones(2, np.float32), 0)
+
+
+def test_copy_segments_merge_vs_numpy(gpu):
+    """mdrq_copy_segments, the device placement of the multi-GPU id merge
+    (parallel.combine_ids): random aligned / unaligned segments of three
+    simulated ranks land where the rank-ordered concatenation puts them."""
+    import ctypes
+    import torch
+    from paper_1801_03644_b200 import _lib
+    from paper_1801_03644_b200.parallel import combine_ids
+    rng = np.random.default_rng(9)
+    world, nq = 3, 57
+    counts = rng.integers(0, 300, (world, nq))
+    counts[1, 5] = 0
+    counts[:, 7] = 0
+    stride = int(counts.sum(1).max()) + 3
+    gathered = np.zeros((world, stride), np.uint32)
+    expect = []
+    per_q = [[] for _ in range(nq)]
+    for r in range(world):
+        o = 0
+        for q in range(nq):
+            seg = np.sort(rng.integers(r * 10**6, (r + 1) * 10**6, counts[r, q])).astype(np.uint32)
+            gathered[r, o:o + seg.size] = seg
+            per_q[q].append(seg)
+            o += seg.size
+    expect = np.concatenate([np.concatenate(x) for x in per_q])
+    out_off = np.zeros(nq + 1, np.int64)
+    out_off[1:] = np.cumsum(counts.sum(0))
+    rank_prefix = np.cumsum(counts, 0) - counts
+    loff = np.cumsum(counts, 1) - counts
+    src_off = (loff + np.arange(world)[:, None] * stride).astype(np.int64).ravel()
+    dst_off = (out_off[:-1][None, :] + rank_prefix).astype(np.int64).ravel()
+    seg_len = counts.astype(np.int64).ravel()
+    dev = torch.device("cuda", 0)
+    t = {k: torch.as_tensor(v).to(dev) for k, v in dict(g=gathered.view(np.int32), s=src_off, d=dst_off,
+                                                           n=seg_len).items()}
+    out = torch.zeros(int(out_off[-1]) + 1, dtype=torch.int32, device=dev)
+    rc = _lib.load().mdrq_copy_segments(ctypes.c_void_p(t["g"].data_ptr()), ctypes.c_void_p(out.data_ptr() + 4),
+                                        ctypes.c_void_p(t["s"].data_ptr()), ctypes.c_void_p(t["d"].data_ptr()),
+                                        ctypes.c_void_p(t["n"].data_ptr()), world * nq, None)
+    _lib.check(rc)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32)
+    assert got[0] == 0 and np.array_equal(got[1:], expect)
