@@ -90,6 +90,16 @@ struct DBuf {
 
 uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
+// a view into a DBuf (same `.p` spelling as DBuf)
+template <class T>
+struct Span {
+    T* p = nullptr;
+};
+
+// u64 words of a batch's accumulator block: counts, offsets, stats,
+// partials, tile counters (u32, rounded up)
+size_t scratch_words(size_t nq) { return nq + (nq + 1) + 4 * nq + nq * kPartialSlots * 4 + (nq + 1) / 2 + 1; }
+
 }  // namespace
 
 // ----------------------------------------------------------------- kernels --
@@ -183,11 +193,14 @@ struct mdrq_batch {
     DBuf<uint32_t> d_vb_tables;
     DBuf<float2> d_vb_qb;
     DBuf<uint32_t> d_vb_cm;
-    DBuf<uint32_t> d_tile_counters;
-    DBuf<unsigned long long> d_counts;
-    DBuf<unsigned long long> d_offsets;
-    DBuf<unsigned long long> d_stats;
-    DBuf<unsigned long long> d_partials;   // [nq][kPartialSlots][4]
+    // per-batch accumulators, carved from one allocation so one memset
+    // zeroes them all per pass (enqueue)
+    DBuf<unsigned long long> d_scratch;
+    Span<unsigned long long> d_counts;     // [nq]
+    Span<unsigned long long> d_offsets;    // [nq+1]
+    Span<unsigned long long> d_stats;      // [nq][4]
+    Span<unsigned long long> d_partials;   // [nq][kPartialSlots][4]
+    Span<uint32_t> d_tile_counters;        // [nq]
     // result pool of its own (stream slots); otherwise the store's pool
     bool own_pool = false;
     DBuf<uint32_t> own_ids;
@@ -544,11 +557,14 @@ void upload_batch(mdrq_store* s, mdrq_batch* b, bool sync = true) {
     upload(b->d_vb_tables, b->vb_tables, s->stream);
     upload(b->d_vb_qb, b->vb_qb, s->stream);
     upload(b->d_vb_cm, b->vb_cm, s->stream);
-    b->d_tile_counters.reserve(b->nq);
-    b->d_counts.reserve(b->nq);
-    b->d_offsets.reserve(size_t(b->nq) + 1);
-    b->d_stats.reserve(size_t(b->nq) * 4);
-    b->d_partials.reserve(size_t(b->nq) * kPartialSlots * 4);
+    const size_t nq = b->nq;
+    b->d_scratch.reserve(scratch_words(b->nq));
+    unsigned long long* p = b->d_scratch.p;
+    b->d_counts.p = p;
+    b->d_offsets.p = p + nq;
+    b->d_stats.p = p + 2 * nq + 1;
+    b->d_partials.p = p + 6 * nq + 1;
+    b->d_tile_counters.p = reinterpret_cast<uint32_t*>(p + 6 * nq + 1 + nq * kPartialSlots * 4);
     // H2D copies above may read pageable host vectors that a later rebuild
     // mutates: make them complete before returning (the ids stream rebuilds
     // a slot only after its previous pass and copies completed).
@@ -724,11 +740,7 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profil
         if (prof) prof->mark(c, nl);
     };
     mark(3, 0);
-    CK(cudaMemsetAsync(b->d_tile_counters.p, 0, sizeof(uint32_t) * nq, st));
-    CK(cudaMemsetAsync(b->d_counts.p, 0, sizeof(unsigned long long) * nq, st));
-    CK(cudaMemsetAsync(b->d_stats.p, 0, sizeof(unsigned long long) * nq * 4, st));
-    CK(cudaMemsetAsync(b->d_partials.p, 0, sizeof(unsigned long long) * nq * kPartialSlots * 4, st));
-    if (ids) CK(cudaMemsetAsync(b->d_offsets.p, 0, sizeof(unsigned long long) * (nq + 1), st));
+    CK(cudaMemsetAsync(b->d_scratch.p, 0, sizeof(unsigned long long) * scratch_words(nq), st));
     if (s->n == 0) return 0;
     uint32_t launches = 0;
     bool used_partials = false;   // single-query column / VA kernels accumulate into partials
