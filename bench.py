@@ -23,6 +23,7 @@ threads) on a bounded sample of the same queries over the same table.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import shutil
@@ -456,9 +457,21 @@ def smem_roofline(binfo, prof, n, clocks):
     mhz = clocks.get("sm_mhz") or 1965.0
     peak = 148 * mhz * 1e6
     achieved = wavefronts / launch_s
-    return {"resource": "shared-memory wavefronts (table rows)", "achieved": achieved, "peak": peak,
-            "unit": "wavefronts/s", "frac": achieved / peak, "algo_wavefronts_per_launch": wavefronts,
-            "sm_mhz": mhz}
+    out = {"resource": "shared-memory wavefronts (table rows)", "achieved": achieved, "peak": peak,
+           "unit": "wavefronts/s", "frac": achieved / peak, "algo_wavefronts_per_launch": wavefronts,
+           "sm_mhz": mhz}
+    # all the kernel's smem wavefronts (tables + shuffles + queue + refinement)
+    # from the committed ncu capture, over this run's launch time
+    key = f"va_batch_kernel<3, {kb}>"
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+        with open(f) as fh:
+            w = json.load(fh).get("smem_wavefronts", {}).get(key)
+        if w:
+            out["ncu_wavefronts_per_launch"] = float(w)
+            out["frac_all_wavefronts"] = w / launch_s / peak
+            out["ncu_source"] = f"{os.path.relpath(f, ROOT)}: smem_wavefronts {key}"
+            break
+    return out
 
 
 SPEC_HBM_GBS = 8000.0   # B200 HBM3e spec, the BASELINE roofline denominator
