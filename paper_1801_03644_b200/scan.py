@@ -135,7 +135,9 @@ class _GpuScan:
             raise ValueError(f"query has {query.m} dimensions, data has {self.m}")
 
     def search(self, query: RangeQuery) -> ResultSet:
-        return self.search_with_stats(query)[0]
+        # the ids alone (search_with_stats adds the counters' readback)
+        self._check(query)
+        return self._ids([query])[0]
 
     def _ids(self, queries):
         lo, hi = stack_queries(queries, self.m)

@@ -108,7 +108,12 @@ class VaFile:
         return np.sort(self._ids[local.astype(np.int64)])
 
     def search(self, query: RangeQuery) -> ResultSet:
-        return self.search_with_stats(query)[0]
+        # the ids alone (search_with_stats adds the counters' readback)
+        if query.m != self.m:
+            raise ValueError(f"query has {query.m} dimensions, grid has {self.m}")
+        lo, hi = stack_queries([query], self.m)
+        offs, ids = self.store.ids(lo, hi, "vafile")
+        return ResultSet(self._map(ids))
 
     def search_with_stats(self, query: RangeQuery) -> tuple[ResultSet, SearchStats]:
         if query.m != self.m:

@@ -20,7 +20,6 @@ for path in ("vafile", "columnar"):
         for i in range(100):
             f(i)
         dt = (time.perf_counter() - t) / 100
-        os.environ["MDRQ_DEBUG_TIMING"] = ""
         print(path, mode, "wall us per call", round(dt * 1e6, 1), flush=True)
 # the reference-API method objects
 data = eng.DataSet(v)
