@@ -53,6 +53,8 @@ __device__ __forceinline__ float f4_get(const float4& w, uint32_t i) {
 // permutes the low 3 bits, so the 8 lanes of a quarter-warp storing the same
 // (tuple-in-lane, half) land on 8 distinct 16-byte bank groups
 __device__ __forceinline__ uint32_t val_slot(uint32_t s) { return s ^ ((s >> 3) & 7u); }
+// the same for 8-byte slots (16 per 128-byte row)
+__device__ __forceinline__ uint32_t val_slot2(uint32_t s) { return s ^ ((s >> 4) & 15u); }
 
 template <int MODE, int KB>
 __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchArgs a) {
@@ -60,15 +62,20 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
     constexpr bool PV = va_batch_pv(KB);           // values + bounds in smem, overlap-only table
     constexpr int KBV = PV ? int(va_batch_vdims(KB)) : KB;
-    constexpr int H = PV ? KBV / 4 : 1;            // float4 slots per staged tuple
+    constexpr int VS = KBV % 4 == 0 ? 4 : 2;       // floats per staging slot (float4 / float2)
+    constexpr int H = PV ? KBV / VS : 1;           // staging slots per tuple
     constexpr bool DENSE = MODE != 2;              // candidates refined lane-parallel from a queue
+    // values staged on chip; the recount fallback of 9/10-dim unions reads
+    // them from global memory instead (its per-warp counters need the room)
+    constexpr bool STAGE = PV && !(MODE == 2 && KB > 8);
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_end = sm + va_batch_table_words(KB, K);
     // PV: exact query bounds [KBV/2][1024] float4 (lo_u, hi_u, lo_u+1, hi_u+1
-    // of dim pair u/2) and every warp's staged block values [128 * H] float4
+    // of dim pair u/2) and every warp's staged block values [128 * H] slots of
+    // VS floats
     float4* s_qb = reinterpret_cast<float4*>(s_end);
-    float4* s_val = s_qb + (PV ? 1024 * KBV / 2 : 0);
-    uint32_t* s_rest = reinterpret_cast<uint32_t*>(s_val + (PV ? VB_WARPS * 128 * H : 0));
+    float* s_val = reinterpret_cast<float*>(s_qb + (PV ? 1024 * KBV / 2 : 0));
+    uint32_t* s_rest = reinterpret_cast<uint32_t*>(s_val + (STAGE ? VB_WARPS * 128 * KBV : 0));
     // DENSE (modes 0, 3): CTA counters u32 [1024], then every warp's candidate
     // queue: entries uint2 [QCAP] = (overlap word, tuple-in-block << 5 | query
     // word), (wide unions) containment words u32 [QCAP].
@@ -105,7 +112,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     // is an immediate.
     const uint32_t lane_off = lane * (PV ? 4 : 8);
     const char* s_tab = reinterpret_cast<const char*>(sm);
-    float4* wval = s_val + warp * 128 * H;         // PV: this warp's staged values
+    float* wval = s_val + warp * 128 * KBV;        // STAGE: this warp's staged values
     uint2* qe = s_qe + warp * VB_QCAP;
     uint32_t* qs = s_qs + warp * VB_QCAP;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 2
@@ -118,16 +125,27 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
         uint32_t hits = PV ? 0u : su;
         uint32_t r = PV ? word : (word & ~su);
         if (r) {
-            float v[PV ? 4 * H : KB];
-            if constexpr (PV) {
+            float v[PV ? KBV : KB];
+            if constexpr (STAGE && VS == 4) {
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    const float4 w4 = wval[val_slot(tl * H + h)];
+                    const float4 w4 = reinterpret_cast<const float4*>(wval)[val_slot(tl * H + h)];
                     v[4 * h] = w4.x;
                     v[4 * h + 1] = w4.y;
                     v[4 * h + 2] = w4.z;
                     v[4 * h + 3] = w4.w;
                 }
+            } else if constexpr (STAGE) {
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                    const float2 w2 = reinterpret_cast<const float2*>(wval)[val_slot2(tl * H + h)];
+                    v[2 * h] = w2.x;
+                    v[2 * h + 1] = w2.y;
+                }
+            } else if constexpr (PV) {
+#pragma unroll
+                for (int u = 0; u < KBV; ++u)
+                    v[u] = u < KB ? __ldg(a.cols + uint64_t(s_dim[u < KB ? u : 0]) * a.stride + t) : 0.0f;
             } else {
                 // the values of the dims some candidate of the word constrains
                 // (partial-match queries leave most of a wide union free)
@@ -175,13 +193,13 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     // tuples: step(t0, j4, jmax, ov4, su4).
     auto for_each_step = [&](uint64_t start, uint64_t end, auto&& before_block, auto&& step) {
         uint32_t cw_n[KB];
-        float4 vv_n[PV ? KB : 1];
+        float4 vv_n[STAGE ? KB : 1];
         auto load_block = [&](uint64_t tb) {
 #pragma unroll
             for (int u = 0; u < KB; ++u) {
                 const uint64_t off = uint64_t(s_dim[u]) * a.stride + tb;
                 cw_n[u] = __ldcs(reinterpret_cast<const unsigned int*>(a.codes + off) + lane);
-                if constexpr (PV) vv_n[u] = __ldcs(reinterpret_cast<const float4*>(a.cols + off) + lane);
+                if constexpr (STAGE) vv_n[u] = __ldcs(reinterpret_cast<const float4*>(a.cols + off) + lane);
             }
         };
         if (start < end) load_block(start);
@@ -192,10 +210,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 // table cells of the 4 tuples of every word: (code >> shift) per byte
                 cw[u] = (cw_n[u] >> shift) & (0x01010101u * (K - 1));
             before_block(t0);
-            if constexpr (PV) {
+            if constexpr (STAGE) {
                 // stage the block's exact values tuple-major (tuple t, dims
-                // 4h..4h+3 in float4 slot t*H + h, zero-padded dims) so a
-                // refinement reads a tuple with H LDS.128
+                // VS*h .. VS*h+VS-1 in slot t*H + h, zero-padded dims) so a
+                // refinement reads a tuple with H LDS.128 / LDS.64
                 __syncwarp();
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj)
@@ -203,11 +221,15 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     for (int h = 0; h < H; ++h) {
                         float c[4];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int u = 4 * h + e;
+                        for (int e = 0; e < VS; ++e) {
+                            const int u = VS * h + e;
                             c[e] = u < KB ? f4_get(vv_n[u < KB ? u : 0], jj) : 0.0f;
                         }
-                        wval[val_slot((4 * lane + jj) * H + h)] = make_float4(c[0], c[1], c[2], c[3]);
+                        if constexpr (VS == 4)
+                            reinterpret_cast<float4*>(wval)[val_slot((4 * lane + jj) * H + h)] =
+                                make_float4(c[0], c[1], c[2], c[3]);
+                        else
+                            reinterpret_cast<float2*>(wval)[val_slot2((4 * lane + jj) * H + h)] = make_float2(c[0], c[1]);
                     }
                 __syncwarp();
             }
@@ -762,7 +784,8 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
     const bool pv = va_batch_pv(kb);
     const size_t vd = va_batch_vdims(kb);
     size_t bytes = size_t(va_batch_table_words(kb, cells)) * 4;
-    if (pv) bytes += vd * 1024 * 8 + size_t(VB_WARPS) * 128 * vd * 4;   // bounds + staged values
+    if (pv) bytes += vd * 1024 * 8;                                      // bounds
+    if (pv && !(mode == 2 && kb > 8)) bytes += size_t(VB_WARPS) * 128 * vd * 4;   // staged values
     if (mode == 2)
         bytes += size_t(VB_WARPS) * 1024 * 2;
     else

@@ -268,7 +268,7 @@ import numpy as np
 import oracle
 import paper_1801_03644_b200 as eng
 rng = np.random.default_rng(3)
-for n, m, nq, s in ((20000, 3, 5, 0.1), (300000, 8, 40, 0.01), (300000, 12, 50, 0.01)):
+for n, m, nq, s in ((20000, 3, 5, 0.1), (300000, 8, 40, 0.01), (300000, 10, 40, 0.01), (300000, 12, 50, 0.01)):
     v = rng.random((n, m), dtype=np.float32)
     w = s ** (1 / m)
     lo = rng.uniform(0, 1 - w, (nq, m)).astype(np.float32)
@@ -336,7 +336,7 @@ def test_ids_stream_pipelined_batches(gpu):
             st.ids_stream(batches[:2], "vafile_batch", outs=[np.empty(10, np.uint32)] * 2)
 
 
-@pytest.mark.parametrize("m", [3, 8, 11])
+@pytest.mark.parametrize("m", [3, 8, 9, 10, 11])
 def test_vafile_batch_multi_pass_vs_oracle(gpu, m):
     """More queries than one bit-sliced pass holds (1 024): three passes, the
     last one partial, narrow (on-chip refinement) and wide (containment
