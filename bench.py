@@ -445,14 +445,14 @@ def smem_roofline(binfo, prof, n, clocks):
     """The resource that bounds the bit-sliced filter pass: shared-memory
     wavefronts.  Algorithmic count per pass: the table row of every tuple
     and union dimension -- 32 lanes x 4 bytes of overlap words (1 wavefront)
-    for unions of <= 8 dims, whose candidates are all refined from staged
+    for unions of <= 10 dims, whose candidates are all refined from staged
     values, else 32 x 8 bytes of (overlap, containment) words (2 wavefronts);
     peak: 1 wavefront per cycle per SM at the SM clock measured during the
     timed region (148 SMs)."""
     if binfo["path"] != "vafile_batch" or not prof["scan"][1]:
         return None
     kb = binfo["max_union_dims"]
-    wavefronts = (1.0 if kb <= 8 else 2.0) * n * kb
+    wavefronts = (1.0 if kb <= 10 else 2.0) * n * kb
     launch_s = prof["scan"][0] / prof["scan"][1] / 1e3
     mhz = clocks.get("sm_mhz") or 1965.0
     peak = 148 * mhz * 1e6
@@ -525,7 +525,7 @@ def roofline_of(path, prof, stats, n, nq, total_ids, peak, peak_kind):
     if path.endswith("_batch"):
         passes = max(1, prof["scan"][1])
         if cls == "scan":
-            # filter pass: the union's code planes (and, for unions of <= 8
+            # filter pass: the union's code planes (and, for unions of <= 10
             # dims, their exact columns, refined on chip) + (ids mode) one
             # 4-byte staged (tuple, query) record per match
             algo = (loaded + ids_bytes) / passes
