@@ -20,6 +20,10 @@ C="python tools/probe_path.py columnar ids 20"
 $C > $OUT/probe_col.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on \
     -k regex:col_scan_kernel -s 10 -c 1 -o $OUT/prof_col $C > $OUT/ncu_col.log 2>&1
 echo "col=$?" >> $OUT/rc.txt
+V="python tools/probe_path.py vafile count 20"
+$V > $OUT/probe_va.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on \
+    -k regex:va_scan_kernel -s 25 -c 1 -o $OUT/prof_va $V > $OUT/ncu_va.log 2>&1
+echo "va=$?" >> $OUT/rc.txt
 P="python tools/probe_path.py rowwise count 3"
 $P > $OUT/probe_row.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on \
     -k regex:row_scan_kernel -s 1 -c 1 -o $OUT/prof_row $P > $OUT/ncu_row.log 2>&1
