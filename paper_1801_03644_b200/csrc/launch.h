@@ -102,6 +102,7 @@ struct VaBatchArgs {
     uint32_t cells;              // table cells per dim (2^tb: 32 or 64)
     uint32_t shift;              // stored code >> shift = table cell
     uint32_t nqp;                // queries in this pass (<= 1024)
+    uint32_t lw;                 // lanes per tuple (32, or 16 / 8 for passes of <= 512 / 256 queries)
     const uint16_t* udims;       // [kb]
     const uint32_t* tables;      // query-mask words, layout per va_batch_pv(kb) (above)
     const float2* qbounds;       // exact (lo, hi), +-inf where unconstrained; layout per va_batch_pv(kb)

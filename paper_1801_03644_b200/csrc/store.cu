@@ -407,6 +407,13 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
                     if (!pv) tab[ov_idx(u, c, w) + 1] |= f;
                 }
             }
+        // narrow passes of narrow unions run LW = 8 / 16 lanes per tuple
+        // (vb_args): the first W words of every row are replicated across
+        // the row, so the 4 / 2 tuples of one instruction read disjoint banks
+        const uint32_t lw = pv ? (ps.nqp <= 256 ? 8u : ps.nqp <= 512 ? 16u : 32u) : 32u;
+        if (lw < 32)
+            for (size_t row = 0; row < tab.size() / 32; ++row)
+                for (uint32_t w = lw; w < 32; ++w) tab[row * 32 + w] = tab[row * 32 + w % lw];
         b->vb_tables.insert(b->vb_tables.end(), tab.begin(), tab.end());
         b->vb_qb.insert(b->vb_qb.end(), qbv.begin(), qbv.end());
         b->vb_cm.insert(b->vb_cm.end(), cmv.begin(), cmv.end());
@@ -582,13 +589,13 @@ uint64_t upload_bytes(const mdrq_batch* b) {
 uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
     if (path == MDRQ_PATH_AUTO) {
         // planner, from the B200 per-query costs of C2:
-        // a bit-sliced VA pass costs about as much as ~18 single-query VA
-        // scans (2.2 ms vs 119-143 us at 8..32 queries), so it wins from 20
+        // a bit-sliced VA pass of <= 256 queries costs about as much as ~10
+        // single-query VA scans (1.0 ms vs 102-124 us), so it wins from 10
         // queries on; below that one query per pass over the code planes
         // (VA) or the columns.
         const bool va = (s->layouts & MDRQ_LAYOUT_VAFILE) != 0;
         if (!(s->layouts & MDRQ_LAYOUT_COLUMNAR)) return MDRQ_PATH_ROWWISE;
-        if (va && nq >= 20) return MDRQ_PATH_VAFILE_BATCH;
+        if (va && nq >= 10) return MDRQ_PATH_VAFILE_BATCH;
         if (va) return MDRQ_PATH_VAFILE;
         if (!ids && nq >= 2) return MDRQ_PATH_COLUMNAR_BATCH;
         return MDRQ_PATH_COLUMNAR;
@@ -649,6 +656,8 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.cells = ps.cells;
     a.shift = ps.shift;
     a.nqp = ps.nqp;
+    // lanes per tuple (vabatch.cu); build_vb_passes replicates the words
+    a.lw = va_batch_pv(ps.kb) ? (ps.nqp <= 256 ? 8u : ps.nqp <= 512 ? 16u : 32u) : 32u;
     a.udims = b->d_vb_udims.p + ps.udim_off;
     a.tables = b->d_vb_tables.p + ps.table_off;
     a.qbounds = b->d_vb_qb.p + ps.qb_off;

@@ -56,8 +56,15 @@ __device__ __forceinline__ uint32_t val_slot(uint32_t s) { return s ^ ((s >> 3) 
 // the same for 8-byte slots (16 per 128-byte row)
 __device__ __forceinline__ uint32_t val_slot2(uint32_t s) { return s ^ ((s >> 4) & 15u); }
 
-template <int MODE, int KB>
+// LW = lanes per tuple: 32 (a pass of up to 1 024 queries, lane w = query
+// word w), or 16 / 8 for passes of <= 512 / <= 256 queries, whose 16 / 8
+// query words leave room for 2 / 4 tuples per warp instruction.
+template <int MODE, int KB, int LW>
 __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchArgs a) {
+    static_assert(LW == 32 || LW == 16 || LW == 8, "lanes per tuple");
+    constexpr int TPI = 32 / LW;                   // tuples per warp instruction
+    constexpr int CWS = LW == 32 ? 1 : 2;          // code words (4 tuples each) per step
+    constexpr int NS = 4 * CWS / TPI;              // sub-steps per step (<= 4)
     extern __shared__ __align__(16) uint32_t sm[];
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
     constexpr bool PV = va_batch_pv(KB);           // values + bounds in smem, overlap-only table
@@ -110,7 +117,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     //   else (overlap, containment) uint2 (u, c, w) at byte (u*K + c)*256 + w*8
     // One PRMT builds (cell << 8) | lane offset from the code word; the rest
     // is an immediate.
+    // (rows of LW < 32 passes hold their LW words replicated 32 / LW times:
+    // lane l reads word l, i.e. query word l % LW, conflict-free)
     const uint32_t lane_off = lane * (PV ? 4 : 8);
+    const uint32_t lane_tup = lane / LW;           // this lane's tuple within a sub-step
     const char* s_tab = reinterpret_cast<const char*>(sm);
     float* wval = s_val + warp * 128 * KBV;        // STAGE: this warp's staged values
     uint2* qe = s_qe + warp * VB_QCAP;
@@ -235,20 +245,28 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             }
             if (t0 + 128 < end) load_block(t0 + 128);
             const uint32_t jmax = uint32_t(end - t0 < 128 ? end - t0 : 128);
-            for (uint32_t j4 = 0; j4 < jmax; j4 += 4) {
-                uint32_t x[KB];
+            for (uint32_t j4 = 0; j4 < jmax; j4 += 4 * CWS) {
+                // the step's CWS code words of every union dim (narrow passes
+                // take 8 tuples per step for more independent work)
+                uint32_t xw[CWS][KB];
 #pragma unroll
-                for (int u = 0; u < KB; ++u) x[u] = __shfl_sync(0xFFFFFFFFu, cw[u], j4 >> 2);
+                for (int c = 0; c < CWS; ++c)
+#pragma unroll
+                    for (int u = 0; u < KB; ++u) xw[c][u] = __shfl_sync(0xFFFFFFFFu, cw[u], (j4 >> 2) + c);
+                // sub-step s: this lane's tuple j4 + s*TPI + lane_tup, query
+                // word lane % LW (LW == 32: tuple j4 + s, word lane)
                 uint32_t ov4[4], su4[4];
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) ov4[jj] = su4[jj] = 0xFFFFFFFFu;
 #pragma unroll
                 for (int u = 0; u < KB; u += 2)
 #pragma unroll
-                    for (uint32_t jj = 0; jj < 4; ++jj) {
-                        // byte 0 = lane offset, byte 1 = cell of tuple jj (cells
+                    for (uint32_t ss = 0; ss < NS; ++ss) {
+                        // byte 0 = lane offset, byte 1 = cell of the tuple (cells
                         // are pre-masked to < K); two dims per 3-input AND
-                        const uint32_t sel = 0x5504u | (jj << 4);
+                        const uint32_t jj = ss * TPI + (LW == 32 ? 0u : lane_tup);   // tuple in the step
+                        const uint32_t* x = xw[(ss * TPI) / 4];   // its code word (compile-time)
+                        const uint32_t sel = 0x5504u | ((jj & 3u) << 4);
                         const uint32_t ca = __byte_perm(x[u], lane_off, sel);
                         if constexpr (PV) {
                             const uint32_t ea = *reinterpret_cast<const uint32_t*>(s_tab + ca + (u / 2) * K * 256);
@@ -256,20 +274,20 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                                 const uint32_t cb = __byte_perm(x[u + 1], lane_off, sel);
                                 const uint32_t eb =
                                     *reinterpret_cast<const uint32_t*>(s_tab + cb + (u / 2) * K * 256 + 128);
-                                ov4[jj] = ov4[jj] & ea & eb;
+                                ov4[ss] = ov4[ss] & ea & eb;
                             } else {
-                                ov4[jj] &= ea;
+                                ov4[ss] &= ea;
                             }
                         } else {
                             const uint2 ea = *reinterpret_cast<const uint2*>(s_tab + ca + u * K * 256);
                             if (u + 1 < KB) {
                                 const uint32_t cb = __byte_perm(x[u + 1], lane_off, sel);
                                 const uint2 eb = *reinterpret_cast<const uint2*>(s_tab + cb + (u + 1) * K * 256);
-                                ov4[jj] = ov4[jj] & ea.x & eb.x;
-                                su4[jj] = su4[jj] & ea.y & eb.y;
+                                ov4[ss] = ov4[ss] & ea.x & eb.x;
+                                su4[ss] = su4[ss] & ea.y & eb.y;
                             } else {
-                                ov4[jj] &= ea.x;
-                                su4[jj] &= ea.y;
+                                ov4[ss] &= ea.x;
+                                su4[ss] &= ea.y;
                             }
                         }
                     }
@@ -380,13 +398,15 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 },
                 [&](uint64_t, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[4], const uint32_t(&su4)[4]) {
 #pragma unroll
-                    for (uint32_t jj = 0; jj < 4; ++jj) {
-                        const bool nz = ov4[jj] != 0u && j4 + jj < jmax;
+                    for (uint32_t ss = 0; ss < NS; ++ss) {
+                        // lanes ascending = tuples ascending, then words
+                        const uint32_t jj = ss * TPI + (LW == 32 ? 0u : lane_tup);
+                        const bool nz = ov4[ss] != 0u && j4 + jj < jmax;
                         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, nz);
                         if (nz) {
                             const uint32_t slot = qn + __popc(bal & lt);
-                            qe[slot] = make_uint2(ov4[jj], ((j4 + jj) << 5) | lane);
-                            if constexpr (!PV) qs[slot] = su4[jj];
+                            qe[slot] = make_uint2(ov4[ss], ((j4 + jj) << 5) | (lane % LW));
+                            if constexpr (!PV) qs[slot] = su4[ss];
                         }
                         qn += __popc(bal);
                     }
@@ -425,8 +445,14 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             uint32_t* pre = a.chunk_counts;
             const uint32_t* wpre = pre + uint64_t(chunk) * 1024;
             bool write_ids = false;
-            auto per_tuple = [&](uint64_t t0, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[4],
+            // rows of narrow passes replicate their words: only lanes that own
+            // a query word of the pass count
+            const uint32_t own = lane * 32 < a.nqp ? 0xFFFFFFFFu : 0u;
+            auto per_tuple = [&](uint64_t t0, uint32_t j4, uint32_t jmax, const uint32_t(&ov4_in)[4],
                                  const uint32_t(&su4)[4]) {
+                uint32_t ov4[4];
+#pragma unroll
+                for (uint32_t jj = 0; jj < 4; ++jj) ov4[jj] = ov4_in[jj] & own;
                 uint32_t nib = 0;
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) nib |= uint32_t(ov4[jj] != 0u) << jj;
@@ -761,15 +787,26 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
     }
 }
 
-template <int MODE, int KB>
-void run_kb(const VaBatchArgs& a, cudaStream_t st) {
+template <int MODE, int KB, int LW>
+void run_kb_lw(const VaBatchArgs& a, cudaStream_t st) {
     const size_t smem = va_batch_smem(KB, va_batch_cells(KB), MODE);
     static size_t configured = 0;   // dynamic smem limit set so far (static smem comes on top)
     if (smem > configured) {
-        cudaFuncSetAttribute(va_batch_kernel<MODE, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(va_batch_kernel<MODE, KB, LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         configured = smem;
     }
-    va_batch_kernel<MODE, KB><<<a.grid, VB_THREADS, smem, st>>>(a);
+    va_batch_kernel<MODE, KB, LW><<<a.grid, VB_THREADS, smem, st>>>(a);
+}
+
+template <int MODE, int KB>
+void run_kb(const VaBatchArgs& a, cudaStream_t st) {
+    // narrow passes of narrow unions pack 2 / 4 tuples per instruction (the
+    // recount fallback keeps one tuple per instruction)
+    if constexpr (MODE != 2 && va_batch_pv(KB)) {
+        if (a.lw == 8) return run_kb_lw<MODE, KB, 8>(a, st);
+        if (a.lw == 16) return run_kb_lw<MODE, KB, 16>(a, st);
+    }
+    run_kb_lw<MODE, KB, 32>(a, st);
 }
 
 template <int MODE, int... Ks>

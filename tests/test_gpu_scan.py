@@ -356,3 +356,22 @@ def test_vafile_batch_multi_pass_vs_oracle(gpu, m):
     pts = rng.integers(0, n, nq // 10)
     lo[: nq // 10, 0] = hi[: nq // 10, 0] = v[pts, 0]
     check_store(gpu, v, lo, hi, paths=("vafile_batch",))
+
+
+@pytest.mark.parametrize("nq", [1, 33, 200, 256, 257, 400, 512, 513])
+def test_vafile_batch_lanes_per_tuple_vs_oracle(gpu, nq):
+    """Passes of <= 256 / <= 512 queries pack 4 / 2 tuples per warp
+    instruction (vabatch.cu LW = 8 / 16); the pass sizes around both
+    thresholds, narrow (3, 8 dims) and 10-dim unions, counts and ids."""
+    rng = np.random.default_rng(nq)
+    n = 150_000
+    for m in (3, 8, 10):
+        v = rng.random((n, m), dtype=np.float32)
+        s = 10 ** rng.uniform(-4, -1.3, nq)
+        w = (s ** (1.0 / m)).astype(np.float32)[:, None]
+        lo = (rng.random((nq, m)) * (1 - w)).astype(np.float32)
+        hi = (lo + w).astype(np.float32)
+        free = rng.random((nq, m)) < 0.2
+        lo[free] = -np.inf
+        hi[free] = np.inf
+        check_store(gpu, v, lo, hi, paths=("vafile_batch",))
