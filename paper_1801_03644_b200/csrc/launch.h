@@ -46,6 +46,9 @@ struct ScanArgs {
     // otherwise serialise thousands of atomics on one address):
     // [nq][32][4] = count, bytes loaded, tuples refined, spare
     unsigned long long* partials;
+    // single-query VA scan: track sure (strictly inside) tuples and refine
+    // only edge cells -- set when the query is expected to return many tuples
+    uint32_t va_sure;
 };
 
 constexpr int kPartialSlots = 32;

@@ -757,6 +757,18 @@ uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profil
     auto single = [&](uint32_t sp, uint32_t q) {
         ScanArgs a = base_args(s, b, sp);
         a.q = q;
+        if (sp == MDRQ_PATH_VAFILE) {
+            // expected fraction of tuples alive after the code test (cells
+            // independent): above ~3e-3 the refinement of every alive tuple
+            // costs more than a second range test per code
+            double sel = 1.0;
+            const double cells = double(s->nb() + 1);
+            for (uint32_t i = 0; i < b->descs[q].k; ++i) {
+                const DimPred& p = b->preds[b->descs[q].off + i];
+                sel *= p.ch >= p.cl ? double(p.ch - p.cl + 1) / cells : 0.0;
+            }
+            a.va_sure = sel > 3e-3 ? 1u : 0u;
+        }
         a.epoch = s->next_epoch();
         if (ids) {
             mark(1, 0);

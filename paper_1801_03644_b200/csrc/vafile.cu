@@ -119,7 +119,10 @@ __device__ __forceinline__ uint32_t flags_to_nib(uint32_t f) {
     return ((f >> 8) & 3u) | ((f >> 22) & 0xCu);
 }
 
-template <bool IDS>
+// SURE: also track "strictly inside the code range" per tuple and refine
+// only the edge-cell tuples (queries expected to return many tuples);
+// otherwise one range test per code and every alive tuple is refined.
+template <bool IDS, bool SURE>
 __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
     __shared__ uint32_t s_cnt[VA_THREADS / 32];
     __shared__ uint32_t s_ld[VA_THREADS / 32];
@@ -134,15 +137,13 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
     const uint64_t wbase = uint64_t(tile) * kVaTile + warp * VA_WARP_TUPLES;
     const uint64_t base = wbase + lane * 16;
 
-    // alive flags in SWAR layout, one word per 4 tuples (every tuple still
-    // alive after the last dimension is refined exactly: at 256 cells per
-    // dimension the alive set is barely larger than the answer, and dropping
-    // a second "strictly inside" test halves the per-code work)
-    uint32_t al[VA_G][4];
+    // alive (and SURE: strictly inside) flags in SWAR layout, one word per
+    // 4 tuples
+    uint32_t al[VA_G][4], su[VA_G][4];
 #pragma unroll
     for (int g = 0; g < VA_G; ++g)
 #pragma unroll
-        for (int w = 0; w < 4; ++w) al[g][w] = 0x03000300u;
+        for (int w = 0; w < 4; ++w) al[g][w] = su[g][w] = 0x03000300u;
     if (uint64_t(tile + 1) * kVaTile > a.n) {
 #pragma unroll
         for (int g = 0; g < VA_G; ++g)
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
         const DimPred p = P[i];
         const uint32_t d = p.dim;
         const uint32_t cl = p.cl, ch = p.ch;
+        const uint32_t sl = cl + p.edge_lo, sh = ch - p.edge_hi;  // strict interior (SURE)
         const uint4* c = reinterpret_cast<const uint4*>(a.codes + uint64_t(d) * a.stride + base);
         uint4 x[VA_G];
 #pragma unroll
@@ -182,19 +184,30 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
             if (ga) {
                 const uint32_t xw[4] = {x[g].x, x[g].y, x[g].z, x[g].w};
 #pragma unroll
-                for (int w = 0; w < 4; ++w) al[g][w] &= swar_in(xw[w], cl, ch);
+                for (int w = 0; w < 4; ++w) {
+                    al[g][w] &= swar_in(xw[w], cl, ch);
+                    // (sh may be "negative": 0x100 + sh wraps below 0x100 -> never <=)
+                    if constexpr (SURE) su[g][w] &= swar_in(xw[w], sl, sh);
+                }
             }
         }
     }
 
-    // exact refinement of every alive tuple
+    // exact refinement of the alive tuples (SURE: only those in an edge cell)
     uint32_t hit[VA_G];
     uint32_t refined = 0;
 #pragma unroll
     for (int g = 0; g < VA_G; ++g) {
         uint32_t h = 0, r = 0;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) r |= flags_to_nib(al[g][w]) << (4 * w);
+        for (int w = 0; w < 4; ++w) {
+            if constexpr (SURE) {
+                h |= flags_to_nib(al[g][w] & su[g][w]) << (4 * w);
+                r |= flags_to_nib(al[g][w] & ~su[g][w]) << (4 * w);
+            } else {
+                r |= flags_to_nib(al[g][w]) << (4 * w);
+            }
+        }
         while (r) {
             const int j = __ffs(r) - 1;
             r &= r - 1;
@@ -248,10 +261,17 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
 
 void launch_va_scan(const ScanArgs& a, bool ids, cudaStream_t st) {
     if (a.num_tiles == 0) return;
-    if (ids)
-        va_scan_kernel<true><<<a.num_tiles, VA_THREADS, 0, st>>>(a);
-    else
-        va_scan_kernel<false><<<a.num_tiles, VA_THREADS, 0, st>>>(a);
+    if (ids) {
+        if (a.va_sure)
+            va_scan_kernel<true, true><<<a.num_tiles, VA_THREADS, 0, st>>>(a);
+        else
+            va_scan_kernel<true, false><<<a.num_tiles, VA_THREADS, 0, st>>>(a);
+    } else {
+        if (a.va_sure)
+            va_scan_kernel<false, true><<<a.num_tiles, VA_THREADS, 0, st>>>(a);
+        else
+            va_scan_kernel<false, false><<<a.num_tiles, VA_THREADS, 0, st>>>(a);
+    }
 }
 
 void launch_va_sample(const float* col, uint64_t n, uint64_t step, uint64_t count, float* out,
