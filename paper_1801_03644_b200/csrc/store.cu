@@ -383,7 +383,9 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
                 // narrow unions: dim-pair-major [u/2][1024 queries][2] (lanes
                 // refining different queries hit different banks); wide
                 // unions: query-major [1024][kb]
-                qbv[pv ? (size_t(u / 2) * 1024 + qi) * 2 + u % 2 : size_t(qi) * qstride + u] = make_float2(p.lo, p.hi);
+                // (narrow: query qi at slot qi ^ ((qi >> 5) & 7), vabatch.cu)
+                const size_t qs = qi ^ ((qi >> 5) & 7u);
+                qbv[pv ? (size_t(u / 2) * 1024 + qs) * 2 + u % 2 : size_t(qi) * qstride + u] = make_float2(p.lo, p.hi);
                 if (p.lo > p.hi) continue;   // empty interval (kernel level only): no cell overlaps
                 // overlap cells [lo_c, hi_c]; containment drops the edge cells
                 const int lo_c = int(p.cl) >> ps.shift, hi_c = int(p.ch) >> ps.shift, top = int(cells) - 1;

@@ -170,7 +170,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 r &= r - 1;
                 bool ok = true;
                 if constexpr (PV) {
-                    const float4* qq = s_qb + (wq + b);
+                    // query q's bounds sit at q ^ (word & 7): the lowest set
+                    // bits the lanes pop are mostly small, the XOR spreads
+                    // them over the bank groups by query word
+                    const float4* qq = s_qb + (wq + (uint32_t(b) ^ ((wq >> 5) & 7u)));
 #pragma unroll
                     for (int u2 = 0; u2 < KBV / 2; ++u2) {
                         const float4 bb = qq[u2 * 1024];
