@@ -633,7 +633,7 @@ __device__ __forceinline__ uint32_t match_q10(uint32_t q, bool act) {
 }
 
 // Scatter the staged records of mode 3 into place.  One CTA per group (grid-
-// strided) takes the group's records in windows of up to 16 blocks, sorts a
+// strided) takes the group's records in windows of up to 20 blocks, sorts a
 // window by query in shared memory (stable counting sort: per-warp segment
 // counts, a prefix over warps and queries, then ballot-match ranking inside
 // each 32-record group) and writes every query's run of ids contiguously at
@@ -642,18 +642,17 @@ __device__ __forceinline__ uint32_t match_q10(uint32_t q, bool act) {
 // instead of read-modify-writing scattered 4-byte stores.
 constexpr int SC_THREADS = 512;
 constexpr int SC_WARPS = SC_THREADS / 32;
-constexpr uint32_t SC_WIN_BLOCKS = 16;
+constexpr uint32_t SC_WIN_BLOCKS = 20;
 constexpr uint32_t SC_WIN = SC_WIN_BLOCKS * kRecBlock;   // records per window
-constexpr size_t SC_SMEM = size_t(SC_WIN) * (4 + 4 + 2) + size_t(SC_WARPS) * 1024 * (2 + 1) + 1025 * 4 + 1024 * 8;
+constexpr size_t SC_SMEM = size_t(SC_WIN) * (4 + 4) + size_t(SC_WARPS) * 1024 * (2 + 1) + 1025 * 4 + 1024 * 8;
 
 __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatchArgs a) {
     extern __shared__ __align__(16) uint32_t ss[];
     unsigned long long* s_pos = reinterpret_cast<unsigned long long*>(ss);   // [1024] next output position
     uint32_t* s_rec = ss + 2 * 1024;                   // [SC_WIN] the window's records, in order
-    uint32_t* s_out = s_rec + SC_WIN;                  // [SC_WIN] tuple offsets, sorted by query
+    uint32_t* s_out = s_rec + SC_WIN;                  // [SC_WIN] the records, sorted by query (stable)
     uint32_t* s_off = s_out + SC_WIN;                  // [1025] window offsets by query
-    uint16_t* s_q = reinterpret_cast<uint16_t*>(s_off + 1025);   // [SC_WIN] query of each sorted slot
-    uint16_t* s_wc = s_q + SC_WIN;                     // [warps][1024] segment counts -> offsets
+    uint16_t* s_wc = reinterpret_cast<uint16_t*>(s_off + 1025);   // [warps][1024] segment counts -> offsets
     uint8_t* s_tag = reinterpret_cast<uint8_t*>(s_wc + SC_WARPS * 1024);   // [warps][1024] duplicate probe
     __shared__ uint32_t s_blk[SC_WIN_BLOCKS], s_bcnt[SC_WIN_BLOCKS], s_boff[SC_WIN_BLOCKS + 1];
     __shared__ uint32_t s_wsum[SC_WARPS];
@@ -769,8 +768,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 const uint32_t same = __any_sync(0xFFFFFFFFu, dup) ? match_q10(q, act) : (1u << lane);
                 if (act) {
                     const uint32_t p = s_off[q] + wc[q] + __popc(same & lt);
-                    s_out[p] = r >> 10;
-                    s_q[p] = uint16_t(q);
+                    s_out[p] = r;
                 }
                 __syncwarp();
                 if (act && (same & lt) == 0) wc[q] += __popc(same);
@@ -779,9 +777,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
             __syncthreads();
             // write the runs: consecutive slots of one query are consecutive ids
             for (uint32_t j = tid; j < n; j += SC_THREADS) {
-                const uint32_t q = s_q[j];
+                const uint32_t r = s_out[j];
+                const uint32_t q = r & 1023u;
                 const unsigned long long at = s_pos[q] + (j - s_off[q]);
-                if (at < a.ids_cap) __stcs(a.ids + at, a.id_base + uint32_t(start + s_out[j]));
+                if (at < a.ids_cap) __stcs(a.ids + at, a.id_base + uint32_t(start + (r >> 10)));
             }
             __syncthreads();
             for (uint32_t q = tid; q < 1024; q += SC_THREADS) s_pos[q] += s_off[q + 1] - s_off[q];
