@@ -654,59 +654,73 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
     uint32_t* s_off = s_out + SC_WIN;                  // [1025] window offsets by query
     uint16_t* s_wc = reinterpret_cast<uint16_t*>(s_off + 1025);   // [warps][1024] segment counts -> offsets
     uint8_t* s_tag = reinterpret_cast<uint8_t*>(s_wc + SC_WARPS * 1024);   // [warps][1024] duplicate probe
-    __shared__ uint32_t s_blk[SC_WIN_BLOCKS], s_bcnt[SC_WIN_BLOCKS], s_boff[SC_WIN_BLOCKS + 1];
+    // the block list of the current and the next window (double-buffered)
+    __shared__ uint32_t s_blk[2][SC_WIN_BLOCKS], s_bcnt[2][SC_WIN_BLOCKS], s_boff[2][SC_WIN_BLOCKS + 1];
     __shared__ uint32_t s_wsum[SC_WARPS];
     if (*reinterpret_cast<volatile const uint32_t*>(a.overflow)) return;   // mode 2 recounts instead
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
+    // window w = blocks w*20 .. w*20+19 of the group's list: ids, counts and
+    // offsets into buffer p (warp 0; the caller synchronises)
+    auto load_list = [&](uint32_t first, uint32_t nblk, uint32_t k0, uint32_t p) {
+        if (warp != 0) return;
+        const uint32_t k = k0 + lane;
+        const bool in = lane < SC_WIN_BLOCKS && k < nblk;
+        const uint32_t blk = in ? a.blk_list[first + k] : 0u;
+        const uint32_t c = in ? a.blk_count[blk] : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= uint32_t(o)) incl += x;
+        }
+        if (lane < SC_WIN_BLOCKS) {
+            s_blk[p][lane] = blk;
+            s_bcnt[p][lane] = c;
+            s_boff[p][lane] = incl - c;
+        }
+        if (lane == SC_WIN_BLOCKS - 1) s_boff[p][SC_WIN_BLOCKS] = incl;
+    };
+    // every record load of a window in flight at once: 2 per thread per block
+    uint32_t v[SC_WIN_BLOCKS][2];
+    auto load_records = [&](uint32_t p) {
+#pragma unroll
+        for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k)
+#pragma unroll
+            for (uint32_t h = 0; h < 2; ++h) {
+                const uint32_t i = tid + h * SC_THREADS;
+                v[k][h] = i < s_bcnt[p][k] ? __ldcs(a.rec + uint64_t(s_blk[p][k]) * kRecBlock + i) : 0u;
+            }
+    };
     for (uint32_t g = blockIdx.x; g < a.ngroups; g += gridDim.x) {
         // group g: the blocks of subchunks 16g .. 16g+15, consecutive in the
         // block list; record tuple offsets are relative to the group start
         const unsigned long long* base = a.base + uint64_t(g) * 1024;
         for (uint32_t q = tid; q < 1024; q += SC_THREADS) s_pos[q] = a.qoff[q] + base[q];
+        for (uint32_t i = tid; i < SC_WARPS * 1024 / 2; i += SC_THREADS) reinterpret_cast<uint32_t*>(s_wc)[i] = 0;
         const uint64_t start = uint64_t(g) * VB_WARPS * a.chunk_tuples;
         const uint32_t c0 = g * VB_WARPS, c1 = min(a.nchunks, c0 + VB_WARPS) - 1;
         const uint32_t first = a.chunk_first[c0];
         const uint32_t nblk = a.chunk_first[c1] + a.chunk_nblk[c1] - first;
-        for (uint32_t k0 = 0; k0 < nblk; k0 += SC_WIN_BLOCKS) {
-            // the window: blocks k0 .. k0+15 of the group's list
-            if (tid < SC_WIN_BLOCKS) {
-                const uint32_t k = k0 + tid;
-                const uint32_t blk = k < nblk ? a.blk_list[first + k] : 0u;
-                s_blk[tid] = blk;
-                s_bcnt[tid] = k < nblk ? a.blk_count[blk] : 0u;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                uint32_t acc = 0;
-                for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k) {
-                    s_boff[k] = acc;
-                    acc += s_bcnt[k];
+        if (nblk == 0) continue;
+        load_list(first, nblk, 0, 0);
+        __syncthreads();
+        load_records(0);
+        uint32_t p = 0;
+        for (uint32_t k0 = 0; k0 < nblk; k0 += SC_WIN_BLOCKS, p ^= 1u) {
+            // software pipeline: this window's records arrived in v during the
+            // previous window; the next window's list and records are fetched
+            // while this one is sorted and written
+            const uint32_t n = s_boff[p][SC_WIN_BLOCKS];
+#pragma unroll
+            for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k)
+#pragma unroll
+                for (uint32_t h = 0; h < 2; ++h) {
+                    const uint32_t i = tid + h * SC_THREADS;
+                    if (i < s_bcnt[p][k]) s_rec[s_boff[p][k] + i] = v[k][h];
                 }
-                s_boff[SC_WIN_BLOCKS] = acc;
-            }
-            for (uint32_t i = tid; i < SC_WARPS * 1024 / 2; i += SC_THREADS) reinterpret_cast<uint32_t*>(s_wc)[i] = 0;
-            __syncthreads();
-            const uint32_t n = s_boff[SC_WIN_BLOCKS];
-            {
-                // every load of the window in flight at once: 2 records per
-                // thread per block
-                uint32_t v[SC_WIN_BLOCKS][2];
-#pragma unroll
-                for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k)
-#pragma unroll
-                    for (uint32_t h = 0; h < 2; ++h) {
-                        const uint32_t i = tid + h * SC_THREADS;
-                        v[k][h] = i < s_bcnt[k] ? __ldcs(a.rec + uint64_t(s_blk[k]) * kRecBlock + i) : 0u;
-                    }
-#pragma unroll
-                for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k)
-#pragma unroll
-                    for (uint32_t h = 0; h < 2; ++h) {
-                        const uint32_t i = tid + h * SC_THREADS;
-                        if (i < s_bcnt[k]) s_rec[s_boff[k] + i] = v[k][h];
-                    }
-            }
+            const bool more = k0 + SC_WIN_BLOCKS < nblk;
+            if (more) load_list(first, nblk, k0 + SC_WIN_BLOCKS, p ^ 1u);
             __syncthreads();
             // warp w owns the contiguous segment [s0, s1) of the window
             const uint32_t seg = (n + SC_WARPS * 32 - 1) / (SC_WARPS * 32) * 32;
@@ -722,6 +736,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 }
             }
             __syncthreads();
+            if (more) load_records(p ^ 1u);   // the next list is visible now
             // per query: exclusive prefix over the warps' segments, window total
             uint32_t tot[2];
 #pragma unroll
@@ -767,8 +782,8 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 const bool dup = act && tag[q] != lane;
                 const uint32_t same = __any_sync(0xFFFFFFFFu, dup) ? match_q10(q, act) : (1u << lane);
                 if (act) {
-                    const uint32_t p = s_off[q] + wc[q] + __popc(same & lt);
-                    s_out[p] = r;
+                    const uint32_t pp = s_off[q] + wc[q] + __popc(same & lt);
+                    s_out[pp] = r;
                 }
                 __syncwarp();
                 if (act && (same & lt) == 0) wc[q] += __popc(same);
@@ -784,6 +799,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
             }
             __syncthreads();
             for (uint32_t q = tid; q < 1024; q += SC_THREADS) s_pos[q] += s_off[q + 1] - s_off[q];
+            for (uint32_t i = tid; i < SC_WARPS * 1024 / 2; i += SC_THREADS) reinterpret_cast<uint32_t*>(s_wc)[i] = 0;
             __syncthreads();
         }
     }
