@@ -730,6 +730,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 // segment counts: two 16-bit counters per word (a segment
                 // holds <= SC_WIN / SC_WARPS records, no carry between halves)
                 uint32_t* wc32 = reinterpret_cast<uint32_t*>(wc);
+#pragma unroll 4
                 for (uint32_t j = s0 + lane; j < s1; j += 32) {
                     const uint32_t q = s_rec[j] & 1023u;
                     atomicAdd(wc32 + (q >> 1), 1u << ((q & 1u) * 16));
@@ -791,6 +792,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
             }
             __syncthreads();
             // write the runs: consecutive slots of one query are consecutive ids
+#pragma unroll 4
             for (uint32_t j = tid; j < n; j += SC_THREADS) {
                 const uint32_t r = s_out[j];
                 const uint32_t q = r & 1023u;
