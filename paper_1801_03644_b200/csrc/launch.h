@@ -78,21 +78,22 @@ struct BatchArgs {
 // bit-sliced multi-query VA pass (vabatch.cu), <= 1024 queries per pass
 constexpr int kVaBatchMaxDims = 24;
 // table cells per dimension for a pass with kb union dims (fits 227 KB smem)
-// (9- and 10-dim unions use 32 cells so their on-chip values and bounds fit)
-__host__ __device__ constexpr uint32_t va_batch_cells(uint32_t kb) {
-    return kb <= 8 ? 64u : kb <= 10 ? 32u : kb <= 12 ? 64u : 32u;
-}
-// Narrow unions (kb <= kVbPvDims) keep the exact values and query bounds in
-// shared memory and refine every overlap candidate exactly, so their table is
-// overlap-only: rows of dims (2p, 2p+1) at cell c are adjacent,
+// (9..16-dim unions use 32 cells so their on-chip values / bounds fit)
+__host__ __device__ constexpr uint32_t va_batch_cells(uint32_t kb) { return kb <= 8 ? 64u : 32u; }
+// Unions of kb <= kVbPvDims keep the exact query bounds in shared memory (and,
+// up to 10 dims, the block's exact values) and refine every overlap candidate
+// exactly, so their table is overlap-only: rows of dims (2p, 2p+1) at cell c
+// are adjacent,
 // word (u, c, w) at ((u/2 * cells + c) * 2 + u%2) * 32 + w.  Their exact
 // bounds are [vdims/2][1024][2] float2 -- float4 (lo, hi of dims 2p, 2p+1)
 // per dim pair p and query -- padded with (-inf, +inf).
 // Wider unions use (overlap, containment) pairs [kb][cells][32][2] and refine
 // only the edge-cell candidates from global memory.
-constexpr uint32_t kVbPvDims = 10;
+constexpr uint32_t kVbPvDims = 16;   // values staged on chip up to 10 dims
 __host__ __device__ constexpr bool va_batch_pv(uint32_t kb) { return kb <= kVbPvDims; }
-__host__ __device__ constexpr uint32_t va_batch_vdims(uint32_t kb) { return kb <= 4 ? 4u : kb <= 8 ? 8u : 10u; }
+__host__ __device__ constexpr uint32_t va_batch_vdims(uint32_t kb) {
+    return kb <= 4 ? 4u : kb <= 8 ? 8u : (kb + 1) / 2 * 2;
+}
 __host__ __device__ constexpr uint32_t va_batch_table_words(uint32_t kb, uint32_t cells) {
     return va_batch_pv(kb) ? (kb + 1) / 2 * cells * 64 : kb * cells * 64;
 }

@@ -1367,7 +1367,7 @@ int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats, uint32_t
         if (path == MDRQ_PATH_VAFILE_BATCH) {
             for (const VbPass& p : b->vb_passes)
                 for (uint32_t q = p.q0; q < p.q0 + p.nqp; ++q)
-                    pass_bytes[q] = p.fallback ? 0 : (s->n * p.kb * (va_batch_pv(p.kb) ? 5 : 1)) / p.nqp;
+                    pass_bytes[q] = p.fallback ? 0 : (s->n * p.kb * (p.kb <= 10 ? 5 : 1)) / p.nqp;
         } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
             for (const Pass& p : b->passes)
                 for (uint32_t q = p.q0; q < p.q0 + p.nqp; ++q)

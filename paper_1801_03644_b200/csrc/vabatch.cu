@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     constexpr bool DENSE = MODE != 2;              // candidates refined lane-parallel from a queue
     // values staged on chip; the recount fallback of 9/10-dim unions reads
     // them from global memory instead (its per-warp counters need the room)
-    constexpr bool STAGE = PV && !(MODE == 2 && KB > 8);
+    constexpr bool STAGE = PV && KB <= 10 && !(MODE == 2 && KB > 8);
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_end = sm + va_batch_table_words(KB, K);
     // PV: exact query bounds [KBV/2][1024] float4 (lo_u, hi_u, lo_u+1, hi_u+1
@@ -153,9 +153,14 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     v[2 * h + 1] = w2.y;
                 }
             } else if constexpr (PV) {
+                // unions too wide to stage: the values of the dims some
+                // candidate of the word constrains, from global memory
+                uint32_t need = 0;
+                for (uint32_t rr = r; rr; rr &= rr - 1) need |= __ldg(a.qcmask + wq + __ffs(rr) - 1);
 #pragma unroll
                 for (int u = 0; u < KBV; ++u)
-                    v[u] = u < KB ? __ldg(a.cols + uint64_t(s_dim[u < KB ? u : 0]) * a.stride + t) : 0.0f;
+                    v[u] = (u < KB && (need >> u & 1u)) ? __ldg(a.cols + uint64_t(s_dim[u < KB ? u : 0]) * a.stride + t)
+                                                        : 0.0f;
             } else {
                 // the values of the dims some candidate of the word constrains
                 // (partial-match queries leave most of a wide union free)
@@ -174,12 +179,16 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     // bits the lanes pop are mostly small, the XOR spreads
                     // them over the bank groups by query word
                     const float4* qq = s_qb + (wq + (uint32_t(b) ^ ((wq >> 5) & 7u)));
+                    // unstaged (wide) unions skip the dim pairs the query leaves
+                    // free (their values were not loaded)
+                    const uint32_t cm = STAGE ? 0xFFFFFFFFu : __ldg(a.qcmask + wq + b);
 #pragma unroll
-                    for (int u2 = 0; u2 < KBV / 2; ++u2) {
-                        const float4 bb = qq[u2 * 1024];
-                        ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
-                             (v[2 * u2 + 1] <= bb.w);
-                    }
+                    for (int u2 = 0; u2 < KBV / 2; ++u2)
+                        if (cm >> (2 * u2) & 3u) {
+                            const float4 bb = qq[u2 * 1024];
+                            ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
+                                 (v[2 * u2 + 1] <= bb.w);
+                        }
                 } else {
                     // only the query's constrained dims
                     const uint32_t q = wq + b;
@@ -842,7 +851,7 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
     const size_t vd = va_batch_vdims(kb);
     size_t bytes = size_t(va_batch_table_words(kb, cells)) * 4;
     if (pv) bytes += vd * 1024 * 8;                                      // bounds
-    if (pv && !(mode == 2 && kb > 8)) bytes += size_t(VB_WARPS) * 128 * vd * 4;   // staged values
+    if (pv && kb <= 10 && !(mode == 2 && kb > 8)) bytes += size_t(VB_WARPS) * 128 * vd * 4;   // staged values
     if (mode == 2)
         bytes += size_t(VB_WARPS) * 1024 * 2;
     else
