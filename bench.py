@@ -323,7 +323,9 @@ def main():
     stats = store.stats(nq)
     roofline = roofline_of(binfo["path"], prof, stats, n, nq, total_local, peak, peak_kind)
     if binfo["path"] == "vafile_batch":
-        key = f"va_batch_kernel<3, {binfo['max_union_dims']}>" if roofline["class"] == "scan" else "vb_scatter_kernel"
+        lw = 32 if nq > 512 else 16 if nq > 256 else 8   # lanes per tuple of the pass (vabatch.cu)
+        key = (f"va_batch_kernel<3, {binfo['max_union_dims']}, {lw}>" if roofline["class"] == "scan"
+               else "vb_scatter_kernel")
         roofline.update(ncu_traffic(key))
 
     rpeak = read_peak(dev)
@@ -462,7 +464,7 @@ def smem_roofline(binfo, prof, n, clocks):
            "sm_mhz": mhz}
     # all the kernel's smem wavefronts (tables + shuffles + queue + refinement)
     # from the committed ncu capture, over this run's launch time
-    key = f"va_batch_kernel<3, {kb}>"
+    key = f"va_batch_kernel<3, {kb}, 32>"
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
         with open(f) as fh:
             w = json.load(fh).get("smem_wavefronts", {}).get(key)
