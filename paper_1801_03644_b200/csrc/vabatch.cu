@@ -33,6 +33,7 @@
 // dimension has a cell outside [code(lo), code(hi)] there, so OV never drops
 // a match; cells strictly inside need no refinement, edge cells are refined.
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 #include "launch.h"
@@ -43,7 +44,9 @@ namespace {
 
 constexpr int VB_THREADS = 512;
 constexpr int VB_WARPS = VB_THREADS / 32;
-constexpr uint32_t VB_QCAP = 160;   // candidate queue per warp: < 32 left over + 4 steps x 32 lanes
+// candidate queue per warp: < 32 left over + 2 ballots x 32 lanes (a step
+// drains the queue after its second and its last ballot)
+constexpr uint32_t VB_QCAP = 96;
 
 __device__ __forceinline__ float f4_get(const float4& w, uint32_t i) {
     return i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w;
@@ -58,13 +61,30 @@ __device__ __forceinline__ uint32_t val_slot2(uint32_t s) { return s ^ ((s >> 4)
 
 // LW = lanes per tuple: 32 (a pass of up to 1 024 queries, lane w = query
 // word w), or 16 / 8 for passes of <= 512 / <= 256 queries, whose 16 / 8
-// query words leave room for 2 / 4 tuples per warp instruction.
+// query words leave room for 2 / 4 tuples per warp instruction.  LW == 64 /
+// 128 mark the multi-word layouts of a full pass: 16 / 8 lanes per tuple,
+// lane l reads query words NW*l .. NW*l+NW-1 (NW = 2 / 4) with one LDS.64 /
+// LDS.128, so one instruction covers 2 / 4 tuples x 1 024 queries (a half /
+// a quarter of the table loads and address builds of LW == 32, the same
+// shared-memory wavefronts).
 template <int MODE, int KB, int LW>
 __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchArgs a) {
-    static_assert(LW == 32 || LW == 16 || LW == 8, "lanes per tuple");
-    constexpr int TPI = 32 / LW;                   // tuples per warp instruction
-    constexpr int CWS = LW == 32 ? 1 : 2;          // code words (4 tuples each) per step
+    static_assert(LW == 128 || LW == 64 || LW == 32 || LW == 16 || LW == 8, "lanes per tuple");
+    constexpr int NW = LW == 128 ? 4 : LW == 64 ? 2 : 1;   // query words per lane
+    constexpr bool W2 = NW > 1;                    // multi-word layout
+    constexpr int LPT = W2 ? 32 / NW : LW;         // lanes per tuple
+    constexpr int TPI = 32 / LPT;                  // tuples per warp instruction
+    constexpr int CWS = (LW == 32 || LW == 64) ? 1 : 2;   // code words (4 tuples each) per step
     constexpr int NS = 4 * CWS / TPI;              // sub-steps per step (<= 4)
+    constexpr int NOV = NS * NW > 4 ? NS * NW : 4; // overlap words per lane and step
+    static_assert(NS * NW <= 8, "at most eight overlap words per lane and step");
+    static_assert(!W2 || (va_batch_pv(KB) && MODE != 2), "multi-word layout: narrow unions, dense modes");
+    // passes with several tuples per instruction (multi-word, or narrow) of
+    // <= 8 union dims stage every block's table cells tuple-major in shared
+    // memory (8 bytes per tuple): one LDS.64 hands the TPI lane groups of an
+    // instruction their tuples' cells of all dims, instead of one SHFL per
+    // dimension and code word (the SHFLs cost data-pipe wavefronts too)
+    constexpr bool SCODE = TPI > 1 && KB <= 8 && MODE != 2;
     extern __shared__ __align__(16) uint32_t sm[];
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
     constexpr bool PV = va_batch_pv(KB);           // values + bounds in smem, overlap-only table
@@ -90,6 +110,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     uint32_t* s_cnt32 = s_rest;
     uint2* s_qe = reinterpret_cast<uint2*>(s_rest + 1024);
     uint32_t* s_qs = reinterpret_cast<uint32_t*>(s_qe + VB_WARPS * VB_QCAP);
+    // SCODE (PV, so no containment words): every warp's staged cells [128] uint2
+    uint2* s_code = reinterpret_cast<uint2*>(s_qe + VB_WARPS * VB_QCAP);
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_rest);
 
     // the recount pass only runs when the single-pass staging overflowed
@@ -119,11 +141,12 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     // is an immediate.
     // (rows of LW < 32 passes hold their LW words replicated 32 / LW times:
     // lane l reads word l, i.e. query word l % LW, conflict-free)
-    const uint32_t lane_off = lane * (PV ? 4 : 8);
-    const uint32_t lane_tup = lane / LW;           // this lane's tuple within a sub-step
+    const uint32_t lane_off = W2 ? (lane % LPT) * (4u * NW) : lane * (PV ? 4 : 8);
+    const uint32_t lane_tup = lane / LPT;          // this lane's tuple within a sub-step
     const char* s_tab = reinterpret_cast<const char*>(sm);
     float* wval = s_val + warp * 128 * KBV;        // STAGE: this warp's staged values
     uint2* qe = s_qe + warp * VB_QCAP;
+    uint2* wcode = s_code + warp * 128;            // SCODE: this warp's staged cells
     uint32_t* qs = s_qs + warp * VB_QCAP;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 2
     const uint32_t lt = lanemask_lt();
@@ -253,6 +276,23 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         else
                             reinterpret_cast<float2*>(wval)[val_slot2((4 * lane + jj) * H + h)] = make_float2(c[0], c[1]);
                     }
+                if constexpr (SCODE) {
+                    // cells of tuples 4*lane + b (b = 0..3), dims 0..3 / 4..7
+                    // byte-transposed into (lo, hi) words
+                    uint32_t c8[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) c8[u] = u < KB ? cw[u < KB ? u : 0] : 0u;
+                    uint32_t lo[4], hi[4];
+#pragma unroll
+                    for (uint32_t b = 0; b < 4; ++b) {
+                        const uint32_t sb = b | ((4u + b) << 4);   // byte b of x, byte b of y
+                        lo[b] = __byte_perm(__byte_perm(c8[0], c8[1], sb), __byte_perm(c8[2], c8[3], sb), 0x5410);
+                        hi[b] = __byte_perm(__byte_perm(c8[4], c8[5], sb), __byte_perm(c8[6], c8[7], sb), 0x5410);
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(wcode) + 2 * lane;
+                    dst[0] = make_uint4(lo[0], hi[0], lo[1], hi[1]);
+                    dst[1] = make_uint4(lo[2], hi[2], lo[3], hi[3]);
+                }
                 __syncwarp();
             }
             if (t0 + 128 < end) load_block(t0 + 128);
@@ -261,15 +301,21 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 // the step's CWS code words of every union dim (narrow passes
                 // take 8 tuples per step for more independent work)
                 uint32_t xw[CWS][KB];
+                uint2 sc[SCODE ? NS : 1];   // SCODE: sub-step ss's tuple cells (dims 0-3, 4-7)
+                if constexpr (SCODE) {
 #pragma unroll
-                for (int c = 0; c < CWS; ++c)
+                    for (int ss = 0; ss < NS; ++ss) sc[ss] = wcode[j4 + ss * TPI + lane_tup];
+                } else {
 #pragma unroll
-                    for (int u = 0; u < KB; ++u) xw[c][u] = __shfl_sync(0xFFFFFFFFu, cw[u], (j4 >> 2) + c);
+                    for (int c = 0; c < CWS; ++c)
+#pragma unroll
+                        for (int u = 0; u < KB; ++u) xw[c][u] = __shfl_sync(0xFFFFFFFFu, cw[u], (j4 >> 2) + c);
+                }
                 // sub-step s: this lane's tuple j4 + s*TPI + lane_tup, query
                 // word lane % LW (LW == 32: tuple j4 + s, word lane)
-                uint32_t ov4[4], su4[4];
+                uint32_t ov4[NOV], su4[NOV];
 #pragma unroll
-                for (uint32_t jj = 0; jj < 4; ++jj) ov4[jj] = su4[jj] = 0xFFFFFFFFu;
+                for (uint32_t jj = 0; jj < NOV; ++jj) ov4[jj] = su4[jj] = 0xFFFFFFFFu;
 #pragma unroll
                 for (int u = 0; u < KB; u += 2)
 #pragma unroll
@@ -279,11 +325,47 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         const uint32_t jj = ss * TPI + (LW == 32 ? 0u : lane_tup);   // tuple in the step
                         const uint32_t* x = xw[(ss * TPI) / 4];   // its code word (compile-time)
                         const uint32_t sel = 0x5504u | ((jj & 3u) << 4);
-                        const uint32_t ca = __byte_perm(x[u], lane_off, sel);
-                        if constexpr (PV) {
+                        // row address of dim uu (SCODE: byte uu % 4 of the
+                        // staged word, a compile-time selector)
+                        auto addr = [&](int uu) -> uint32_t {
+                            if constexpr (SCODE)
+                                return __byte_perm(uu < 4 ? sc[ss].x : sc[ss].y, lane_off, 0x5504u | ((uint32_t(uu) & 3u) << 4));
+                            else
+                                return __byte_perm(x[uu], lane_off, sel);
+                        };
+                        const uint32_t ca = addr(u);
+                        if constexpr (W2) {
+                            // words NW*l .. NW*l+NW-1 of the rows: sub-step ss
+                            // keeps word h in ov4[ss + NS*h]
+                            uint32_t ea[NW], eb[NW];
+                            const char* ra = s_tab + ca + (u / 2) * K * 256;
+                            if constexpr (NW == 4) {
+                                const uint4 t4 = *reinterpret_cast<const uint4*>(ra);
+                                ea[0] = t4.x, ea[1] = t4.y, ea[2] = t4.z, ea[3] = t4.w;
+                            } else {
+                                const uint2 t2 = *reinterpret_cast<const uint2*>(ra);
+                                ea[0] = t2.x, ea[1] = t2.y;
+                            }
+                            if (u + 1 < KB) {
+                                const uint32_t cb = addr(u + 1);
+                                const char* rb = s_tab + cb + (u / 2) * K * 256 + 128;
+                                if constexpr (NW == 4) {
+                                    const uint4 t4 = *reinterpret_cast<const uint4*>(rb);
+                                    eb[0] = t4.x, eb[1] = t4.y, eb[2] = t4.z, eb[3] = t4.w;
+                                } else {
+                                    const uint2 t2 = *reinterpret_cast<const uint2*>(rb);
+                                    eb[0] = t2.x, eb[1] = t2.y;
+                                }
+#pragma unroll
+                                for (int h = 0; h < NW; ++h) ov4[ss + NS * h] = ov4[ss + NS * h] & ea[h] & eb[h];
+                            } else {
+#pragma unroll
+                                for (int h = 0; h < NW; ++h) ov4[ss + NS * h] &= ea[h];
+                            }
+                        } else if constexpr (PV) {
                             const uint32_t ea = *reinterpret_cast<const uint32_t*>(s_tab + ca + (u / 2) * K * 256);
                             if (u + 1 < KB) {
-                                const uint32_t cb = __byte_perm(x[u + 1], lane_off, sel);
+                                const uint32_t cb = addr(u + 1);
                                 const uint32_t eb =
                                     *reinterpret_cast<const uint32_t*>(s_tab + cb + (u / 2) * K * 256 + 128);
                                 ov4[ss] = ov4[ss] & ea & eb;
@@ -293,7 +375,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         } else {
                             const uint2 ea = *reinterpret_cast<const uint2*>(s_tab + ca + u * K * 256);
                             if (u + 1 < KB) {
-                                const uint32_t cb = __byte_perm(x[u + 1], lane_off, sel);
+                                const uint32_t cb = addr(u + 1);
                                 const uint2 eb = *reinterpret_cast<const uint2*>(s_tab + cb + (u + 1) * K * 256);
                                 ov4[ss] = ov4[ss] & ea.x & eb.x;
                                 su4[ss] = su4[ss] & ea.y & eb.y;
@@ -351,9 +433,13 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     const uint32_t anyb = __ballot_sync(0xFFFFFFFFu, cnt_h != 0);
                     if (anyb) {
                         uint32_t excl, tot;
-                        if (__ballot_sync(0xFFFFFFFFu, cnt_h > 1) == 0) {
-                            excl = __popc(anyb & lt);
-                            tot = __popc(anyb);
+                        // hit counts below 4 (nearly always): prefix from two
+                        // bit-plane ballots instead of a shuffle scan
+                        if (__ballot_sync(0xFFFFFFFFu, cnt_h > 3) == 0) {
+                            const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, cnt_h & 1u);
+                            const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, cnt_h & 2u);
+                            excl = __popc(b0 & lt) + 2u * __popc(b1 & lt);
+                            tot = __popc(b0) + 2u * __popc(b1);
                         } else {
                             uint32_t incl = cnt_h;
 #pragma unroll
@@ -402,45 +488,54 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     qn = 0;
                 }
             };
+            // refine every full 32 entries, keep the rest at the front
+            auto drain = [&]() {
+                if (qn >= 32) {
+                    __syncwarp();
+                    uint32_t e0 = 0;
+                    for (; e0 + 32 <= qn; e0 += 32) process(e0, 32);
+                    // move the < 32 remaining entries to the front
+                    const uint32_t rem = qn - e0;
+                    uint2 me = make_uint2(0u, 0u);
+                    uint32_t ms = 0;
+                    if (lane < rem) {
+                        me = qe[e0 + lane];
+                        if constexpr (!PV) ms = qs[e0 + lane];
+                    }
+                    __syncwarp();
+                    if (lane < rem) {
+                        qe[lane] = me;
+                        if constexpr (!PV) qs[lane] = ms;
+                    }
+                    __syncwarp();
+                    qn = rem;
+                }
+            };
             for_each_step(
                 start, end,
                 [&](uint64_t t0) {
                     flush();   // the queued entries need the previous block's staged values
                     blk_t0 = t0;
                 },
-                [&](uint64_t, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[4], const uint32_t(&su4)[4]) {
+                [&](uint64_t, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[NOV], const uint32_t(&su4)[NOV]) {
 #pragma unroll
-                    for (uint32_t ss = 0; ss < NS; ++ss) {
-                        // lanes ascending = tuples ascending, then words
+                    for (uint32_t s2 = 0; s2 < uint32_t(NS * NW); ++s2) {
+                        // lanes ascending = tuples ascending, then words (W2:
+                        // word h of every tuple of the instruction, then word
+                        // h + 1 -- every query's entries stay in tuple order)
+                        const uint32_t ss = s2 % NS, h = s2 / NS;
                         const uint32_t jj = ss * TPI + (LW == 32 ? 0u : lane_tup);
-                        const bool nz = ov4[ss] != 0u && j4 + jj < jmax;
+                        const uint32_t wd = W2 ? NW * (lane % LPT) + h : lane % LW;
+                        const bool nz = ov4[s2] != 0u && j4 + jj < jmax;
                         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, nz);
                         if (nz) {
                             const uint32_t slot = qn + __popc(bal & lt);
-                            qe[slot] = make_uint2(ov4[ss], ((j4 + jj) << 5) | (lane % LW));
-                            if constexpr (!PV) qs[slot] = su4[ss];
+                            qe[slot] = make_uint2(ov4[s2], ((j4 + jj) << 5) | wd);
+                            if constexpr (!PV) qs[slot] = su4[s2];
                         }
                         qn += __popc(bal);
-                    }
-                    if (qn >= 32) {
-                        __syncwarp();
-                        uint32_t e0 = 0;
-                        for (; e0 + 32 <= qn; e0 += 32) process(e0, 32);
-                        // move the < 32 remaining entries to the front
-                        const uint32_t rem = qn - e0;
-                        uint2 me = make_uint2(0u, 0u);
-                        uint32_t ms = 0;
-                        if (lane < rem) {
-                            me = qe[e0 + lane];
-                            if constexpr (!PV) ms = qs[e0 + lane];
-                        }
-                        __syncwarp();
-                        if (lane < rem) {
-                            qe[lane] = me;
-                            if constexpr (!PV) qs[lane] = ms;
-                        }
-                        __syncwarp();
-                        qn = rem;
+                        // the queue holds < 32 + 2 ballots: drain after every second
+                        if (s2 % 2 == 1 || s2 + 1 == uint32_t(NS * NW)) drain();
                     }
                 });
             flush();
@@ -827,6 +922,17 @@ void run_kb_lw(const VaBatchArgs& a, cudaStream_t st) {
     va_batch_kernel<MODE, KB, LW><<<a.grid, VB_THREADS, smem, st>>>(a);
 }
 
+// query words per lane of a full pass (1, 2 or 4; MDRQ_VB_WORDS overrides the
+// default, for comparison and tests)
+int vb_words() {
+    static const int v = [] {
+        const char* e = std::getenv("MDRQ_VB_WORDS");
+        const int w = e ? std::atoi(e) : 4;
+        return (w == 1 || w == 2 || w == 4) ? w : 4;
+    }();
+    return v;
+}
+
 template <int MODE, int KB>
 void run_kb(const VaBatchArgs& a, cudaStream_t st) {
     // narrow passes of narrow unions pack 2 / 4 tuples per instruction (the
@@ -834,6 +940,9 @@ void run_kb(const VaBatchArgs& a, cudaStream_t st) {
     if constexpr (MODE != 2 && va_batch_pv(KB)) {
         if (a.lw == 8) return run_kb_lw<MODE, KB, 8>(a, st);
         if (a.lw == 16) return run_kb_lw<MODE, KB, 16>(a, st);
+        // full passes: NW query words per lane, NW tuples per instruction
+        if (vb_words() == 4) return run_kb_lw<MODE, KB, 128>(a, st);
+        if (vb_words() == 2) return run_kb_lw<MODE, KB, 64>(a, st);
     }
     run_kb_lw<MODE, KB, 32>(a, st);
 }
@@ -856,6 +965,7 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
         bytes += size_t(VB_WARPS) * 1024 * 2;
     else
         bytes += 1024 * 4 + size_t(VB_WARPS) * VB_QCAP * (8 + (pv ? 0 : 4));
+    if (mode != 2 && pv && kb <= 8) bytes += size_t(VB_WARPS) * 128 * 8;   // staged cells (multi-word passes)
     return bytes;
 }
 

@@ -303,6 +303,50 @@ def test_vafile_batch_recount_fallback(gpu, cap):
     assert r.returncode == 0 and "recount ok" in r.stdout, r.stdout + r.stderr
 
 
+_WORDS_SCRIPT = r"""
+import numpy as np
+import oracle
+import paper_1801_03644_b200 as eng
+rng = np.random.default_rng(5)
+# full passes (> 512 queries) over 3 / 8 / 12 / 16-dim unions: staged cells
+# (<= 8 dims) and shuffled code words (wider), duplicates, point predicates,
+# partial matches, a ragged tail
+for n, m, nq, s in ((70001, 3, 600, 1e-2), (200003, 8, 1000, 1e-3), (100003, 12, 700, 1e-2), (50001, 16, 1024, 1e-2)):
+    v = rng.random((n, m), dtype=np.float32)
+    w = s ** (1 / m)
+    lo = rng.uniform(0, 1 - w, (nq, m)).astype(np.float32)
+    hi = (lo + w).astype(np.float32)
+    lo[1], hi[1] = lo[0], hi[0]
+    lo[2, 1:], hi[2, 1:] = -np.inf, np.inf
+    lo[3, 0] = hi[3, 0] = v[17, 0]
+    if m > 8:
+        lo[4:40, 2:], hi[4:40, 2:] = -np.inf, np.inf
+    ec = oracle.count_batch(v, lo, hi)
+    eo, ei = oracle.ids_batch(v, lo, hi, counts=ec)
+    with eng.DeviceStore(v, layouts=1 | 4) as st:
+        assert np.array_equal(st.count(lo, hi, "vafile_batch"), ec), (n, m, nq)
+        o, i = st.ids(lo, hi, "vafile_batch")
+        assert np.array_equal(o, eo) and np.array_equal(i.astype(np.int64), ei), (n, m, nq)
+print("words ok")
+"""
+
+
+@pytest.mark.parametrize("words", ["1", "2", "4"])
+def test_vafile_batch_word_layouts(gpu, words):
+    """Every query-word layout of a full bit-sliced pass (vabatch.cu LW 32 /
+    64 / 128: 1, 2 or 4 query words per lane, 1, 2 or 4 tuples per table
+    load; MDRQ_VB_WORDS, read once per process, hence the subprocess) gives
+    the oracle's counts and ids."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MDRQ_VB_WORDS=words, PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _WORDS_SCRIPT], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "words ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_ids_stream_pipelined_batches(gpu):
     """DeviceStore.ids_stream (mdrq_query_ids_stream): several batches of
     different sizes and paths through the three pipelined slots (slot reuse,

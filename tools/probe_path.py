@@ -1,6 +1,6 @@
 """Probe one path on C2: python tools/probe_path.py <path> <mode> [nq]"""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("PKGROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1801_03644_b200 as eng
 from paper_1801_03644_b200 import workload, _lib
@@ -14,4 +14,4 @@ b = st.prepare(lo, hi, path)
 if mode == "ids":
     b.reserve()
 pr = b.profile(ids=(mode == "ids"))
-print(path, mode, {k: (round(v[0] * 1e3 / nq, 1), v[1]) for k, v in pr.items()}, "us/query")
+print(path, mode, {k: (round(v[0] * 1e3 / nq, 3), v[1]) for k, v in pr.items()}, "us/query")
