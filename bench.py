@@ -323,7 +323,7 @@ def main():
     stats = store.stats(nq)
     roofline = roofline_of(binfo["path"], prof, stats, n, nq, total_local, peak, peak_kind)
     if binfo["path"] == "vafile_batch":
-        lw = 32 if nq > 512 else 16 if nq > 256 else 8   # lanes per tuple of the pass (vabatch.cu)
+        lw = vb_lw(nq, binfo["max_union_dims"])
         key = (f"va_batch_kernel<3, {binfo['max_union_dims']}, {lw}>" if roofline["class"] == "scan"
                else "vb_scatter_kernel")
         roofline.update(ncu_traffic(key))
@@ -417,7 +417,7 @@ def main():
             "queries_per_s": nq / (ms / 1e3),
             "hbm_gbs_per_gpu": roofline["achieved"],
             "roofline": roofline,
-            "smem_roofline": smem_roofline(binfo, prof, n, clocks.summary()),
+            "smem_roofline": smem_roofline(binfo, prof, n, nq, clocks.summary()),
             "columnar_scan_roofline": col_roof,
             "pass_profile": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in prof.items()},
             "paths_us_per_query": paths,
@@ -443,7 +443,22 @@ def main():
     return 0
 
 
-def smem_roofline(binfo, prof, n, clocks):
+def vb_lw(nq: int, kb: int) -> int:
+    """The LW template argument of the bit-sliced pass's filter kernel
+    (vabatch.cu run_kb): 8 / 16 lanes per tuple for passes of <= 256 / 512
+    queries, else the multi-word layout (128: 4 query words per lane, the
+    default of MDRQ_VB_WORDS) for unions of <= 16 dims, 32 for wider ones."""
+    if kb > 16:
+        return 32
+    if nq <= 256:
+        return 8
+    if nq <= 512:
+        return 16
+    words = os.environ.get("MDRQ_VB_WORDS", "4")
+    return {"1": 32, "2": 64}.get(words, 128)
+
+
+def smem_roofline(binfo, prof, n, nq, clocks):
     """The resource that bounds the bit-sliced filter pass: shared-memory
     wavefronts.  Algorithmic count per pass: the table row of every tuple
     and union dimension -- 32 lanes x 4 bytes of overlap words (1 wavefront)
@@ -464,7 +479,7 @@ def smem_roofline(binfo, prof, n, clocks):
            "sm_mhz": mhz}
     # all the kernel's smem wavefronts (tables + shuffles + queue + refinement)
     # from the committed ncu capture, over this run's launch time
-    key = f"va_batch_kernel<3, {kb}, 32>"
+    key = f"va_batch_kernel<3, {kb}, {vb_lw(nq, kb)}>"
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
         with open(f) as fh:
             w = json.load(fh).get("smem_wavefronts", {}).get(key)

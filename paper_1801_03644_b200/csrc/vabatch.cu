@@ -518,24 +518,45 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     blk_t0 = t0;
                 },
                 [&](uint64_t, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[NOV], const uint32_t(&su4)[NOV]) {
+                    // lanes ascending = tuples ascending, then words (W2: word
+                    // h of every tuple of the instruction, then word h + 1 --
+                    // every query's entries stay in tuple order)
+                    constexpr uint32_t NB = NS * NW;   // ballots per step
+                    uint32_t bal[NB], meta[NB], nb = 0;
 #pragma unroll
-                    for (uint32_t s2 = 0; s2 < uint32_t(NS * NW); ++s2) {
-                        // lanes ascending = tuples ascending, then words (W2:
-                        // word h of every tuple of the instruction, then word
-                        // h + 1 -- every query's entries stay in tuple order)
+                    for (uint32_t s2 = 0; s2 < NB; ++s2) {
                         const uint32_t ss = s2 % NS, h = s2 / NS;
                         const uint32_t jj = ss * TPI + (LW == 32 ? 0u : lane_tup);
                         const uint32_t wd = W2 ? NW * (lane % LPT) + h : lane % LW;
-                        const bool nz = ov4[s2] != 0u && j4 + jj < jmax;
-                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, nz);
-                        if (nz) {
-                            const uint32_t slot = qn + __popc(bal & lt);
-                            qe[slot] = make_uint2(ov4[s2], ((j4 + jj) << 5) | wd);
-                            if constexpr (!PV) qs[slot] = su4[s2];
+                        meta[s2] = ((j4 + jj) << 5) | wd;
+                        bal[s2] = __ballot_sync(0xFFFFFFFFu, ov4[s2] != 0u && j4 + jj < jmax);
+                        nb += __popc(bal[s2]);
+                    }
+                    if (qn + nb <= VB_QCAP) {
+                        // the whole step fits the queue: all entries at once
+                        // (independent ballots, no drain between them)
+#pragma unroll
+                        for (uint32_t s2 = 0; s2 < NB; ++s2) {
+                            if (bal[s2] >> lane & 1u) {
+                                const uint32_t slot = qn + __popc(bal[s2] & lt);
+                                qe[slot] = make_uint2(ov4[s2], meta[s2]);
+                                if constexpr (!PV) qs[slot] = su4[s2];
+                            }
+                            qn += __popc(bal[s2]);
                         }
-                        qn += __popc(bal);
-                        // the queue holds < 32 + 2 ballots: drain after every second
-                        if (s2 % 2 == 1 || s2 + 1 == uint32_t(NS * NW)) drain();
+                        drain();
+                    } else {
+                        // dense step: < 32 + 2 ballots between drains
+#pragma unroll
+                        for (uint32_t s2 = 0; s2 < NB; ++s2) {
+                            if (bal[s2] >> lane & 1u) {
+                                const uint32_t slot = qn + __popc(bal[s2] & lt);
+                                qe[slot] = make_uint2(ov4[s2], meta[s2]);
+                                if constexpr (!PV) qs[slot] = su4[s2];
+                            }
+                            qn += __popc(bal[s2]);
+                            if (s2 % 2 == 1 || s2 + 1 == NB) drain();
+                        }
                     }
                 });
             flush();
