@@ -518,17 +518,68 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     blk_t0 = t0;
                 },
                 [&](uint64_t, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[NOV], const uint32_t(&su4)[NOV]) {
-                    // lanes ascending = tuples ascending, then words (W2: word
-                    // h of every tuple of the instruction, then word h + 1 --
-                    // every query's entries stay in tuple order)
+                    if constexpr (W2) {
+                        // multi-word layouts queue tuple-major -- tuple, then
+                        // query word ascending (lane order is (tuple, l), a
+                        // lane's words 4l..4l+3 are consecutive) -- so a
+                        // refinement round covers few tuples and consecutive
+                        // words (the bound slots' swizzle keys on the word) and
+                        // the records of a query stay far apart for the scatter.
+                        // A lane's rank = the prefix of its nonzero-word count
+                        // over the lanes below, from the count's bit planes.
+                        uint32_t pl[NS][3], nzm[NS], nb = 0;
+#pragma unroll
+                        for (uint32_t ss = 0; ss < NS; ++ss) {
+                            const uint32_t jj = ss * TPI + lane_tup;
+                            uint32_t m = 0;
+#pragma unroll
+                            for (int h = 0; h < NW; ++h) m |= uint32_t(ov4[ss + NS * h] != 0u) << h;
+                            if (j4 + jj >= jmax) m = 0;
+                            nzm[ss] = m;
+                            const uint32_t c = __popc(m);
+                            pl[ss][0] = __ballot_sync(0xFFFFFFFFu, c & 1u);
+                            pl[ss][1] = __ballot_sync(0xFFFFFFFFu, c & 2u);
+                            pl[ss][2] = NW == 4 ? __ballot_sync(0xFFFFFFFFu, c & 4u) : 0u;
+                            nb += __popc(pl[ss][0]) + 2u * __popc(pl[ss][1]) + 4u * __popc(pl[ss][2]);
+                        }
+                        // queue the entries of sub-step ss's lanes in `lanes`
+                        auto put = [&](uint32_t ss, uint32_t lanes) {
+                            const uint32_t below = lt & lanes;
+                            uint32_t slot = qn + __popc(pl[ss][0] & below) + 2u * __popc(pl[ss][1] & below) +
+                                            4u * __popc(pl[ss][2] & below);
+                            if (lanes >> lane & 1u) {
+                                const uint32_t mb = (((j4 + ss * TPI + lane_tup) << 5) | (NW * (lane % LPT)));
+#pragma unroll
+                                for (int h = 0; h < NW; ++h)
+                                    if (nzm[ss] >> h & 1u) qe[slot++] = make_uint2(ov4[ss + NS * h], mb + h);
+                            }
+                            qn += __popc(pl[ss][0] & lanes) + 2u * __popc(pl[ss][1] & lanes) +
+                                  4u * __popc(pl[ss][2] & lanes);
+                        };
+                        if (qn + nb <= VB_QCAP) {
+                            // the whole step fits the queue: one drain
+#pragma unroll
+                            for (uint32_t ss = 0; ss < NS; ++ss) put(ss, 0xFFFFFFFFu);
+                            drain();
+                        } else {
+                            // dense step: half a sub-step (<= 64 entries) between drains
+#pragma unroll
+                            for (uint32_t ss = 0; ss < NS; ++ss) {
+                                put(ss, 0x0000FFFFu);
+                                drain();
+                                put(ss, 0xFFFF0000u);
+                                drain();
+                            }
+                        }
+                    } else {
+                    // lanes ascending = tuples ascending, then words
                     constexpr uint32_t NB = NS * NW;   // ballots per step
                     uint32_t bal[NB], meta[NB], nb = 0;
 #pragma unroll
                     for (uint32_t s2 = 0; s2 < NB; ++s2) {
-                        const uint32_t ss = s2 % NS, h = s2 / NS;
+                        const uint32_t ss = s2 % NS;
                         const uint32_t jj = ss * TPI + (LW == 32 ? 0u : lane_tup);
-                        const uint32_t wd = W2 ? NW * (lane % LPT) + h : lane % LW;
-                        meta[s2] = ((j4 + jj) << 5) | wd;
+                        meta[s2] = ((j4 + jj) << 5) | (lane % LW);
                         bal[s2] = __ballot_sync(0xFFFFFFFFu, ov4[s2] != 0u && j4 + jj < jmax);
                         nb += __popc(bal[s2]);
                     }
@@ -557,6 +608,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             qn += __popc(bal[s2]);
                             if (s2 % 2 == 1 || s2 + 1 == NB) drain();
                         }
+                    }
                     }
                 });
             flush();
@@ -765,9 +817,17 @@ __device__ __forceinline__ uint32_t match_q10(uint32_t q, bool act) {
 // pos[q] = qoff[q] + base[group][q] + ids of earlier windows.  Runs of
 // adjacent groups abut in the output, so the L2 assembles full sectors
 // instead of read-modify-writing scattered 4-byte stores.
-constexpr int SC_THREADS = 512;
+#ifndef MDRQ_SC_THREADS
+#define MDRQ_SC_THREADS 512
+#endif
+#ifndef MDRQ_SC_WIN_BLOCKS
+#define MDRQ_SC_WIN_BLOCKS 20
+#endif
+constexpr int SC_THREADS = MDRQ_SC_THREADS;
 constexpr int SC_WARPS = SC_THREADS / 32;
-constexpr uint32_t SC_WIN_BLOCKS = 20;
+constexpr uint32_t SC_WIN_BLOCKS = MDRQ_SC_WIN_BLOCKS;
+constexpr uint32_t SC_PER = kRecBlock / SC_THREADS;      // records per thread per block
+constexpr uint32_t SC_QPT = 1024 / SC_THREADS;           // queries per thread in the prefix
 constexpr uint32_t SC_WIN = SC_WIN_BLOCKS * kRecBlock;   // records per window
 constexpr size_t SC_SMEM = size_t(SC_WIN) * (4 + 4) + size_t(SC_WARPS) * 1024 * (2 + 1) + 1025 * 4 + 1024 * 8;
 
@@ -807,12 +867,12 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
         if (lane == SC_WIN_BLOCKS - 1) s_boff[p][SC_WIN_BLOCKS] = incl;
     };
     // every record load of a window in flight at once: 2 per thread per block
-    uint32_t v[SC_WIN_BLOCKS][2];
+    uint32_t v[SC_WIN_BLOCKS][SC_PER];
     auto load_records = [&](uint32_t p) {
 #pragma unroll
         for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k)
 #pragma unroll
-            for (uint32_t h = 0; h < 2; ++h) {
+            for (uint32_t h = 0; h < SC_PER; ++h) {
                 const uint32_t i = tid + h * SC_THREADS;
                 v[k][h] = i < s_bcnt[p][k] ? __ldcs(a.rec + uint64_t(s_blk[p][k]) * kRecBlock + i) : 0u;
             }
@@ -840,7 +900,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
 #pragma unroll
             for (uint32_t k = 0; k < SC_WIN_BLOCKS; ++k)
 #pragma unroll
-                for (uint32_t h = 0; h < 2; ++h) {
+                for (uint32_t h = 0; h < SC_PER; ++h) {
                     const uint32_t i = tid + h * SC_THREADS;
                     if (i < s_bcnt[p][k]) s_rec[s_boff[p][k] + i] = v[k][h];
                 }
@@ -864,10 +924,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
             __syncthreads();
             if (more) load_records(p ^ 1u);   // the next list is visible now
             // per query: exclusive prefix over the warps' segments, window total
-            uint32_t tot[2];
+            uint32_t tot[SC_QPT];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t q = tid * 2 + h;
+            for (uint32_t h = 0; h < SC_QPT; ++h) {
+                const uint32_t q = tid * SC_QPT + h;
                 uint32_t run = 0;
 #pragma unroll
                 for (int w = 0; w < SC_WARPS; ++w) {
@@ -878,7 +938,9 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 tot[h] = run;
             }
             // exclusive scan of the totals over the 1024 queries
-            const uint32_t pair = tot[0] + tot[1];
+            uint32_t pair = 0;
+#pragma unroll
+            for (uint32_t h = 0; h < SC_QPT; ++h) pair += tot[h];
             uint32_t incl = pair;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -889,9 +951,12 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
             __syncthreads();
             uint32_t wbase = 0;
             for (uint32_t w = 0; w < warp; ++w) wbase += s_wsum[w];
-            const uint32_t ex = wbase + incl - pair;
-            s_off[tid * 2] = ex;
-            s_off[tid * 2 + 1] = ex + tot[0];
+            uint32_t ex = wbase + incl - pair;
+#pragma unroll
+            for (uint32_t h = 0; h < SC_QPT; ++h) {
+                s_off[tid * SC_QPT + h] = ex;
+                ex += tot[h];
+            }
             if (tid == 0) s_off[1024] = n;
             __syncthreads();
             // stable placement: rank = earlier warps' segments + earlier
