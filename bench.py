@@ -446,15 +446,15 @@ def main():
 def vb_lw(nq: int, kb: int) -> int:
     """The LW template argument of the bit-sliced pass's filter kernel
     (vabatch.cu run_kb): 8 / 16 lanes per tuple for passes of <= 256 / 512
-    queries, else the multi-word layout (128: 4 query words per lane, the
-    default of MDRQ_VB_WORDS) for unions of <= 16 dims, 32 for wider ones."""
+    queries, else the four-word layout (128) for unions of <= 10 dims and 32
+    for wider ones (MDRQ_VB_WORDS overrides)."""
     if kb > 16:
         return 32
     if nq <= 256:
         return 8
     if nq <= 512:
         return 16
-    words = os.environ.get("MDRQ_VB_WORDS", "4")
+    words = os.environ.get("MDRQ_VB_WORDS") or ("4" if kb <= 10 else "1")
     return {"1": 32, "2": 64}.get(words, 128)
 
 

@@ -1008,15 +1008,18 @@ void run_kb_lw(const VaBatchArgs& a, cudaStream_t st) {
     va_batch_kernel<MODE, KB, LW><<<a.grid, VB_THREADS, smem, st>>>(a);
 }
 
-// query words per lane of a full pass (1, 2 or 4; MDRQ_VB_WORDS overrides the
-// default, for comparison and tests)
-int vb_words() {
+// query words per lane of a full pass over a union of kb dims: 4 where the
+// values are staged on chip (<= 10 dims), 1 where the refinement reads them
+// from global memory (11..16 dims: the four-word order measured 20 % slower
+// in ids mode on C3); MDRQ_VB_WORDS (1, 2 or 4) overrides it for every union,
+// for comparison and tests
+int vb_words(uint32_t kb) {
     static const int v = [] {
         const char* e = std::getenv("MDRQ_VB_WORDS");
-        const int w = e ? std::atoi(e) : 4;
-        return (w == 1 || w == 2 || w == 4) ? w : 4;
+        const int w = e ? std::atoi(e) : 0;
+        return (w == 1 || w == 2 || w == 4) ? w : 0;
     }();
-    return v;
+    return v ? v : kb <= 10 ? 4 : 1;
 }
 
 template <int MODE, int KB>
@@ -1027,8 +1030,8 @@ void run_kb(const VaBatchArgs& a, cudaStream_t st) {
         if (a.lw == 8) return run_kb_lw<MODE, KB, 8>(a, st);
         if (a.lw == 16) return run_kb_lw<MODE, KB, 16>(a, st);
         // full passes: NW query words per lane, NW tuples per instruction
-        if (vb_words() == 4) return run_kb_lw<MODE, KB, 128>(a, st);
-        if (vb_words() == 2) return run_kb_lw<MODE, KB, 64>(a, st);
+        if (vb_words(KB) == 4) return run_kb_lw<MODE, KB, 128>(a, st);
+        if (vb_words(KB) == 2) return run_kb_lw<MODE, KB, 64>(a, st);
     }
     run_kb_lw<MODE, KB, 32>(a, st);
 }
