@@ -309,9 +309,11 @@ import oracle
 import paper_1801_03644_b200 as eng
 rng = np.random.default_rng(5)
 # full passes (> 512 queries) over 3 / 8 / 12 / 16-dim unions: staged cells
-# (<= 8 dims) and shuffled code words (wider), duplicates, point predicates,
-# partial matches, a ragged tail
-for n, m, nq, s in ((70001, 3, 600, 1e-2), (200003, 8, 1000, 1e-3), (100003, 12, 700, 1e-2), (50001, 16, 1024, 1e-2)):
+# (<= 8 dims) and shuffled code words (wider), a dense pass (s = 0.2: steps
+# that overflow the queue and drain per half sub-step), duplicates, point
+# predicates, partial matches, a ragged tail
+for n, m, nq, s in ((70001, 3, 600, 1e-2), (200003, 8, 1000, 1e-3), (60013, 8, 700, 0.2), (100003, 12, 700, 1e-2),
+                    (50001, 16, 1024, 1e-2)):
     v = rng.random((n, m), dtype=np.float32)
     w = s ** (1 / m)
     lo = rng.uniform(0, 1 - w, (nq, m)).astype(np.float32)
