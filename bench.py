@@ -393,9 +393,11 @@ def main():
     e2e_val = n * world * nq / e2e_s
 
     cpu = None
+    ref_methods = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, kind, qn, thr, dt = cpu_reference_rate(values, lo, hi, budget_s=15.0,
                                                      threads=os.cpu_count() or 1)
+        ref_methods = reference_methods()
         cpu = {"value": rate, "unit": "tuples/s", "cores": thr, "kind": kind,
                "sample": f"{qn} of the {nq} queries over all {n} tuples ({dt:.1f} s)"}
 
@@ -433,6 +435,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
+            "reference_methods": ref_methods,
             "setup_s": {"generate": round(t_gen, 2), "store_build": round(t_build, 2)},
         }
         print(json.dumps(line), flush=True)
@@ -456,6 +459,22 @@ def vb_lw(nq: int, kb: int) -> int:
         return 16
     words = os.environ.get("MDRQ_VB_WORDS") or ("4" if kb <= 10 else "1")
     return {"1": 32, "2": 64}.get(words, 128)
+
+
+def reference_methods():
+    """The reference's own access methods (scan, VA-file, kd-tree, R*-tree)
+    through its public API on this host, bounded (tools/reference_methods.py
+    bench_leg; the package pip-installed into baseline/_ref by build()), or
+    None when it is not installed."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("reference_methods",
+                                                  os.path.join(ROOT, "tools", "reference_methods.py"))
+    mod = importlib.util.module_from_spec(spec)
+    try:
+        spec.loader.exec_module(mod)
+        return mod.bench_leg()
+    except Exception as e:   # the baseline table is informative; never fail the bench on it
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
 
 
 def smem_roofline(binfo, prof, n, nq, clocks):

@@ -73,6 +73,35 @@ def _time(mdrq, name, mode, values, lo, hi, nq, threads):
             "us_per_query": round(t * 1e6, 1), "tuples_per_s": values.shape[0] / t}
 
 
+def bench_leg(threads: int | None = None) -> dict | None:
+    """The bounded table bench.py prints beside its line (~20-30 s of host
+    work): the reference's own scan, VA-file, kd-tree and R*-tree methods on
+    C1 (the trees on a 1e5-row prefix), 10-20 queries each, from
+    baseline/_ref.  None when the reference package is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mdrq")):
+        return None
+    import psutil
+    from paper_1801_03644_b200 import workload
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import mdrq
+    threads = threads or os.cpu_count() or 1
+    values = workload.c1_data()
+    lo, hi = workload.c1_queries()
+    out = {"host_threads": threads, "physical_cores": psutil.cpu_count(logical=False), "cpu_model": _cpu_model(),
+           "reference": f"baseline/_ref (backend {mdrq.BACKEND})",
+           "data": "C1: 1e6 x 3 uniform seed 0, queries at 1 % selectivity; kd-tree / R*-tree on the first 1e5 rows",
+           "methods": []}
+    plan = [("sequential", "scalar", 1_000_000, 10), ("horizontal", "scalar", 1_000_000, 20),
+            ("vertical", "scalar", 1_000_000, 10), ("vafile", "scalar", 1_000_000, 10),
+            ("kdtree", "scalar", 100_000, 20), ("rstar", "scalar", 100_000, 20)]
+    for name, mode, n, nq in plan:
+        e = _time(mdrq, name, mode, values[:n], lo, hi, nq, threads)
+        out["methods"].append({k: e[k] for k in ("method", "n", "queries", "build_s", "us_per_query")})
+    return out
+
+
 def main():
     import psutil
     from paper_1801_03644_b200 import workload
