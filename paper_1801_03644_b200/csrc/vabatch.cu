@@ -8,16 +8,20 @@
 //
 //   * per union dimension u and coarse cell c the host builds a 1024-bit
 //     query mask OV[u][c] (queries whose box overlaps cell c in dimension u)
-//     and, for unions wider than 8 dims, SU[u][c] (queries that contain cell
-//     c entirely).  Word w of a mask covers queries 32w .. 32w+31 and lives
-//     in shared memory, so a warp whose LANE w owns word w reads a whole
-//     1024-bit row with one conflict-free LDS per lane;
+//     and, for unions wider than 16 dims, SU[u][c] (queries that contain
+//     cell c entirely).  Word w of a mask covers queries 32w .. 32w+31 and
+//     lives in shared memory; a full pass reads a 1024-bit row with 8 lanes
+//     x LDS.128 (4 words each), so one instruction serves 4 tuples (LW ==
+//     128; 1 / 2 words per lane remain selectable), narrow passes replicate
+//     their words across the row;
 //   * the warp walks its chunk of tuples in order; per tuple it ANDs the rows
-//     of the tuple's cells: maybe = AND_u OV.  Narrow unions (<= 8 dims)
-//     refine every candidate in maybe exactly -- the block's float32 values
-//     are staged tuple-major in shared memory and the query bounds live
-//     there too, so a refinement is a few LDS.128; wider unions AND the SU
-//     rows as well and refine only maybe & ~sure (edge cells) from global;
+//     of the tuple's cells: maybe = AND_u OV.  The cells come from a
+//     tuple-major staged copy of the block's codes (<= 8 dims) or from
+//     shuffles of the loaded code words.  Unions of <= 16 dims queue every
+//     nonzero (tuple, word) and refine the queue lane-parallel against the
+//     query bounds in shared memory and the tuple's float32 values (staged
+//     tuple-major for <= 10 dims, else from global); wider unions AND the
+//     SU rows as well and refine only maybe & ~sure (edge cells) from global;
 //   * matches are counted per query (mode 0), per (chunk, query) (mode 1),
 //     or, in ids mode, counted per (chunk, query) while (tuple, query)
 //     records are staged in tuple order (mode 3); a scan over the chunk
