@@ -77,3 +77,44 @@ def test_null_store_and_arguments_are_einval():
     assert lib.mdrq_query_ids_stream(None, None, None, None, 1, 0, None, None, None, None, None) == _lib.MDRQ_EINVAL
     assert lib.mdrq_fetch_ids(None, None, 0) == _lib.MDRQ_EINVAL
     assert lib.mdrq_last_error()
+
+
+_C_PROGRAM = r"""
+#include <stdio.h>
+#include <stdint.h>
+#include "mdrq_b200.h"
+int main(void) {
+    /* a C99 caller of the drop-in boundary: version, an invalid store
+       (EINVAL + message), the null-store guard -- no device needed */
+    mdrq_store* s = 0;
+    uint64_t total = 0;
+    if (mdrq_abi_version() != 1) return 2;
+    if (mdrq_store_create(0, 0, 0, 0, 1, 0, 0, &s) != MDRQ_EINVAL) return 3;
+    if (!mdrq_last_error() || !mdrq_last_error()[0]) return 4;
+    if (mdrq_query_ids(0, 0, 0, 0, MDRQ_PATH_AUTO, 0, 0, 0, &total) != MDRQ_EINVAL) return 5;
+    printf("c abi ok\n");
+    return 0;
+}
+"""
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/mdrq_b200.h compiles as C99 (what a cgo / FFI binding sees),
+    and a C program links against libmdrq_b200.so and runs its device-free
+    entry points."""
+    import shutil
+    import subprocess
+    from paper_1801_03644_b200 import _lib
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if not cc:
+        pytest.skip("no C compiler")
+    src = tmp_path / "abi.c"
+    src.write_text(_C_PROGRAM)
+    exe = tmp_path / "abi"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    r = subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-pedantic", "-I", os.path.join(ROOT, "include"),
+                        str(src), "-o", str(exe), "-L", libdir, "-l:libmdrq_b200.so",
+                        f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "c abi ok" in r.stdout, (r.returncode, r.stdout, r.stderr)
