@@ -100,30 +100,72 @@ __global__ void minmax_finish(float* out2) {
     }
 }
 
-// SWAR range test of 4 byte-codes packed in x against [lo, hi] (0..256):
-// returns flag bits at positions 8, 9, 24, 25 for bytes 0, 1, 2, 3.
-__device__ __forceinline__ uint32_t swar_in(uint32_t x, uint32_t lo, uint32_t hi) {
-    const uint32_t e = x & 0x00FF00FFu;          // bytes 0, 2 in 16-bit lanes
-    const uint32_t o = (x >> 8) & 0x00FF00FFu;   // bytes 1, 3
-    const uint32_t klo = (0x100u - lo) * 0x00010001u;
-    const uint32_t khi = (0x100u + hi) * 0x00010001u;
-    const uint32_t ge_e = e + klo, ge_o = o + klo;   // bit 8 of lane: v >= lo
-    const uint32_t le_e = khi - e, le_o = khi - o;   // bit 8 of lane: v <= hi
-    const uint32_t ie = ge_e & le_e & 0x01000100u;
-    const uint32_t io = ge_o & le_o & 0x01000100u;
-    return ie | (io << 1);
+// SWAR range test of 4 byte-codes packed in one word against a code range
+// [lo, hi] (0 <= lo <= hi <= 255): v is in range iff (v - lo) mod 256 <=
+// hi - lo.  Per byte, B = (v | 0x80) - (lo & 0x7f) never borrows across
+// bytes; its low 7 bits are those of v - lo and bit 7 of v - lo is
+// B7 ^ v7 ^ ~lo7 (all folded into one LOP3 with the per-range mask km); the
+// compare d <= w takes the low-7-bit borrow t7 of (w | 0x80) - (d & 0x7f)
+// and the two top bits.  Seven ALU ops per word (the v | 0x80 shared by the
+// two tests of the SURE path); the verdict is bit 7 of every byte, the
+// other bits are don't-care (the alive flags keep only bits 7, 15, 23, 31).
+// The formula is checked exhaustively over (v, lo, hi) by a numpy
+// restatement in tests/test_host.py; the kernel by the -m gpu parity tests.
+constexpr uint32_t kSwarHi = 0x80808080u;
+
+struct SwarRange {
+    uint32_t c1;    // lo replicated, bit 7 of every byte cleared
+    uint32_t km;    // ~0 if lo7 == 0 (bit 7 of v - lo = B7 ^ v7 ^ 1), else 0
+    uint32_t wH;    // (hi - lo) replicated with bit 7 set
+    uint32_t wm;    // ~0 if bit 7 of hi - lo is set
+    uint32_t live;  // 0 for an empty range (every code rejected)
+};
+
+__device__ __forceinline__ SwarRange swar_range(int lo, int hi) {
+    SwarRange r;
+    const bool empty = lo > hi || lo > 255 || hi < 0;
+    const uint32_t l = empty ? 0u : uint32_t(lo), w = empty ? 0u : uint32_t(hi - lo);
+    r.c1 = (l * 0x01010101u) & ~kSwarHi;
+    r.km = (l & 0x80u) ? 0u : ~0u;
+    r.wH = (w * 0x01010101u) | kSwarHi;
+    r.wm = (w & 0x80u) ? ~0u : 0u;
+    r.live = empty ? 0u : ~0u;
+    return r;
 }
 
-// flags (bits 8, 9, 24, 25) of word w -> 4-bit tuple mask
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3t(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return r;
+}
+
+// flags &= in-range verdicts of the 4 codes of x (xh = x | 0x80808080).  The
+// boolean stages are explicit LOP3s: left to itself the compiler turns the
+// 0 / ~0 range masks into predicates and spends a SEL per word on each.
+__device__ __forceinline__ uint32_t swar_and(uint32_t flags, uint32_t x, uint32_t xh, const SwarRange& r) {
+    const uint32_t b = xh - r.c1;
+    const uint32_t t = r.wH - (b & ~kSwarHi);
+    const uint32_t d = lop3t<0x96>(b, x, r.km);            // b ^ x ^ km
+    const uint32_t le = lop3t<0x8E>(d, r.wm, t);           // (wm & ~d) | (~(d ^ wm) & t)
+    return lop3t<0x80>(flags, le, r.live);                 // flags & le & live
+}
+
+// flags (bits 7, 15, 23, 31) of word w -> 4-bit tuple mask
 __device__ __forceinline__ uint32_t flags_to_nib(uint32_t f) {
-    return ((f >> 8) & 3u) | ((f >> 22) & 0xCu);
+    return ((((f >> 7) & 0x01010101u) * 0x00204081u) >> 21) & 15u;
 }
 
 // SURE: also track "strictly inside the code range" per tuple and refine
 // only the edge-cell tuples (queries expected to return many tuples);
 // otherwise one range test per code and every alive tuple is refined.
+//
+// Occupancy decides this latency-bound loop: 8 CTAs per SM (32 registers, a
+// few bytes of L1 spill) measured fastest for the plain test, 6 (40
+// registers) with the second (SURE) test -- C2 single queries, 1e-3: 95 us
+// vs 136 us at 61 registers; tools/probe_va_single.py.
 template <bool IDS, bool SURE>
-__global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
+__global__ void __launch_bounds__(VA_THREADS, SURE ? 6 : 8) va_scan_kernel(const ScanArgs a) {
     __shared__ uint32_t s_cnt[VA_THREADS / 32];
     __shared__ uint32_t s_ld[VA_THREADS / 32];
     __shared__ uint32_t s_rf[VA_THREADS / 32];
@@ -143,7 +185,7 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
 #pragma unroll
     for (int g = 0; g < VA_G; ++g)
 #pragma unroll
-        for (int w = 0; w < 4; ++w) al[g][w] = su[g][w] = 0x03000300u;
+        for (int w = 0; w < 4; ++w) al[g][w] = su[g][w] = kSwarHi;
     if (uint64_t(tile + 1) * kVaTile > a.n) {
 #pragma unroll
         for (int g = 0; g < VA_G; ++g)
@@ -151,43 +193,61 @@ __global__ void __launch_bounds__(VA_THREADS) va_scan_kernel(const ScanArgs a) {
             for (int w = 0; w < 4; ++w) {
                 uint32_t f = 0;
                 const uint64_t t0 = base + g * 512 + w * 4;
-                if (t0 + 0 < a.n) f |= 1u << 8;
-                if (t0 + 1 < a.n) f |= 1u << 9;
-                if (t0 + 2 < a.n) f |= 1u << 24;
-                if (t0 + 3 < a.n) f |= 1u << 25;
+                if (t0 + 0 < a.n) f |= 1u << 7;
+                if (t0 + 1 < a.n) f |= 1u << 15;
+                if (t0 + 2 < a.n) f |= 1u << 23;
+                if (t0 + 3 < a.n) f |= 1u << 31;
                 al[g][w] = f;
             }
     }
 
     uint32_t nload = 0;  // 16-byte code loads issued
-    for (uint32_t i = 0; i < k; ++i) {
+    // two dimensions per step: both planes' loads are issued together (the
+    // second one's skip decided by the alive flags before the first), so a
+    // lane has 4 independent 16-byte loads in flight instead of 2
+    for (uint32_t i = 0; i < k; i += 2) {
         uint32_t any = 0;
 #pragma unroll
         for (int g = 0; g < VA_G; ++g) any |= al[g][0] | al[g][1] | al[g][2] | al[g][3];
         if (!__any_sync(0xFFFFFFFFu, any)) break;
-        const DimPred p = P[i];
-        const uint32_t d = p.dim;
-        const uint32_t cl = p.cl, ch = p.ch;
-        const uint32_t sl = cl + p.edge_lo, sh = ch - p.edge_hi;  // strict interior (SURE)
-        const uint4* c = reinterpret_cast<const uint4*>(a.codes + uint64_t(d) * a.stride + base);
-        uint4 x[VA_G];
-#pragma unroll
-        for (int g = 0; g < VA_G; ++g) nload += (al[g][0] | al[g][1] | al[g][2] | al[g][3]) ? 1u : 0u;
+        const bool two = i + 1 < k;
+        const DimPred p0 = P[i];
+        const DimPred p1 = P[two ? i + 1 : i];
+        const SwarRange r0 = swar_range(p0.cl, p0.ch), r1 = swar_range(p1.cl, p1.ch);
+        // strict interior (SURE): the edge cells excluded
+        const SwarRange s0 = swar_range(int(p0.cl) + p0.edge_lo, int(p0.ch) - p0.edge_hi);
+        const SwarRange s1 = swar_range(int(p1.cl) + p1.edge_lo, int(p1.ch) - p1.edge_hi);
+        const uint4* c0 = reinterpret_cast<const uint4*>(a.codes + uint64_t(p0.dim) * a.stride + base);
+        const uint4* c1 = reinterpret_cast<const uint4*>(a.codes + uint64_t(p1.dim) * a.stride + base);
+        uint4 x0[VA_G], x1[VA_G];
 #pragma unroll
         for (int g = 0; g < VA_G; ++g) {
             const uint32_t ga = al[g][0] | al[g][1] | al[g][2] | al[g][3];
-            if (ga) x[g] = ld_stream_u4(c + g * 32);
+            nload += ga ? (two ? 2u : 1u) : 0u;
+            if (ga) {
+                x0[g] = ld_stream_u4(c0 + g * 32);
+                if (two) x1[g] = ld_stream_u4(c1 + g * 32);
+            }
         }
 #pragma unroll
         for (int g = 0; g < VA_G; ++g) {
             const uint32_t ga = al[g][0] | al[g][1] | al[g][2] | al[g][3];
             if (ga) {
-                const uint32_t xw[4] = {x[g].x, x[g].y, x[g].z, x[g].w};
+                const uint32_t xw[4] = {x0[g].x, x0[g].y, x0[g].z, x0[g].w};
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
-                    al[g][w] &= swar_in(xw[w], cl, ch);
-                    // (sh may be "negative": 0x100 + sh wraps below 0x100 -> never <=)
-                    if constexpr (SURE) su[g][w] &= swar_in(xw[w], sl, sh);
+                    const uint32_t xh = xw[w] | kSwarHi;
+                    al[g][w] = swar_and(al[g][w], xw[w], xh, r0);
+                    if constexpr (SURE) su[g][w] = swar_and(su[g][w], xw[w], xh, s0);
+                }
+                if (two) {
+                    const uint32_t yw[4] = {x1[g].x, x1[g].y, x1[g].z, x1[g].w};
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const uint32_t yh = yw[w] | kSwarHi;
+                        al[g][w] = swar_and(al[g][w], yw[w], yh, r1);
+                        if constexpr (SURE) su[g][w] = swar_and(su[g][w], yw[w], yh, s1);
+                    }
                 }
             }
         }

@@ -181,3 +181,48 @@ def test_cli_parser_and_report_columns():
                                                                                    "nodes_visited")
     a = build_parser().parse_args(["bench", "--n", "10", "--queries", "3", "--out", "x.csv"])
     assert (a.cmd, a.n, a.count, a.out) == ("bench", 10, 3, "x.csv")
+
+
+def _lop3(a, b, c, lut):
+    """PTX lop3.b32: bit i of the result = bit (a_i << 2 | b_i << 1 | c_i) of lut."""
+    r = np.zeros_like(a)
+    for mt in range(8):
+        if (lut >> mt) & 1:
+            ta = a if mt & 4 else ~a
+            tb = b if mt & 2 else ~b
+            tc = c if mt & 1 else ~c
+            r |= ta & tb & tc
+    return r
+
+
+def test_va_swar_range_test_exhaustive():
+    """numpy restatement of vafile.cu swar_range / swar_and (the single-query
+    VA filter's byte-code range test, LOP3 tables as in the kernel), checked
+    for every code byte in every byte position against every code range
+    0 <= lo <= hi <= 255 and the empty encodings (lo > hi, lo = 256, hi = -1)."""
+    H = np.uint32(0x80808080)
+    v = np.arange(256, dtype=np.uint32)
+    words = [v << np.uint32(8 * p) | (np.uint32(0x5A) << np.uint32(8 * ((p + 1) & 3))) for p in range(4)]
+    ranges = [(lo, hi) for lo in range(256) for hi in range(lo, 256)] + [(5, 4), (256, 0), (0, -1), (256, 255)]
+    for lo, hi in ranges:
+        empty = lo > hi or lo > 255 or hi < 0
+        l = 0 if empty else lo
+        w = 0 if empty else hi - lo
+        c1 = np.uint32((l * 0x01010101) & 0x7F7F7F7F)
+        km = np.uint32(0 if l & 0x80 else 0xFFFFFFFF)
+        wH = np.uint32((w * 0x01010101) | 0x80808080)
+        wm = np.uint32(0xFFFFFFFF if w & 0x80 else 0)
+        live = np.uint32(0 if empty else 0xFFFFFFFF)
+        for p, x in enumerate(words):
+            b = (x | H) - c1
+            t = wH - (b & ~H)
+            d = _lop3(b, x, np.full_like(x, km), 0x96)
+            le = _lop3(d, np.full_like(x, wm), t, 0x8E)
+            got = (_lop3(np.full_like(x, H), le, np.full_like(x, live), 0x80) >> np.uint32(8 * p + 7)) & 1
+            want = np.zeros(256, np.uint32) if empty else ((v >= lo) & (v <= hi)).astype(np.uint32)
+            assert np.array_equal(got, want), (lo, hi, p)
+    # flags_to_nib: bits 7, 15, 23, 31 -> bits 0..3
+    f = np.arange(16, dtype=np.uint32)
+    flags = sum(((f >> np.uint32(i)) & 1) << np.uint32(8 * i + 7) for i in range(4))
+    nib = ((((flags >> np.uint32(7)) & np.uint32(0x01010101)) * np.uint32(0x00204081)) >> np.uint32(21)) & 15
+    assert np.array_equal(nib, f)
