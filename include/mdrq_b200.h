@@ -155,6 +155,16 @@ int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper,
                    uint32_t nq, uint32_t path, uint64_t* offsets,
                    uint32_t* ids, uint64_t ids_cap, uint64_t* total);
 int mdrq_fetch_ids(mdrq_store* s, uint32_t* ids, uint64_t ids_cap);
+/* The same with the ids widened to int64 on the host, the dtype of the
+ * reference's ResultSet (core.py:185, ResultSet.from_ids): the Python
+ * search() builds its ResultSet straight from this buffer.  A call with
+ * ids_cap == 0 returns MDRQ_ETRUNC with *total (the result stays cached,
+ * small results in a pinned host buffer), so the caller can allocate exactly
+ * *total ids and collect them with mdrq_fetch_ids64.                        */
+int mdrq_query_ids64(mdrq_store* s, const float* lower, const float* upper,
+                     uint32_t nq, uint32_t path, uint64_t* offsets,
+                     int64_t* ids, uint64_t ids_cap, uint64_t* total);
+int mdrq_fetch_ids64(mdrq_store* s, int64_t* ids, uint64_t ids_cap);
 /* A stream of nbatches ids batches (replaces the reference's loop of
  * search_batch / search calls over successive query batches, bench.py:178-186,
  * methods.py search_batch): batch k holds nqs[k] queries, its bounds follow

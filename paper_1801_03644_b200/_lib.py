@@ -54,7 +54,7 @@ EXPORTED = (
     "mdrq_mask_popcount", "mdrq_mask_to_ids",
     "mdrq_store_create", "mdrq_store_destroy", "mdrq_store_get_info",
     "mdrq_store_va_boundaries", "mdrq_store_bounds",
-    "mdrq_query_count", "mdrq_query_ids", "mdrq_fetch_ids", "mdrq_query_ids_stream", "mdrq_query_stats",
+    "mdrq_query_count", "mdrq_query_ids", "mdrq_fetch_ids", "mdrq_query_ids64", "mdrq_fetch_ids64", "mdrq_query_ids_stream", "mdrq_query_stats",
     "mdrq_batch_prepare", "mdrq_batch_destroy", "mdrq_batch_count_async",
     "mdrq_batch_ids_async", "mdrq_batch_reserve", "mdrq_result_device",
     "mdrq_batch_launches", "mdrq_batch_profile", "mdrq_batch_info",
@@ -114,6 +114,8 @@ _SIGS = {
     "mdrq_query_count": (_int, [_vp, _f32p, _f32p, _u32, _u32, _u64p]),
     "mdrq_query_ids": (_int, [_vp, _f32p, _f32p, _u32, _u32, _u64p, _u32p, _u64, _u64p]),
     "mdrq_fetch_ids": (_int, [_vp, _u32p, _u64]),
+    "mdrq_query_ids64": (_int, [_vp, _f32p, _f32p, _u32, _u32, _u64p, _i64p, _u64, _u64p]),
+    "mdrq_fetch_ids64": (_int, [_vp, _i64p, _u64]),
     "mdrq_query_ids_stream": (_int, [_vp, _f32p, _f32p, _u32p, _u32, _u32, ctypes.POINTER(_u64p),
                                      ctypes.POINTER(_u32p), _u64p, _u64p, _u64p]),
     "mdrq_query_stats": (_int, [_vp, _int, ctypes.POINTER(SearchStatsC), _u32]),

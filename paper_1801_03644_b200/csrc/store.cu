@@ -251,7 +251,15 @@ struct mdrq_store {
     // pipelined ids stream: a copy stream + slots, created on first use
     cudaStream_t copy_stream = nullptr;
     StreamSlot* slots = nullptr;
+    // pinned bounce buffer of the synchronous ids calls: the offsets, the VA
+    // overflow flag and a speculative prefix of the ids come back in one
+    // copy + one synchronisation; bounce_ids = ids of the last call held in
+    // it (0 = none; mdrq_fetch_ids copies from here when they cover the result)
+    uint8_t* h_bounce = nullptr;
+    size_t h_bounce_cap = 0;
+    uint64_t bounce_ids = 0;
     ~mdrq_store() {
+        if (h_bounce) cudaFreeHost(h_bounce);
         if (slots) {
             for (int i = 0; i < kStreamSlots; ++i) {
                 if (slots[i].comp) cudaEventDestroy(slots[i].comp);
@@ -919,6 +927,7 @@ void grow_vb_staging(mdrq_store* s, uint64_t total) {
 }
 
 uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
+    s->bounce_ids = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         enqueue(s, b, true, s->stream);
         unsigned long long total = 0;
@@ -941,6 +950,137 @@ uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
         pool.reserve(size_t(total + total / 8 + 4096));
     }
     raise(MDRQ_ECUDA, "result pool did not converge");
+}
+
+void check_store(const mdrq_store* s);
+
+constexpr size_t kBounceMaxBytes = size_t(64) << 20;
+
+uint8_t* bounce(mdrq_store* s, size_t bytes) {
+    if (bytes > s->h_bounce_cap) {
+        if (s->h_bounce) {
+            cudaFreeHost(s->h_bounce);
+            s->h_bounce = nullptr;
+            s->h_bounce_cap = 0;
+        }
+        const size_t cap = (std::max<size_t>(bytes, size_t(1) << 20) + (size_t(1) << 20) - 1) & ~((size_t(1) << 20) - 1);
+        CK(cudaMallocHost(reinterpret_cast<void**>(&s->h_bounce), cap));
+        s->h_bounce_cap = cap;
+    }
+    return s->h_bounce;
+}
+
+// total ids from src (host) to the caller's buffer: as uint32, or widened to
+// int64 (src may be the upper half of that int64 buffer: front-to-back
+// widening never overwrites a source word before it is read)
+void deliver_ids(const uint32_t* src, void* ids, uint64_t total, bool wide) {
+    if (wide) {
+        int64_t* o = static_cast<int64_t*>(ids);
+        for (uint64_t i = 0; i < total; ++i) o[i] = int64_t(src[i]);
+    } else if (src != ids) {
+        std::memcpy(ids, src, sizeof(uint32_t) * total);
+    }
+}
+
+// the cached result of the last ids call into the caller's buffer
+void fetch_ids_impl(mdrq_store* s, void* ids, uint64_t ids_cap, bool wide) {
+    if (s->last_total > ids_cap) raise(MDRQ_ETRUNC, "ids buffer too small");
+    const uint64_t total = s->last_total;
+    if (!total) return;
+    if (!ids) raise(MDRQ_EINVAL, "null ids");
+    if (s->bounce_ids >= total) {
+        const size_t head = (size_t(s->last_nq) + 1) * 8 + 8;
+        deliver_ids(reinterpret_cast<const uint32_t*>(s->h_bounce + head), ids, total, wide);
+        return;
+    }
+    uint32_t* dst = wide ? static_cast<uint32_t*>(ids) + total : static_cast<uint32_t*>(ids);
+    CK(cudaMemcpyAsync(dst, s->ids.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    deliver_ids(dst, ids, total, wide);
+}
+
+// Synchronous ids call (mdrq_query_ids / mdrq_query_ids64): one pass, then
+// offsets + overflow flag + a speculative prefix of the ids (the previous
+// call's total + 25 %, >= 64 K ids) in one pinned copy and one
+// synchronisation; the remainder, if any, in a second copy.
+int query_ids_impl(mdrq_store* s, const float* lower, const float* upper, uint32_t nq, uint32_t path,
+                   uint64_t* offsets, void* ids, bool wide, uint64_t ids_cap, uint64_t* total_out) {
+    int trunc = 0;
+    int rc = guard([&] {
+        check_store(s);
+        if (!offsets || !total_out) raise(MDRQ_EINVAL, "null argument");
+        if (nq && (!lower || !upper)) raise(MDRQ_EINVAL, "null bounds");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        mdrq_batch* b = &s->scratch;
+        b->owner = s;
+        static const bool tdbg = getenv("MDRQ_DEBUG_TIMING") != nullptr;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        const auto t0 = now();
+        build_descs(s, lower, upper, nq, resolve_path(s, path, nq, true), true, b);
+        const auto t1 = now();
+        // no synchronisation here: this call synchronises before it returns,
+        // so the host descriptors stay untouched until their copies are done
+        upload_batch(s, b, false);
+        const auto t2 = now();
+        s->bounce_ids = 0;
+        const bool have = nq && s->n;
+        const size_t head = (size_t(nq) + 1) * 8 + 8;
+        if (head > kBounceMaxBytes) raise(MDRQ_EINVAL, "too many queries in one call");
+        uint64_t total = 0, spec = 0;
+        uint8_t* hb = nullptr;
+        for (int attempt = 0;; ++attempt) {
+            if (attempt == 2) raise(MDRQ_ECUDA, "result pool did not converge");
+            enqueue(s, b, true, s->stream);
+            DBuf<uint32_t>& pool = pool_of(s, b);
+            const uint64_t pcap = pool.p ? pool.cap : 0;
+            spec = have ? std::min<uint64_t>(std::min<uint64_t>(pcap, (kBounceMaxBytes - head) / 4),
+                                             std::max<uint64_t>(uint64_t(1) << 16, s->last_total + s->last_total / 4))
+                        : 0;
+            hb = bounce(s, head + spec * 4);
+            uint64_t* h_off = reinterpret_cast<uint64_t*>(hb);
+            uint32_t* h_flag = reinterpret_cast<uint32_t*>(hb + (size_t(nq) + 1) * 8);
+            *h_flag = 0;
+            const bool vb = b->path == MDRQ_PATH_VAFILE_BATCH && s->vb_flags.p;
+            if (have)
+                CK(cudaMemcpyAsync(h_off, b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
+                                   s->stream));
+            if (vb) CK(cudaMemcpyAsync(h_flag, s->vb_flags.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
+            if (spec) CK(cudaMemcpyAsync(hb + head, pool.p, sizeof(uint32_t) * spec, cudaMemcpyDeviceToHost, s->stream));
+            CK(cudaStreamSynchronize(s->stream));
+            total = have ? h_off[nq] : 0;
+            if (vb && *h_flag) grow_vb_staging(s, total);   // the recount pass kept this result correct
+            if (total <= pcap) break;
+            pool.reserve(size_t(total + total / 8 + 4096));
+        }
+        const auto t3 = now();
+        s->last_total = total;
+        s->last_nq = nq;
+        s->last_path = b->path;
+        s->last_batch = b;
+        s->bounce_ids = spec >= total ? spec : 0;
+        *total_out = total;
+        if (have)
+            std::memcpy(offsets, hb, sizeof(uint64_t) * (size_t(nq) + 1));
+        else
+            std::memset(offsets, 0, sizeof(uint64_t) * (size_t(nq) + 1));
+        if (total > ids_cap) {
+            trunc = 1;
+        } else {
+            fetch_ids_impl(s, ids, ids_cap, wide);
+        }
+        if (tdbg) {
+            const auto t4 = now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            fprintf(stderr, "query_ids: prepare %.3f upload %.3f run %.3f copy %.3f ms\n", ms(t0, t1), ms(t1, t2),
+                    ms(t2, t3), ms(t3, t4));
+        }
+    });
+    if (rc == MDRQ_OK && trunc) {
+        g_err = "ids buffer too small";
+        return MDRQ_ETRUNC;
+    }
+    return rc;
 }
 
 void check_store(const mdrq_store* s) {
@@ -1177,7 +1317,7 @@ int mdrq_query_count(mdrq_store* s, const float* lower, const float* upper, uint
         mdrq_batch* b = &s->scratch;
         b->owner = s;
         build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false), true, b);
-        upload_batch(s, b);
+        upload_batch(s, b, false);   // synchronised below, before the descriptors change
         enqueue(s, b, false, s->stream);
         if (nq) CK(cudaMemcpyAsync(counts, b->d_counts.p, sizeof(uint64_t) * nq, cudaMemcpyDeviceToHost, s->stream));
         CK(cudaStreamSynchronize(s->stream));
@@ -1189,50 +1329,12 @@ int mdrq_query_count(mdrq_store* s, const float* lower, const float* upper, uint
 
 int mdrq_query_ids(mdrq_store* s, const float* lower, const float* upper, uint32_t nq, uint32_t path,
                    uint64_t* offsets, uint32_t* ids, uint64_t ids_cap, uint64_t* total) {
-    int trunc = 0;
-    int rc = guard([&] {
-        check_store(s);
-        if (!offsets || !total) raise(MDRQ_EINVAL, "null argument");
-        if (nq && (!lower || !upper)) raise(MDRQ_EINVAL, "null bounds");
-        std::lock_guard<std::mutex> lk(s->mu);
-        DeviceGuard dg(s->device);
-        mdrq_batch* b = &s->scratch;
-        b->owner = s;
-        static const bool tdbg = getenv("MDRQ_DEBUG_TIMING") != nullptr;
-        auto now = [] { return std::chrono::steady_clock::now(); };
-        const auto t0 = now();
-        build_descs(s, lower, upper, nq, resolve_path(s, path, nq, true), true, b);
-        const auto t1 = now();
-        upload_batch(s, b);
-        const auto t2 = now();
-        const uint64_t tot = run_ids_sync(s, b);
-        const auto t3 = now();
-        *total = tot;
-        if (nq && s->n) {
-            CK(cudaMemcpyAsync(offsets, b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
-                               s->stream));
-        } else {
-            std::memset(offsets, 0, sizeof(uint64_t) * (size_t(nq) + 1));
-        }
-        if (tot > ids_cap) {
-            trunc = 1;
-        } else if (tot) {
-            if (!ids) raise(MDRQ_EINVAL, "null ids");
-            CK(cudaMemcpyAsync(ids, s->ids.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost, s->stream));
-        }
-        CK(cudaStreamSynchronize(s->stream));
-        if (tdbg) {
-            const auto t4 = now();
-            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-            fprintf(stderr, "query_ids: prepare %.3f upload %.3f run %.3f copy %.3f ms\n", ms(t0, t1), ms(t1, t2),
-                    ms(t2, t3), ms(t3, t4));
-        }
-    });
-    if (rc == MDRQ_OK && trunc) {
-        g_err = "ids buffer too small";
-        return MDRQ_ETRUNC;
-    }
-    return rc;
+    return query_ids_impl(s, lower, upper, nq, path, offsets, ids, false, ids_cap, total);
+}
+
+int mdrq_query_ids64(mdrq_store* s, const float* lower, const float* upper, uint32_t nq, uint32_t path,
+                     uint64_t* offsets, int64_t* ids, uint64_t ids_cap, uint64_t* total) {
+    return query_ids_impl(s, lower, upper, nq, path, offsets, ids, true, ids_cap, total);
 }
 
 int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper, const uint32_t* nqs,
@@ -1243,6 +1345,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
         check_store(s);
         if (nbatches && (!nqs || !offsets_out || !ids_out || !ids_caps || !totals)) raise(MDRQ_EINVAL, "null argument");
         std::lock_guard<std::mutex> lk(s->mu);
+        s->bounce_ids = 0;
         DeviceGuard dg(s->device);
         std::vector<uint64_t> q0(size_t(nbatches) + 1, 0);
         for (uint32_t k = 0; k < nbatches; ++k) {
@@ -1337,12 +1440,16 @@ int mdrq_fetch_ids(mdrq_store* s, uint32_t* ids, uint64_t ids_cap) {
         check_store(s);
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard dg(s->device);
-        if (s->last_total > ids_cap) raise(MDRQ_ETRUNC, "ids buffer too small");
-        if (s->last_total) {
-            if (!ids) raise(MDRQ_EINVAL, "null ids");
-            CK(cudaMemcpyAsync(ids, s->ids.p, sizeof(uint32_t) * s->last_total, cudaMemcpyDeviceToHost, s->stream));
-            CK(cudaStreamSynchronize(s->stream));
-        }
+        fetch_ids_impl(s, ids, ids_cap, false);
+    });
+}
+
+int mdrq_fetch_ids64(mdrq_store* s, int64_t* ids, uint64_t ids_cap) {
+    return guard([&] {
+        check_store(s);
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        fetch_ids_impl(s, ids, ids_cap, true);
     });
 }
 
@@ -1453,6 +1560,7 @@ int mdrq_batch_ids_async(mdrq_store* s, mdrq_batch* b, void* stream) {
         check_store(s);
         if (!b || b->owner != s) raise(MDRQ_EINVAL, "batch does not belong to store");
         std::lock_guard<std::mutex> lk(s->mu);
+        s->bounce_ids = 0;
         DeviceGuard dg(s->device);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
         enqueue(s, b, true, st);

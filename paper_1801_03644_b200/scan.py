@@ -137,7 +137,9 @@ class _GpuScan:
     def search(self, query: RangeQuery) -> ResultSet:
         # the ids alone (search_with_stats adds the counters' readback)
         self._check(query)
-        return self._ids([query])[0]
+        lo, hi = stack_queries([query], self.m)
+        # int64 ids straight from the C ABI: the reference ResultSet dtype
+        return ResultSet(self.store.ids64(lo, hi, self._path)[1])
 
     def _ids(self, queries):
         lo, hi = stack_queries(queries, self.m)

@@ -21,7 +21,7 @@ import os
 import numpy as np
 
 from . import _lib
-from ._lib import check, f32p, u32p, u64p
+from ._lib import check, f32p, i64p, u32p, u64p
 
 DEFAULT_VA_BITS = 8
 
@@ -172,6 +172,26 @@ class DeviceStore:
         else:
             check(rc)
         return offsets.astype(np.int64), buf[: int(total.value)]
+
+    def ids64(self, lower, upper, path: str | int = "auto"):
+        """-> (offsets int64[nq+1], ids int64[total]): ``ids`` with the ids
+        widened on the host into an exactly sized array -- the dtype of the
+        reference's ResultSet (core.py:185).  Two C calls: the query (which
+        reports the total and keeps a small result in pinned host memory),
+        then the widening copy into the fresh array."""
+        lib = _lib.load()
+        lo, hi = _bounds(lower, upper, self.m)
+        nq = lo.shape[0]
+        offsets = np.zeros(nq + 1, np.uint64)
+        total = ctypes.c_uint64(0)
+        rc = lib.mdrq_query_ids64(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p), nq,
+                                  _path(path), offsets.ctypes.data_as(u64p), None, 0, ctypes.byref(total))
+        ids = np.empty(int(total.value), np.int64)
+        if rc == _lib.MDRQ_ETRUNC:
+            check(lib.mdrq_fetch_ids64(self.handle, ids.ctypes.data_as(i64p), ids.size))
+        else:
+            check(rc)
+        return offsets.view(np.int64), ids
 
     def ids_stream(self, batches, path: str | int = "auto", outs=None, info: dict | None = None):
         """Pipelined ids for a sequence of query batches ``[(lower, upper),

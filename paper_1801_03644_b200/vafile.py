@@ -104,7 +104,7 @@ class VaFile:
 
     def _map(self, local: np.ndarray) -> np.ndarray:
         if self._ids is None:
-            return local.astype(np.int64)
+            return local if local.dtype == np.int64 else local.astype(np.int64)
         return np.sort(self._ids[local.astype(np.int64)])
 
     def search(self, query: RangeQuery) -> ResultSet:
@@ -112,14 +112,14 @@ class VaFile:
         if query.m != self.m:
             raise ValueError(f"query has {query.m} dimensions, grid has {self.m}")
         lo, hi = stack_queries([query], self.m)
-        offs, ids = self.store.ids(lo, hi, "vafile")
+        offs, ids = self.store.ids64(lo, hi, "vafile")
         return ResultSet(self._map(ids))
 
     def search_with_stats(self, query: RangeQuery) -> tuple[ResultSet, SearchStats]:
         if query.m != self.m:
             raise ValueError(f"query has {query.m} dimensions, grid has {self.m}")
         lo, hi = stack_queries([query], self.m)
-        offs, ids = self.store.ids(lo, hi, "vafile")
+        offs, ids = self.store.ids64(lo, hi, "vafile")
         st = self.store.stats(1)[0]
         stats = SearchStats(objects_compared=int(st.objects_compared), nodes_visited=int(st.nodes_visited),
                             columns_scanned=int(st.columns_scanned))

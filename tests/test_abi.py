@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "mdrq_b200.h")
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(mdrq_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(mdrq_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_expected_entry_points():
@@ -76,6 +76,8 @@ def test_null_store_and_arguments_are_einval():
     assert lib.mdrq_query_count(None, None, None, 0, 0, None) == _lib.MDRQ_EINVAL
     assert lib.mdrq_query_ids_stream(None, None, None, None, 1, 0, None, None, None, None, None) == _lib.MDRQ_EINVAL
     assert lib.mdrq_fetch_ids(None, None, 0) == _lib.MDRQ_EINVAL
+    assert lib.mdrq_query_ids64(None, None, None, 0, 0, None, None, 0, ctypes.byref(total)) == _lib.MDRQ_EINVAL
+    assert lib.mdrq_fetch_ids64(None, None, 0) == _lib.MDRQ_EINVAL
     assert lib.mdrq_last_error()
 
 

@@ -421,3 +421,51 @@ def test_vafile_batch_lanes_per_tuple_vs_oracle(gpu, nq):
         lo[free] = -np.inf
         hi[free] = np.inf
         check_store(gpu, v, lo, hi, paths=("vafile_batch",))
+
+
+def test_ids64_and_bounce_buffer_paths(gpu):
+    """mdrq_query_ids64 / DeviceStore.ids64 (the int64 ResultSet path of
+    search()) and the pinned bounce buffer of the synchronous ids calls: a
+    sequence of queries whose totals grow and shrink (speculative prefix hit,
+    miss -> second copy, empty result) on every path equals ids() and the
+    oracle; a result larger than the 64 MB bounce cap goes straight to the
+    caller's buffer (int64: widened in place)."""
+    rng = np.random.default_rng(5)
+    n, m = 400_000, 4
+    values = rng.random((n, m), dtype=np.float32)
+    widths = (0.05, 0.9, 0.3, 1e-4, 1.0, 0.6, 0.0)
+    with gpu.DeviceStore(values, layouts=ALL_LAYOUTS) as st_:
+        for p in PATHS:
+            for w in widths:
+                lo = rng.uniform(0, 1 - w, (1, m)).astype(np.float32) if w < 1 else np.zeros((1, m), np.float32)
+                hi = (lo + w).astype(np.float32)
+                if w == 0.0:
+                    lo[:] = 2.0
+                    hi[:] = 3.0
+                ec = oracle.count_batch(values, lo, hi)
+                eo, ei = oracle.ids_batch(values, lo, hi, counts=ec)
+                offs64, ids64 = st_.ids64(lo, hi, p)
+                assert ids64.dtype == np.int64 and ids64.flags.owndata
+                assert np.array_equal(offs64, eo) and np.array_equal(ids64, ei), (p, w)
+                offs, ids = st_.ids(lo, hi, p)
+                assert np.array_equal(offs, eo) and np.array_equal(ids.astype(np.int64), ei), (p, w)
+            # a multi-query batch through ids64
+            lo = rng.uniform(0, 0.5, (7, m)).astype(np.float32)
+            hi = (lo + 0.5).astype(np.float32)
+            ec = oracle.count_batch(values, lo, hi)
+            eo, ei = oracle.ids_batch(values, lo, hi, counts=ec)
+            offs64, ids64 = st_.ids64(lo, hi, p)
+            assert np.array_equal(offs64, eo) and np.array_equal(ids64, ei), p
+        with pytest.raises(ValueError, match="ids buffer"):
+            st_.ids(np.zeros((1, m), np.float32), np.ones((1, m), np.float32), "columnar",
+                    out=np.empty(10, np.uint32))
+    big = 20_000_000   # 80 MB of ids > the 64 MB bounce buffer
+    col = np.zeros((big, 1), np.float32)
+    col[::3] = 1.0
+    with gpu.DeviceStore(col, layouts=1) as st_:
+        for lo_, hi_ in ((-1.0, 2.0), (0.5, 2.0), (-1.0, 2.0)):
+            offs64, ids64 = st_.ids64(np.array([[lo_]], np.float32), np.array([[hi_]], np.float32), "columnar")
+            want = np.arange(big, dtype=np.int64) if lo_ < 0 else np.arange(0, big, 3, dtype=np.int64)
+            assert offs64.tolist() == [0, want.size] and np.array_equal(ids64, want)
+        offs, ids = st_.ids(np.array([[-1.0]], np.float32), np.array([[2.0]], np.float32), "columnar")
+        assert ids.size == big and ids[0] == 0 and ids[-1] == big - 1 and (np.diff(ids.astype(np.int64)) == 1).all()
