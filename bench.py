@@ -361,6 +361,22 @@ def main():
                 entry[f"{mode}_us_per_query"] = round(sum(v[0] for v in pr.values()) * 1e3 / q, 2)
             paths[p] = entry
             pb.close()
+        # wall time of one reference-API call per query (what search() /
+        # count() do: host bounds in, int64 ResultSet / count out, one
+        # synchronous C call each), single-query paths
+        from paper_1801_03644_b200.core import ResultSet
+        for p in ("vafile", "columnar"):
+            q = min(nq, 50)
+            for i in range(3):
+                ResultSet(store.ids64(lo[i:i + 1], hi[i:i + 1], p)[1])
+            t0 = time.perf_counter()
+            for i in range(q):
+                ResultSet(store.ids64(lo[i:i + 1], hi[i:i + 1], p)[1])
+            paths[p]["search_wall_us"] = round((time.perf_counter() - t0) * 1e6 / q, 1)
+            t0 = time.perf_counter()
+            for i in range(q):
+                int(store.count(lo[i:i + 1], hi[i:i + 1], p)[0])
+            paths[p]["count_wall_us"] = round((time.perf_counter() - t0) * 1e6 / q, 1)
 
     # ---- e2e through the public API: host queries in, host ids out (pinned).
     # DeviceStore.ids_stream over K steps (one batch of the same queries per
