@@ -258,6 +258,7 @@ struct mdrq_store {
     uint8_t* h_bounce = nullptr;
     size_t h_bounce_cap = 0;
     uint64_t bounce_ids = 0;
+    size_t bounce_head = 0;          // byte offset of those ids in the buffer
     ~mdrq_store() {
         if (h_bounce) cudaFreeHost(h_bounce);
         if (slots) {
@@ -989,8 +990,7 @@ void fetch_ids_impl(mdrq_store* s, void* ids, uint64_t ids_cap, bool wide) {
     if (!total) return;
     if (!ids) raise(MDRQ_EINVAL, "null ids");
     if (s->bounce_ids >= total) {
-        const size_t head = (size_t(s->last_nq) + 1) * 8 + 8;
-        deliver_ids(reinterpret_cast<const uint32_t*>(s->h_bounce + head), ids, total, wide);
+        deliver_ids(reinterpret_cast<const uint32_t*>(s->h_bounce + s->bounce_head), ids, total, wide);
         return;
     }
     uint32_t* dst = wide ? static_cast<uint32_t*>(ids) + total : static_cast<uint32_t*>(ids);
@@ -1059,6 +1059,7 @@ int query_ids_impl(mdrq_store* s, const float* lower, const float* upper, uint32
         s->last_path = b->path;
         s->last_batch = b;
         s->bounce_ids = spec >= total ? spec : 0;
+        s->bounce_head = head;
         *total_out = total;
         if (have)
             std::memcpy(offsets, hb, sizeof(uint64_t) * (size_t(nq) + 1));
@@ -1319,8 +1320,15 @@ int mdrq_query_count(mdrq_store* s, const float* lower, const float* upper, uint
         build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false), true, b);
         upload_batch(s, b, false);   // synchronised below, before the descriptors change
         enqueue(s, b, false, s->stream);
-        if (nq) CK(cudaMemcpyAsync(counts, b->d_counts.p, sizeof(uint64_t) * nq, cudaMemcpyDeviceToHost, s->stream));
+        // counts through the pinned bounce buffer (the cached ids, if any,
+        // stay on the device: mdrq_fetch_ids copies them from the pool)
+        s->bounce_ids = 0;
+        const size_t cb = sizeof(uint64_t) * nq;
+        uint8_t* hb = nq && cb <= kBounceMaxBytes ? bounce(s, cb) : nullptr;
+        if (nq) CK(cudaMemcpyAsync(hb ? static_cast<void*>(hb) : static_cast<void*>(counts), b->d_counts.p, cb,
+                                   cudaMemcpyDeviceToHost, s->stream));
         CK(cudaStreamSynchronize(s->stream));
+        if (hb) std::memcpy(counts, hb, cb);
         s->last_batch = b;
         s->last_nq = nq;
         s->last_path = b->path;

@@ -469,3 +469,35 @@ def test_ids64_and_bounce_buffer_paths(gpu):
             assert offs64.tolist() == [0, want.size] and np.array_equal(ids64, want)
         offs, ids = st_.ids(np.array([[-1.0]], np.float32), np.array([[2.0]], np.float32), "columnar")
         assert ids.size == big and ids[0] == 0 and ids[-1] == big - 1 and (np.diff(ids.astype(np.int64)) == 1).all()
+
+
+def test_fetch_after_count_and_truncation(gpu):
+    """A truncated ids call (ids_cap 0 -> MDRQ_ETRUNC) keeps its result for
+    mdrq_fetch_ids / mdrq_fetch_ids64 even when a count call with another
+    batch size runs in between (the counts reuse the pinned bounce buffer)."""
+    import ctypes
+    from paper_1801_03644_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(9)
+    n, m = 200_000, 3
+    values = rng.random((n, m), dtype=np.float32)
+    lo = rng.uniform(0, 0.6, (4, m)).astype(np.float32)
+    hi = (lo + 0.4).astype(np.float32)
+    ec = oracle.count_batch(values, lo, hi)
+    eo, ei = oracle.ids_batch(values, lo, hi, counts=ec)
+    with gpu.DeviceStore(values, layouts=ALL_LAYOUTS) as st_:
+        for p in ("vafile", "columnar", "vafile_batch"):
+            offs = np.zeros(5, np.uint64)
+            total = ctypes.c_uint64(0)
+            rc = lib.mdrq_query_ids(st_.handle, lo.ctypes.data_as(_lib.f32p), hi.ctypes.data_as(_lib.f32p), 4,
+                                    _lib.PATHS[p], offs.ctypes.data_as(_lib.u64p), None, 0, ctypes.byref(total))
+            assert rc == _lib.MDRQ_ETRUNC and int(total.value) == ei.size
+            assert np.array_equal(offs.astype(np.int64), eo)
+            c = st_.count(lo[:1], hi[:1], p)          # another batch size in between
+            assert int(c[0]) == int(ec[0])
+            got = np.empty(ei.size, np.uint32)
+            _lib.check(lib.mdrq_fetch_ids(st_.handle, got.ctypes.data_as(_lib.u32p), got.size))
+            assert np.array_equal(got.astype(np.int64), ei), p
+            got64 = np.empty(ei.size, np.int64)
+            _lib.check(lib.mdrq_fetch_ids64(st_.handle, got64.ctypes.data_as(_lib.i64p), got64.size))
+            assert np.array_equal(got64, ei), p
