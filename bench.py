@@ -407,6 +407,22 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s, sync_s = (float(x) for x in t.tolist())
     e2e_val = n * world * nq / e2e_s
+    # the bound of e2e: this box's pinned device->host bandwidth for a copy
+    # of the same size (one stream; 2 or 4 streams measured no faster,
+    # tools/probe_d2h.py)
+    d2h_bytes = int(total_local * 4 + (nq + 1) * 8)
+    d_src = torch.empty(d2h_bytes, dtype=torch.uint8, device="cuda")
+    h_dst = torch.empty(d2h_bytes, dtype=torch.uint8, pin_memory=True)
+    d2h_ms = []
+    for _ in range(3):
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        h_dst.copy_(d_src, non_blocking=True)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        d2h_ms.append(c0.elapsed_time(c1))
+    d2h_peak = d2h_bytes / (min(d2h_ms) / 1e3) / 1e9
+    del d_src, h_dst
 
     cpu = None
     ref_methods = None
@@ -445,6 +461,10 @@ def main():
                     "api": f"DeviceStore.ids_stream, {e2e_steps} steps pipelined (copy of step k under the "
                            f"scan of step k+1); wall clock",
                     "ms_per_step": e2e_s * 1e3,
+                    "d2h_roofline": {"achieved_gbs": d2h_bytes / e2e_s / 1e9, "peak_gbs": d2h_peak,
+                                     "frac": d2h_bytes / e2e_s / 1e9 / d2h_peak,
+                                     "peak_kind": "measured in this run: one pinned copy of the step's "
+                                                  "result size"},
                     "sync_call": {"value": n * world * nq / sync_s, "ms_per_step": sync_s * 1e3,
                                   "api": "DeviceStore.ids, one synchronous call per step"}},
             "id_exchange": xchg,
