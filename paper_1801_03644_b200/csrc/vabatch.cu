@@ -813,6 +813,41 @@ __device__ __forceinline__ uint32_t match_q10(uint32_t q, bool act) {
     return m;
 }
 
+// 32-bit shared-window accesses for the scatter's placement loop: the
+// addresses are formed once per kernel (kept opaque, so the compiler holds
+// them in registers instead of re-deriving the window base with an
+// S2R SR_CgaCtaId in every iteration, which it did under the register
+// pressure of the prefetched records)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("" : "+r"(a));
+    return a;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" : : "r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" : : "r"(a), "h"(uint16_t(v)) : "memory");
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" : : "r"(a), "r"(v) : "memory");
+}
+
 // Scatter the staged records of mode 3 into place.  One CTA per group (grid-
 // strided) takes the group's records in windows of up to 20 blocks, sorts a
 // window by query in shared memory (stable counting sort: per-warp segment
@@ -823,6 +858,9 @@ __device__ __forceinline__ uint32_t match_q10(uint32_t q, bool act) {
 // instead of read-modify-writing scattered 4-byte stores.
 #ifndef MDRQ_SC_THREADS
 #define MDRQ_SC_THREADS 512
+#endif
+#ifndef MDRQ_SC_PTX
+#define MDRQ_SC_PTX 1
 #endif
 #ifndef MDRQ_SC_WIN_BLOCKS
 #define MDRQ_SC_WIN_BLOCKS 20
@@ -849,6 +887,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
     if (*reinterpret_cast<volatile const uint32_t*>(a.overflow)) return;   // mode 2 recounts instead
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
+#if MDRQ_SC_PTX
+    const uint32_t a_rec = smem_addr(s_rec), a_out = smem_addr(s_out), a_off = smem_addr(s_off);
+    const uint32_t a_wc = smem_addr(s_wc + warp * 1024), a_tag = smem_addr(s_tag + warp * 1024);
+#endif
     // window w = blocks w*20 .. w*20+19 of the group's list: ids, counts and
     // offsets into buffer p (warp 0; the caller synchronises)
     auto load_list = [&](uint32_t first, uint32_t nblk, uint32_t k0, uint32_t p) {
@@ -966,7 +1008,25 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
             // stable placement: rank = earlier warps' segments + earlier
             // groups of this segment + lanes below with the same query
             uint8_t* tag = s_tag + warp * 1024;
-            for (uint32_t j = s0; j < s1; j += 32) {
+            uint32_t j = s0;
+#if MDRQ_SC_PTX
+            // full 32-record groups: no tail predicates, explicit addressing
+            for (; j + 32 <= s1; j += 32) {
+                const uint32_t r = lds_u32(a_rec + 4u * (j + lane));
+                const uint32_t q = r & 1023u;
+                sts_u8(a_tag + q, lane);
+                __syncwarp();
+                const bool dup = lds_u8(a_tag + q) != lane;
+                const uint32_t same = __any_sync(0xFFFFFFFFu, dup) ? match_q10(q, true) : (1u << lane);
+                const uint32_t c = lds_u16(a_wc + 2u * q);
+                const uint32_t pp = lds_u32(a_off + 4u * q) + c + __popc(same & lt);
+                sts_u32(a_out + 4u * pp, r);
+                __syncwarp();
+                if ((same & lt) == 0) sts_u16(a_wc + 2u * q, c + __popc(same));
+                __syncwarp();
+            }
+#endif
+            for (; j < s1; j += 32) {
                 const bool act = j + lane < s1;
                 const uint32_t r = act ? s_rec[j + lane] : 0u;
                 const uint32_t q = act ? (r & 1023u) : 0xFFFFFFFFu;
