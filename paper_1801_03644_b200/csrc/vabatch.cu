@@ -838,6 +838,11 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned long long lds_u64(uint32_t a) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return v;
+}
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" : : "r"(a), "r"(v) : "memory");
 }
@@ -890,6 +895,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
 #if MDRQ_SC_PTX
     const uint32_t a_rec = smem_addr(s_rec), a_out = smem_addr(s_out), a_off = smem_addr(s_off);
     const uint32_t a_wc = smem_addr(s_wc + warp * 1024), a_tag = smem_addr(s_tag + warp * 1024);
+    const uint32_t a_pos = smem_addr(s_pos);
 #endif
     // window w = blocks w*20 .. w*20+19 of the group's list: ids, counts and
     // offsets into buffer p (warp 0; the caller synchronises)
@@ -961,11 +967,20 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 // segment counts: two 16-bit counters per word (a segment
                 // holds <= SC_WIN / SC_WARPS records, no carry between halves)
                 uint32_t* wc32 = reinterpret_cast<uint32_t*>(wc);
+#if MDRQ_SC_PTX
+#pragma unroll 4
+                for (uint32_t j = s0 + lane; j < s1; j += 32) {
+                    const uint32_t q = lds_u32(a_rec + 4u * j) & 1023u;
+                    asm volatile("red.shared.add.u32 [%0], %1;" : : "r"(a_wc + 4u * (q >> 1)),
+                                 "r"(1u << ((q & 1u) * 16)) : "memory");
+                }
+#else
 #pragma unroll 4
                 for (uint32_t j = s0 + lane; j < s1; j += 32) {
                     const uint32_t q = s_rec[j] & 1023u;
                     atomicAdd(wc32 + (q >> 1), 1u << ((q & 1u) * 16));
                 }
+#endif
             }
             __syncthreads();
             if (more) load_records(p ^ 1u);   // the next list is visible now
@@ -1016,8 +1031,22 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 const uint32_t q = r & 1023u;
                 sts_u8(a_tag + q, lane);
                 __syncwarp();
-                const bool dup = lds_u8(a_tag + q) != lane;
-                const uint32_t same = __any_sync(0xFFFFFFFFu, dup) ? match_q10(q, true) : (1u << lane);
+                // a lane whose tag was overwritten shares its query with the
+                // lane that wrote it: only those lanes (usually one pair)
+                // need the group mask, one ballot per duplicated query
+                const uint32_t w = lds_u8(a_tag + q);
+                const bool dup = w != lane;
+                uint32_t same = 1u << lane;
+                const uint32_t losers = __ballot_sync(0xFFFFFFFFu, dup);
+                if (losers) {
+                    uint32_t rem = losers | __reduce_or_sync(0xFFFFFFFFu, dup ? 1u << w : 0u);
+                    while (rem) {
+                        const uint32_t qi = __shfl_sync(0xFFFFFFFFu, q, __ffs(rem) - 1);
+                        const uint32_t grp = __ballot_sync(0xFFFFFFFFu, q == qi);
+                        if (q == qi) same = grp;
+                        rem &= ~grp;
+                    }
+                }
                 const uint32_t c = lds_u16(a_wc + 2u * q);
                 const uint32_t pp = lds_u32(a_off + 4u * q) + c + __popc(same & lt);
                 sts_u32(a_out + 4u * pp, r);
@@ -1046,6 +1075,15 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
             }
             __syncthreads();
             // write the runs: consecutive slots of one query are consecutive ids
+#if MDRQ_SC_PTX
+#pragma unroll 4
+            for (uint32_t j = tid; j < n; j += SC_THREADS) {
+                const uint32_t r = lds_u32(a_out + 4u * j);
+                const uint32_t q = r & 1023u;
+                const unsigned long long at = lds_u64(a_pos + 8u * q) + (j - lds_u32(a_off + 4u * q));
+                if (at < a.ids_cap) __stcs(a.ids + at, a.id_base + uint32_t(start + (r >> 10)));
+            }
+#else
 #pragma unroll 4
             for (uint32_t j = tid; j < n; j += SC_THREADS) {
                 const uint32_t r = s_out[j];
@@ -1053,6 +1091,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 const unsigned long long at = s_pos[q] + (j - s_off[q]);
                 if (at < a.ids_cap) __stcs(a.ids + at, a.id_base + uint32_t(start + (r >> 10)));
             }
+#endif
             __syncthreads();
             for (uint32_t q = tid; q < 1024; q += SC_THREADS) s_pos[q] += s_off[q + 1] - s_off[q];
             for (uint32_t i = tid; i < SC_WARPS * 1024 / 2; i += SC_THREADS) reinterpret_cast<uint32_t*>(s_wc)[i] = 0;
