@@ -1025,34 +1025,42 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
             uint8_t* tag = s_tag + warp * 1024;
             uint32_t j = s0;
 #if MDRQ_SC_PTX
-            // full 32-record groups: no tail predicates, explicit addressing
-            for (; j + 32 <= s1; j += 32) {
-                const uint32_t r = lds_u32(a_rec + 4u * (j + lane));
-                const uint32_t q = r & 1023u;
-                sts_u8(a_tag + q, lane);
-                __syncwarp();
-                // a lane whose tag was overwritten shares its query with the
-                // lane that wrote it: only those lanes (usually one pair)
-                // need the group mask, one ballot per duplicated query
-                const uint32_t w = lds_u8(a_tag + q);
-                const bool dup = w != lane;
-                uint32_t same = 1u << lane;
-                const uint32_t losers = __ballot_sync(0xFFFFFFFFu, dup);
-                if (losers) {
-                    uint32_t rem = losers | __reduce_or_sync(0xFFFFFFFFu, dup ? 1u << w : 0u);
-                    while (rem) {
-                        const uint32_t qi = __shfl_sync(0xFFFFFFFFu, q, __ffs(rem) - 1);
-                        const uint32_t grp = __ballot_sync(0xFFFFFFFFu, q == qi);
-                        if (q == qi) same = grp;
-                        rem &= ~grp;
+            // full 32-record groups: no tail predicates, explicit addressing;
+            // the next group's record and this group's window offset are
+            // loaded ahead of the dependent tag / count round trips
+            if (j + 32 <= s1) {
+                uint32_t r = lds_u32(a_rec + 4u * (j + lane));
+                for (; j + 32 <= s1; j += 32) {
+                    const uint32_t q = r & 1023u;
+                    sts_u8(a_tag + q, lane);
+                    const uint32_t off = lds_u32(a_off + 4u * q);
+                    __syncwarp();
+                    // a lane whose tag was overwritten shares its query with
+                    // the lane that wrote it: only those lanes (usually one
+                    // pair) need the group mask, one ballot per duplicated query
+                    const uint32_t w = lds_u8(a_tag + q);
+                    const uint32_t c = lds_u16(a_wc + 2u * q);
+                    const uint32_t rn = j + 64 <= s1 ? lds_u32(a_rec + 4u * (j + 32 + lane)) : 0u;
+                    const bool dup = w != lane;
+                    uint32_t same = 1u << lane;
+                    const uint32_t losers = __ballot_sync(0xFFFFFFFFu, dup);
+                    if (losers) {
+                        uint32_t rem = losers | __reduce_or_sync(0xFFFFFFFFu, dup ? 1u << w : 0u);
+                        while (rem) {
+                            const uint32_t qi = __shfl_sync(0xFFFFFFFFu, q, __ffs(rem) - 1);
+                            const uint32_t grp = __ballot_sync(0xFFFFFFFFu, q == qi);
+                            if (q == qi) same = grp;
+                            rem &= ~grp;
+                        }
                     }
+                    sts_u32(a_out + 4u * (off + c + __popc(same & lt)), r);
+                    __syncwarp();   // every lane has read wc[q] before its leader bumps it
+                    if ((same & lt) == 0) sts_u16(a_wc + 2u * q, c + __popc(same));
+                    // (the next group's first __syncwarp orders this update
+                    // before its count reads and these tag reads before its
+                    // tag writes)
+                    r = rn;
                 }
-                const uint32_t c = lds_u16(a_wc + 2u * q);
-                const uint32_t pp = lds_u32(a_off + 4u * q) + c + __popc(same & lt);
-                sts_u32(a_out + 4u * pp, r);
-                __syncwarp();
-                if ((same & lt) == 0) sts_u16(a_wc + 2u * q, c + __popc(same));
-                __syncwarp();
             }
 #endif
             for (; j < s1; j += 32) {
