@@ -122,6 +122,10 @@ def main():
         "",
         "The scatter moves the records in and the ids out (the algorithmic volume): one CTA per group sorts",
         "20-block windows in shared memory while the next window's block list and records are in flight.",
+        "It is latency-bound (short-scoreboard and barrier stalls), not DRAM-bound: this round its",
+        "placement loop lost the per-iteration `S2R SR_CgaCtaId` (shared addresses formed once) and the",
+        "10-ballot duplicate match (one ballot per duplicated query): 215 M -> 169 M warp instructions,",
+        "0.38 -> 0.33 ms.",
         "",
         "### Single-query columnar scan (`tools/probe_path.py columnar ids 20`, 11th launch)",
         "",
@@ -136,8 +140,10 @@ def main():
         "",
         ncu_summary.full(os.path.join(src, "prof_va.ncu-rep")),
         "",
-        "Reading: ALU-bound SWAR range tests; 0.38 GB of code planes in ~103 us (one range test per code",
-        "for selective queries; every tuple alive after the last dimension refined exactly).",
+        "Reading: 0.40 GB of code planes in ~96 us = ~4.2 TB/s; latency / issue-limited (one 7-op SWAR",
+        "range test per 4 codes, a vote per pair of planes, every tuple alive after the last dimension",
+        "refined exactly).  Before this round's SWAR rewrite, two planes per step and the 32-register",
+        "bound: ~102 us and 70 M warp instructions (now 62 M).",
         "",
         "### Row-wise scan (`tools/probe_path.py rowwise count 3`, 2nd launch)",
         "",
