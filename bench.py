@@ -84,7 +84,35 @@ class ClockSampler:
         self._t = None
         self.exe = shutil.which("nvidia-smi")
 
+    def _run_nvml(self) -> bool:
+        """NVML directly (sub-millisecond queries): a sample every ~2 ms, so a
+        timed region of a few tens of ms still gets a median; False when NVML
+        is unavailable (then nvidia-smi, ~10 samples/s)."""
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception:
+            return False
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        try:
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.002)
+        finally:
+            try:
+                nv.nvmlShutdown()
+            except Exception:
+                pass
+        return True
+
     def _run(self):
+        if self._run_nvml() or not self.exe:
+            return
         while not self._stop.is_set():
             try:
                 out = subprocess.run([self.exe, "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -97,9 +125,8 @@ class ClockSampler:
             self._stop.wait(0.1)
 
     def __enter__(self):
-        if self.exe:
-            self._t = threading.Thread(target=self._run, daemon=True)
-            self._t.start()
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
         return self
 
     def __exit__(self, *exc):
