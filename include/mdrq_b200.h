@@ -25,6 +25,7 @@
  *     mdrq_query_count    <- len(method.search(q))  (bench.py:176)
  *     mdrq_query_ids      <- method.search(q).ids   (scan.py:103-111, 187-211,
  *                            vafile.py:201-219)
+ *     mdrq_query_ids64    <- the same as int64, ResultSet's dtype (core.py:185)
  *     mdrq_query_stats    <- SearchStats counters of search_with_stats
  *                            (core.py:218-237)
  *     mdrq_store_va_boundaries <- VaGrid (vafile.py:25-64) -- here a quantile
