@@ -1,19 +1,28 @@
 #!/usr/bin/env python
 """Benchmark of the MDRQ scan hot path (BASELINE.json metric: tuples
-scanned/s and achieved HBM GB/s per GPU).
+scanned/s and achieved HBM GB/s per GPU at 1/2/4/8 B200).
 
-Workload (N=1): BASELINE.json configs[1] (C2) -- n = 5e7 tuples, m = 8,
-float32 uniform [0, 1) from default_rng(0) (the reference's gen_uniform),
-1000 full-match queries at selectivity 1e-3 (width 0.001**(1/8), lower
-bound U[0, 1-w) from default_rng(1); workload.c2_queries).  One STEP = the
-whole batch of 1000 queries evaluated over the device-resident table in ids
-mode (sorted uint32 ids per query + counts).  ``value`` = tuples scanned per
-second = n_total * queries / step time (each query scans every tuple), the
-same unit the reference's CPU scan is measured in.
+Workload: BASELINE.json configs[4] (C5), the configuration the metric is
+quoted on -- n = 5e8 tuples, m = 10, float32 uniform [0, 1) from
+default_rng(0) (the reference's gen_uniform, generated chunk-parallel,
+bit-identical), one batch of 10 000 full-match queries at selectivity 1e-3
+(width 0.001**(1/10), lower bounds U[0, 1-w) from default_rng(1);
+workload.c5_queries) evaluated in multi-query passes.  One STEP = the whole
+10 000-query batch over the device-resident table in ids mode (ascending
+uint32 ids per query + offsets, ~5e9 ids = 20 GB); the count-only mode of the
+same batch is measured beside it (``modes.count``).
 
-With N>1 (torchrun, one rank per GPU) every rank holds its own 5e7-row
-contiguous shard of a larger uniform table (weak scaling), scans it, and the
-per-query ids are merged in rank order with NCCL all_gathers over NVLink.
+``value`` = tuple-query evaluations per second = n x queries / step time
+(every query is decided for every tuple; the unit the reference's CPU scan is
+measured in by ``--impl reference``).  ``tuples_per_s`` (= n x HBM passes /
+t) and ``queries_per_s`` are reported beside it.
+
+With N > 1 (torchrun, one rank per GPU) the SAME 5e8-row table is split into
+N contiguous row shards (strong scaling): rank r generates and
+holds rows shard_range(n, N, r) with global ids, scans them, and the step
+ends with the NCCL all_gather of the per-query counts (every rank learns the
+global result offsets); the full id exchange and the per-rank direct copy
+of each rank's ids into one host buffer are timed separately.
 
 ``--impl reference`` times the reference's own CPU scan (the reference's
 compiled ``scan_rows`` from oracle/_ref driven like HorizontalScan, all host
@@ -38,10 +47,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-N_PER_GPU = 50_000_000
-M = 8
+N_TOTAL = 500_000_000
+M = 10
 SELECTIVITY = 1e-3
-NQ = 1000
+NQ = 10_000
 
 
 def parse():
@@ -52,15 +61,16 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-paths", action="store_true",
-                    help="skip the per-path cost table and the columnar roofline probe")
+                    help="skip the per-path cost table, the columnar roofline probe and the C2 line")
     ap.add_argument("--force-merge", action="store_true",
                     help="run the NCCL combine even with one rank (torchrun --nproc-per-node 1)")
     ap.add_argument("--merge-in-step", action="store_true",
                     help="include the full id exchange (all ids on every rank) in the timed step")
-    ap.add_argument("--n", type=int, default=N_PER_GPU, help="tuples per GPU")
+    ap.add_argument("--n", type=int, default=N_TOTAL, help="tuples in the whole table (split over ranks)")
     ap.add_argument("--queries", type=int, default=NQ)
+    ap.add_argument("--count-steps", type=int, default=None, help="timed steps of the count-mode batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--explore", action="store_true", help="print per-path / per-level timings to stderr")
+    ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
@@ -180,13 +190,35 @@ def cpu_reference_rate(values, lo, hi, budget_s: float, threads: int, max_querie
         scan.close()
 
 
+def load_workload(n: int, nq: int, world: int, rank: int):
+    """This rank's contiguous shard of the C5 table (global row ids
+    [start, stop)) and the query batch."""
+    from paper_1801_03644_b200 import workload
+    from paper_1801_03644_b200.parallel import shard_range
+    start, stop = shard_range(n, world, rank)
+    workers = max(1, (os.cpu_count() or 1) // world)
+    t = time.perf_counter()
+    values = workload.c5_data(start, stop, n=n, workers=workers)
+    gen_s = time.perf_counter() - t
+    lo, hi = workload.c5_queries(count=nq)
+    return values, start, stop, lo, hi, gen_s
+
+
+def workload_name(n, nq, world):
+    return (f"C5 (BASELINE.json configs[4]): n={n} m={M} float32 uniform seed 0, one batch of {nq} full-match "
+            f"queries at selectivity {SELECTIVITY:g} per step, ids mode (ascending uint32 ids per query)"
+            + (f", rows sharded over {world} GPUs" if world > 1 else ""))
+
+
 def run_reference(args):
+    """The reference's own CPU scan (oracle/_ref: its compiled scan_rows,
+    driven like HorizontalScan over all host threads) on the same C5 table
+    and queries; each step a bounded sample of the batch."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1801_03644_b200 import workload
-    values = workload.uniform_rows(0, M, 0, args.n)
-    lo, hi = workload.c2_queries(count=args.queries, levels=(SELECTIVITY,))[SELECTIVITY]
+    values, _, _, lo, hi, gen_s = load_workload(args.n, args.queries, 1, 0)
+    n = values.shape[0]
     threads = os.cpu_count() or 1
     import oracle
     scan = oracle.ReferenceHorizontalScan(values, threads=threads, seed=0)
@@ -194,11 +226,10 @@ def run_reference(args):
         t0 = time.perf_counter()
         scan.search(lo[0], hi[0])
         per_q = time.perf_counter() - t0
-        # each step a bounded sample: <= 2 s, and the whole run <= ~2 minutes
-        step_budget = min(2.0, 120.0 / max(1, args.steps + args.warmup))
+        # each step a bounded sample: <= 6 s, and the whole run <= ~2.5 minutes
+        step_budget = min(6.0, 150.0 / max(1, args.steps + args.warmup))
         q_per_step = max(1, min(args.queries, int(step_budget / max(per_q, 1e-6))))
-        # warmup
-        qi = 0
+        qi = 1
         for _ in range(args.warmup):
             for _ in range(q_per_step):
                 scan.search(lo[qi % args.queries], hi[qi % args.queries])
@@ -214,23 +245,59 @@ def run_reference(args):
     finally:
         scan.close()
     step = float(np.mean(times))
-    value = args.n * q_per_step / step
+    value = n * q_per_step / step
     line = {
-        "impl": "reference", "metric": "tuples_scanned_per_s", "value": value, "unit": "tuples/s",
+        "impl": "reference", "metric": "tuple_queries_per_s", "value": value, "unit": "tuple-queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"C2: n={args.n} m={M} uniform seed 0, full-match queries at selectivity "
-                               f"{SELECTIVITY}, ids mode", "queries_per_step": q_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(n, args.queries, 1), "queries_per_step": q_per_step,
+                   "same_config": "same table and query batch; each step a bounded sample of its queries",
                    "parallelism": f"host threads={threads}"},
-        "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": threads, "kind": kind,
-                         "sample": f"{q_per_step} queries per step over all {args.n} tuples"},
-        "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "queries_per_s": q_per_step / step,
+        "cpu_baseline": {"value": value, "unit": "tuple-queries/s", "cores": threads, "kind": kind,
+                         "sample": f"{q_per_step} of the {args.queries} queries per step over all {n} tuples"},
+        "e2e": {"value": value, "unit": "tuple-queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": {"generate": round(gen_s, 2)},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------ GPU leg --
+
+def timed(fn, steps, stream, world):
+    """Device time per call of fn over `steps` calls (CUDA events on the
+    launching stream, barrier + synchronize on both sides, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
 
 def main():
     args = parse()
@@ -240,11 +307,11 @@ def main():
     import torch.distributed as dist
 
     import paper_1801_03644_b200 as eng
-    from paper_1801_03644_b200 import _lib, workload
+    from paper_1801_03644_b200 import _lib
 
     world, rank, local = dist_env()
     # the NCCL merge runs whenever there is more than one rank; --force-merge
-    # exercises it with a single torchrun rank (the only GPU count here)
+    # exercises it with a single torchrun rank
     merge = world > 1 or args.force_merge
     if merge:
         torch.cuda.set_device(local)
@@ -252,20 +319,16 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    n = args.n
-    start = rank * n
-    t_gen = time.perf_counter()
-    values = workload.uniform_rows(0, M, start, start + n)
-    t_gen = time.perf_counter() - t_gen
-    lo, hi = workload.c2_queries(count=args.queries, levels=(SELECTIVITY,))[SELECTIVITY]
+    n_total = args.n
+    values, start, stop, lo, hi, t_gen = load_workload(n_total, args.queries, world, rank)
+    n = stop - start
     nq = lo.shape[0]
-    layouts = _lib.LAYOUT_COLUMNAR | _lib.LAYOUT_VAFILE | _lib.LAYOUT_ROWWISE
+    layouts = _lib.LAYOUT_COLUMNAR | _lib.LAYOUT_VAFILE
     t_build = time.perf_counter()
     store = eng.DeviceStore(values, layouts=layouts, va_bits=8, device=dev, id_base=start)
     t_build = time.perf_counter() - t_build
-    # a dedicated stream: the library launches on it and the CUDA events
-    # below are recorded on it (torch's legacy default stream would be NULL
-    # and the library would fall back to the store's own stream)
+    # a dedicated stream: the library launches on it and the CUDA events are
+    # recorded on it
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
@@ -274,7 +337,9 @@ def main():
     batch = store.prepare(lo, hi, args.path)
     binfo = batch.info()
     total_local = batch.reserve()
-    launches_per_step = batch.launches(ids=True)
+    launches_ids = batch.launches(ids=True)
+    launches_count = batch.launches(ids=False)
+    d_counts = torch.empty(nq, dtype=torch.int64, device=dev)
 
     def exchange():
         # every rank's ids of every query, rank-ordered (NCCL all_gather of
@@ -284,7 +349,7 @@ def main():
         offs_t = _wrap(d_offs, nq + 1, torch.int64, dev)
         return eng.combine_ids(offs_t, ids_t)
 
-    def step():
+    def step_ids():
         batch.ids_async(sptr)
         if merge:
             if args.merge_in_step:
@@ -293,52 +358,38 @@ def main():
                 # the counts combine: every rank learns the global offsets
                 # (where its rank-ordered slices go); the id exchange itself
                 # is timed separately below
-                d_ids, d_offs, tot = batch.result_device()
+                _, d_offs, _ = batch.result_device()
                 offs_t = _wrap(d_offs, nq + 1, torch.int64, dev)
                 eng.combine_counts(offs_t[1:] - offs_t[:-1])
 
+    def step_count():
+        batch.count_async(d_counts.data_ptr(), sptr)
+        if merge:
+            eng.combine_counts(d_counts)
+
     for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        step_ids()
     with ClockSampler(dev) as clocks:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = n * world * nq / (ms / 1e3)
+        ms = timed(step_ids, args.steps, stream, world)
+    for _ in range(2):
+        step_count()
+    count_steps = args.count_steps or max(3, min(args.steps, 10))
+    with ClockSampler(dev) as clocks_count:
+        ms_count = timed(step_count, count_steps, stream, world)
+    passes = binfo["passes"]
+    value = n_total * nq / (ms / 1e3)
+    total_ids = total_local
+    if merge:
+        tt = torch.tensor([total_local], device="cuda", dtype=torch.int64)
+        dist.all_reduce(tt)
+        total_ids = int(tt.item())
 
     # ---- the id exchange on its own (all ids of every query on every rank)
     xchg = None
     if merge and not args.merge_in_step:
         exchange()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        x0.record(stream)
-        for _ in range(3):
-            offs_all, _ = exchange()
-        x1.record(stream)
-        torch.cuda.synchronize()
-        xms = x0.elapsed_time(x1) / 3
-        if world > 1:
-            t = torch.tensor([xms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            xms = float(t.item())
-        ids_all = int(offs_all[-1].item())
-        xchg = {"ms_per_step": xms, "ids_total": ids_all, "bytes_in_per_rank": 4 * (ids_all - total_local),
+        xms = timed(exchange, 3, stream, world)
+        xchg = {"ms_per_step": xms, "ids_total": total_ids, "bytes_in_per_rank": 4 * (total_ids - total_local),
                 "included_in_value": False,
                 "how": "NCCL all_gather of every rank's padded id slices + mdrq_copy_segments placement; "
                        "the step itself ends with the counts combine (global offsets on every rank)"}
@@ -350,19 +401,24 @@ def main():
     stats = store.stats(nq)
     roofline = roofline_of(binfo["path"], prof, stats, n, nq, total_local, peak, peak_kind)
     if binfo["path"] == "vafile_batch":
-        lw = vb_lw(nq, binfo["max_union_dims"])
+        lw = vb_lw(min(nq, 1024), binfo["max_union_dims"])
         key = (f"va_batch_kernel<3, {binfo['max_union_dims']}, {lw}>" if roofline["class"] == "scan"
                else "vb_scatter_kernel")
         roofline.update(ncu_traffic(key))
-
     rpeak = read_peak(dev)
     add_peaks(roofline, rpeak)
+    prof_count = batch.profile(ids=False, stream=sptr)
+    stats_count = store.stats(nq)
+    roof_count = roofline_of(binfo["path"], prof_count, stats_count, n, nq, 0, peak, peak_kind)
+    add_peaks(roof_count, rpeak)
 
     # ---- the single-query columnar scan kernel (HBM-bound by design), same
-    # data; skipped with --no-paths so a profiled run holds only the step
+    # data, and the per-path cost table; skipped with --no-paths
     col_roof = None
+    paths = {}
+    c2 = None
     if not args.no_paths:
-        col_q = min(nq, 100)
+        col_q = min(nq, 20)
         cb = store.prepare(lo[:col_q], hi[:col_q], "columnar")
         cb.reserve()
         cprof = cb.profile(ids=True, stream=sptr)
@@ -371,31 +427,23 @@ def main():
         col_roof.update(ncu_traffic("col_scan_kernel<1>"))
         add_peaks(col_roof, rpeak)
         cb.close()
-
-    # ---- per-path cost at this workload (device time per query)
-    paths = {}
-    if not args.no_paths:
-        for p in ("vafile_batch", "columnar_batch", "vafile", "columnar", "rowwise"):
-            q = nq if p.endswith("_batch") else min(nq, 50)
+        for p, q in (("vafile_batch", nq), ("columnar_batch", min(nq, 1024)), ("vafile", min(nq, 16)),
+                     ("columnar", min(nq, 16))):
             pb = store.prepare(lo[:q], hi[:q], p)
-            entry = {}
+            entry = {"queries": q}
             for mode in ("count", "ids"):
-                if mode == "ids" and p == "columnar_batch":
-                    continue
                 if mode == "ids":
                     pb.reserve()
                 pr = pb.profile(ids=(mode == "ids"), stream=sptr)
                 entry[f"{mode}_us_per_query"] = round(sum(v[0] for v in pr.values()) * 1e3 / q, 2)
             paths[p] = entry
             pb.close()
-        # wall time of one reference-API call per query (what search() /
-        # count() do: host bounds in, int64 ResultSet / count out, one
-        # synchronous C call each), single-query paths
+        # wall time of one reference-API call per query (search() / count():
+        # host bounds in, int64 ResultSet / count out, one synchronous C call)
         from paper_1801_03644_b200.core import ResultSet
         for p in ("vafile", "columnar"):
-            q = min(nq, 50)
-            for i in range(3):
-                ResultSet(store.ids64(lo[i:i + 1], hi[i:i + 1], p)[1])
+            q = min(nq, 8)
+            ResultSet(store.ids64(lo[:1], hi[:1], p)[1])
             t0 = time.perf_counter()
             for i in range(q):
                 ResultSet(store.ids64(lo[i:i + 1], hi[i:i + 1], p)[1])
@@ -406,40 +454,118 @@ def main():
             paths[p]["count_wall_us"] = round((time.perf_counter() - t0) * 1e6 / q, 1)
 
     # ---- e2e through the public API: host queries in, host ids out (pinned).
-    # DeviceStore.ids_stream over K steps (one batch of the same queries per
-    # step): every step builds + uploads its descriptors and copies its ids
-    # and offsets to pinned host memory; step k's copy overlaps step k+1's
-    # scan.  Three pinned output buffers rotate (a step's ids land in a
-    # buffer whose previous copy has completed).  Also the one-call
-    # synchronous DeviceStore.ids for reference.
+    # DeviceStore.ids_stream over K steps (the same batch each step): every
+    # step builds + uploads its descriptors and copies its ids and offsets to
+    # pinned host memory; step k's copy overlaps step k+1's scan.
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream)
+
+    # ---- C2 beside it (BASELINE.json configs[1], 1000 queries at 1e-3)
+    if not args.no_paths and world == 1:
+        batch.close()
+        c2 = measure_c2(eng, _lib, dev, stream, args.steps, args.warmup)
+
+    cpu = None
+    ref_methods = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, kind, qn, thr, dt = cpu_reference_rate(values, lo, hi, budget_s=15.0,
+                                                     threads=os.cpu_count() or 1)
+        ref_methods = reference_methods()
+        cpu = {"value": rate, "unit": "tuple-queries/s", "cores": thr, "kind": kind,
+               "sample": f"{qn} of the {nq} queries over all {n} tuples ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "tuple_queries_per_s", "value": value, "unit": "tuple-queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(n_total, nq, world),
+                       "path": binfo["path"], "requested_path": args.path, "passes_per_step": passes,
+                       "queries_per_step": nq, "ids_per_step": total_ids,
+                       "l2": "inputs (20 GB columns + 5 GB code planes in total) larger than L2 (126 MB); "
+                             "no flush",
+                       "parallelism": f"contiguous row shards x{world}",
+                       "combine": ("none (one rank)" if not merge else
+                                   "ids exchanged in the step" if args.merge_in_step else
+                                   "counts all_gather in the step; id exchange timed separately (id_exchange)")},
+            "tuples_per_s": n_total * passes / (ms / 1e3),
+            "queries_per_s": nq / (ms / 1e3),
+            "hbm_gbs_per_gpu": roofline["achieved"],
+            "roofline": roofline,
+            "smem_roofline": smem_roofline(binfo, prof, n, nq, clocks.summary()),
+            "modes": {
+                "ids": {"value": value, "ms_per_step": ms, "queries_per_s": nq / (ms / 1e3),
+                        "gpu_launches_per_step": launches_ids},
+                "count": {"value": n_total * nq / (ms_count / 1e3), "ms_per_step": ms_count,
+                          "steps": count_steps, "queries_per_s": nq / (ms_count / 1e3),
+                          "gpu_launches_per_step": launches_count, "roofline": roof_count,
+                          "smem_roofline": smem_roofline(binfo, prof_count, n, nq, clocks_count.summary()),
+                          "clocks": clocks_count.summary()},
+            },
+            "columnar_scan_roofline": col_roof,
+            "pass_profile": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in prof.items()},
+            "pass_profile_count": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in prof_count.items()},
+            "paths_us_per_query": paths,
+            "e2e": e2e,
+            "id_exchange": xchg,
+            "c2": c2,
+            "gpu_launches": launches_ids * args.steps,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+            "reference_methods": ref_methods,
+            "setup_s": {"generate": round(t_gen, 2), "store_build": round(t_build, 2)},
+        }
+        print(json.dumps(line), flush=True)
+    if not (not args.no_paths and world == 1):
+        batch.close()
+    store.close()
+    if merge:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
+    """e2e through the public API (DeviceStore.ids_stream): per step the
+    query bounds go host->device and the step's ids + offsets come back into
+    pinned host memory; step k's copy overlaps step k+1's device pass."""
+    import torch
+    import torch.distributed as dist
+    ids_bytes = int(total_local * 4 + (nq + 1) * 8)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    nbuf = 2 if avail > 3 * (total_local * 4 + (1 << 30)) * world else 1
+    t0 = time.perf_counter()
     pinned = [torch.empty(max(1, total_local + 1024), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-              for _ in range(3)]
-    e2e_steps = max(3, min(args.steps, 20))
-    store.ids_stream([(lo, hi)] * 3, args.path, outs=pinned)   # warm: slots and their result pools
+              for _ in range(nbuf)]
+    pin_s = time.perf_counter() - t0
+    e2e_steps = max(3, min(args.steps, 10))
+    store.ids_stream([(lo, hi)] * 2, args.path, outs=[pinned[k % nbuf] for k in range(2)])   # warm
     info = {}
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    res = store.ids_stream([(lo, hi)] * e2e_steps, args.path, outs=[pinned[k % 3] for k in range(e2e_steps)],
+    res = store.ids_stream([(lo, hi)] * e2e_steps, args.path, outs=[pinned[k % nbuf] for k in range(e2e_steps)],
                            info=info)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     assert all(int(o[-1]) == total_local for o, _ in res), "stream result differs from the timed batch"
+    del res
     store.ids(lo, hi, args.path, out=pinned[0])   # warm
     t0 = time.perf_counter()
-    for _ in range(3):
+    sync_n = 2
+    for _ in range(sync_n):
         store.ids(lo, hi, args.path, out=pinned[0])
-    sync_s = (time.perf_counter() - t0) / 3
-    if world > 1:
-        t = torch.tensor([e2e_s, sync_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s, sync_s = (float(x) for x in t.tolist())
-    e2e_val = n * world * nq / e2e_s
-    # the bound of e2e: this box's pinned device->host bandwidth for a copy
-    # of the same size (one stream; 2 or 4 streams measured no faster,
-    # tools/probe_d2h.py)
-    d2h_bytes = int(total_local * 4 + (nq + 1) * 8)
-    d_src = torch.empty(d2h_bytes, dtype=torch.uint8, device="cuda")
-    h_dst = torch.empty(d2h_bytes, dtype=torch.uint8, pin_memory=True)
+    sync_s = (time.perf_counter() - t0) / sync_n
+    e2e_s = max_over_ranks(e2e_s, world)
+    sync_s = max_over_ranks(sync_s, world)
+    # the bound of e2e: this box's pinned device->host bandwidth for one copy
+    # of (up to 4 GB of) the step's result
+    probe = min(ids_bytes, 4 << 30)
+    d_src = torch.empty(probe, dtype=torch.uint8, device="cuda")
+    h_dst = torch.from_numpy(pinned[0].view(np.uint8)[:probe])
     d2h_ms = []
     for _ in range(3):
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -448,65 +574,45 @@ def main():
         c1.record(stream)
         torch.cuda.synchronize()
         d2h_ms.append(c0.elapsed_time(c1))
-    d2h_peak = d2h_bytes / (min(d2h_ms) / 1e3) / 1e9
-    del d_src, h_dst
+    d2h_peak = probe / (min(d2h_ms) / 1e3) / 1e9
+    del d_src, h_dst, pinned
+    return {"value": n_total * nq / e2e_s, "unit": "tuple-queries/s",
+            "h2d_bytes_per_step": int(info.get("h2d_bytes", 0) // e2e_steps),
+            "d2h_bytes_per_step": ids_bytes * world,
+            "api": f"DeviceStore.ids_stream, {e2e_steps} steps pipelined (copy of step k under the device pass "
+                   f"of step k+1), {nbuf} pinned output buffer(s); wall clock, max over ranks",
+            "ms_per_step": e2e_s * 1e3,
+            "d2h_roofline": {"achieved_gbs": ids_bytes / e2e_s / 1e9, "peak_gbs": d2h_peak,
+                             "frac": ids_bytes / e2e_s / 1e9 / d2h_peak,
+                             "peak_kind": "measured in this run: one pinned copy of min(result, 4 GB) per GPU"},
+            "sync_call": {"value": n_total * nq / sync_s, "ms_per_step": sync_s * 1e3,
+                          "api": "DeviceStore.ids into a pinned buffer, one synchronous call per step"},
+            "pin_s": round(pin_s, 2)}
 
-    cpu = None
-    ref_methods = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, kind, qn, thr, dt = cpu_reference_rate(values, lo, hi, budget_s=15.0,
-                                                     threads=os.cpu_count() or 1)
-        ref_methods = reference_methods()
-        cpu = {"value": rate, "unit": "tuples/s", "cores": thr, "kind": kind,
-               "sample": f"{qn} of the {nq} queries over all {n} tuples ({dt:.1f} s)"}
 
-    if rank == 0:
-        line = {
-            "metric": "tuples_scanned_per_s", "value": value, "unit": "tuples/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"C2: n={n}/GPU m={M} uniform seed 0, {nq} full-match queries at "
-                                   f"selectivity {SELECTIVITY}, ids mode (sorted uint32 ids per query)",
-                       "path": binfo["path"], "requested_path": args.path,
-                       "queries_per_step": nq, "ids_per_step": int(total_local) * world,
-                       "l2": "inputs (1.6 GB/GPU columns, 400 MB/GPU code planes) larger than L2 (126 MB); "
-                             "no flush",
-                       "parallelism": f"row shards x{world}",
-                       "combine": ("none (one rank)" if not merge else
-                                   "ids exchanged in the step" if args.merge_in_step else
-                                   "counts all_gather in the step; id exchange timed separately (id_exchange)")},
-            "queries_per_s": nq / (ms / 1e3),
-            "hbm_gbs_per_gpu": roofline["achieved"],
-            "roofline": roofline,
-            "smem_roofline": smem_roofline(binfo, prof, n, nq, clocks.summary()),
-            "columnar_scan_roofline": col_roof,
-            "pass_profile": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in prof.items()},
-            "paths_us_per_query": paths,
-            "e2e": {"value": e2e_val, "unit": "tuples/s",
-                    "h2d_bytes_per_step": int(info.get("h2d_bytes", 0) // e2e_steps),
-                    "d2h_bytes_per_step": int(total_local * 4 + (nq + 1) * 8),
-                    "api": f"DeviceStore.ids_stream, {e2e_steps} steps pipelined (copy of step k under the "
-                           f"scan of step k+1); wall clock",
-                    "ms_per_step": e2e_s * 1e3,
-                    "d2h_roofline": {"achieved_gbs": d2h_bytes / e2e_s / 1e9, "peak_gbs": d2h_peak,
-                                     "frac": d2h_bytes / e2e_s / 1e9 / d2h_peak,
-                                     "peak_kind": "measured in this run: one pinned copy of the step's "
-                                                  "result size"},
-                    "sync_call": {"value": n * world * nq / sync_s, "ms_per_step": sync_s * 1e3,
-                                  "api": "DeviceStore.ids, one synchronous call per step"}},
-            "id_exchange": xchg,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks.summary(),
-            "cpu_baseline": cpu,
-            "reference_methods": ref_methods,
-            "setup_s": {"generate": round(t_gen, 2), "store_build": round(t_build, 2)},
-        }
-        print(json.dumps(line), flush=True)
-    batch.close()
-    store.close()
-    if merge:
-        dist.destroy_process_group()
-    return 0
+def measure_c2(eng, _lib, dev, stream, steps, warmup):
+    """BASELINE.json configs[1] at selectivity 1e-3 (1000 queries, 5e7 x 8),
+    the round-1 headline, kept as a secondary number."""
+    from paper_1801_03644_b200 import workload
+    values = workload.c2_data()
+    lo, hi = workload.c2_queries(levels=(1e-3,))[1e-3]
+    sptr = stream.cuda_stream
+    with eng.DeviceStore(values, layouts=_lib.LAYOUT_COLUMNAR | _lib.LAYOUT_VAFILE, va_bits=8, device=dev) as st:
+        b = st.prepare(lo, hi, "auto")
+        total = b.reserve()
+        for _ in range(warmup):
+            b.ids_async(sptr)
+        ms = timed(lambda: b.ids_async(sptr), steps, stream, 1)
+        for _ in range(2):
+            b.count_async(0, sptr)
+        msc = timed(lambda: b.count_async(0, sptr), steps, stream, 1)
+        prof = b.profile(ids=True, stream=sptr)
+        b.close()
+    n, nq = values.shape[0], lo.shape[0]
+    return {"workload": "C2: 5e7 x 8 uniform seed 0, 1000 full-match queries at 1e-3",
+            "ids_ms_per_step": ms, "count_ms_per_step": msc, "value": n * nq / (ms / 1e3),
+            "unit": "tuple-queries/s", "ids_per_step": total,
+            "pass_profile": {k: {"ms": round(v[0], 4), "launches": v[1]} for k, v in prof.items()}}
 
 
 def vb_lw(nq: int, kb: int) -> int:
@@ -653,36 +759,6 @@ def _wrap(ptr: int, count: int, dtype, dev):
         __cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr, "data": (int(ptr), False),
                                     "version": 3, "strides": None}
     return torch.as_tensor(_CAI(), device=torch.device("cuda", dev))
-
-
-def explore(store, lo, hi, n, stream):
-    """Per-path / per-level / per-mode timings (stderr), for tuning."""
-    import torch
-    from paper_1801_03644_b200 import workload
-    levels = workload.c2_queries(count=lo.shape[0])
-    sptr = stream.cuda_stream
-    for s, (l, h) in levels.items():
-        for path in ("vafile_batch", "columnar", "columnar_batch", "vafile", "rowwise"):
-            for mode in ("count", "ids"):
-                if mode == "ids" and path == "columnar_batch":
-                    continue
-                nq = l.shape[0] if path != "rowwise" else min(100, l.shape[0])
-                b = store.prepare(l[:nq], h[:nq], path)
-                if mode == "ids":
-                    b.reserve()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                run = (lambda: b.ids_async(sptr)) if mode == "ids" else (lambda: b.count_async(0, sptr))
-                run()
-                e0.record(stream)
-                run()
-                run()
-                e1.record(stream)
-                torch.cuda.synchronize()
-                msq = e0.elapsed_time(e1) / 2 / nq
-                sys.stderr.write(f"explore s={s:g} path={path:15s} mode={mode:5s} "
-                                 f"{msq * 1e3:9.1f} us/query  {n / (msq / 1e3) / 1e9:8.1f} Gtuples/s  "
-                                 f"{4 * n * 8 / (msq / 1e3) / 1e9:8.0f} GB/s(4nk)\n")
-                b.close()
 
 
 if __name__ == "__main__":

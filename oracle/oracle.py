@@ -15,7 +15,7 @@ __all__ = [
     "HERE", "lib", "build_oracle",
     "match_code", "match_row", "scan_rows", "scan_column",
     "and_masks", "mask_popcount", "mask_to_ids",
-    "count_batch", "ids_batch", "va_code", "va_encode",
+    "count_batch", "ids_batch", "hash_batch", "id_hash", "set_hash", "va_code", "va_encode",
     "brute_ids", "brute_mask", "packbits_mask", "chunk_spans",
     "and_masks_chunked", "np_mask_to_ids",
     "load_reference_kernels", "reference_kind", "ReferenceHorizontalScan",
@@ -70,6 +70,11 @@ def lib():
     L.oracle_va_encode.restype = None
     L.oracle_va_encode.argtypes = [_f32p, ctypes.c_int64, _f32p, ctypes.c_int32, _u8p]
     L.oracle_has_openmp.restype = ctypes.c_int
+    L.oracle_hash_batch.restype = ctypes.c_int
+    L.oracle_hash_batch.argtypes = [_f32p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _f32p, _f32p,
+                                    ctypes.c_int64, _i64p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+    L.oracle_id_hash.restype = ctypes.c_uint64
+    L.oracle_id_hash.argtypes = [ctypes.c_uint64]
     _LIB = L
     return L
 
@@ -173,6 +178,52 @@ def ids_batch(values, lower, upper, threads: int = 0, counts=None):
         lib().oracle_ids_batch(_p(values, _f32p), n, m, _p(lo, _f32p), _p(hi, _f32p), nq,
                                _p(offsets, _i64p), _p(ids, _i64p), threads)
     return offsets, ids[:offsets[-1]]
+
+
+def hash_batch(values, lower, upper, id0: int = 0, counts=None, hashes=None, threads: int = 0):
+    """SequentialScan (scan.py:103-111) over a batch reduced to per-query
+    (count, set hash): hashes[q] = sum of id_hash(id) over the matching ids,
+    mod 2**64 (mdrq_oracle.c oracle_hash_batch).  ``values`` are rows
+    id0 .. id0+n-1; results are accumulated into ``counts`` / ``hashes`` when
+    given, so a table can be streamed through in row chunks."""
+    values = _f32(values)
+    n, m = values.shape
+    lo = _f32(lower).reshape(-1, m)
+    hi = _f32(upper).reshape(-1, m)
+    nq = lo.shape[0]
+    if counts is None:
+        counts = np.zeros(nq, dtype=np.int64)
+    if hashes is None:
+        hashes = np.zeros(nq, dtype=np.uint64)
+    assert counts.dtype == np.int64 and hashes.dtype == np.uint64 and counts.flags.c_contiguous
+    rc = lib().oracle_hash_batch(_p(values, _f32p), n, m, int(id0), _p(lo, _f32p), _p(hi, _f32p), nq,
+                                 _p(counts, _i64p), hashes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                 threads)
+    if rc != 0:
+        raise ValueError("NaN values are rejected at ingestion")
+    return counts, hashes
+
+
+_MIX = (np.uint64(0x9E3779B97F4A7C15), np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB))
+
+
+def id_hash(ids) -> np.ndarray:
+    """splitmix64 finalizer of every id (numpy, uint64 wraparound); the C
+    oracle's oracle_mix64."""
+    z = np.asarray(ids).astype(np.uint64) + _MIX[0]
+    z = (z ^ (z >> np.uint64(30))) * _MIX[1]
+    z = (z ^ (z >> np.uint64(27))) * _MIX[2]
+    return z ^ (z >> np.uint64(31))
+
+
+def set_hash(offsets, ids) -> np.ndarray:
+    """Per-query set hash of an (offsets, ids) result, as hash_batch
+    computes it: the sum mod 2**64 of id_hash over each query's ids."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    h = id_hash(ids)
+    c = np.zeros(h.size + 1, dtype=np.uint64)
+    np.cumsum(h, out=c[1:])
+    return c[offsets[1:]] - c[offsets[:-1]]
 
 
 def va_code(boundaries, v: float) -> int:

@@ -18,6 +18,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "launch.h"
@@ -204,6 +205,17 @@ struct mdrq_batch {
     // result pool of its own (stream slots); otherwise the store's pool
     bool own_pool = false;
     DBuf<uint32_t> own_ids;
+    // mdrq_batch_reserve: the ids total of this batch and the pool capacity
+    // that held it (mdrq_batch_ids_async refuses to run unreserved batches or
+    // into a pool that has since been replaced by a smaller one)
+    bool reserved = false;
+    uint64_t reserved_total = 0;
+    // device buffers freed (the owning store was destroyed first)
+    void release_device() {
+        d_descs.release(); d_preds.release(); d_udims.release(); d_bounds.release(); d_cmask.release();
+        d_vb_udims.release(); d_vb_tables.release(); d_vb_qb.release(); d_vb_cm.release();
+        d_scratch.release(); own_ids.release();
+    }
 };
 
 // One slot of the pipelined ids stream (mdrq_query_ids_stream): a batch with
@@ -248,6 +260,13 @@ struct mdrq_store {
     mdrq_batch* last_batch = nullptr;
     mdrq_batch scratch;
     std::mutex mu;
+    // prepared batches still alive (detached when the store goes first)
+    std::unordered_set<mdrq_batch*> batches;
+    // cross-stream order of the shared scratch (verdict mask, chunk counts,
+    // VA staging, result pool): every enqueue records `done` on its stream,
+    // an enqueue on another stream waits for it first
+    cudaEvent_t done = nullptr;
+    cudaStream_t done_stream = nullptr;
     // pipelined ids stream: a copy stream + slots, created on first use
     cudaStream_t copy_stream = nullptr;
     StreamSlot* slots = nullptr;
@@ -260,6 +279,7 @@ struct mdrq_store {
     uint64_t bounce_ids = 0;
     size_t bounce_head = 0;          // byte offset of those ids in the buffer
     ~mdrq_store() {
+        if (done) cudaEventDestroy(done);
         if (h_bounce) cudaFreeHost(h_bounce);
         if (slots) {
             for (int i = 0; i < kStreamSlots; ++i) {
@@ -753,7 +773,27 @@ struct Profiler {
     }
 };
 
+uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profiler* prof);
+
+// order work on `st` after the store's last pass (which may have run on a
+// caller's stream)
+void join(mdrq_store* s, cudaStream_t st) {
+    if (s->done && s->done_stream && s->done_stream != st) CK(cudaStreamWaitEvent(st, s->done, 0));
+}
+
+// Every pass goes through here: it orders the pass after the last pass the
+// store ran on another stream (shared scratch and result pool), and marks
+// its own end for the next one.
 uint32_t enqueue(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profiler* prof = nullptr) {
+    if (!s->done) CK(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
+    if (s->done_stream && s->done_stream != st) CK(cudaStreamWaitEvent(st, s->done, 0));
+    const uint32_t nl = enqueue_impl(s, b, ids, st, prof);
+    CK(cudaEventRecord(s->done, st));
+    s->done_stream = st;
+    return nl;
+}
+
+uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, Profiler* prof) {
     const uint32_t nq = b->nq;
     if (!nq) return 0;
     auto mark = [&](int c, uint32_t nl) {
@@ -994,6 +1034,7 @@ void fetch_ids_impl(mdrq_store* s, void* ids, uint64_t ids_cap, bool wide) {
         return;
     }
     uint32_t* dst = wide ? static_cast<uint32_t*>(ids) + total : static_cast<uint32_t*>(ids);
+    join(s, s->stream);
     CK(cudaMemcpyAsync(dst, s->ids.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     deliver_ids(dst, ids, total, wide);
@@ -1034,9 +1075,11 @@ int query_ids_impl(mdrq_store* s, const float* lower, const float* upper, uint32
             enqueue(s, b, true, s->stream);
             DBuf<uint32_t>& pool = pool_of(s, b);
             const uint64_t pcap = pool.p ? pool.cap : 0;
-            spec = have ? std::min<uint64_t>(std::min<uint64_t>(pcap, (kBounceMaxBytes - head) / 4),
-                                             std::max<uint64_t>(uint64_t(1) << 16, s->last_total + s->last_total / 4))
-                        : 0;
+            // a speculative prefix only when the expected result fits the
+            // bounce buffer: a larger one goes to the caller in ONE copy
+            // (a prefix would be copied twice)
+            const uint64_t want = std::max<uint64_t>(uint64_t(1) << 16, s->last_total + s->last_total / 4);
+            spec = have && want <= (kBounceMaxBytes - head) / 4 ? std::min<uint64_t>(pcap, want) : 0;
             hb = bounce(s, head + spec * 4);
             uint64_t* h_off = reinterpret_cast<uint64_t*>(hb);
             uint32_t* h_flag = reinterpret_cast<uint32_t*>(hb + (size_t(nq) + 1) * 8);
@@ -1206,10 +1249,19 @@ int mdrq_store_create(const float* rows, uint64_t n, uint32_t m, int device, uin
                 DBuf<float> mm;
                 mm.reserve(size_t(2) * m);
                 s->h_minmax.assign(size_t(2) * m, 0.f);
-                if (n && (layouts & MDRQ_LAYOUT_COLUMNAR)) {
+                if (n) {
+                    // a row-wise-only store: one column at a time through a
+                    // temporary transpose of the staged rows
+                    DBuf<float> tmp;
+                    if (!(layouts & MDRQ_LAYOUT_COLUMNAR)) {
+                        tmp.reserve(s->n_pad * m);
+                        launch_transpose_rows_to_cols(s->rows.p, n, m, tmp.p, s->n_pad, st);
+                    }
+                    const float* cols = (layouts & MDRQ_LAYOUT_COLUMNAR) ? s->cols.p : tmp.p;
                     for (uint32_t d = 0; d < m; ++d)
-                        launch_min_max(s->cols.p + uint64_t(d) * s->n_pad, n, mm.p + 2 * d, st);
+                        launch_min_max(cols + uint64_t(d) * s->n_pad, n, mm.p + 2 * d, st);
                     CK(cudaMemcpyAsync(s->h_minmax.data(), mm.p, sizeof(float) * 2 * m, cudaMemcpyDeviceToHost, st));
+                    CK(cudaStreamSynchronize(st));
                 }
                 CK(cudaStreamSynchronize(st));
             }
@@ -1270,6 +1322,15 @@ int mdrq_store_destroy(mdrq_store* s) {
         if (!s) return;
         DeviceGuard dg(s->device);
         cudaStreamSynchronize(s->stream);
+        if (s->done_stream) cudaStreamSynchronize(s->done_stream);
+        {
+            std::lock_guard<std::mutex> lk(s->mu);
+            for (mdrq_batch* b : s->batches) {   // the caller still holds these handles
+                b->release_device();
+                b->owner = nullptr;
+            }
+            s->batches.clear();
+        }
         cudaStream_t st = s->stream;
         delete s;
         cudaStreamDestroy(st);
@@ -1470,6 +1531,7 @@ int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats, uint32_t
         if (!b || b->nq != nq) raise(MDRQ_EINVAL, "no query batch of that size to report");
         if (nq && !stats) raise(MDRQ_EINVAL, "null stats");
         std::vector<unsigned long long> dev(size_t(nq) * 4, 0);
+        join(s, s->stream);
         if (nq && s->n)
             CK(cudaMemcpyAsync(dev.data(), b->d_stats.p, sizeof(unsigned long long) * 4 * nq, cudaMemcpyDeviceToHost,
                                s->stream));
@@ -1525,6 +1587,7 @@ int mdrq_batch_prepare(mdrq_store* s, const float* lower, const float* upper, ui
             // the ids flavour of AUTO is resolved at run time
             build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false), true, b);
             upload_batch(s, b);
+            s->batches.insert(b);
         } catch (...) {
             delete b;
             throw;
@@ -1541,7 +1604,9 @@ int mdrq_batch_destroy(mdrq_batch* b) {
             std::lock_guard<std::mutex> lk(s->mu);
             DeviceGuard dg(s->device);
             cudaStreamSynchronize(s->stream);
+            if (s->done_stream) cudaStreamSynchronize(s->done_stream);
             if (s->last_batch == b) s->last_batch = nullptr;
+            s->batches.erase(b);
             delete b;
         } else {
             delete b;
@@ -1570,11 +1635,15 @@ int mdrq_batch_ids_async(mdrq_store* s, mdrq_batch* b, void* stream) {
         std::lock_guard<std::mutex> lk(s->mu);
         s->bounce_ids = 0;
         DeviceGuard dg(s->device);
+        if (!b->reserved) raise(MDRQ_EINVAL, "ids_async needs mdrq_batch_reserve on this batch first");
+        if (b->reserved_total > (pool_of(s, b).p ? pool_of(s, b).cap : 0))
+            raise(MDRQ_ETRUNC, "the result pool no longer holds this batch's ids (reserve it again)");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
         enqueue(s, b, true, st);
         s->last_batch = b;
         s->last_nq = b->nq;
         s->last_path = b->path;
+        s->last_total = b->reserved_total;
     });
 }
 
@@ -1585,6 +1654,8 @@ int mdrq_batch_reserve(mdrq_store* s, mdrq_batch* b, uint64_t* total) {
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard dg(s->device);
         const uint64_t t = run_ids_sync(s, b);
+        b->reserved = true;
+        b->reserved_total = t;
         if (total) *total = t;
     });
 }

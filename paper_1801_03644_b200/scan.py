@@ -119,7 +119,8 @@ class _GpuScan:
     """Shared machinery: one device store + the reference search protocol."""
 
     name = "gpu"
-    _path = "auto"
+    _path = "auto"          # one query: search() / search_with_stats()
+    _batch_path = "auto"    # many: search_batch() / search_stream() -- the planner
     _layouts = _lib.LAYOUT_COLUMNAR
 
     def _open(self, values, device=None, va_bits=0):
@@ -141,17 +142,31 @@ class _GpuScan:
         # int64 ids straight from the C ABI: the reference ResultSet dtype
         return ResultSet(self.store.ids64(lo, hi, self._path)[1])
 
-    def _ids(self, queries):
+    def _ids(self, queries, path=None):
         lo, hi = stack_queries(queries, self.m)
-        offsets, ids = self.store.ids(lo, hi, self._path)
+        offsets, ids = self.store.ids(lo, hi, path or self._path)
         return BatchResult(offsets, ids)
+
+    def search_stream(self, batches, outs=None) -> list:
+        """Pipelined ids of a sequence of query batches (a serving loop /
+        the reference harness's repetitions, bench.py:178-186): one
+        BatchResult per batch; batch k's device->host copy runs under batch
+        k+1's device pass (DeviceStore.ids_stream).  ``outs`` optionally
+        gives one caller-owned (pinned) uint32 buffer per batch."""
+        pairs = []
+        for queries in batches:
+            queries = list(queries)
+            for q in queries:
+                self._check(q)
+            pairs.append(stack_queries(queries, self.m))
+        return [BatchResult(o, i) for o, i in self.store.ids_stream(pairs, self._batch_path, outs=outs)]
 
     def search_batch(self, queries) -> BatchResult:
         """Ids of every query of the batch, ascending per query."""
         queries = list(queries)
         for q in queries:
             self._check(q)
-        return self._ids(queries)
+        return self._ids(queries, self._batch_path)
 
     def count(self, query: RangeQuery) -> int:
         self._check(query)
@@ -187,9 +202,10 @@ class SequentialScan(_GpuScan):
 
     def search_with_stats(self, query: RangeQuery) -> tuple[ResultSet, SearchStats]:
         self._check(query)
-        res = self._ids([query])
-        st = self.store.stats(1, MODE_BLOCKED if self.mode is KernelMode.VECTORIZED else MODE_SCALAR)[0]
-        return res[0], SearchStats(objects_compared=self.n, early_breaks=int(st.early_breaks))
+        lo, hi = stack_queries([query], self.m)
+        _, ids, st = self.store.ids64_with_stats(
+            lo, hi, self._path, MODE_BLOCKED if self.mode is KernelMode.VECTORIZED else MODE_SCALAR)
+        return ResultSet(ids), SearchStats(objects_compared=self.n, early_breaks=int(st[0].early_breaks))
 
 
 class HorizontalScan(_GpuScan):
@@ -220,9 +236,10 @@ class HorizontalScan(_GpuScan):
 
     def search_with_stats(self, query: RangeQuery) -> tuple[ResultSet, SearchStats]:
         self._check(query)
-        res = self._ids([query])
-        st = self.store.stats(1, MODE_BLOCKED if self.mode is KernelMode.VECTORIZED else MODE_SCALAR)[0]
-        return res[0], SearchStats(objects_compared=self.n, early_breaks=int(st.early_breaks))
+        lo, hi = stack_queries([query], self.m)
+        _, ids, st = self.store.ids64_with_stats(
+            lo, hi, self._path, MODE_BLOCKED if self.mode is KernelMode.VECTORIZED else MODE_SCALAR)
+        return ResultSet(ids), SearchStats(objects_compared=self.n, early_breaks=int(st[0].early_breaks))
 
 
 class VerticalScan(_GpuScan):

@@ -17,6 +17,8 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
+import weakref
 
 import numpy as np
 
@@ -65,6 +67,10 @@ class DeviceStore:
         check(lib.mdrq_store_create(values.ctypes.data_as(f32p), self.n, self.m, self.device,
                                     layouts, va_bits, self.id_base, ctypes.byref(handle)))
         self._h = handle
+        # one store is not re-entrant across paired C calls (query + fetch,
+        # ids + stats share the store's cached result): one lock per store
+        self._lock = threading.RLock()
+        self._batches = weakref.WeakSet()
         info = _lib.StoreInfo()
         check(lib.mdrq_store_get_info(self._h, ctypes.byref(info)))
         self.layouts = int(info.layouts)
@@ -107,6 +113,8 @@ class DeviceStore:
         return self._h
 
     def close(self) -> None:
+        for b in list(getattr(self, "_batches", ())):
+            b.close()   # prepared batches first (the C side also detaches them)
         h, self._h = getattr(self, "_h", None), None
         if h:
             _lib.load().mdrq_store_destroy(h)
@@ -145,8 +153,9 @@ class DeviceStore:
         lo, hi = _bounds(lower, upper, self.m)
         nq = lo.shape[0]
         counts = np.zeros(nq, np.uint64)
-        check(_lib.load().mdrq_query_count(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p),
-                                           nq, _path(path), counts.ctypes.data_as(u64p)))
+        with self._lock:
+            check(_lib.load().mdrq_query_count(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p),
+                                               nq, _path(path), counts.ctypes.data_as(u64p)))
         return counts.astype(np.int64)
 
     def ids(self, lower, upper, path: str | int = "auto", out: np.ndarray | None = None):
@@ -161,16 +170,17 @@ class DeviceStore:
         offsets = np.zeros(nq + 1, np.uint64)
         total = ctypes.c_uint64(0)
         buf = out if out is not None else np.empty(max(1, _guess(self.n, nq)), np.uint32)
-        rc = lib.mdrq_query_ids(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p), nq,
-                                _path(path), offsets.ctypes.data_as(u64p), buf.ctypes.data_as(u32p),
-                                buf.size, ctypes.byref(total))
-        if rc == _lib.MDRQ_ETRUNC:
-            if out is not None:
-                raise ValueError(f"ids buffer holds {out.size} ids, the batch produced {total.value}")
-            buf = np.empty(int(total.value), np.uint32)
-            check(lib.mdrq_fetch_ids(self.handle, buf.ctypes.data_as(u32p), buf.size))
-        else:
-            check(rc)
+        with self._lock:
+            rc = lib.mdrq_query_ids(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p), nq,
+                                    _path(path), offsets.ctypes.data_as(u64p), buf.ctypes.data_as(u32p),
+                                    buf.size, ctypes.byref(total))
+            if rc == _lib.MDRQ_ETRUNC:
+                if out is not None:
+                    raise ValueError(f"ids buffer holds {out.size} ids, the batch produced {total.value}")
+                buf = np.empty(int(total.value), np.uint32)
+                check(lib.mdrq_fetch_ids(self.handle, buf.ctypes.data_as(u32p), buf.size))
+            else:
+                check(rc)
         return offsets.astype(np.int64), buf[: int(total.value)]
 
     def ids64(self, lower, upper, path: str | int = "auto"):
@@ -184,14 +194,23 @@ class DeviceStore:
         nq = lo.shape[0]
         offsets = np.zeros(nq + 1, np.uint64)
         total = ctypes.c_uint64(0)
-        rc = lib.mdrq_query_ids64(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p), nq,
-                                  _path(path), offsets.ctypes.data_as(u64p), None, 0, ctypes.byref(total))
-        ids = np.empty(int(total.value), np.int64)
-        if rc == _lib.MDRQ_ETRUNC:
-            check(lib.mdrq_fetch_ids64(self.handle, ids.ctypes.data_as(i64p), ids.size))
-        else:
-            check(rc)
+        with self._lock:
+            rc = lib.mdrq_query_ids64(self.handle, lo.ctypes.data_as(f32p), hi.ctypes.data_as(f32p), nq,
+                                      _path(path), offsets.ctypes.data_as(u64p), None, 0, ctypes.byref(total))
+            ids = np.empty(int(total.value), np.int64)
+            if rc == _lib.MDRQ_ETRUNC:
+                check(lib.mdrq_fetch_ids64(self.handle, ids.ctypes.data_as(i64p), ids.size))
+            else:
+                check(rc)
         return offsets.view(np.int64), ids
+
+    def ids64_with_stats(self, lower, upper, path: str | int = "auto", mode: int = _lib.MODE_SCALAR):
+        """ids64 and the pass's per-query counters, under one hold of the
+        store's lock (no other thread's call can replace the cached batch
+        between the two)."""
+        with self._lock:
+            offs, ids = self.ids64(lower, upper, path)
+            return offs, ids, self.stats(offs.size - 1, mode)
 
     def ids_stream(self, batches, path: str | int = "auto", outs=None, info: dict | None = None):
         """Pipelined ids for a sequence of query batches ``[(lower, upper),
@@ -222,10 +241,11 @@ class DeviceStore:
         h2d = ctypes.c_uint64(0)
         offs_p = (u64p * nb)(*[o.ctypes.data_as(u64p) for o in offs])
         ids_p = (u32p * nb)(*[b.ctypes.data_as(u32p) for b in bufs])
-        rc = lib.mdrq_query_ids_stream(self.handle, lo_all.ctypes.data_as(f32p), hi_all.ctypes.data_as(f32p),
-                                       nqs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), nb, _path(path),
-                                       offs_p, ids_p, caps.ctypes.data_as(u64p), totals.ctypes.data_as(u64p),
-                                       ctypes.byref(h2d))
+        with self._lock:
+            rc = lib.mdrq_query_ids_stream(self.handle, lo_all.ctypes.data_as(f32p), hi_all.ctypes.data_as(f32p),
+                                           nqs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), nb,
+                                           _path(path), offs_p, ids_p, caps.ctypes.data_as(u64p),
+                                           totals.ctypes.data_as(u64p), ctypes.byref(h2d))
         if rc != _lib.MDRQ_ETRUNC:
             check(rc)
         out = []
@@ -243,12 +263,15 @@ class DeviceStore:
 
     def stats(self, nq: int, mode: int = _lib.MODE_SCALAR):
         arr = (_lib.SearchStatsC * max(nq, 1))()
-        check(_lib.load().mdrq_query_stats(self.handle, mode, arr, nq))
+        with self._lock:
+            check(_lib.load().mdrq_query_stats(self.handle, mode, arr, nq))
         return [arr[i] for i in range(nq)]
 
     # -- prepared batches (device-resident; bench / multi-GPU) --------------
     def prepare(self, lower, upper, path: str | int = "auto") -> "PreparedBatch":
-        return PreparedBatch(self, lower, upper, path)
+        b = PreparedBatch(self, lower, upper, path)
+        self._batches.add(b)
+        return b
 
 
 def _guess(n: int, nq: int) -> int:
@@ -280,6 +303,7 @@ class PreparedBatch:
     def close(self):
         h, self._h = getattr(self, "_h", None), None
         if h:
+            # safe after the store is gone too: the store detached it
             _lib.load().mdrq_batch_destroy(h)
 
     def __del__(self):

@@ -119,8 +119,8 @@ class VaFile:
         if query.m != self.m:
             raise ValueError(f"query has {query.m} dimensions, grid has {self.m}")
         lo, hi = stack_queries([query], self.m)
-        offs, ids = self.store.ids64(lo, hi, "vafile")
-        st = self.store.stats(1)[0]
+        offs, ids, st = self.store.ids64_with_stats(lo, hi, "vafile")
+        st = st[0]
         stats = SearchStats(objects_compared=int(st.objects_compared), nodes_visited=int(st.nodes_visited),
                             columns_scanned=int(st.columns_scanned))
         return ResultSet(self._map(ids)), stats
@@ -131,7 +131,9 @@ class VaFile:
             if q.m != self.m:
                 raise ValueError(f"query has {q.m} dimensions, grid has {self.m}")
         lo, hi = stack_queries(queries, self.m)
-        offs, ids = self.store.ids(lo, hi, "vafile")
+        # the planner: >= 10 queries go through the bit-sliced multi-query
+        # pass (<= 1024 queries per pass over the code planes)
+        offs, ids = self.store.ids(lo, hi, "auto")
         if self._ids is not None:
             parts = [self._map(ids[offs[q]:offs[q + 1]]) for q in range(len(queries))]
             ids = np.concatenate(parts) if parts else np.empty(0, np.int64)
@@ -141,8 +143,31 @@ class VaFile:
         return int(self.count_batch([query])[0])
 
     def count_batch(self, queries) -> np.ndarray:
-        lo, hi = stack_queries(list(queries), self.m)
-        return self.store.count(lo, hi, "vafile")
+        queries = list(queries)
+        for q in queries:
+            if q.m != self.m:
+                raise ValueError(f"query has {q.m} dimensions, grid has {self.m}")
+        lo, hi = stack_queries(queries, self.m)
+        return self.store.count(lo, hi, "auto")
+
+    def search_stream(self, batches, outs=None) -> list:
+        """Pipelined ids of a sequence of query batches (see
+        _GpuScan.search_stream)."""
+        pairs = []
+        for queries in batches:
+            queries = list(queries)
+            for q in queries:
+                if q.m != self.m:
+                    raise ValueError(f"query has {q.m} dimensions, grid has {self.m}")
+            pairs.append(stack_queries(queries, self.m))
+        res = self.store.ids_stream(pairs, "auto", outs=outs)
+        if self._ids is not None:
+            out = []
+            for offs, ids in res:
+                parts = [self._map(ids[offs[q]:offs[q + 1]]) for q in range(offs.size - 1)]
+                out.append(BatchResult(offs, np.concatenate(parts) if parts else np.empty(0, np.int64)))
+            return out
+        return [BatchResult(o, i) for o, i in res]
 
     def close(self) -> None:
         self.store.close()

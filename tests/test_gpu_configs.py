@@ -1,10 +1,18 @@
-"""Full-size configuration parity on the GPU (BASELINE.json configs).
+"""Full-size configuration parity on the GPU (BASELINE.json configs C2-C5).
 
-C2 (5e7 x 8): the first 20 queries of every selectivity level against the
-reference's own id lists (sha1, tests/golden/c2.npz, recorded with the
-reference's HorizontalScan), and all 5000 queries through every path with
-size-independent properties: count == len(ids), ids strictly ascending and
-< n, and the paths agree with each other id for id.
+EVERY query of every configuration is compared with the CPU oracle: the
+committed fixtures tests/golden/all_<cfg>.npz hold, per query, the oracle's
+count and set hash (sum of splitmix64(id) mod 2**64; oracle/mdrq_oracle.c
+oracle_hash_batch, pinned against the reference's own id lists by
+tests/golden/make_all_queries.py).  The device result is checked in place
+(tests/devhash.py): ids strictly ascending and < n within every query, then
+(count, hash) per query == the oracle's.  That is every query on the
+multi-query VA pass (what the planner runs for a batch), counts of every
+query on the multi-query columnar pass, and a stratified sample of >= 500
+queries on each single-query path (columnar, VA scan).
+
+The first queries are also compared with the reference's OWN id lists
+(sha1; tests/golden/c*.npz, recorded from the reference by make_golden.py).
 """
 
 import hashlib
@@ -14,6 +22,7 @@ import pytest
 
 import oracle
 from conftest import golden
+from devhash import batch_hashes
 
 pytestmark = pytest.mark.gpu
 
@@ -48,6 +57,25 @@ def test_c2_vs_reference_golden(c2_store):
                 assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G[f"level{li}_sha1"][i].tobytes(), (s, path, i)
 
 
+def _every_query(st, lo, hi, counts, hashes, name, single=500, single_paths=("columnar", "vafile")):
+    """Every query on the planner's batch path (ids: count + hash; count
+    mode: counts) and a stratified sample on the single-query paths."""
+    c, h, path = batch_hashes(st, lo, hi, "auto")
+    assert path == "vafile_batch", (name, path)
+    assert np.array_equal(c, counts), (name, "vafile_batch counts", np.flatnonzero(c != counts)[:10])
+    assert np.array_equal(h, hashes), (name, "vafile_batch ids", np.flatnonzero(h != hashes)[:10])
+    assert np.array_equal(st.count(lo, hi, "vafile_batch"), counts), (name, "vafile_batch count mode")
+    nq = lo.shape[0]
+    k = min(nq, 1024)
+    assert np.array_equal(st.count(lo[:k], hi[:k], "columnar_batch"), counts[:k]), (name, "columnar_batch")
+    sel = np.unique(np.linspace(0, nq - 1, min(single, nq)).astype(np.int64))
+    for p in single_paths:
+        c, h, ran = batch_hashes(st, lo[sel], hi[sel], p)
+        assert ran == p
+        assert np.array_equal(c, counts[sel]), (name, p, "counts")
+        assert np.array_equal(h, hashes[sel]), (name, p, "ids")
+
+
 def _check_generated(gpu, name, values):
     """C3 / C4: the reference's id lists for the first queries (sha1) and the
     pinned oracle's counts for every query, on the full table."""
@@ -64,11 +92,10 @@ def _check_generated(gpu, name, values):
             assert np.array_equal(np.diff(offs), G["ref_counts"]), (name, path)
             for i in range(k):
                 assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G["ref_sha1"][i].tobytes(), (name, path, i)
-        # every query in ids mode: counts and cross-path id equality
-        offs, ids = st.ids(lo, hi, "vafile_batch")
-        assert np.array_equal(np.diff(offs), G["oracle_counts"]), name
-        o2, i2 = st.ids(lo[:200], hi[:200], "columnar")
-        assert np.array_equal(o2, offs[:201]) and np.array_equal(i2, ids[:o2[-1]]), name
+        # every query against the oracle's (count, set hash)
+        A = golden(f"all_{name}.npz")
+        assert np.array_equal(A["counts"], G["oracle_counts"])
+        _every_query(st, lo, hi, A["counts"], A["hash"], name)
 
 
 def test_c3_vs_reference_golden(gpu):
@@ -85,8 +112,8 @@ def test_c5_full_size_vs_reference_golden(gpu):
     """C5: 5e8 x 10 (20 GB) on one GPU.  The table is generated chunk-parallel
     (PCG64 advanced per chunk) and checked against slice hashes of the
     one-shot generator; the first 8 queries against the reference's
-    SequentialScan id lists, the first 200 counts against the oracle, 1024
-    queries in ids mode for size-independent properties."""
+    SequentialScan id lists; EVERY query (10 000, 5e9 ids, checked in place)
+    against the oracle's (count, set hash)."""
     from paper_1801_03644_b200 import workload
     G = golden("c5.npz")
     values = workload.c5_data()
@@ -94,7 +121,6 @@ def test_c5_full_size_vs_reference_golden(gpu):
         assert hashlib.sha1(values[s:s + 1_000_000].tobytes()).digest() == h.tobytes(), s
     lo, hi = workload.c5_queries()
     k = G["ref_counts"].size
-    n = values.shape[0]
     with gpu.DeviceStore(values, layouts=1 | 4, va_bits=8) as st:
         del values
         nq = G["oracle_counts"].size
@@ -105,34 +131,16 @@ def test_c5_full_size_vs_reference_golden(gpu):
             assert np.array_equal(np.diff(offs), G["ref_counts"]), path
             for i in range(k):
                 assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G["ref_sha1"][i].tobytes(), (path, i)
-        offs, ids = st.ids(lo[:1024], hi[:1024], "vafile_batch")
-        assert np.array_equal(np.diff(offs), st.count(lo[:1024], hi[:1024], "vafile_batch"))
-        d = np.diff(ids.astype(np.int64))
-        starts = offs[1:-1]
-        d[starts[(starts > 0) & (starts < ids.size)] - 1] = 1
-        assert (d > 0).all() and ids.max() < n
+        A = golden("all_c5.npz")
+        assert np.array_equal(A["counts"][:nq], G["oracle_counts"])
+        _every_query(st, lo, hi, A["counts"], A["hash"], "c5")
 
 
-def test_c2_all_queries_paths_agree(c2_store):
+def test_c2_every_query_vs_oracle(c2_store):
+    """C2: all 5 x 1000 queries (1e-5 .. 1e-1) against the oracle."""
     from paper_1801_03644_b200 import workload
-    st, values = c2_store
-    n = values.shape[0]
-    for s, (lo, hi) in workload.c2_queries().items():
-        ref_offs, ref_ids = st.ids(lo, hi, "vafile_batch")
-        counts = np.diff(ref_offs)
-        assert np.array_equal(st.count(lo, hi, "vafile_batch"), counts), s
-        assert np.array_equal(st.count(lo, hi, "columnar_batch"), counts), s
-        # strictly ascending within every query, all < n
-        d = np.diff(ref_ids.astype(np.int64))
-        starts = ref_offs[1:-1]
-        d[starts[(starts > 0) & (starts < ref_ids.size)] - 1] = 1
-        assert (d > 0).all() and (ref_ids.size == 0 or ref_ids.max() < n)
-        sub = slice(0, 100) if s < 0.1 else slice(0, 20)   # keep the single-query paths quick
-        for path in ("columnar", "vafile"):
-            offs, ids = st.ids(lo[sub], hi[sub], path)
-            m = offs[-1]
-            assert np.array_equal(offs, ref_offs[: offs.size]), (s, path)
-            assert np.array_equal(ids, ref_ids[:m]), (s, path)
-        # a few queries against the OpenMP oracle on the full table
-        exp = oracle.count_batch(values, lo[:4], hi[:4])
-        assert np.array_equal(counts[:4], exp), s
+    st, _ = c2_store
+    A = golden("all_c2.npz")
+    for li, (s, (lo, hi)) in enumerate(workload.c2_queries().items()):
+        assert A[f"level{li}_s"][0] == s
+        _every_query(st, lo, hi, A[f"level{li}_counts"], A[f"level{li}_hash"], f"c2 {s:g}", single=100)

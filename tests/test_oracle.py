@@ -159,3 +159,83 @@ def test_reference_horizontal_scan_matches_oracle():
             assert np.array_equal(scan.search(lo, hi), oracle.brute_ids(v, lo, hi))
     finally:
         scan.close()
+
+
+# -- the every-query checker (oracle_hash_batch) ---------------------------------
+
+def test_hash_batch_vs_reference_c1_all_queries():
+    """oracle.hash_batch against the reference's own id lists: for all 1000
+    C1 queries the reference-pinned ids (sha1 vs the reference for 1000 of
+    them) hash to hash_batch's value, and the counts agree; C1 partial-match
+    counts too (the +-inf sentinel dims are skipped by hash_batch)."""
+    from paper_1801_03644_b200 import workload
+    G = golden("c1.npz")
+    values = workload.c1_data()
+    lo, hi = workload.c1_queries()
+    c, h = oracle.hash_batch(values, lo, hi)
+    assert np.array_equal(c, G["counts"])
+    offs, ids = oracle.ids_batch(values, lo, hi, counts=c)
+    for i in range(lo.shape[0]):
+        assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G["sha1"][i].tobytes(), i
+    assert np.array_equal(h, oracle.set_hash(offs, ids))
+    pc, _ = oracle.hash_batch(values, G["p_lo"], G["p_hi"])
+    assert np.array_equal(pc, G["p_counts"])
+
+
+def test_hash_batch_chunked_and_edges():
+    """Streaming in row chunks with id offsets equals one call; ragged tails,
+    empty results, all-unconstrained queries, +-inf / -0.0 / subnormal values
+    (the edge goldens' data) agree with the scalar restatement."""
+    E = golden("edge.npz")
+    rng = np.random.default_rng(3)
+    v = rng.random((30_011, 6), dtype=np.float32)
+    v[::97, 2] = -0.0
+    v[5::101, 3] = np.float32(1e-45)
+    lo = rng.uniform(0, 0.5, (33, 6)).astype(np.float32)
+    hi = (lo + 0.5).astype(np.float32)
+    lo[0] = 2.0
+    hi[0] = 3.0                                # empty
+    lo[1], hi[1] = -np.inf, np.inf             # every row
+    lo[2, 2], hi[2, 2] = 0.0, 0.0              # -0.0 == 0.0
+    offs, ids = oracle.ids_batch(v, lo, hi)
+    c, h = oracle.hash_batch(v, lo, hi)
+    assert np.array_equal(c, np.diff(offs)) and np.array_equal(h, oracle.set_hash(offs, ids))
+    c2 = np.zeros_like(c)
+    h2 = np.zeros_like(h)
+    for s in range(0, v.shape[0], 7_000):
+        oracle.hash_batch(v[s:s + 7_000], lo, hi, id0=s, counts=c2, hashes=h2)
+    assert np.array_equal(c2, c) and np.array_equal(h2, h)
+    for pre in ("", "cat_"):   # the reference-recorded edge cases
+        vals, el, eh = E[pre + "values"], E[pre + "lo"], E[pre + "hi"]
+        o, i = oracle.ids_batch(vals, el, eh)
+        cc, hh = oracle.hash_batch(vals, el, eh)
+        assert np.array_equal(cc, E[pre + "counts"]), pre
+        assert np.array_equal(cc, np.diff(o)) and np.array_equal(hh, oracle.set_hash(o, i)), pre
+
+
+def test_hash_batch_rejects_nan():
+    v = np.zeros((10, 2), np.float32)
+    v[3, 1] = np.nan
+    with pytest.raises(ValueError):
+        oracle.hash_batch(v, np.zeros((1, 2), np.float32), np.ones((1, 2), np.float32))
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
+def test_every_query_fixtures_consistent(cfg):
+    """The committed every-query fixtures agree with the earlier pinned
+    counts (reference counts and oracle counts in c*.npz)."""
+    import os
+    from conftest import GOLDEN
+    path = os.path.join(GOLDEN, f"all_{cfg}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"all_{cfg}.npz not generated")
+    A, G = golden(f"all_{cfg}.npz"), golden(f"{cfg}.npz")
+    if cfg == "c2":
+        for li in range(5):
+            k = G[f"level{li}_counts"].size
+            assert A[f"level{li}_counts"].size == 1000 and A[f"level{li}_hash"].dtype == np.uint64
+            assert np.array_equal(A[f"level{li}_counts"][:k], G[f"level{li}_counts"])
+    else:
+        assert A["hash"].dtype == np.uint64 and A["counts"].size == A["hash"].size
+        assert np.array_equal(A["counts"][:G["ref_counts"].size], G["ref_counts"])
+        assert np.array_equal(A["counts"][:G["oracle_counts"].size], G["oracle_counts"])
