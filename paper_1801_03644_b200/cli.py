@@ -4,10 +4,12 @@
     python -m paper_1801_03644_b200 bench  --n 1000000 --dims 3 --queries 1000 --out r.csv
 
 ``verify`` restates the reference's oracle-equivalence audit
-(cli.py:210-246): every method's id set for every query must equal the
-sequential scan's; exit code 2 on a mismatch.  On the GPU the "sequential"
-method is the row-wise kernel, so verify cross-checks the kernels against
-each other; the CPU oracle check lives in tests/ (pinned to the reference).
+(cli.py:210-246): every GPU method's id set for every query must equal the
+ground truth computed ON THE CPU -- the reference's own
+``SequentialScan(KernelMode.SCALAR)`` (cli.py:222) when the reference package
+``mdrq`` is importable (``--reference`` path, default baseline/_ref), else a
+numpy containment test (the reference suite's independent oracle,
+pkg/tests/test_scan.py:22-28); exit code 2 on a mismatch.
 ``bench`` restates run_benchmark (bench.py:146-212): build, one untimed
 warm-up batch, the median of ``--repetitions`` timed batches (each batch one
 ``search_batch`` call over all queries), selectivity from the exact counts,
@@ -55,15 +57,45 @@ def _methods(spec: str):
     return names
 
 
+def _reference_module(path):
+    """The reference package ``mdrq`` (compiled backend), or None."""
+    import importlib
+    if path and os.path.isdir(os.path.join(path, "mdrq")) and path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        return importlib.import_module("mdrq")
+    except ImportError:
+        return None
+
+
+def ground_truth(data, queries, reference_path=None):
+    """CPU ground truth per query -> (list of int64 id arrays, source)."""
+    ref = _reference_module(reference_path)
+    if ref is not None and hasattr(ref, "SequentialScan"):
+        scan = ref.SequentialScan(ref.DataSet(data.values), ref.KernelMode.SCALAR)
+        try:
+            exp = [scan.search(ref.RangeQuery(q.lower, q.upper)).ids for q in queries]
+        finally:
+            getattr(scan, "close", lambda: None)()
+        return exp, f"reference SequentialScan(SCALAR) (mdrq backend {getattr(ref, 'BACKEND', '?')})"
+    v = data.values
+    exp = []
+    for q in queries:
+        ok = np.ones(v.shape[0], dtype=bool)
+        for j in range(v.shape[1]):
+            ok &= (v[:, j] >= q.lower[j]) & (v[:, j] <= q.upper[j])
+        exp.append(np.flatnonzero(ok).astype(np.int64))
+    return exp, "numpy containment on the CPU (pkg/tests/test_scan.py:22-28)"
+
+
 def cmd_verify(args) -> int:
     from .core import KernelMode
     from .methods import build_method
     data, queries = _data_and_queries(args)
-    oracle = build_method("sequential", data, mode=KernelMode.SCALAR)
-    try:
-        expected = oracle.search_batch(queries)
-    finally:
-        oracle.close()
+    ref_path = args.reference if args.reference is not None else os.path.join(
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    expected, source = ground_truth(data, queries, ref_path)
+    print(f"ground truth: {source}, {len(queries)} queries")
     failures = 0
     for name in _methods(args.method):
         method = build_method(name, data, threads=args.threads, mode=KernelMode.parse(args.kernel), seed=args.seed)
@@ -71,7 +103,7 @@ def cmd_verify(args) -> int:
         try:
             got = method.search_batch(queries)
             for qi in range(len(queries)):
-                g, e = got.ids_of(qi), expected.ids_of(qi)
+                g, e = got.ids_of(qi).astype(np.int64), expected[qi]
                 if not np.array_equal(g, e):
                     missing = np.setdiff1d(e, g)
                     extra = np.setdiff1d(g, e)
@@ -84,7 +116,7 @@ def cmd_verify(args) -> int:
     if failures:
         print(f"verification failed: {failures} mismatching result sets")
         return 2
-    print("verification passed: all methods match the sequential scan")
+    print("verification passed: all methods match the CPU ground truth")
     return 0
 
 
@@ -142,6 +174,9 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--kernel", default="scalar")
         p.add_argument("--data", default=None, help="dataset file (reference binary format)")
         p.add_argument("--queries-file", default=None, help="JSONL query batch")
+        if name == "verify":
+            p.add_argument("--reference", default=None,
+                           help="directory holding the reference package mdrq (default baseline/_ref)")
         if name == "bench":
             p.add_argument("--repetitions", type=int, default=3)
             p.add_argument("--out", default=None)

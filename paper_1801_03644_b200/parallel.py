@@ -149,105 +149,261 @@ def _all_gather(t, world: int, group):
     return out.view(world, t.numel())
 
 
+def global_layout(all_counts):
+    """all_counts [world, nq] (ids of query q on rank r) -> (out_offsets
+    int64[nq+1] of the merged result, rank_prefix [world, nq]: where rank r's
+    slice of query q starts inside query q's run).  Rank order is id order
+    (contiguous shards), so the merge is the reference's concat + sort
+    (scan.py:160, parallel.py:156-157) without the sort."""
+    import torch
+    nq = all_counts.shape[1]
+    out_offsets = torch.zeros(nq + 1, dtype=torch.int64, device=all_counts.device)
+    torch.cumsum(all_counts.sum(0), 0, out=out_offsets[1:])
+    rank_prefix = torch.cumsum(all_counts, 0) - all_counts
+    return out_offsets, rank_prefix
+
+
+def rank_segments(all_counts, rank: int, out_offsets, rank_prefix):
+    """Segments (src_off, dst_off, len), one per query, that place rank
+    `rank`'s local result (query-major) into the merged query-major result."""
+    import torch
+    c = all_counts[rank]
+    src_off = torch.cumsum(c, 0) - c
+    dst_off = out_offsets[:-1] + rank_prefix[rank]
+    return src_off.contiguous(), dst_off.contiguous(), c.contiguous()
+
+
+def _place_segments(src, dst, src_off, dst_off, seg_len, stream=None):
+    """dst[dst_off[i] : +len[i]] = src[src_off[i] : +len[i]] for every
+    segment: one mdrq_copy_segments kernel when src lives on a GPU (dst may be
+    device memory or registered host memory the device can write), torch
+    index arithmetic on CPU tensors (the gloo tests)."""
+    import torch
+    nseg = seg_len.numel()
+    if nseg == 0 or int(seg_len.sum()) == 0:
+        return
+    if src.device.type == "cuda" and src.element_size() == 4:
+        import ctypes
+        from . import _lib
+        dptr = dst.data_ptr() if hasattr(dst, "data_ptr") else int(dst)
+        st = stream if stream is not None else torch.cuda.current_stream(src.device).cuda_stream
+        _lib.check(_lib.load().mdrq_copy_segments(
+            ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dptr),
+            ctypes.c_void_p(src_off.data_ptr()), ctypes.c_void_p(dst_off.data_ptr()),
+            ctypes.c_void_p(seg_len.data_ptr()), nseg, ctypes.c_void_p(st)))
+        return
+    total = int(seg_len.sum())
+    base_dst = torch.repeat_interleave(dst_off - src_off, seg_len)
+    src_idx = torch.repeat_interleave(src_off, seg_len)
+    within = torch.arange(total, dtype=torch.int64, device=src.device) - torch.repeat_interleave(
+        torch.cumsum(seg_len, 0) - seg_len, seg_len)
+    dst[base_dst + src_idx + within] = src[src_idx + within]
+
+
 def combine_ids(local_offsets, local_ids, group=None):
     """Rank-ordered merge of per-rank id lists.
 
     ``local_offsets`` int64[nq+1] and ``local_ids`` (global ids of this rank's
     shard, ascending per query) -> (offsets int64[nq+1], ids) identical on
-    every rank.  Because shards are contiguous and ranks are ordered, the
-    concatenation in rank order is ascending: the reference's concat + sort
-    (scan.py:160, parallel.py:156-157) without the sort.
+    every rank (NCCL all_gather of the padded slices + one placement kernel).
     """
     import torch
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
+    world = dist_world(group)
     dev = local_ids.device
     local_offsets = local_offsets.to(device=dev, dtype=torch.int64)
     counts = local_offsets[1:] - local_offsets[:-1]
-    nq = counts.numel()
     all_counts = _all_gather(counts.contiguous(), world, group)
-    totals = all_counts.sum(1)                      # ids per rank
-    per_query = all_counts.sum(0)                   # ids per query
-    out_offsets = torch.zeros(nq + 1, dtype=torch.int64, device=dev)
-    torch.cumsum(per_query, 0, out=out_offsets[1:])
-    # rank r's segment of query q starts after ranks < r
-    rank_prefix = torch.cumsum(all_counts, 0) - all_counts       # [world, nq]
-    maxlen = int(totals.max().item()) if world else 0
-    ids_dtype = local_ids.dtype
-    padded = torch.zeros(max(maxlen, 1), dtype=ids_dtype, device=dev)
-    nloc = local_ids.numel()
-    if nloc:
-        padded[:nloc] = local_ids
+    out_offsets, rank_prefix = global_layout(all_counts)
+    maxlen = int(all_counts.sum(1).max().item()) if world else 0
+    padded = torch.zeros(max(maxlen, 1), dtype=local_ids.dtype, device=dev)
+    if local_ids.numel():
+        padded[:local_ids.numel()] = local_ids
     gathered = _all_gather(padded, world, group)
-    total = int(out_offsets[-1].item())
-    out = torch.empty(total, dtype=ids_dtype, device=dev)
-    if dev.type == "cuda" and ids_dtype.itemsize == 4:
-        # one segmented-copy kernel (mdrq_copy_segments): segment (r, q) is
-        # rank r's slice of query q
-        import ctypes
-        from . import _lib
-        loff = torch.cumsum(all_counts, 1) - all_counts                 # [world, nq] within rank r
-        stride = gathered.shape[1]
-        src_off = (loff + torch.arange(world, device=dev, dtype=torch.int64)[:, None] * stride).contiguous()
-        dst_off = (out_offsets[:-1][None, :] + rank_prefix).contiguous()
-        seg_len = all_counts.contiguous()
-        if total:
-            _lib.check(_lib.load().mdrq_copy_segments(
-                ctypes.c_void_p(gathered.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                ctypes.c_void_p(src_off.data_ptr()), ctypes.c_void_p(dst_off.data_ptr()),
-                ctypes.c_void_p(seg_len.data_ptr()), world * nq,
-                ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
-        return out_offsets, out
+    out = torch.empty(int(out_offsets[-1].item()), dtype=local_ids.dtype, device=dev)
+    stride = gathered.shape[1]
     for r in range(world):
-        tr = int(totals[r].item())
-        if tr == 0:
-            continue
-        c = all_counts[r]
-        loff = torch.zeros(nq, dtype=torch.int64, device=dev)
-        if nq > 1:
-            torch.cumsum(c[:-1], 0, out=loff[1:])
-        # destination of local element i of query q: out_off[q] + prefix[r,q] + (i - loff[q])
-        base = torch.repeat_interleave(out_offsets[:-1] + rank_prefix[r] - loff, c)
-        dst = base + torch.arange(tr, dtype=torch.int64, device=dev)
-        out[dst] = gathered[r, :tr]
+        src_off, dst_off, seg = rank_segments(all_counts, r, out_offsets, rank_prefix)
+        _place_segments(gathered.reshape(-1)[r * stride:(r + 1) * stride], out, src_off, dst_off, seg)
     return out_offsets, out
 
 
-class ShardedScan:
-    """One rank's part of a row-sharded scan over W GPUs (one process each).
+def dist_world(group=None) -> int:
+    import torch.distributed as dist
+    return dist.get_world_size(group)
 
-    ``values`` is this rank's shard (rows [start, stop) of the dataset);
-    results of ``count_batch`` / ``search_batch`` are global and identical on
-    every rank.
+
+class SharedHostBuffer:
+    """One host buffer mapped by every rank of the node (POSIX shared
+    memory), registered with CUDA in every rank that has a device, so each
+    rank's kernel writes its slices straight into it over its own PCIe link
+    (rank-ordered offsets; no NCCL exchange of the ids, no second copy)."""
+
+    def __init__(self, nbytes: int, group=None, device: int | None = None):
+        import torch.distributed as dist
+        from multiprocessing import shared_memory
+        self.nbytes = max(int(nbytes), 1)
+        rank = dist.get_rank(group)
+        name = [None]
+        if rank == 0:
+            self._shm = shared_memory.SharedMemory(create=True, size=self.nbytes)
+            name = [self._shm.name]
+        dist.broadcast_object_list(name, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        if rank != 0:
+            self._shm = shared_memory.SharedMemory(name=name[0])
+        self.group = group
+        self.rank = rank
+        self._registered = False
+        import numpy as _np
+        self._arr = _np.ndarray((self.nbytes,), _np.uint8, buffer=self._shm.buf)
+        if device is not None:
+            import torch
+            rc = torch.cuda.cudart().cudaHostRegister(self._arr.ctypes.data, self.nbytes, 3)  # portable | mapped
+            if int(rc) != 0:
+                raise RuntimeError(f"cudaHostRegister failed ({rc})")
+            self._registered = True
+        dist.barrier(group)
+
+    @property
+    def ptr(self) -> int:
+        return int(self._arr.ctypes.data)
+
+    def view(self, dtype, count: int):
+        import numpy as _np
+        return _np.ndarray((int(count),), dtype, buffer=self._shm.buf)
+
+    def close(self):
+        import torch.distributed as dist
+        if getattr(self, "_shm", None) is None:
+            return
+        if self._registered:
+            import torch
+            torch.cuda.cudart().cudaHostUnregister(self._arr.ctypes.data)
+            self._registered = False
+        self._arr = None
+        dist.barrier(self.group)
+        self._shm.close()
+        if self.rank == 0:
+            self._shm.unlink()
+        self._shm = None
+
+
+def gather_ids_to_host(local_offsets, local_ids, group=None, out: SharedHostBuffer | None = None):
+    """Merged ids of every rank in ONE host buffer, written by the ranks
+    themselves: the per-query counts are all_gathered (8 B per query and
+    rank), every rank computes where its slice of each query goes and copies
+    it there (on a GPU: one placement kernel into the registered shared host
+    buffer, i.e. each rank's own PCIe link; on CPU: torch indexing).
+    -> (offsets int64[nq+1] numpy, ids uint32 numpy view of the shared
+    buffer, the buffer).  Rank order = id order, so no sort."""
+    import numpy as _np
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = local_ids.device
+    local_offsets = local_offsets.to(device=dev, dtype=torch.int64)
+    counts = local_offsets[1:] - local_offsets[:-1]
+    all_counts = _all_gather(counts.contiguous(), world, group)
+    out_offsets, rank_prefix = global_layout(all_counts)
+    total = int(out_offsets[-1].item())
+    buf = out if out is not None else SharedHostBuffer(4 * total, group,
+                                                       device=dev.index if dev.type == "cuda" else None)
+    if buf.nbytes < 4 * total:
+        raise ValueError(f"host buffer holds {buf.nbytes // 4} ids, the merge needs {total}")
+    src_off, dst_off, seg = rank_segments(all_counts, rank, out_offsets, rank_prefix)
+    if dev.type == "cuda":
+        _place_segments(local_ids, buf.ptr, src_off, dst_off, seg)
+        torch.cuda.current_stream(dev).synchronize()
+    else:
+        host = torch.from_numpy(buf.view(_np.int32, total)) if total else torch.empty(0, dtype=torch.int32)
+        _place_segments(local_ids.to(torch.int32), host, src_off, dst_off, seg)
+    dist.barrier(group)
+    return out_offsets.cpu().numpy(), buf.view(_np.uint32, total), buf
+
+
+class ShardedScan:
+    """One rank's part of a row-sharded scan over W GPUs (one process each),
+    the analog of the reference's PartitionedIndex (parallel.py:126-167):
+    fan-out = every rank scans its contiguous shard, fan-in = the rank-ordered
+    merge (no sort).  Results of ``count_batch`` / ``search_batch`` are
+    global and identical on every rank; ``search_batch_host`` leaves the
+    merged ids in one node-shared host buffer written by every rank directly.
+
+    ``store`` may be any object with the DeviceStore query interface (the
+    gloo tests inject the CPU oracle scan of the shard); by default a
+    DeviceStore over ``shard_values`` with ``id_base`` = the shard start.
     """
 
     def __init__(self, shard_values, start: int, n_total: int, *, group=None, path: str = "auto",
-                 layouts=None, va_bits: int = 8, device: int | None = None):
+                 layouts=None, va_bits: int = 8, device: int | None = None, store=None):
         from . import _lib
         from .store import DeviceStore
         self.group = group
         self.start = int(start)
         self.n_total = int(n_total)
         self.path = path
-        if layouts is None:
-            layouts = _lib.LAYOUT_COLUMNAR
-        self.store = DeviceStore(shard_values, layouts=layouts, va_bits=va_bits, device=device,
-                                 id_base=self.start)
-        self.m = self.store.m
+        if store is None:
+            if layouts is None:
+                layouts = _lib.LAYOUT_COLUMNAR | _lib.LAYOUT_VAFILE
+            store = DeviceStore(shard_values, layouts=layouts, va_bits=va_bits, device=device, id_base=self.start)
+        self.store = store
+        self.m = store.m
+
+    def _comm_device(self):
+        import torch
+        import torch.distributed as dist
+        if dist.get_backend(self.group) == "nccl":
+            return torch.device("cuda", self.store.device)
+        return torch.device("cpu")
 
     def count_batch(self, lower, upper, path: str | None = None):
         import torch
         local = self.store.count(lower, upper, path or self.path)
-        dev = torch.device("cuda", self.store.device)
-        return combine_counts(torch.as_tensor(local, device=dev), self.group).cpu().numpy()
+        return combine_counts(torch.as_tensor(local, device=self._comm_device()), self.group).cpu().numpy()
+
+    def _local(self, lower, upper, path):
+        """This shard's result as tensors on the communication device; on a
+        GPU the ids stay in HBM (a prepared batch, its pool read in place)."""
+        import torch
+        dev = self._comm_device()
+        if dev.type == "cuda" and hasattr(self.store, "prepare"):
+            b = self.store.prepare(lower, upper, path or self.path)
+            try:
+                total = b.reserve()
+                d_ids, d_offs, _ = b.result_device()
+                ids = _wrap_device(d_ids, total, torch.int32, dev).clone()
+                offs = _wrap_device(d_offs, b.nq + 1, torch.int64, dev).clone()
+            finally:
+                b.close()
+            return offs, ids
+        offs, ids = self.store.ids(lower, upper, path or self.path)
+        return (torch.as_tensor(np.asarray(offs, np.int64), device=dev),
+                torch.as_tensor(np.asarray(ids).astype(np.int32, copy=False), device=dev))
 
     def search_batch(self, lower, upper, path: str | None = None):
-        import torch
-        offs, ids = self.store.ids(lower, upper, path or self.path)
-        dev = torch.device("cuda", self.store.device)
-        o, i = combine_ids(torch.as_tensor(offs, device=dev),
-                           torch.as_tensor(ids.astype(np.int64), device=dev), self.group)
-        return o.cpu().numpy(), i.cpu().numpy()
+        """-> (offsets int64[nq+1], ids uint32), the whole table's result."""
+        offs, ids = self._local(lower, upper, path)
+        o, i = combine_ids(offs, ids, self.group)
+        return o.cpu().numpy(), i.cpu().numpy().view(np.uint32)
+
+    def search_batch_host(self, lower, upper, path: str | None = None, out: SharedHostBuffer | None = None):
+        """-> (offsets, ids uint32 view of the shared host buffer, buffer):
+        every rank writes its own slices (SharedHostBuffer); the caller
+        closes the buffer when done with the ids."""
+        offs, ids = self._local(lower, upper, path)
+        return gather_ids_to_host(offs, ids, self.group, out)
 
     def close(self):
         self.store.close()
+
+
+def _wrap_device(ptr: int, count: int, dtype, dev):
+    """Device pointer -> torch tensor (no copy)."""
+    import torch
+    typestr = {torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr, "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_CAI(), device=dev)

@@ -226,3 +226,20 @@ def test_va_swar_range_test_exhaustive():
     flags = sum(((f >> np.uint32(i)) & 1) << np.uint32(8 * i + 7) for i in range(4))
     nib = ((((flags >> np.uint32(7)) & np.uint32(0x01010101)) * np.uint32(0x00204081)) >> np.uint32(21)) & 15
     assert np.array_equal(nib, f)
+
+
+def test_verify_ground_truth_on_cpu():
+    """cli.ground_truth: the reference's SequentialScan(SCALAR) when the
+    reference is importable (baseline/_ref), else numpy containment; both
+    equal the C oracle's ids (no device involved)."""
+    import os
+    import oracle
+    from paper_1801_03644_b200.cli import ground_truth
+    from paper_1801_03644_b200.workload import GeneratorSpec, gen_dataset, pair_query_batch
+    from conftest import ROOT
+    data = gen_dataset(GeneratorSpec("uniform", 5000, 4, seed=3))
+    queries = pair_query_batch(data, 20, 4)
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/nonexistent"):
+        exp, src = ground_truth(data, queries, path)
+        for q, e in zip(queries, exp):
+            assert np.array_equal(e, oracle.brute_ids(data.values, q.lower, q.upper)), src

@@ -115,3 +115,78 @@ def test_rank_ordered_merge_equals_whole_scan(world, n):
             if p.is_alive():
                 p.kill()
     assert len(results) == world and all(ok for _, ok in results), results
+
+
+class _OracleShardStore:
+    """The DeviceStore query interface over one row shard, answered by the
+    CPU oracle (the gloo stand-in for a rank's device store; ids global)."""
+
+    def __init__(self, values, start):
+        self.values, self.start = values, start
+        self.m = values.shape[1]
+        self.device = 0
+
+    def count(self, lo, hi, path="auto"):
+        return oracle.count_batch(self.values, lo, hi)
+
+    def ids(self, lo, hi, path="auto"):
+        offs, ids = oracle.ids_batch(self.values, lo, hi)
+        return offs, (ids + self.start).astype(np.uint32)
+
+    def close(self):
+        pass
+
+
+def _sharded_worker(rank, world, port, n, m, nq, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1801_03644_b200.parallel import ShardedScan
+        rng = np.random.default_rng(seed)
+        values = rng.random((n, m), dtype=np.float32)
+        w = 0.4 ** (1 / m)
+        lo = rng.uniform(0, 1 - w, (nq, m)).astype(np.float32)
+        hi = (lo + w).astype(np.float32)
+        lo[1, 1:], hi[1, 1:] = -np.inf, np.inf     # partial match
+        lo[2], hi[2] = 5.0, 6.0                     # empty
+        start, stop = shard_range(n, world, rank)
+        scan = ShardedScan(values[start:stop], start, n, store=_OracleShardStore(values[start:stop], start))
+        exp_offs, exp_ids = oracle.ids_batch(values, lo, hi)
+        ok = np.array_equal(scan.count_batch(lo, hi), np.diff(exp_offs))
+        o, i = scan.search_batch(lo, hi)
+        ok &= np.array_equal(o, exp_offs) and np.array_equal(i.astype(np.int64), exp_ids)
+        # every rank writes its own slices into one node-shared host buffer
+        o2, i2, buf = scan.search_batch_host(lo, hi)
+        ok &= np.array_equal(o2, exp_offs) and np.array_equal(i2.astype(np.int64), exp_ids)
+        del i2
+        buf.close()
+        q.put((rank, bool(ok)))
+    except Exception as e:   # report instead of hanging the parent
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 30_001), (3, 1_000), (2, 1)])
+def test_sharded_scan_end_to_end_on_gloo(world, n):
+    """ShardedScan (PartitionedIndex analog, parallel.py:126-167): counts,
+    the NCCL-style merge and the direct per-rank host write all equal the
+    oracle scan of the whole table."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, n, 5, 12, 11 + n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = []
+    try:
+        for _ in procs:
+            results.append(q.get(timeout=180))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert len(results) == world and all(ok is True for _, ok in results), results
