@@ -22,10 +22,17 @@ namespace {
 
 constexpr int SCAN_THREADS = 1024;
 
+// CHAIN: one query, its output base chained from the previous query's.
+// Otherwise CTA y scans query q + y's counts (at chunk_counts + y * nchunks)
+// and only reports its total (pass_offsets_kernel chains the bases).
+template <bool CHAIN>
 __global__ void __launch_bounds__(SCAN_THREADS) chunk_scan_kernel(const uint32_t* __restrict__ chunk_counts,
                                                                   uint32_t nchunks, uint32_t* __restrict__ chunk_offs,
                                                                   unsigned long long* offsets,
                                                                   unsigned long long* counts, uint32_t q) {
+    chunk_counts += uint64_t(blockIdx.x) * nchunks;
+    chunk_offs += uint64_t(blockIdx.x) * nchunks;
+    q += blockIdx.x;
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_carry;
     if (threadIdx.x == 0) s_carry = 0;
@@ -61,19 +68,39 @@ __global__ void __launch_bounds__(SCAN_THREADS) chunk_scan_kernel(const uint32_t
     }
     if (threadIdx.x == 0) {
         const unsigned long long total = s_carry;
-        offsets[q + 1] = offsets[q] + total;
+        if (CHAIN) offsets[q + 1] = offsets[q] + total;
         counts[q] = total;
     }
 }
 
+// offsets[q0 + 1 + i] = offsets[q0] + counts[q0] + ... + counts[q0 + i], i < nqp <= 32
+__global__ void pass_offsets_kernel(const unsigned long long* __restrict__ counts, uint32_t nqp,
+                                    unsigned long long* offsets, uint32_t q0) {
+    const uint32_t lane = threadIdx.x;
+    unsigned long long incl = lane < nqp ? counts[q0 + lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= uint32_t(o)) incl += t;
+    }
+    const unsigned long long base = offsets[q0];
+    if (lane < nqp) offsets[q0 + 1 + lane] = base + incl;
+}
+
 // one CTA per 65536-tuple chunk: 256 threads x 8 consecutive mask words
+// blockIdx.y selects query q + y of a multi-query pass (mask and chunk
+// offsets at y * mask_stride / y * coff_stride)
 __global__ void __launch_bounds__(256) expand_kernel(const uint32_t* __restrict__ mask, uint64_t n,
                                                      const uint32_t* __restrict__ chunk_offs,
                                                      const unsigned long long* __restrict__ offsets, uint32_t q,
-                                                     uint32_t* __restrict__ ids, uint64_t cap, uint32_t id_base) {
+                                                     uint32_t* __restrict__ ids, uint64_t cap, uint32_t id_base,
+                                                     uint64_t mask_stride, uint32_t coff_stride) {
     constexpr int WPT = kChunkTuples / 32 / 256;   // words per thread
     __shared__ uint32_t s_warp[8];
     const uint32_t chunk = blockIdx.x;
+    mask += blockIdx.y * mask_stride;
+    chunk_offs += uint64_t(blockIdx.y) * coff_stride;
+    q += blockIdx.y;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t w0 = uint64_t(chunk) * (kChunkTuples / 32) + uint64_t(threadIdx.x) * WPT;
     const uint64_t nwords = (n + 31) / 32;
@@ -155,8 +182,21 @@ void launch_reduce_partials(const unsigned long long* partials, uint32_t nq, boo
 void launch_expand(const ScanArgs& a, cudaStream_t st) {
     const uint32_t nchunks = uint32_t((a.n + kChunkTuples - 1) / kChunkTuples);
     if (!nchunks) return;
-    chunk_scan_kernel<<<1, SCAN_THREADS, 0, st>>>(a.chunk_counts, nchunks, a.chunk_offs, a.offsets, a.counts, a.q);
-    expand_kernel<<<nchunks, 256, 0, st>>>(a.mask, a.n, a.chunk_offs, a.offsets, a.q, a.ids, a.ids_cap, a.id_base);
+    chunk_scan_kernel<true><<<1, SCAN_THREADS, 0, st>>>(a.chunk_counts, nchunks, a.chunk_offs, a.offsets, a.counts,
+                                                        a.q);
+    expand_kernel<<<nchunks, 256, 0, st>>>(a.mask, a.n, a.chunk_offs, a.offsets, a.q, a.ids, a.ids_cap, a.id_base, 0,
+                                           0);
+}
+
+void launch_expand_pass(const ScanArgs& a, uint32_t q0, uint32_t nqp, const uint32_t* masks, uint64_t mask_words,
+                        const uint32_t* chunk_counts, uint32_t* chunk_offs, cudaStream_t st) {
+    const uint32_t nchunks = uint32_t((a.n + kChunkTuples - 1) / kChunkTuples);
+    if (!nchunks || !nqp) return;
+    chunk_scan_kernel<false><<<nqp, SCAN_THREADS, 0, st>>>(chunk_counts, nchunks, chunk_offs, a.offsets, a.counts,
+                                                           q0);
+    pass_offsets_kernel<<<1, 32, 0, st>>>(a.counts, nqp, a.offsets, q0);
+    expand_kernel<<<dim3(nchunks, nqp), 256, 0, st>>>(masks, a.n, chunk_offs, a.offsets, q0, a.ids, a.ids_cap,
+                                                      a.id_base, mask_words, nchunks);
 }
 
 }  // namespace mdrq

@@ -159,6 +159,15 @@ void launch_row_scan(const ScanArgs& a, bool ids, cudaStream_t st);
 void launch_va_scan(const ScanArgs& a, bool ids, cudaStream_t st);
 void launch_expand(const ScanArgs& a, cudaStream_t st);
 void launch_col_batch_count(const BatchArgs& a, int num_sms, cudaStream_t st);
+// ids mode of the multi-query columnar pass: masks [nqp][mask_words] (one bit
+// per tuple, query-major) + chunk_counts [nqp][n / kChunkTuples rounded up]
+void launch_col_batch_ids(const BatchArgs& a, uint32_t* masks, uint64_t mask_words, uint32_t* chunk_counts,
+                          int num_sms, cudaStream_t st);
+// expansion of a multi-query pass's masks into ascending ids at the batch
+// offsets (a.offsets[q0] must hold the pass's base): chunk scans per query,
+// the pass's offsets, one expand grid (chunks x queries)
+void launch_expand_pass(const ScanArgs& a, uint32_t q0, uint32_t nqp, const uint32_t* masks, uint64_t mask_words,
+                        const uint32_t* chunk_counts, uint32_t* chunk_offs, cudaStream_t st);
 int col_batch_max_dims();
 uint32_t col_batch_padded_dims(uint32_t kb);   // union dims the kernel evaluates
 uint32_t row_tile_rows(uint32_t m);

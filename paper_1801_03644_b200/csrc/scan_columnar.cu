@@ -12,6 +12,8 @@
 // col_scan_kernel        one query per launch, dimension-at-a-time (HBM bound)
 // col_batch_count_kernel up to 32 queries per pass over the union of their
 //                        dimensions, every column byte read once per pass
+// col_batch_ids_kernel   the same pass in ids mode: one verdict bitmask per
+//                        query + per-chunk counts, expanded by expand.cu
 #include <utility>
 
 #include "launch.h"
@@ -155,6 +157,63 @@ __global__ void __launch_bounds__(256) col_batch_count_kernel(const BatchArgs a)
         atomicAdd(a.counts + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
 }
 
+// ---------------------------------------------------------------------------
+// Multi-query ids pass (VerticalScan.search over a batch, scan.py:190-211,
+// with the column bytes read once per <= 32 queries).  A CTA owns whole
+// 65536-tuple compaction chunks (grid-stride); each of its 8 warps takes 32
+// consecutive tuples per step, one tuple per lane (128-byte coalesced loads
+// of every union column; the NaN padding up to n_pad never matches).  The
+// pass's queries are walked with their bounds broadcast from shared memory:
+// query q's verdicts of the warp's 32 tuples are one ballot, kept by lane q,
+// which stores it as word t/32 of query q's mask (query-major, the layout the
+// single-query expansion reads) and adds its popcount to q's chunk count.
+// No atomics leave the CTA: every chunk count is written once.
+template <int KB>
+__global__ void __launch_bounds__(256) col_batch_ids_kernel(const BatchArgs a, uint32_t* __restrict__ masks,
+                                                            uint64_t mask_words, uint32_t* __restrict__ chunk_counts,
+                                                            uint32_t nchunks) {
+    __shared__ float2 s_b[32][KB];
+    __shared__ uint32_t s_cnt[32];
+    __shared__ uint16_t s_ud[KB];
+    const uint32_t nqp = a.nqp;
+    for (uint32_t i = threadIdx.x; i < nqp * KB; i += blockDim.x) s_b[i / KB][i % KB] = a.bounds[i];
+    for (uint32_t i = threadIdx.x; i < KB; i += blockDim.x) s_ud[i] = a.udims[i];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    for (uint32_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+        if (threadIdx.x < 32) s_cnt[threadIdx.x] = 0;
+        __syncthreads();
+        uint32_t acc = 0;
+        const uint64_t c0 = uint64_t(chunk) * kChunkTuples;
+        const uint64_t c1 = c0 + kChunkTuples < a.n ? c0 + kChunkTuples : a.n;
+        for (uint64_t t0 = c0 + warp * 32; t0 < c1; t0 += 256) {
+            // t0 < n <= n_pad and n_pad is a multiple of 32: the whole warp
+            // reads inside the padded columns
+            float v[KB];
+#pragma unroll
+            for (int d = 0; d < KB; ++d) v[d] = __ldcs(a.cols + uint64_t(s_ud[d]) * a.stride + t0 + lane);
+            uint32_t mine = 0;
+            for (uint32_t q = 0; q < nqp; ++q) {
+                bool ok = true;
+#pragma unroll
+                for (int d = 0; d < KB; ++d) {
+                    const float2 b = s_b[q][d];
+                    ok = ok && (b.x <= v[d]) && (v[d] <= b.y);
+                }
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ok);
+                if (lane == q) mine = bal;
+            }
+            if (lane < nqp) {
+                masks[uint64_t(lane) * mask_words + t0 / 32] = mine;
+                acc += __popc(mine);
+            }
+        }
+        if (acc) atomicAdd(&s_cnt[lane], acc);
+        __syncthreads();
+        if (threadIdx.x < nqp) chunk_counts[uint64_t(threadIdx.x) * nchunks + chunk] = s_cnt[threadIdx.x];
+        __syncthreads();   // s_cnt is reset for the next chunk
+    }
+}
+
 template <int KB, int TPT>
 void run_batch(const BatchArgs& a, int num_sms, cudaStream_t st) {
     static int blocks_per_sm = -1;
@@ -176,7 +235,39 @@ void dispatch_exact(const BatchArgs& a, int num_sms, cudaStream_t st, std::integ
     ((a.kb == uint32_t(Ks + 1) ? run_batch<Ks + 1, 4>(a, num_sms, st) : void()), ...);
 }
 
+template <int KB>
+void run_batch_ids(const BatchArgs& a, uint32_t* masks, uint64_t mask_words, uint32_t* chunk_counts, int num_sms,
+                   cudaStream_t st) {
+    static int blocks_per_sm = -1;
+    if (blocks_per_sm < 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, col_batch_ids_kernel<KB>, 256, 0);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const uint32_t nchunks = uint32_t((a.n + kChunkTuples - 1) / kChunkTuples);
+    uint64_t grid = uint64_t(num_sms) * blocks_per_sm;
+    if (grid > nchunks) grid = nchunks;
+    if (grid == 0) return;
+    col_batch_ids_kernel<KB><<<unsigned(grid), 256, 0, st>>>(a, masks, mask_words, chunk_counts, nchunks);
+}
+
+template <int... Ks>
+void dispatch_ids(const BatchArgs& a, uint32_t* masks, uint64_t mask_words, uint32_t* chunk_counts, int num_sms,
+                  cudaStream_t st, std::integer_sequence<int, Ks...>) {
+    ((a.kb == uint32_t(Ks + 1) ? run_batch_ids<Ks + 1>(a, masks, mask_words, chunk_counts, num_sms, st) : void()),
+     ...);
+}
+
 }  // namespace
+
+void launch_col_batch_ids(const BatchArgs& a, uint32_t* masks, uint64_t mask_words, uint32_t* chunk_counts,
+                          int num_sms, cudaStream_t st) {
+    if (a.kb <= 16)
+        dispatch_ids(a, masks, mask_words, chunk_counts, num_sms, st, std::make_integer_sequence<int, 16>{});
+    else if (a.kb == 32)
+        run_batch_ids<32>(a, masks, mask_words, chunk_counts, num_sms, st);
+    else
+        run_batch_ids<64>(a, masks, mask_words, chunk_counts, num_sms, st);
+}
 
 void launch_col_scan(const ScanArgs& a, bool ids, cudaStream_t st) {
     if (a.num_tiles == 0) return;

@@ -244,6 +244,9 @@ struct mdrq_store {
     DBuf<uint64_t> status;
     uint32_t epoch = 0;
     DBuf<uint32_t> mask;             // ids mode: verdict bitmask of one query
+    // multi-query columnar ids pass: [32][mask words] masks, [32][chunks]
+    // chunk counts / offsets (allocated on first use)
+    DBuf<uint32_t> bmask, bchunk_counts, bchunk_offs;
     DBuf<uint32_t> chunk_counts, chunk_offs;
     uint32_t nchunks = 0;
     // bit-sliced VA batch scratch ([chunks][1024] per pass)
@@ -628,7 +631,10 @@ uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids)
         if (!(s->layouts & MDRQ_LAYOUT_COLUMNAR)) return MDRQ_PATH_ROWWISE;
         if (va && nq >= 10) return MDRQ_PATH_VAFILE_BATCH;
         if (va) return MDRQ_PATH_VAFILE;
-        if (!ids && nq >= 2) return MDRQ_PATH_COLUMNAR_BATCH;
+        // multi-query columnar pass (<= 32 queries per read of the union's
+        // columns): counts from 2 queries, ids from 4 (its masks + expansion
+        // cost about one single-query scan)
+        if (nq >= (ids ? 4u : 2u)) return MDRQ_PATH_COLUMNAR_BATCH;
         return MDRQ_PATH_COLUMNAR;
     }
     switch (path) {
@@ -880,7 +886,15 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
                 launches += 6;
             }
         }
-    } else if (path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
+    } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
+        // ids: query-major masks (word count a multiple of 4: 16-byte rows)
+        const uint64_t mask_words = round_up(s->n_pad / 32, 4);
+        const uint32_t nch = uint32_t((s->n + kChunkTuples - 1) / kChunkTuples);
+        if (ids) {
+            s->bmask.reserve(32 * mask_words);
+            s->bchunk_counts.reserve(size_t(32) * nch);
+            s->bchunk_offs.reserve(size_t(32) * nch);
+        }
         for (const Pass& ps : b->passes) {
             if (ps.fallback) {
                 for (uint32_t q = ps.q0; q < ps.q0 + ps.nqp; ++q) single(MDRQ_PATH_COLUMNAR, q);
@@ -897,8 +911,16 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
             ba.cmask = b->d_cmask.p + ps.cmask_off;
             ba.counts = b->d_counts.p + ps.q0;
             mark(0, 1);
-            launch_col_batch_count(ba, s->num_sms, st);
-            ++launches;
+            if (!ids) {
+                launch_col_batch_count(ba, s->num_sms, st);
+                ++launches;
+                continue;
+            }
+            launch_col_batch_ids(ba, s->bmask.p, mask_words, s->bchunk_counts.p, s->num_sms, st);
+            mark(1, 3);
+            launch_expand_pass(base_args(s, b, MDRQ_PATH_COLUMNAR), ps.q0, ps.nqp, s->bmask.p, mask_words,
+                               s->bchunk_counts.p, s->bchunk_offs.p, st);
+            launches += 4;
         }
     } else {
         const uint32_t sp = path == MDRQ_PATH_COLUMNAR_BATCH ? MDRQ_PATH_COLUMNAR : path;
@@ -926,11 +948,11 @@ uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
         }
         return l + (single ? 1 : 0);
     }
-    if (b->path == MDRQ_PATH_COLUMNAR_BATCH && !ids) {
+    if (b->path == MDRQ_PATH_COLUMNAR_BATCH) {
         uint32_t l = 0;
         bool single = false;
         for (const Pass& ps : b->passes) {
-            l += ps.fallback ? ps.nqp : 1;
+            l += ps.fallback ? ps.nqp * (ids ? 3 : 1) : (ids ? 4 : 1);
             single |= ps.fallback;
         }
         return l + (single ? 1 : 0);

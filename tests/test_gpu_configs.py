@@ -57,7 +57,7 @@ def test_c2_vs_reference_golden(c2_store):
                 assert sha1_ids(ids[offs[i]:offs[i + 1]]) == G[f"level{li}_sha1"][i].tobytes(), (s, path, i)
 
 
-def _every_query(st, lo, hi, counts, hashes, name, single=500, single_paths=("columnar", "vafile")):
+def _every_query(st, lo, hi, counts, hashes, name, single=500, single_paths=("columnar", "vafile", "columnar_batch")):
     """Every query on the planner's batch path (ids: count + hash; count
     mode: counts) and a stratified sample on the single-query paths."""
     c, h, path = batch_hashes(st, lo, hi, "auto")
