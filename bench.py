@@ -334,7 +334,9 @@ def main():
     sptr = stream.cuda_stream
     assert sptr != 0
 
+    t_prep = time.perf_counter()
     batch = store.prepare(lo, hi, args.path)
+    t_prep = time.perf_counter() - t_prep
     binfo = batch.info()
     total_local = batch.reserve()
     launches_ids = batch.launches(ids=True)
@@ -514,7 +516,8 @@ def main():
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
             "reference_methods": ref_methods,
-            "setup_s": {"generate": round(t_gen, 2), "store_build": round(t_build, 2)},
+            "setup_s": {"generate": round(t_gen, 2), "store_build": round(t_build, 2),
+                        "prepare_batch": round(t_prep, 3)},
         }
         print(json.dumps(line), flush=True)
     if not (not args.no_paths and world == 1):
@@ -543,7 +546,8 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
               for _ in range(nbuf)]
     pin_s = time.perf_counter() - t0
     e2e_steps = max(3, min(args.steps, 10))
-    store.ids_stream([(lo, hi)] * 2, args.path, outs=[pinned[k % nbuf] for k in range(2)])   # warm
+    # warm: every slot of the stream (3) sizes its result pool once
+    store.ids_stream([(lo, hi)] * 3, args.path, outs=[pinned[k % nbuf] for k in range(3)])
     info = {}
     if world > 1:
         dist.barrier()

@@ -273,6 +273,7 @@ struct mdrq_store {
     // pipelined ids stream: a copy stream + slots, created on first use
     cudaStream_t copy_stream = nullptr;
     StreamSlot* slots = nullptr;
+    uint64_t stream_hint = 0;        // largest batch total seen by the stream (pre-sizes fresh slot pools)
     // pinned bounce buffer of the synchronous ids calls: the offsets, the VA
     // overflow flag and a speculative prefix of the ids come back in one
     // copy + one synchronisation; bounce_ids = ids of the last call held in
@@ -1466,7 +1467,11 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             mdrq_batch* b = &sl.b;
             const uint32_t nq = nqs[k];
             build_descs(s, lower + q0[k] * s->m, upper + q0[k] * s->m, nq, resolve_path(s, path, nq, true), true, b);
-                upload_batch(s, b, false);
+            upload_batch(s, b, false);
+            // a slot's pool starts at the size of the largest batch seen so
+            // far: a fresh slot must not run its first batch twice
+            if (s->stream_hint && (!b->own_ids.p || b->own_ids.cap < s->stream_hint))
+                b->own_ids.reserve(size_t(s->stream_hint + s->stream_hint / 8 + 4096));
             up += upload_bytes(b);
             enqueue(s, b, true, s->stream);
             sl.h_flags[0] = sl.h_flags[1] = 0;
@@ -1496,6 +1501,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
                 CK(cudaEventRecord(sl.comp, s->stream));
             }
             totals[k] = total;
+            s->stream_hint = std::max<uint64_t>(s->stream_hint, total);
             CK(cudaStreamWaitEvent(s->copy_stream, sl.comp, 0));
             if (nq && s->n)
                 CK(cudaMemcpyAsync(offsets_out[k], b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
