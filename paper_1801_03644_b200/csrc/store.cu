@@ -704,7 +704,14 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     // < 65536 tuples (16-bit per-warp counters), identical in every mode
     a.grid = uint32_t(s->num_sms);
     const uint64_t warps = uint64_t(a.grid) * va_batch_warps();
-    a.chunk_tuples = std::min<uint64_t>(65408, round_up((s->n + warps - 1) / warps, 128));
+    // k groups per CTA with k the smallest that keeps a subchunk under the
+    // 16-bit counter limit: the groups divide evenly over the CTAs (C5 on
+    // one GPU: 4 groups of 52 864-tuple subchunks per CTA; capping the
+    // subchunk at 65 408 tuples instead gave 478 groups over 148 CTAs, i.e.
+    // 4 rounds for some SMs and 3 for others, ~20 % of the SMs idle)
+    const uint64_t per_warp = (s->n + warps - 1) / warps;
+    const uint64_t k = std::max<uint64_t>(1, (per_warp + 65407) / 65408);
+    a.chunk_tuples = std::min<uint64_t>(65408, round_up((s->n + warps * k - 1) / (warps * k), 128));
     a.nchunks = uint32_t((s->n + a.chunk_tuples - 1) / a.chunk_tuples);
     a.ngroups = (a.nchunks + va_batch_warps() - 1) / va_batch_warps();
     const uint64_t chunks = a.nchunks;
