@@ -139,6 +139,13 @@ struct VaBatchArgs {
     uint32_t* cursor;            // block allocator
     uint32_t* overflow;          // set when the staging pool ran out (mode 2 then runs)
     uint32_t max_blocks;
+    // tuple pruning (multi-word passes): bit c of cellmask[u] = some query of
+    // the pass overlaps table cell c of union dim u; a tuple whose cell is
+    // clear in any dim of prune_dims cannot match and is skipped before its
+    // table rows are read (the host sorts a batch's queries into passes so
+    // these masks are sparse, store.cu build_vb_passes)
+    uint32_t prune_dims;         // bit u: cellmask[u] is not all ones
+    unsigned long long cellmask[kVaBatchMaxDims];
 };
 constexpr uint32_t kRecBlock = 1024;
 constexpr uint32_t kNoBlock = 0xFFFFFFFFu;
@@ -150,6 +157,12 @@ void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st);
 void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st);
 void launch_va_batch_scans(const VaBatchArgs& a, uint32_t q0, cudaStream_t st);
 void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st);
+// sorted batches: slot-order counts / offsets / ids back to query order;
+// returns the number of kernels launched
+uint32_t launch_va_batch_unpermute(const uint32_t* perm, const unsigned long long* counts_p,
+                                   const unsigned long long* offsets_p, unsigned long long* counts,
+                                   unsigned long long* offsets, const uint32_t* ids_p, uint32_t* ids, uint64_t cap,
+                                   uint32_t nq, bool with_ids, int num_sms, cudaStream_t st);
 
 constexpr int kColTile = 4096;     // tuples per CTA tile, single-query columnar
 constexpr int kVaTile = 8192;      // tuples per CTA tile, VA-file filter

@@ -99,7 +99,9 @@ struct Span {
 
 // u64 words of a batch's accumulator block: counts, offsets, stats,
 // partials, tile counters (u32, rounded up)
-size_t scratch_words(size_t nq) { return nq + (nq + 1) + 4 * nq + nq * kPartialSlots * 4 + (nq + 1) / 2 + 1; }
+size_t scratch_words_base(size_t nq) { return nq + (nq + 1) + 4 * nq + nq * kPartialSlots * 4 + (nq + 1) / 2 + 1; }
+// + slot-order counts / offsets of a sorted VA batch
+size_t scratch_words(size_t nq) { return scratch_words_base(nq) + nq + (nq + 1); }
 
 }  // namespace
 
@@ -165,6 +167,8 @@ struct VbPass {
     uint32_t q0 = 0, nqp = 0, kb = 0, cells = 0, shift = 0;
     bool fallback = false;   // union wider than kVaBatchMaxDims: per-query VA
     size_t udim_off = 0, table_off = 0, qb_off = 0, cm_off = 0;
+    uint32_t prune = 0;                  // union dims whose cell mask is not full
+    unsigned long long cellmask[kVaBatchMaxDims] = {};
 };
 
 }  // namespace
@@ -190,6 +194,9 @@ struct mdrq_batch {
     std::vector<uint32_t> vb_tables;
     std::vector<float2> vb_qb;
     std::vector<uint32_t> vb_cm;   // per query of a pass: constrained union dims
+    // sorted batch: slot i of the passes holds query vb_perm[i] (empty: slot = query)
+    std::vector<uint32_t> vb_perm;
+    DBuf<uint32_t> d_vb_perm;
     DBuf<uint16_t> d_vb_udims;
     DBuf<uint32_t> d_vb_tables;
     DBuf<float2> d_vb_qb;
@@ -202,6 +209,8 @@ struct mdrq_batch {
     Span<unsigned long long> d_stats;      // [nq][4]
     Span<unsigned long long> d_partials;   // [nq][kPartialSlots][4]
     Span<uint32_t> d_tile_counters;        // [nq]
+    Span<unsigned long long> d_counts_p;   // [nq]   sorted VA batch: slot order
+    Span<unsigned long long> d_offsets_p;  // [nq+1]
     // result pool of its own (stream slots); otherwise the store's pool
     bool own_pool = false;
     DBuf<uint32_t> own_ids;
@@ -247,6 +256,8 @@ struct mdrq_store {
     // multi-query columnar ids pass: [32][mask words] masks, [32][chunks]
     // chunk counts / offsets (allocated on first use)
     DBuf<uint32_t> bmask, bchunk_counts, bchunk_offs;
+    // sorted VA batches: ids in slot order before they move to query order
+    DBuf<uint32_t> vb_ids_slot;
     DBuf<uint32_t> chunk_counts, chunk_offs;
     uint32_t nchunks = 0;
     // bit-sliced VA batch scratch ([chunks][1024] per pass)
@@ -350,22 +361,98 @@ uint16_t host_code(const float* b, uint32_t nb, float v) {
 // Passes of the bit-sliced VA batch: <= 1024 queries each; per union
 // dimension u and table cell c the overlap / containment masks of the pass's
 // queries (vabatch.cu).  Table cells are the stored 8-bit codes >> shift.
+// A batch of more than one pass is split into passes of queries that are
+// close in one dimension: sorted by their low cell there, a pass's queries
+// overlap only a band of that dimension's cells, so the pass's cell mask is
+// sparse and the kernel drops every tuple outside the band before reading
+// its table rows (vabatch.cu, W2 passes).  The dimension is the one whose
+// sorted passes cover the fewest cells (quantile cells hold ~equal tuple
+// counts, so covered cells ~ surviving tuples); no reordering when even that
+// one leaves > 85 % of the cells, or for a single pass.  Returns slot ->
+// query, empty for the identity.
+std::vector<uint32_t> choose_vb_order(const mdrq_store* s, const mdrq_batch* b) {
+    const uint32_t nq = b->nq, m = s->m, bits = s->va_bits;
+    if (nq <= 1024 || !bits) return {};
+    const uint32_t cb = std::min<uint32_t>(bits, 6), cells = 1u << cb, sh = bits - cb;
+    const unsigned long long full = cells == 64 ? ~0ull : ((1ull << cells) - 1);
+    // per (query, dim): cell range in `cells` units; lo > hi = empty; none = unconstrained
+    constexpr int16_t kFree = -1;
+    std::vector<int16_t> clo(size_t(nq) * m, kFree), chi(size_t(nq) * m, kFree);
+    std::vector<uint8_t> used(m, 0);
+    for (uint32_t q = 0; q < nq; ++q)
+        for (uint32_t i = 0; i < b->descs[q].k; ++i) {
+            const DimPred& p = b->preds[b->descs[q].off + i];
+            used[p.dim] = 1;
+            const bool empty = p.lo > p.hi;
+            clo[size_t(q) * m + p.dim] = int16_t(empty ? 1 : (p.cl >> sh));
+            chi[size_t(q) * m + p.dim] = int16_t(empty ? 0 : (p.ch >> sh));
+        }
+    double best = 0.85;
+    std::vector<uint32_t> best_order, order(nq);
+    for (uint32_t d = 0; d < m; ++d) {
+        if (!used[d]) continue;
+        for (uint32_t q = 0; q < nq; ++q) order[q] = q;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+            return clo[size_t(x) * m + d] < clo[size_t(y) * m + d];
+        });
+        double cov = 0;
+        for (uint32_t q0 = 0; q0 < nq; q0 += 1024) {
+            unsigned long long mk = 0;
+            const uint32_t q1 = std::min<uint32_t>(nq, q0 + 1024);
+            for (uint32_t i = q0; i < q1 && mk != full; ++i) {
+                const int lo = clo[size_t(order[i]) * m + d], hi = chi[size_t(order[i]) * m + d];
+                if (lo == kFree) {
+                    mk = full;
+                } else if (lo <= hi) {
+                    const int l = std::max(lo, 0), h = std::min(hi, int(cells) - 1);
+                    if (l <= h) mk |= (h - l == 63 ? ~0ull : ((1ull << (h - l + 1)) - 1)) << l;
+                }
+            }
+            cov += double(__builtin_popcountll(mk & full)) / cells * (q1 - q0);
+        }
+        cov /= nq;
+        if (cov < best) {
+            best = cov;
+            best_order = order;
+        }
+    }
+    return best_order;
+}
+
+void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b);
+
 void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
+    static const bool no_sort = getenv("MDRQ_VB_NO_SORT") != nullptr;   // measurement / test switch
+    b->vb_perm = no_sort ? std::vector<uint32_t>() : choose_vb_order(s, b);
+    build_vb_passes_ordered(s, b);
+    bool fb = false;
+    for (const VbPass& ps : b->vb_passes) fb |= ps.fallback;
+    if (fb && !b->vb_perm.empty()) {
+        // a pass fell back to per-query scans, which write in query order:
+        // keep the batch order
+        b->vb_perm.clear();
+        build_vb_passes_ordered(s, b);
+    }
+}
+
+void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
     b->vb_passes.clear();
     b->vb_udims.clear();
     b->vb_tables.clear();
     b->vb_qb.clear();
     b->vb_cm.clear();
     const uint32_t m = s->m, bits = s->va_bits;
+    const bool sorted = !b->vb_perm.empty();
+    auto query_of = [&](uint32_t slot) { return sorted ? b->vb_perm[slot] : slot; };
     for (uint32_t q0 = 0; q0 < b->nq; q0 += 1024) {
         VbPass ps;
         ps.q0 = q0;
         ps.nqp = std::min<uint32_t>(1024, b->nq - q0);
         std::vector<int> uidx(m, -1);
         std::vector<uint16_t> ud;
-        for (uint32_t q = q0; q < q0 + ps.nqp; ++q)
-            for (uint32_t i = 0; i < b->descs[q].k; ++i) {
-                const uint32_t d = b->preds[b->descs[q].off + i].dim;
+        for (uint32_t sl = q0; sl < q0 + ps.nqp; ++sl)
+            for (uint32_t i = 0; i < b->descs[query_of(sl)].k; ++i) {
+                const uint32_t d = b->preds[b->descs[query_of(sl)].off + i].dim;
                 if (uidx[d] < 0) {
                     uidx[d] = 0;
                     ud.push_back(uint16_t(d));
@@ -405,8 +492,10 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
         // queries unconstrained in dimension u: every cell, set once per word below
         std::vector<uint32_t> free_mask(size_t(ps.kb) * 32, 0u);
         std::vector<uint32_t> cmv(1024, 0u);
+        std::vector<unsigned long long> cmask(ps.kb, 0ull);
+        const unsigned long long cfull = cells == 64 ? ~0ull : ((1ull << cells) - 1);
         for (uint32_t qi = 0; qi < ps.nqp; ++qi) {
-            const QueryDesc& qd = b->descs[q0 + qi];
+            const QueryDesc& qd = b->descs[query_of(q0 + qi)];
             const uint32_t w = qi >> 5, bit = 1u << (qi & 31);
             uint32_t constrained = 0;   // bit per union dim (kb <= 24)
             for (uint32_t i = 0; i < qd.k; ++i) {
@@ -422,7 +511,10 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
                 if (p.lo > p.hi) continue;   // empty interval (kernel level only): no cell overlaps
                 // overlap cells [lo_c, hi_c]; containment drops the edge cells
                 const int lo_c = int(p.cl) >> ps.shift, hi_c = int(p.ch) >> ps.shift, top = int(cells) - 1;
-                for (int c = std::max(lo_c, 0); c <= std::min(hi_c, top); ++c) tab[ov_idx(u, uint32_t(c), w)] |= bit;
+                for (int c = std::max(lo_c, 0); c <= std::min(hi_c, top); ++c) {
+                    tab[ov_idx(u, uint32_t(c), w)] |= bit;
+                    cmask[u] |= 1ull << c;
+                }
                 if (!pv) {
                     const int s_lo = lo_c + (p.edge_lo ? 1 : 0), s_hi = hi_c - (p.edge_hi ? 1 : 0);
                     for (int c = std::max(s_lo, 0); c <= std::min(s_hi, top); ++c)
@@ -430,8 +522,15 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
                 }
             }
             for (uint32_t u = 0; u < ps.kb; ++u)
-                if (!(constrained >> u & 1u)) free_mask[size_t(u) * 32 + w] |= bit;
+                if (!(constrained >> u & 1u)) {
+                    free_mask[size_t(u) * 32 + w] |= bit;
+                    cmask[u] = cfull;
+                }
             cmv[qi] = constrained;
+        }
+        for (uint32_t u = 0; u < ps.kb; ++u) {
+            ps.cellmask[u] = cmask[u] & cfull;
+            if (ps.cellmask[u] != cfull) ps.prune |= 1u << u;
         }
         for (uint32_t u = 0; u < ps.kb; ++u)
             for (uint32_t w = 0; w < 32; ++w) {
@@ -599,6 +698,7 @@ void upload_batch(mdrq_store* s, mdrq_batch* b, bool sync = true) {
     upload(b->d_vb_tables, b->vb_tables, s->stream);
     upload(b->d_vb_qb, b->vb_qb, s->stream);
     upload(b->d_vb_cm, b->vb_cm, s->stream);
+    upload(b->d_vb_perm, b->vb_perm, s->stream);
     const size_t nq = b->nq;
     b->d_scratch.reserve(scratch_words(b->nq));
     unsigned long long* p = b->d_scratch.p;
@@ -607,6 +707,8 @@ void upload_batch(mdrq_store* s, mdrq_batch* b, bool sync = true) {
     b->d_stats.p = p + 2 * nq + 1;
     b->d_partials.p = p + 6 * nq + 1;
     b->d_tile_counters.p = reinterpret_cast<uint32_t*>(p + 6 * nq + 1 + nq * kPartialSlots * 4);
+    b->d_counts_p.p = p + scratch_words_base(nq);
+    b->d_offsets_p.p = p + scratch_words_base(nq) + nq;
     // H2D copies above may read pageable host vectors that a later rebuild
     // mutates: make them complete before returning (the ids stream rebuilds
     // a slot only after its previous pass and copies completed).
@@ -618,7 +720,7 @@ uint64_t upload_bytes(const mdrq_batch* b) {
            b->udims.size() * sizeof(uint16_t) + b->bounds.size() * sizeof(float2) +
            b->cmask.size() * sizeof(unsigned long long) + b->vb_udims.size() * sizeof(uint16_t) +
            b->vb_tables.size() * sizeof(uint32_t) + b->vb_qb.size() * sizeof(float2) +
-           b->vb_cm.size() * sizeof(uint32_t);
+           b->vb_cm.size() * sizeof(uint32_t) + b->vb_perm.size() * sizeof(uint32_t);
 }
 
 uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
@@ -719,16 +821,21 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     s->vb_base.reserve(chunks * 1024);
     s->vb_total.reserve(1024);
     s->vb_qoff.reserve(1024);
-    a.counts = b->d_counts.p + ps.q0;
+    // sorted batch: the passes write in slot order (unpermuted by enqueue)
+    const bool sorted = !b->vb_perm.empty();
+    a.counts = (sorted ? b->d_counts_p.p : b->d_counts.p) + ps.q0;
     a.chunk_counts = s->vb_chunk_counts.p;
     a.base = s->vb_base.p;
     a.total = s->vb_total.p;
     a.qoff = s->vb_qoff.p;
-    a.offsets = b->d_offsets.p;
-    a.counts_all = b->d_counts.p;
-    a.ids = pool_of(s, b).p;
-    a.ids_cap = pool_of(s, b).p ? pool_of(s, b).cap : 0;
+    a.offsets = sorted ? b->d_offsets_p.p : b->d_offsets.p;
+    a.counts_all = sorted ? b->d_counts_p.p : b->d_counts.p;
+    DBuf<uint32_t>& dst = sorted ? s->vb_ids_slot : pool_of(s, b);
+    a.ids = dst.p;
+    a.ids_cap = dst.p ? dst.cap : 0;
     a.id_base = s->id_base;
+    a.prune_dims = ps.prune;
+    for (uint32_t u = 0; u < ps.kb && u < uint32_t(kVaBatchMaxDims); ++u) a.cellmask[u] = ps.cellmask[u];
     s->vb_rec.reserve(size_t(s->vb_max_blocks) * kRecBlock);
     s->vb_blk_count.reserve(s->vb_max_blocks);
     s->vb_blk_chunk.reserve(s->vb_max_blocks);
@@ -857,6 +964,9 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
         }
     };
     if (path == MDRQ_PATH_VAFILE_BATCH) {
+        const bool sorted = !b->vb_perm.empty();
+        DBuf<uint32_t>& pool = pool_of(s, b);
+        if (sorted && ids && pool.p) s->vb_ids_slot.reserve(pool.cap);   // slot-order ids, as large as the result pool
         for (const VbPass& ps : b->vb_passes) {
             if (ps.fallback) {
                 for (uint32_t q = ps.q0; q < ps.q0 + ps.nqp; ++q) single(MDRQ_PATH_VAFILE, q);
@@ -893,6 +1003,13 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
                 dsync("mode2");
                 launches += 6;
             }
+        }
+        if (sorted) {
+            mark(ids ? 2 : 1, ids ? 3 : 2);
+            launches += launch_va_batch_unpermute(b->d_vb_perm.p, b->d_counts_p.p, b->d_offsets_p.p, b->d_counts.p,
+                                                  b->d_offsets.p, s->vb_ids_slot.p, pool.p,
+                                                  pool.p ? std::min<uint64_t>(pool.cap, s->vb_ids_slot.cap) : 0, nq,
+                                                  ids && pool.p, s->num_sms, st);
         }
     } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
         // ids: query-major masks (word count a multiple of 4: 16-byte rows)
@@ -954,6 +1071,7 @@ uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
             l += ps.fallback ? ps.nqp * (ids ? 3 : 1) : (ids ? 6 : 1);
             single |= ps.fallback;
         }
+        if (!b->vb_perm.empty()) l += ids ? 3 : 2;
         return l + (single ? 1 : 0);
     }
     if (b->path == MDRQ_PATH_COLUMNAR_BATCH) {
@@ -1579,7 +1697,8 @@ int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats, uint32_t
         if (path == MDRQ_PATH_VAFILE_BATCH) {
             for (const VbPass& p : b->vb_passes)
                 for (uint32_t q = p.q0; q < p.q0 + p.nqp; ++q)
-                    pass_bytes[q] = p.fallback ? 0 : (s->n * p.kb * (p.kb <= 10 ? 5 : 1)) / p.nqp;
+                    pass_bytes[b->vb_perm.empty() ? q : b->vb_perm[q]] =
+                        p.fallback ? 0 : (s->n * p.kb * (p.kb <= 10 ? 5 : 1)) / p.nqp;
         } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
             for (const Pass& p : b->passes)
                 for (uint32_t q = p.q0; q < p.q0 + p.nqp; ++q)

@@ -117,6 +117,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     // SCODE (PV, so no containment words): every warp's staged cells [128] uint2
     uint2* s_code = reinterpret_cast<uint2*>(s_qe + VB_WARPS * VB_QCAP);
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_rest);
+    // W2 (multi-word) dense passes: every warp's compacted list of the block's
+    // unpruned tuples [128] u8, after the queues and staged cells
+    uint8_t* s_alive = reinterpret_cast<uint8_t*>(s_qe + VB_WARPS * VB_QCAP) + (SCODE ? VB_WARPS * 128 * 8 : 0);
 
     // the recount pass only runs when the single-pass staging overflowed
     if (MODE == 2 && *reinterpret_cast<volatile const uint32_t*>(a.overflow) == 0) return;
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     uint2* wcode = s_code + warp * 128;            // SCODE: this warp's staged cells
     uint32_t* qs = s_qs + warp * VB_QCAP;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 2
+    uint8_t* walive = s_alive + warp * 128;        // W2: compacted tuple list of the block
     const uint32_t lt = lanemask_lt();
 
     // Exact refinement of one query word for one tuple: bit b of the result
@@ -301,14 +305,69 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             }
             if (t0 + 128 < end) load_block(t0 + 128);
             const uint32_t jmax = uint32_t(end - t0 < 128 ? end - t0 : 128);
-            for (uint32_t j4 = 0; j4 < jmax; j4 += 4 * CWS) {
+            // W2: the block's tuples whose cell lies outside every query of
+            // the pass in some pruned dim are dropped here; the sub-steps walk
+            // the compacted list (tuple index, ascending) of the rest
+            uint32_t nalive = jmax;
+            bool compact = false;
+            if constexpr (W2 && MODE != 2) {
+                if (a.prune_dims) {
+                    uint32_t nib = 0xFu;
+#pragma unroll
+                    for (int u = 0; u < KB; ++u)
+                        if (a.prune_dims >> u & 1u) {
+                            const unsigned long long cm = a.cellmask[u];
+#pragma unroll
+                            for (uint32_t bb = 0; bb < 4; ++bb)
+                                if (!((cm >> ((cw[u] >> (8 * bb)) & 0xFFu)) & 1ull)) nib &= ~(1u << bb);
+                        }
+                    if (4 * lane + 4 > jmax) nib &= 4 * lane >= jmax ? 0u : (1u << (jmax - 4 * lane)) - 1u;
+                    const uint32_t c = __popc(nib);
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t x2 = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (lane >= uint32_t(o)) incl += x2;
+                    }
+                    nalive = __shfl_sync(0xFFFFFFFFu, incl, 31);
+                    compact = nalive < jmax;
+                    if (compact) {
+                        uint32_t pos = incl - c;
+#pragma unroll
+                        for (uint32_t bb = 0; bb < 4; ++bb)
+                            if (nib >> bb & 1u) walive[pos++] = uint8_t(4 * lane + bb);
+                        __syncwarp();
+                    }
+                }
+            }
+            for (uint32_t j4 = 0; j4 < nalive; j4 += 4 * CWS) {
+                // this lane's tuple (index in the block) of every sub-step and
+                // whether it exists: tix / tvm
+                uint32_t tix[NS];
+                uint32_t tvm = 0;
+#pragma unroll
+                for (int ss = 0; ss < NS; ++ss) {
+                    const uint32_t pos = j4 + ss * TPI + (LW == 32 ? 0u : lane_tup);
+                    const bool ok = pos < nalive;
+                    tvm |= uint32_t(ok) << ss;
+                    tix[ss] = (W2 && compact) ? (ok ? uint32_t(walive[pos]) : 0u) : pos;
+                }
                 // the step's CWS code words of every union dim (narrow passes
                 // take 8 tuples per step for more independent work)
-                uint32_t xw[CWS][KB];
+                // (W2: one word per sub-step, fetched for the lane's own tuple)
+                constexpr int NXW = W2 ? NS : CWS;
+                uint32_t xw[NXW][KB];
                 uint2 sc[SCODE ? NS : 1];   // SCODE: sub-step ss's tuple cells (dims 0-3, 4-7)
                 if constexpr (SCODE) {
 #pragma unroll
-                    for (int ss = 0; ss < NS; ++ss) sc[ss] = wcode[j4 + ss * TPI + lane_tup];
+                    for (int ss = 0; ss < NS; ++ss) sc[ss] = wcode[tix[ss]];
+                } else if constexpr (W2) {
+                    // sub-step ss = code word ss: each lane group fetches the
+                    // word holding its own (compacted) tuple
+#pragma unroll
+                    for (int c = 0; c < NS; ++c)
+#pragma unroll
+                        for (int u = 0; u < KB; ++u) xw[c][u] = __shfl_sync(0xFFFFFFFFu, cw[u], tix[c] >> 2);
                 } else {
 #pragma unroll
                     for (int c = 0; c < CWS; ++c)
@@ -327,8 +386,9 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         // byte 0 = lane offset, byte 1 = cell of the tuple (cells
                         // are pre-masked to < K); two dims per 3-input AND
                         const uint32_t jj = ss * TPI + (LW == 32 ? 0u : lane_tup);   // tuple in the step
-                        const uint32_t* x = xw[(ss * TPI) / 4];   // its code word (compile-time)
-                        const uint32_t sel = 0x5504u | ((jj & 3u) << 4);
+                        const uint32_t* x = xw[W2 ? ss : (ss * TPI) / 4];   // its code word (compile-time)
+                        // W2: byte (tuple % 4) of the word fetched for this lane's tuple
+                        const uint32_t sel = 0x5504u | (((W2 ? tix[ss] : jj) & 3u) << 4);
                         // row address of dim uu (SCODE: byte uu % 4 of the
                         // staged word, a compile-time selector)
                         auto addr = [&](int uu) -> uint32_t {
@@ -389,7 +449,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             }
                         }
                     }
-                step(t0, j4, jmax, ov4, su4);
+                step(t0, j4, jmax, ov4, su4, tix, tvm);
             }
         }
     };
@@ -521,7 +581,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     flush();   // the queued entries need the previous block's staged values
                     blk_t0 = t0;
                 },
-                [&](uint64_t, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[NOV], const uint32_t(&su4)[NOV]) {
+                [&](uint64_t, uint32_t j4, uint32_t jmax, const uint32_t(&ov4)[NOV], const uint32_t(&su4)[NOV],
+                    const uint32_t(&tix)[NS], uint32_t tvm) {
                     if constexpr (W2) {
                         // multi-word layouts queue tuple-major -- tuple, then
                         // query word ascending (lane order is (tuple, l), a
@@ -534,11 +595,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         uint32_t pl[NS][3], nzm[NS], nb = 0;
 #pragma unroll
                         for (uint32_t ss = 0; ss < NS; ++ss) {
-                            const uint32_t jj = ss * TPI + lane_tup;
                             uint32_t m = 0;
 #pragma unroll
                             for (int h = 0; h < NW; ++h) m |= uint32_t(ov4[ss + NS * h] != 0u) << h;
-                            if (j4 + jj >= jmax) m = 0;
+                            if (!(tvm >> ss & 1u)) m = 0;
                             nzm[ss] = m;
                             const uint32_t c = __popc(m);
                             pl[ss][0] = __ballot_sync(0xFFFFFFFFu, c & 1u);
@@ -552,7 +612,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             uint32_t slot = qn + __popc(pl[ss][0] & below) + 2u * __popc(pl[ss][1] & below) +
                                             4u * __popc(pl[ss][2] & below);
                             if (lanes >> lane & 1u) {
-                                const uint32_t mb = (((j4 + ss * TPI + lane_tup) << 5) | (NW * (lane % LPT)));
+                                const uint32_t mb = ((tix[ss] << 5) | (NW * (lane % LPT)));
 #pragma unroll
                                 for (int h = 0; h < NW; ++h)
                                     if (nzm[ss] >> h & 1u) qe[slot++] = make_uint2(ov4[ss + NS * h], mb + h);
@@ -633,7 +693,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             // a query word of the pass count
             const uint32_t own = lane * 32 < a.nqp ? 0xFFFFFFFFu : 0u;
             auto per_tuple = [&](uint64_t t0, uint32_t j4, uint32_t jmax, const uint32_t(&ov4_in)[4],
-                                 const uint32_t(&su4)[4]) {
+                                 const uint32_t(&su4)[4], const uint32_t(&)[NS], uint32_t) {
                 uint32_t ov4[4];
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj) ov4[jj] = ov4_in[jj] & own;
@@ -1108,6 +1168,65 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
     }
 }
 
+// ---------------------------------------------------------------------------
+// Sorted batches (store.cu build_vb_passes): the passes ran over the batch's
+// queries in slot order perm (slot i = query perm[i]), their counts, offsets
+// and ids landed in slot order.  Back to query order: counts, then the
+// offsets (exclusive scan), then every slot's id run moved to its query's
+// place -- one CTA per run, 16-byte copies when both ends are aligned.
+__global__ void vb_unpermute_counts_kernel(const uint32_t* __restrict__ perm, const unsigned long long* __restrict__ cp,
+                                           unsigned long long* __restrict__ counts, uint32_t nq) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += gridDim.x * blockDim.x)
+        counts[perm[i]] = cp[i];
+}
+
+__global__ void __launch_bounds__(1024) vb_offsets_scan_kernel(const unsigned long long* __restrict__ counts,
+                                                               uint32_t nq, unsigned long long* __restrict__ offsets) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_tot;
+    unsigned long long carry = 0;
+    for (uint32_t base = 0; base < nq; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const unsigned long long v = i < nq ? counts[i] : 0ull;
+        const unsigned long long ex = cta_scan_excl(v, s_w);
+        if (i < nq) offsets[i] = carry + ex;
+        // the block total: the last thread's exclusive + value
+        if (threadIdx.x == 1023) s_tot = ex + v;
+        __syncthreads();
+        carry += s_tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) offsets[nq] = carry;
+}
+
+__global__ void __launch_bounds__(256) vb_unpermute_ids_kernel(const uint32_t* __restrict__ perm,
+                                                               const unsigned long long* __restrict__ op,
+                                                               const unsigned long long* __restrict__ cp,
+                                                               const unsigned long long* __restrict__ offsets,
+                                                               const uint32_t* __restrict__ src,
+                                                               uint32_t* __restrict__ dst, uint64_t cap, uint32_t nq) {
+    for (uint32_t i = blockIdx.x; i < nq; i += gridDim.x) {
+        const uint64_t n = cp[i];
+        const uint64_t d0 = offsets[perm[i]];
+        if (!n || d0 + n > cap) continue;   // truncated result: the caller grows the pool and reruns
+        const uint32_t* s = src + op[i];
+        uint32_t* d = dst + d0;
+        uint64_t j = 0;
+        // align the destination to 16 bytes, then 16-byte copies when the
+        // source shares the alignment
+        const uint64_t head = ((16u - (reinterpret_cast<uintptr_t>(d) & 15u)) & 15u) / 4;
+        if (((reinterpret_cast<uintptr_t>(s) ^ reinterpret_cast<uintptr_t>(d)) & 15u) == 0 && n > head) {
+            if (threadIdx.x < head) d[threadIdx.x] = s[threadIdx.x];
+            const uint64_t n4 = (n - head) / 4;
+            const uint4* s4 = reinterpret_cast<const uint4*>(s + head);
+            uint4* d4 = reinterpret_cast<uint4*>(d + head);
+            for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x) __stcs(d4 + k, __ldcs(s4 + k));
+            j = head + n4 * 4;
+        }
+        for (uint64_t k = j + threadIdx.x; k < n; k += blockDim.x) d[k] = __ldcs(s + k);
+    }
+}
+
 template <int MODE, int KB, int LW>
 void run_kb_lw(const VaBatchArgs& a, cudaStream_t st) {
     const size_t smem = va_batch_smem(KB, va_batch_cells(KB), MODE);
@@ -1166,6 +1285,7 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
     else
         bytes += 1024 * 4 + size_t(VB_WARPS) * VB_QCAP * (8 + (pv ? 0 : 4));
     if (mode != 2 && pv && kb <= 8) bytes += size_t(VB_WARPS) * 128 * 8;   // staged cells (multi-word passes)
+    if (mode != 2 && pv) bytes += size_t(VB_WARPS) * 128;                 // compacted tuple lists
     return bytes;
 }
 
@@ -1199,6 +1319,19 @@ void launch_va_batch_scans(const VaBatchArgs& a, uint32_t q0, cudaStream_t st) {
     vb_chunk_scan_kernel<<<(a.nqp + 31) / 32, 1024, 0, st>>>(a.chunk_counts, a.ngroups, a.nqp, a.base, a.total);
     vb_query_scan_kernel<<<1, 1024, 0, st>>>(a.total, a.nqp, a.offsets, a.counts_all, a.qoff, q0, a.chunk_nblk,
                                              a.chunk_first, a.nchunks);
+}
+
+uint32_t launch_va_batch_unpermute(const uint32_t* perm, const unsigned long long* counts_p,
+                                   const unsigned long long* offsets_p, unsigned long long* counts,
+                                   unsigned long long* offsets, const uint32_t* ids_p, uint32_t* ids, uint64_t cap,
+                                   uint32_t nq, bool with_ids, int num_sms, cudaStream_t st) {
+    if (!nq) return 0;
+    vb_unpermute_counts_kernel<<<(nq + 255) / 256, 256, 0, st>>>(perm, counts_p, counts, nq);
+    vb_offsets_scan_kernel<<<1, 1024, 0, st>>>(counts, nq, offsets);
+    if (!with_ids) return 2;
+    const uint32_t grid = std::min<uint32_t>(nq, uint32_t(num_sms) * 8);
+    vb_unpermute_ids_kernel<<<grid, 256, 0, st>>>(perm, offsets_p, counts_p, offsets, ids_p, ids, cap, nq);
+    return 3;
 }
 
 void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st) {

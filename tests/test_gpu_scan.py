@@ -501,3 +501,34 @@ def test_fetch_after_count_and_truncation(gpu):
             got64 = np.empty(ei.size, np.int64)
             _lib.check(lib.mdrq_fetch_ids64(st_.handle, got64.ctypes.data_as(_lib.i64p), got64.size))
             assert np.array_equal(got64, ei), p
+
+
+@pytest.mark.parametrize("m,nq,width", [(10, 3000, 0.501), (8, 2500, 0.43), (5, 4100, 0.3), (12, 2100, 0.6)])
+def test_sorted_multi_pass_batches_vs_oracle(gpu, m, nq, width):
+    """Batches of several 1024-query passes: the host sorts the queries into
+    passes (band-sparse cell masks) and the kernel skips pruned tuples; the
+    ids come back in the batch's query order.  Every query is compared with
+    the oracle (count + set hash), also with a share of partial-match,
+    empty and unconstrained queries in the batch."""
+    from devhash import batch_hashes
+    rng = np.random.default_rng(m * 1000 + nq)
+    n = 200_003
+    values = rng.random((n, m), dtype=np.float32)
+    lo = rng.uniform(0, 1 - width, (nq, m)).astype(np.float32)
+    hi = (lo + width).astype(np.float32)
+    part = rng.random(nq) < 0.1
+    free = rng.random((nq, m)) < 0.5
+    lo[part[:, None] & free] = -np.inf
+    hi[part[:, None] & free] = np.inf
+    lo[7], hi[7] = 2.0, 3.0          # empty
+    lo[11], hi[11] = -np.inf, np.inf  # every tuple
+    exp_c, exp_h = oracle.hash_batch(values, lo, hi)
+    with gpu.DeviceStore(values, layouts=1 | 4, va_bits=8) as st_:
+        c, h, path = batch_hashes(st_, lo, hi, "vafile_batch")
+        assert path == "vafile_batch"
+        assert np.array_equal(c, exp_c), np.flatnonzero(c != exp_c)[:10]
+        assert np.array_equal(h, exp_h), np.flatnonzero(h != exp_h)[:10]
+        assert np.array_equal(st_.count(lo, hi, "vafile_batch"), exp_c)
+        offs, ids = st_.ids(lo[:1500], hi[:1500], "vafile_batch")   # the synchronous path too
+        assert np.array_equal(np.diff(offs), exp_c[:1500])
+        assert np.array_equal(oracle.set_hash(offs, ids), exp_h[:1500])
