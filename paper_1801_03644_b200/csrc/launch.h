@@ -161,8 +161,8 @@ void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st);
 // returns the number of kernels launched
 uint32_t launch_va_batch_unpermute(const uint32_t* perm, const unsigned long long* counts_p,
                                    const unsigned long long* offsets_p, unsigned long long* counts,
-                                   unsigned long long* offsets, const uint32_t* ids_p, uint32_t* ids, uint64_t cap,
-                                   uint32_t nq, bool with_ids, int num_sms, cudaStream_t st);
+                                   unsigned long long* offsets, const uint32_t* ids_p, uint64_t src_cap,
+                                   uint32_t* ids, uint64_t cap, uint32_t nq, bool with_ids, cudaStream_t st);
 
 constexpr int kColTile = 4096;     // tuples per CTA tile, single-query columnar
 constexpr int kVaTile = 8192;      // tuples per CTA tile, VA-file filter

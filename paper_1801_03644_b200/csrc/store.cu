@@ -1007,9 +1007,9 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
         if (sorted) {
             mark(ids ? 2 : 1, ids ? 3 : 2);
             launches += launch_va_batch_unpermute(b->d_vb_perm.p, b->d_counts_p.p, b->d_offsets_p.p, b->d_counts.p,
-                                                  b->d_offsets.p, s->vb_ids_slot.p, pool.p,
-                                                  pool.p ? std::min<uint64_t>(pool.cap, s->vb_ids_slot.cap) : 0, nq,
-                                                  ids && pool.p, s->num_sms, st);
+                                                  b->d_offsets.p, s->vb_ids_slot.p,
+                                                  s->vb_ids_slot.p ? s->vb_ids_slot.cap : 0, pool.p,
+                                                  pool.p ? pool.cap : 0, nq, ids && pool.p && s->vb_ids_slot.p, st);
         }
     } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
         // ids: query-major masks (word count a multiple of 4: 16-byte rows)

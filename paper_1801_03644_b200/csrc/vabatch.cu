@@ -1203,12 +1203,14 @@ __global__ void __launch_bounds__(256) vb_unpermute_ids_kernel(const uint32_t* _
                                                                const unsigned long long* __restrict__ op,
                                                                const unsigned long long* __restrict__ cp,
                                                                const unsigned long long* __restrict__ offsets,
-                                                               const uint32_t* __restrict__ src,
+                                                               const uint32_t* __restrict__ src, uint64_t src_cap,
                                                                uint32_t* __restrict__ dst, uint64_t cap, uint32_t nq) {
     for (uint32_t i = blockIdx.x; i < nq; i += gridDim.x) {
         const uint64_t n = cp[i];
         const uint64_t d0 = offsets[perm[i]];
-        if (!n || d0 + n > cap) continue;   // truncated result: the caller grows the pool and reruns
+        // truncated result (either buffer too small): the caller grows the
+        // pool and reruns
+        if (!n || d0 + n > cap || op[i] + n > src_cap) continue;
         const uint32_t* s = src + op[i];
         uint32_t* d = dst + d0;
         uint64_t j = 0;
@@ -1223,6 +1225,7 @@ __global__ void __launch_bounds__(256) vb_unpermute_ids_kernel(const uint32_t* _
             for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x) __stcs(d4 + k, __ldcs(s4 + k));
             j = head + n4 * 4;
         }
+#pragma unroll 4
         for (uint64_t k = j + threadIdx.x; k < n; k += blockDim.x) d[k] = __ldcs(s + k);
     }
 }
@@ -1323,14 +1326,15 @@ void launch_va_batch_scans(const VaBatchArgs& a, uint32_t q0, cudaStream_t st) {
 
 uint32_t launch_va_batch_unpermute(const uint32_t* perm, const unsigned long long* counts_p,
                                    const unsigned long long* offsets_p, unsigned long long* counts,
-                                   unsigned long long* offsets, const uint32_t* ids_p, uint32_t* ids, uint64_t cap,
-                                   uint32_t nq, bool with_ids, int num_sms, cudaStream_t st) {
+                                   unsigned long long* offsets, const uint32_t* ids_p, uint64_t src_cap,
+                                   uint32_t* ids, uint64_t cap, uint32_t nq, bool with_ids, cudaStream_t st) {
     if (!nq) return 0;
     vb_unpermute_counts_kernel<<<(nq + 255) / 256, 256, 0, st>>>(perm, counts_p, counts, nq);
     vb_offsets_scan_kernel<<<1, 1024, 0, st>>>(counts, nq, offsets);
     if (!with_ids) return 2;
-    const uint32_t grid = std::min<uint32_t>(nq, uint32_t(num_sms) * 8);
-    vb_unpermute_ids_kernel<<<grid, 256, 0, st>>>(perm, offsets_p, counts_p, offsets, ids_p, ids, cap, nq);
+    // one CTA per id run (a run is a query's ids: ~5e5 on C5)
+    vb_unpermute_ids_kernel<<<std::min<uint32_t>(nq, 65535), 256, 0, st>>>(perm, offsets_p, counts_p, offsets, ids_p,
+                                                                         src_cap, ids, cap, nq);
     return 3;
 }
 
