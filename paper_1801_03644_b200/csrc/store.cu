@@ -832,7 +832,7 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.counts_all = sorted ? b->d_counts_p.p : b->d_counts.p;
     DBuf<uint32_t>& dst = sorted ? s->vb_ids_slot : pool_of(s, b);
     a.ids = dst.p;
-    a.ids_cap = dst.p ? dst.cap : 0;
+    a.ids_cap = dst.p ? dst.cap - (sorted ? std::min<size_t>(dst.cap, 4) : 0) : 0;
     a.id_base = s->id_base;
     a.prune_dims = ps.prune;
     for (uint32_t u = 0; u < ps.kb && u < uint32_t(kVaBatchMaxDims); ++u) a.cellmask[u] = ps.cellmask[u];
@@ -966,7 +966,9 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
     if (path == MDRQ_PATH_VAFILE_BATCH) {
         const bool sorted = !b->vb_perm.empty();
         DBuf<uint32_t>& pool = pool_of(s, b);
-        if (sorted && ids && pool.p) s->vb_ids_slot.reserve(pool.cap);   // slot-order ids, as large as the result pool
+        // slot-order ids, as large as the result pool (+ 4 words of slack
+        // for the realigning copy's reads)
+        if (sorted && ids && pool.p) s->vb_ids_slot.reserve(pool.cap + 4);
         for (const VbPass& ps : b->vb_passes) {
             if (ps.fallback) {
                 for (uint32_t q = ps.q0; q < ps.q0 + ps.nqp; ++q) single(MDRQ_PATH_VAFILE, q);
@@ -1008,7 +1010,7 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
             mark(ids ? 2 : 1, ids ? 3 : 2);
             launches += launch_va_batch_unpermute(b->d_vb_perm.p, b->d_counts_p.p, b->d_offsets_p.p, b->d_counts.p,
                                                   b->d_offsets.p, s->vb_ids_slot.p,
-                                                  s->vb_ids_slot.p ? s->vb_ids_slot.cap : 0, pool.p,
+                                                  s->vb_ids_slot.cap > 4 ? s->vb_ids_slot.cap - 4 : 0, pool.p,
                                                   pool.p ? pool.cap : 0, nq, ids && pool.p && s->vb_ids_slot.p, st);
         }
     } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {

@@ -1199,6 +1199,12 @@ __global__ void __launch_bounds__(1024) vb_offsets_scan_kernel(const unsigned lo
     if (threadIdx.x == 0) offsets[nq] = carry;
 }
 
+// The run of slot i (n ids at src + op[i]) to its query's place: the
+// destination is 16-byte aligned after a head of <= 3 words, the source is
+// read as aligned 16-byte words and realigned in registers (k = source word
+// offset mod 4), so every load and store is a full 16-byte access.  The
+// source buffer has >= 4 words of slack past its capacity (the realigning
+// read of a run's last vector may touch up to 3 words beyond it).
 __global__ void __launch_bounds__(256) vb_unpermute_ids_kernel(const uint32_t* __restrict__ perm,
                                                                const unsigned long long* __restrict__ op,
                                                                const unsigned long long* __restrict__ cp,
@@ -1206,27 +1212,41 @@ __global__ void __launch_bounds__(256) vb_unpermute_ids_kernel(const uint32_t* _
                                                                const uint32_t* __restrict__ src, uint64_t src_cap,
                                                                uint32_t* __restrict__ dst, uint64_t cap, uint32_t nq) {
     for (uint32_t i = blockIdx.x; i < nq; i += gridDim.x) {
-        const uint64_t n = cp[i];
+        uint64_t n = cp[i];
         const uint64_t d0 = offsets[perm[i]];
         // truncated result (either buffer too small): the caller grows the
         // pool and reruns
         if (!n || d0 + n > cap || op[i] + n > src_cap) continue;
         const uint32_t* s = src + op[i];
         uint32_t* d = dst + d0;
-        uint64_t j = 0;
-        // align the destination to 16 bytes, then 16-byte copies when the
-        // source shares the alignment
-        const uint64_t head = ((16u - (reinterpret_cast<uintptr_t>(d) & 15u)) & 15u) / 4;
-        if (((reinterpret_cast<uintptr_t>(s) ^ reinterpret_cast<uintptr_t>(d)) & 15u) == 0 && n > head) {
-            if (threadIdx.x < head) d[threadIdx.x] = s[threadIdx.x];
-            const uint64_t n4 = (n - head) / 4;
-            const uint4* s4 = reinterpret_cast<const uint4*>(s + head);
-            uint4* d4 = reinterpret_cast<uint4*>(d + head);
-            for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x) __stcs(d4 + k, __ldcs(s4 + k));
-            j = head + n4 * 4;
-        }
+        uint64_t head = ((16u - (reinterpret_cast<uintptr_t>(d) & 15u)) & 15u) / 4;
+        if (head > n) head = n;
+        if (threadIdx.x < head) d[threadIdx.x] = __ldcs(s + threadIdx.x);
+        s += head;
+        d += head;
+        n -= head;
+        const uint32_t k = uint32_t(reinterpret_cast<uintptr_t>(s) & 15u) / 4;
+        const uint4* sa = reinterpret_cast<const uint4*>(s - k);
+        uint4* d4 = reinterpret_cast<uint4*>(d);
+        const uint64_t n4 = n / 4;
+        if (k == 0) {
 #pragma unroll 4
-        for (uint64_t k = j + threadIdx.x; k < n; k += blockDim.x) d[k] = __ldcs(s + k);
+            for (uint64_t j = threadIdx.x; j < n4; j += blockDim.x) __stcs(d4 + j, __ldcs(sa + j));
+        } else {
+#pragma unroll 2
+            for (uint64_t j = threadIdx.x; j < n4; j += blockDim.x) {
+                const uint4 x = __ldcs(sa + j), y = __ldcs(sa + j + 1);
+                uint4 o;
+                if (k == 1)
+                    o = make_uint4(x.y, x.z, x.w, y.x);
+                else if (k == 2)
+                    o = make_uint4(x.z, x.w, y.x, y.y);
+                else
+                    o = make_uint4(x.w, y.x, y.y, y.z);
+                __stcs(d4 + j, o);
+            }
+        }
+        for (uint64_t t = n4 * 4 + threadIdx.x; t < n; t += blockDim.x) d[t] = __ldcs(s + t);
     }
 }
 

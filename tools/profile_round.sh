@@ -1,30 +1,33 @@
 #!/bin/bash
-# Profiling recipe of one round (run under gpurun, 1 GPU).  Every ncu command
-# is preceded by the same command line exiting 0 without ncu.
+# Round-2 profiling recipe (run under gpurun, 1 GPU).  Every ncu command is
+# preceded by the same command line exiting 0 without ncu; captures land in
+# gpurun_out/ and tools/write_ncu_summary.py turns them into profiles/r02_*.
 set -u
 OUT=gpurun_out
+mkdir -p $OUT
+: > $OUT/rc.txt
+NCU="ncu --target-processes application-only --clock-control none"
 python bench.py > $OUT/bench_default.log 2> $OUT/bench_default.err
 echo "bench=$?" >> $OUT/rc.txt
-B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-paths"
+# launch list of one bench step (+ store build, warm-up, profiling passes)
+B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-paths --no-e2e"
 $B > $OUT/plain.log 2>&1
 echo "plain=$?" >> $OUT/rc.txt
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file $OUT/launches.csv $B > $OUT/ncu_launches.log 2>&1
+timeout 1500 $NCU --metrics gpu__time_duration.sum --csv --log-file $OUT/launches.csv $B > $OUT/ncu_launches.log 2>&1
 echo "launches=$?" >> $OUT/rc.txt
-# the second ids pass of the batch (the first one sizes the result pool):
-# launches 4..5 of the filter / scatter kernels = mode 3 filter + scatter
-timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"va_batch_kernel|vb_scatter" -s 3 -c 2 -o $OUT/prof_vab $B > $OUT/ncu_vab.log 2>&1
-echo "vab=$?" >> $OUT/rc.txt
-C="python tools/probe_path.py columnar ids 20"
-$C > $OUT/probe_col.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:col_scan_kernel -s 10 -c 1 -o $OUT/prof_col $C > $OUT/ncu_col.log 2>&1
-echo "col=$?" >> $OUT/rc.txt
-V="python tools/probe_path.py vafile count 20"
-$V > $OUT/probe_va.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on \
-    -k regex:va_scan_kernel -s 25 -c 1 -o $OUT/prof_va $V > $OUT/ncu_va.log 2>&1
-echo "va=$?" >> $OUT/rc.txt
-P="python tools/probe_path.py rowwise count 3"
-$P > $OUT/probe_row.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on \
-    -k regex:row_scan_kernel -s 1 -c 1 -o $OUT/prof_row $P > $OUT/ncu_row.log 2>&1
-echo "row=$?" >> $OUT/rc.txt
+# full sets: the bench batch (C5, 10 000 queries) -- first filter pass + its
+# scatter in ids mode, the first filter pass in count mode
+full() {   # name, nvtx range, kernel regex, env...
+    local name=$1 range=$2 regex=$3; shift 3
+    env "$@" python tools/prof_c5.py > $OUT/probe_$name.log 2>&1 && \
+    timeout 1800 $NCU --set full --import-source on --kernel-name-base demangled --nvtx --nvtx-include "$range/" \
+        -k regex:"$regex" -c 2 -o $OUT/prof_$name -f env "$@" python tools/prof_c5.py > $OUT/ncu_$name.log 2>&1
+    echo "$name=$?" >> $OUT/rc.txt
+}
+full vab ids 'va_batch_kernel<\(int\)3|vb_scatter' PROF_NQ=10000 PROF_MODE=ids
+full vac count 'va_batch_kernel<\(int\)0' PROF_NQ=10000 PROF_MODE=count
+full colb ids 'col_batch_ids|expand' PROF_NQ=32 PROF_MODE=ids PROF_PATH=columnar_batch
+full col ids 'col_scan_kernel' PROF_NQ=4 PROF_MODE=ids PROF_PATH=columnar
+full va count 'va_scan_kernel' PROF_NQ=4 PROF_MODE=count PROF_PATH=vafile
+full row count 'row_scan_kernel' PROF_NQ=2 PROF_MODE=count PROF_PATH=rowwise PROF_CFG=c2
+cat $OUT/rc.txt
