@@ -391,6 +391,7 @@ def main():
     if merge and not args.merge_in_step:
         exchange()
         xms = timed(exchange, 3, stream, world)
+        torch.cuda.empty_cache()   # the exchange's buffers (every rank's ids) before the e2e pools
         xchg = {"ms_per_step": xms, "ids_total": total_ids, "bytes_in_per_rank": 4 * (total_ids - total_local),
                 "included_in_value": False,
                 "how": "NCCL all_gather of every rank's padded id slices + mdrq_copy_segments placement; "

@@ -362,20 +362,23 @@ uint16_t host_code(const float* b, uint32_t nb, float v) {
 // dimension u and table cell c the overlap / containment masks of the pass's
 // queries (vabatch.cu).  Table cells are the stored 8-bit codes >> shift.
 // A batch of more than one pass is split into passes of queries that are
-// close in one dimension: sorted by their low cell there, a pass's queries
-// overlap only a band of that dimension's cells, so the pass's cell mask is
-// sparse and the kernel drops every tuple outside the band before reading
-// its table rows (vabatch.cu, W2 passes).  The dimension is the one whose
-// sorted passes cover the fewest cells (quantile cells hold ~equal tuple
-// counts, so covered cells ~ surviving tuples); no reordering when even that
-// one leaves > 85 % of the cells, or for a single pass.  Returns slot ->
-// query, empty for the identity.
+// close in one or two dimensions: sorted by their low cell there, a pass's
+// queries overlap only a band of those dimensions' cells, so the pass's cell
+// masks are sparse and the kernel drops every tuple outside the band before
+// reading its table rows (vabatch.cu, W2 passes).  Orders tried: every
+// constrained dimension alone, and pairs of the four best ones (groups of
+// g_a x 1024 queries sorted by dimension a, each group's passes sorted by b);
+// the score of an order is the mean over its passes of the product of the
+// sorted dimensions' covered-cell fractions -- the surviving tuples, since
+// quantile cells hold ~equal tuple counts.  No reordering when even the best
+// keeps > 85 % of the tuples, or for a single pass.  Returns slot -> query,
+// empty for the identity.
 std::vector<uint32_t> choose_vb_order(const mdrq_store* s, const mdrq_batch* b) {
     const uint32_t nq = b->nq, m = s->m, bits = s->va_bits;
     if (nq <= 1024 || !bits) return {};
     const uint32_t cb = std::min<uint32_t>(bits, 6), cells = 1u << cb, sh = bits - cb;
     const unsigned long long full = cells == 64 ? ~0ull : ((1ull << cells) - 1);
-    // per (query, dim): cell range in `cells` units; lo > hi = empty; none = unconstrained
+    // per (query, dim): cell range in `cells` units; lo > hi = empty; kFree = unconstrained
     constexpr int16_t kFree = -1;
     std::vector<int16_t> clo(size_t(nq) * m, kFree), chi(size_t(nq) * m, kFree);
     std::vector<uint8_t> used(m, 0);
@@ -387,35 +390,70 @@ std::vector<uint32_t> choose_vb_order(const mdrq_store* s, const mdrq_batch* b) 
             clo[size_t(q) * m + p.dim] = int16_t(empty ? 1 : (p.cl >> sh));
             chi[size_t(q) * m + p.dim] = int16_t(empty ? 0 : (p.ch >> sh));
         }
+    // covered-cell fraction of dimension d over slots [q0, q1) of `order`
+    auto coverage = [&](const std::vector<uint32_t>& order, uint32_t d, uint32_t q0, uint32_t q1) {
+        unsigned long long mk = 0;
+        for (uint32_t i = q0; i < q1 && mk != full; ++i) {
+            const int lo = clo[size_t(order[i]) * m + d], hi = chi[size_t(order[i]) * m + d];
+            if (lo == kFree) {
+                mk = full;
+            } else if (lo <= hi) {
+                const int l = std::max(lo, 0), h = std::min(hi, int(cells) - 1);
+                if (l <= h) mk |= (h - l == 63 ? ~0ull : ((1ull << (h - l + 1)) - 1)) << l;
+            }
+        }
+        return double(__builtin_popcountll(mk & full)) / cells;
+    };
+    auto by_dim = [&](std::vector<uint32_t>& order, uint32_t d, size_t from, size_t to) {
+        std::stable_sort(order.begin() + from, order.begin() + to, [&](uint32_t x, uint32_t y) {
+            return clo[size_t(x) * m + d] < clo[size_t(y) * m + d];
+        });
+    };
+    // mean surviving fraction of an order whose passes are sorted on dims ds
+    auto score = [&](const std::vector<uint32_t>& order, std::initializer_list<uint32_t> ds) {
+        double sum = 0;
+        for (uint32_t q0 = 0; q0 < nq; q0 += 1024) {
+            const uint32_t q1 = std::min<uint32_t>(nq, q0 + 1024);
+            double f = 1.0;
+            for (uint32_t d : ds) f *= coverage(order, d, q0, q1);
+            sum += f * (q1 - q0);
+        }
+        return sum / nq;
+    };
     double best = 0.85;
     std::vector<uint32_t> best_order, order(nq);
+    std::vector<std::pair<double, uint32_t>> one;
     for (uint32_t d = 0; d < m; ++d) {
         if (!used[d]) continue;
         for (uint32_t q = 0; q < nq; ++q) order[q] = q;
-        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
-            return clo[size_t(x) * m + d] < clo[size_t(y) * m + d];
-        });
-        double cov = 0;
-        for (uint32_t q0 = 0; q0 < nq; q0 += 1024) {
-            unsigned long long mk = 0;
-            const uint32_t q1 = std::min<uint32_t>(nq, q0 + 1024);
-            for (uint32_t i = q0; i < q1 && mk != full; ++i) {
-                const int lo = clo[size_t(order[i]) * m + d], hi = chi[size_t(order[i]) * m + d];
-                if (lo == kFree) {
-                    mk = full;
-                } else if (lo <= hi) {
-                    const int l = std::max(lo, 0), h = std::min(hi, int(cells) - 1);
-                    if (l <= h) mk |= (h - l == 63 ? ~0ull : ((1ull << (h - l + 1)) - 1)) << l;
-                }
-            }
-            cov += double(__builtin_popcountll(mk & full)) / cells * (q1 - q0);
-        }
-        cov /= nq;
-        if (cov < best) {
-            best = cov;
+        by_dim(order, d, 0, nq);
+        const double sc = score(order, {d});
+        one.push_back({sc, d});
+        if (sc < best) {
+            best = sc;
             best_order = order;
         }
     }
+    std::sort(one.begin(), one.end());
+    const uint32_t passes = (nq + 1023) / 1024;
+    const size_t top = std::min<size_t>(one.size(), 4);
+    for (size_t ia = 0; ia < top; ++ia)
+        for (size_t ib = 0; ib < top; ++ib) {
+            if (ia == ib) continue;
+            const uint32_t da = one[ia].second, db = one[ib].second;
+            for (uint32_t ga = 2; ga <= passes / 2; ++ga) {
+                const uint32_t gb = (passes + ga - 1) / ga;   // passes per group
+                for (uint32_t q = 0; q < nq; ++q) order[q] = q;
+                by_dim(order, da, 0, nq);
+                for (size_t g0 = 0; g0 < nq; g0 += size_t(gb) * 1024)
+                    by_dim(order, db, g0, std::min<size_t>(nq, g0 + size_t(gb) * 1024));
+                const double sc = score(order, {da, db});
+                if (sc < best) {
+                    best = sc;
+                    best_order = order;
+                }
+            }
+        }
     return best_order;
 }
 

@@ -7,6 +7,7 @@ OUT=gpurun_out
 mkdir -p $OUT
 : > $OUT/rc.txt
 NCU="ncu --target-processes application-only --clock-control none"
+if [ -z "${SKIP_BENCH:-}" ]; then
 python bench.py > $OUT/bench_default.log 2> $OUT/bench_default.err
 echo "bench=$?" >> $OUT/rc.txt
 # launch list of one bench step (+ store build, warm-up, profiling passes)
@@ -15,13 +16,18 @@ $B > $OUT/plain.log 2>&1
 echo "plain=$?" >> $OUT/rc.txt
 timeout 1500 $NCU --metrics gpu__time_duration.sum --csv --log-file $OUT/launches.csv $B > $OUT/ncu_launches.log 2>&1
 echo "launches=$?" >> $OUT/rc.txt
+fi
 # full sets: the bench batch (C5, 10 000 queries) -- first filter pass + its
 # scatter in ids mode, the first filter pass in count mode
-full() {   # name, nvtx range, kernel regex, env...
+full() {   # name, nvtx range, kernel regex, VAR=value...
     local name=$1 range=$2 regex=$3; shift 3
-    env "$@" python tools/prof_c5.py > $OUT/probe_$name.log 2>&1 && \
-    timeout 1800 $NCU --set full --import-source on --kernel-name-base demangled --nvtx --nvtx-include "$range/" \
-        -k regex:"$regex" -c 2 -o $OUT/prof_$name -f env "$@" python tools/prof_c5.py > $OUT/ncu_$name.log 2>&1
+    (
+        for kv in "$@"; do export "$kv"; done
+        python tools/prof_c5.py > $OUT/probe_$name.log 2>&1 && \
+        timeout 1800 $NCU --set full --import-source on --kernel-name-base demangled --nvtx \
+            --nvtx-include "$range/" -k regex:"$regex" -c 2 -o $OUT/prof_$name -f \
+            python tools/prof_c5.py > $OUT/ncu_$name.log 2>&1
+    )
     echo "$name=$?" >> $OUT/rc.txt
 }
 full vab ids 'va_batch_kernel<\(int\)3|vb_scatter' PROF_NQ=10000 PROF_MODE=ids
