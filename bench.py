@@ -530,11 +530,18 @@ def main():
 
 
 def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
-    """e2e through the public API (DeviceStore.ids_stream): per step the
-    query bounds go host->device and the step's ids + offsets come back into
-    pinned host memory; step k's copy overlaps step k+1's device pass."""
+    """e2e through the reference-facing API: the VA-file access method over
+    this store (what build_method("vafile") returns) answers K repetitions of
+    the batch with ``search_stream`` -- per step the RangeQuery batch is
+    stacked and its bounds go host->device, the planner runs the sorted
+    multi-query passes, and the step's ids + offsets come back into pinned
+    host memory; step k's copy overlaps step k+1's device pass."""
     import torch
     import torch.distributed as dist
+    from paper_1801_03644_b200 import workload
+    from paper_1801_03644_b200.vafile import VaFile
+    method = VaFile(store, None)
+    queries = workload.queries_from_arrays(lo, hi)
     ids_bytes = int(total_local * 4 + (nq + 1) * 8)
     try:
         import psutil
@@ -548,16 +555,16 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
     pin_s = time.perf_counter() - t0
     e2e_steps = max(3, min(args.steps, 10))
     # warm: every slot of the stream (3) sizes its result pool once
-    store.ids_stream([(lo, hi)] * 3, args.path, outs=[pinned[k % nbuf] for k in range(3)])
-    info = {}
+    method.search_stream([queries] * 3, outs=[pinned[k % nbuf] for k in range(3)])
     if world > 1:
         dist.barrier()
+    info = {}
     t0 = time.perf_counter()
-    res = store.ids_stream([(lo, hi)] * e2e_steps, args.path, outs=[pinned[k % nbuf] for k in range(e2e_steps)],
-                           info=info)
+    res = method.search_stream([queries] * e2e_steps, outs=[pinned[k % nbuf] for k in range(e2e_steps)], info=info)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    assert all(int(o[-1]) == total_local for o, _ in res), "stream result differs from the timed batch"
+    assert all(int(r.offsets[-1]) == total_local for r in res), "stream result differs from the timed batch"
     del res
+    h2d = info.get("h2d_bytes", 0) // e2e_steps   # the batch's descriptors: bounds, query-mask tables, order
     store.ids(lo, hi, args.path, out=pinned[0])   # warm
     t0 = time.perf_counter()
     sync_n = 2
@@ -582,10 +589,11 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
     d2h_peak = probe / (min(d2h_ms) / 1e3) / 1e9
     del d_src, h_dst, pinned
     return {"value": n_total * nq / e2e_s, "unit": "tuple-queries/s",
-            "h2d_bytes_per_step": int(info.get("h2d_bytes", 0) // e2e_steps),
+            "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": ids_bytes * world,
-            "api": f"DeviceStore.ids_stream, {e2e_steps} steps pipelined (copy of step k under the device pass "
-                   f"of step k+1), {nbuf} pinned output buffer(s); wall clock, max over ranks",
+            "api": f"VaFile.search_stream (the build_method('vafile') object over the bench store): {e2e_steps} "
+                   f"repetitions of the RangeQuery batch pipelined (copy of step k under the device pass of step "
+                   f"k+1), {nbuf} pinned output buffer(s); wall clock, max over ranks",
             "ms_per_step": e2e_s * 1e3,
             "d2h_roofline": {"achieved_gbs": ids_bytes / e2e_s / 1e9, "peak_gbs": d2h_peak,
                              "frac": ids_bytes / e2e_s / 1e9 / d2h_peak,

@@ -160,15 +160,16 @@ __global__ void __launch_bounds__(256) col_batch_count_kernel(const BatchArgs a)
 // ---------------------------------------------------------------------------
 // Multi-query ids pass (VerticalScan.search over a batch, scan.py:190-211,
 // with the column bytes read once per <= 32 queries).  A CTA owns whole
-// 65536-tuple compaction chunks (grid-stride); each of its 8 warps takes 32
-// consecutive tuples per step, one tuple per lane (128-byte coalesced loads
-// of every union column; the NaN padding up to n_pad never matches).  The
-// pass's queries are walked with their bounds broadcast from shared memory:
-// query q's verdicts of the warp's 32 tuples are one ballot, kept by lane q,
-// which stores it as word t/32 of query q's mask (query-major, the layout the
-// single-query expansion reads) and adds its popcount to q's chunk count.
-// No atomics leave the CTA: every chunk count is written once.
-template <int KB>
+// 65536-tuple compaction chunks (grid-stride); each of its 8 warps takes 128
+// consecutive tuples per step, lane l the tuples l, l+32, l+64, l+96 (four
+// 128-byte coalesced loads per union column; the NaN padding up to n_pad
+// never matches), so a query's bounds -- broadcast from shared memory -- are
+// read once per 4 tuples, and ballot t of a query IS its mask word for
+// tuples 32t..32t+31.  Lane q keeps query q's four words, stores them to
+// query q's mask (query-major, the layout the expansion reads) and adds their
+// popcounts to q's chunk count.  No atomics leave the CTA: every chunk count
+// is written once.
+template <int KB, int TPT>
 __global__ void __launch_bounds__(256) col_batch_ids_kernel(const BatchArgs a, uint32_t* __restrict__ masks,
                                                             uint64_t mask_words, uint32_t* __restrict__ chunk_counts,
                                                             uint32_t nchunks) {
@@ -185,26 +186,43 @@ __global__ void __launch_bounds__(256) col_batch_ids_kernel(const BatchArgs a, u
         uint32_t acc = 0;
         const uint64_t c0 = uint64_t(chunk) * kChunkTuples;
         const uint64_t c1 = c0 + kChunkTuples < a.n ? c0 + kChunkTuples : a.n;
-        for (uint64_t t0 = c0 + warp * 32; t0 < c1; t0 += 256) {
-            // t0 < n <= n_pad and n_pad is a multiple of 32: the whole warp
-            // reads inside the padded columns
-            float v[KB];
+        for (uint64_t t0 = c0 + warp * (32 * TPT); t0 < c1; t0 += 8 * 32 * TPT) {
+            // words t0/32 .. +3; a word starting at or past n is not stored
+            // (tuples past n inside a word read the NaN padding)
+            float v[KB][TPT];
 #pragma unroll
-            for (int d = 0; d < KB; ++d) v[d] = __ldcs(a.cols + uint64_t(s_ud[d]) * a.stride + t0 + lane);
-            uint32_t mine = 0;
+            for (int d = 0; d < KB; ++d) {
+                const float* col = a.cols + uint64_t(s_ud[d]) * a.stride + t0 + lane;
+#pragma unroll
+                for (int t = 0; t < TPT; ++t)
+                    v[d][t] = t0 + 32 * t < a.n ? __ldcs(col + 32 * t) : __int_as_float(0x7fc00000);
+            }
+            uint32_t mine[TPT];
+#pragma unroll
+            for (int t = 0; t < TPT; ++t) mine[t] = 0u;
             for (uint32_t q = 0; q < nqp; ++q) {
-                bool ok = true;
+                bool ok[TPT];
+#pragma unroll
+                for (int t = 0; t < TPT; ++t) ok[t] = true;
 #pragma unroll
                 for (int d = 0; d < KB; ++d) {
                     const float2 b = s_b[q][d];
-                    ok = ok && (b.x <= v[d]) && (v[d] <= b.y);
+#pragma unroll
+                    for (int t = 0; t < TPT; ++t) ok[t] = ok[t] && (b.x <= v[d][t]) && (v[d][t] <= b.y);
                 }
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ok);
-                if (lane == q) mine = bal;
+#pragma unroll
+                for (int t = 0; t < TPT; ++t) {
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, ok[t]);
+                    if (lane == q) mine[t] = bal;
+                }
             }
             if (lane < nqp) {
-                masks[uint64_t(lane) * mask_words + t0 / 32] = mine;
-                acc += __popc(mine);
+#pragma unroll
+                for (int t = 0; t < TPT; ++t)
+                    if (t0 + 32 * t < a.n) {
+                        masks[uint64_t(lane) * mask_words + t0 / 32 + t] = mine[t];
+                        acc += __popc(mine[t]);
+                    }
             }
         }
         if (acc) atomicAdd(&s_cnt[lane], acc);
@@ -238,16 +256,18 @@ void dispatch_exact(const BatchArgs& a, int num_sms, cudaStream_t st, std::integ
 template <int KB>
 void run_batch_ids(const BatchArgs& a, uint32_t* masks, uint64_t mask_words, uint32_t* chunk_counts, int num_sms,
                    cudaStream_t st) {
+    // tuples per lane: as many as the registers allow (the count pass's choice)
+    constexpr int TPT = KB <= 16 ? 4 : KB <= 32 ? 2 : 1;
     static int blocks_per_sm = -1;
     if (blocks_per_sm < 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, col_batch_ids_kernel<KB>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, col_batch_ids_kernel<KB, TPT>, 256, 0);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     const uint32_t nchunks = uint32_t((a.n + kChunkTuples - 1) / kChunkTuples);
     uint64_t grid = uint64_t(num_sms) * blocks_per_sm;
     if (grid > nchunks) grid = nchunks;
     if (grid == 0) return;
-    col_batch_ids_kernel<KB><<<unsigned(grid), 256, 0, st>>>(a, masks, mask_words, chunk_counts, nchunks);
+    col_batch_ids_kernel<KB, TPT><<<unsigned(grid), 256, 0, st>>>(a, masks, mask_words, chunk_counts, nchunks);
 }
 
 template <int... Ks>

@@ -147,7 +147,7 @@ class _GpuScan:
         offsets, ids = self.store.ids(lo, hi, path or self._path)
         return BatchResult(offsets, ids)
 
-    def search_stream(self, batches, outs=None) -> list:
+    def search_stream(self, batches, outs=None, info: dict | None = None) -> list:
         """Pipelined ids of a sequence of query batches (a serving loop /
         the reference harness's repetitions, bench.py:178-186): one
         BatchResult per batch; batch k's device->host copy runs under batch
@@ -159,7 +159,7 @@ class _GpuScan:
             for q in queries:
                 self._check(q)
             pairs.append(stack_queries(queries, self.m))
-        return [BatchResult(o, i) for o, i in self.store.ids_stream(pairs, self._batch_path, outs=outs)]
+        return [BatchResult(o, i) for o, i in self.store.ids_stream(pairs, self._batch_path, outs=outs, info=info)]
 
     def search_batch(self, queries) -> BatchResult:
         """Ids of every query of the batch, ascending per query."""

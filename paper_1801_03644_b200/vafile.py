@@ -150,7 +150,7 @@ class VaFile:
         lo, hi = stack_queries(queries, self.m)
         return self.store.count(lo, hi, "auto")
 
-    def search_stream(self, batches, outs=None) -> list:
+    def search_stream(self, batches, outs=None, info: dict | None = None) -> list:
         """Pipelined ids of a sequence of query batches (see
         _GpuScan.search_stream)."""
         pairs = []
@@ -160,7 +160,7 @@ class VaFile:
                 if q.m != self.m:
                     raise ValueError(f"query has {q.m} dimensions, grid has {self.m}")
             pairs.append(stack_queries(queries, self.m))
-        res = self.store.ids_stream(pairs, "auto", outs=outs)
+        res = self.store.ids_stream(pairs, "auto", outs=outs, info=info)
         if self._ids is not None:
             out = []
             for offs, ids in res:

@@ -1,7 +1,7 @@
 """Summarise ncu outputs (run here, no GPU needed) into a markdown table.
 
     python tools/ncu_summary.py launches gpurun_out/launches.csv
-    python tools/ncu_summary.py full gpurun_out/prof.ncu-rep
+    python tools/ncu_summary.py full gpurun_out/prof.ncu-rep   (or prof.raw.csv)
 """
 
 from __future__ import annotations
@@ -55,9 +55,18 @@ def launches(path: str) -> str:
     return "\n".join(out)
 
 
+def raw_rows(path: str):
+    """The raw page of a capture: an .ncu-rep (exported here) or the
+    .raw.csv tools/profile_round.sh exports on the GPU box."""
+    if path.endswith(".csv"):
+        text = open(path).read()
+    else:
+        text = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    return list(csv.reader(io.StringIO(text)))
+
+
 def full(path: str) -> str:
-    text = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(text)))
+    rows = raw_rows(path)
     hdr, units = rows[0], rows[1]
     out = []
     for r in rows[2:]:

@@ -19,8 +19,9 @@ echo "launches=$?" >> $OUT/rc.txt
 fi
 # full sets: the bench batch (C5, 10 000 queries) -- first filter pass + its
 # scatter in ids mode, the first filter pass in count mode
-full() {   # name, nvtx range, kernel regex, VAR=value...
+full() {   # name, nvtx range, kernel regex, VAR=value...   (ONLY="a b": just those)
     local name=$1 range=$2 regex=$3; shift 3
+    if [ -n "${ONLY:-}" ] && [[ " $ONLY " != *" $name "* ]]; then return; fi
     (
         for kv in "$@"; do export "$kv"; done
         python tools/prof_c5.py > $OUT/probe_$name.log 2>&1 && \
@@ -37,3 +38,12 @@ full col ids 'col_scan_kernel' PROF_NQ=4 PROF_MODE=ids PROF_PATH=columnar
 full va count 'va_scan_kernel' PROF_NQ=4 PROF_MODE=count PROF_PATH=vafile
 full row count 'row_scan_kernel' PROF_NQ=2 PROF_MODE=count PROF_PATH=rowwise PROF_CFG=c2
 cat $OUT/rc.txt
+# export what the summary needs (raw metrics, per-instruction source view of
+# the bit-sliced kernels) and drop captures too large to bring back
+for r in $OUT/prof_*.ncu-rep; do
+    b=${r%.ncu-rep}
+    ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
+    case $b in *vab|*vac) ncu -i $r --page source --csv --print-source sass > $b.src.csv 2>/dev/null; gzip -f $b.src.csv;; esac
+    [ $(stat -c %s $r) -gt 15000000 ] && rm -f $r
+done
+ls -la $OUT
