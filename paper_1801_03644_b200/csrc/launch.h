@@ -111,13 +111,6 @@ struct VaBatchArgs {
     const uint32_t* tables;      // query-mask words, layout per va_batch_pv(kb) (above)
     const float2* qbounds;       // exact (lo, hi), +-inf where unconstrained; layout per va_batch_pv(kb)
     const uint32_t* qcmask;      // [1024] constrained union dims per query (bit u)
-    // dense passes of unions of <= 16 dims (code refinement), at the query's
-    // swizzled slot j = q ^ ((q >> 5) & 7): code bounds [1024][1 or 2] uint4
-    // (<= 8 dims: lo codes of dims 0-7, hi codes of dims 0-7; else lo codes
-    // of dims 0-15, hi codes of dims 0-15; an unconstrained dim 0 .. max)
-    // and the float bounds [1024][vdims] float2 for the edge compares
-    const uint4* qcb;
-    const float2* qfb;
     uint32_t grid;               // CTAs (chunks = grid * warps)
     uint64_t chunk_tuples;       // tuples per chunk (multiple of 128, < 65536: u16 counters)
     uint32_t nchunks;            // subchunks: ceil(n / chunk_tuples), one warp each

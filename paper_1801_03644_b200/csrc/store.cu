@@ -166,7 +166,7 @@ struct Pass {
 struct VbPass {
     uint32_t q0 = 0, nqp = 0, kb = 0, cells = 0, shift = 0;
     bool fallback = false;   // union wider than kVaBatchMaxDims: per-query VA
-    size_t udim_off = 0, table_off = 0, qb_off = 0, cm_off = 0, qcb_off = 0, qfb_off = 0;
+    size_t udim_off = 0, table_off = 0, qb_off = 0, cm_off = 0;
     uint32_t prune = 0;                  // union dims whose cell mask is not full
     unsigned long long cellmask[kVaBatchMaxDims] = {};
 };
@@ -194,8 +194,6 @@ struct mdrq_batch {
     std::vector<uint32_t> vb_tables;
     std::vector<float2> vb_qb;
     std::vector<uint32_t> vb_cm;   // per query of a pass: constrained union dims
-    std::vector<uint32_t> vb_qcb;  // code bounds (uint4 words) of the passes of <= 16 dims
-    std::vector<float2> vb_qfb;    // their query-major float bounds
     // sorted batch: slot i of the passes holds query vb_perm[i] (empty: slot = query)
     std::vector<uint32_t> vb_perm;
     DBuf<uint32_t> d_vb_perm;
@@ -203,8 +201,6 @@ struct mdrq_batch {
     DBuf<uint32_t> d_vb_tables;
     DBuf<float2> d_vb_qb;
     DBuf<uint32_t> d_vb_cm;
-    DBuf<uint32_t> d_vb_qcb;
-    DBuf<float2> d_vb_qfb;
     // per-batch accumulators, carved from one allocation so one memset
     // zeroes them all per pass (enqueue)
     DBuf<unsigned long long> d_scratch;
@@ -227,7 +223,7 @@ struct mdrq_batch {
     void release_device() {
         d_descs.release(); d_preds.release(); d_udims.release(); d_bounds.release(); d_cmask.release();
         d_vb_udims.release(); d_vb_tables.release(); d_vb_qb.release(); d_vb_cm.release();
-        d_scratch.release(); own_ids.release(); d_vb_qcb.release(); d_vb_qfb.release();
+        d_scratch.release(); own_ids.release();
     }
 };
 
@@ -483,10 +479,7 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
     b->vb_tables.clear();
     b->vb_qb.clear();
     b->vb_cm.clear();
-    b->vb_qcb.clear();
-    b->vb_qfb.clear();
     const uint32_t m = s->m, bits = s->va_bits;
-    const uint32_t maxcode = (1u << bits) - 1u;
     const bool sorted = !b->vb_perm.empty();
     auto query_of = [&](uint32_t slot) { return sorted ? b->vb_perm[slot] : slot; };
     for (uint32_t q0 = 0; q0 < b->nq; q0 += 1024) {
@@ -523,8 +516,6 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         ps.table_off = b->vb_tables.size();
         ps.qb_off = b->vb_qb.size();
         ps.cm_off = b->vb_cm.size();
-        ps.qcb_off = b->vb_qcb.size() / 4;   // in uint4
-        ps.qfb_off = b->vb_qfb.size();
         b->vb_udims.insert(b->vb_udims.end(), ud.begin(), ud.end());
         const bool pv = va_batch_pv(ps.kb);
         const uint32_t qstride = pv ? va_batch_vdims(ps.kb) : ps.kb;
@@ -539,14 +530,6 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         // queries unconstrained in dimension u: every cell, set once per word below
         std::vector<uint32_t> free_mask(size_t(ps.kb) * 32, 0u);
         std::vector<uint32_t> cmv(1024, 0u);
-        // code refinement (dense passes of <= 16 dims): code bounds as bytes
-        // lo[16] / hi[16] per swizzled slot, unconstrained 0 .. maxcode, and
-        // the float bounds query-major
-        const uint32_t cbw = qstride <= 8 ? 1 : 2;
-        std::vector<uint8_t> cbl(size_t(1024) * 16, 0), cbh(size_t(1024) * 16, 0xFF);
-        std::vector<float2> qfv(pv ? size_t(1024) * qstride : 0, make_float2(-INFINITY, INFINITY));
-        if (pv)
-            for (size_t i = 0; i < size_t(1024) * 16; ++i) cbh[i] = uint8_t(maxcode);
         std::vector<unsigned long long> cmask(ps.kb, 0ull);
         const unsigned long long cfull = cells == 64 ? ~0ull : ((1ull << cells) - 1);
         for (uint32_t qi = 0; qi < ps.nqp; ++qi) {
@@ -563,11 +546,6 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
                 // (narrow: query qi at slot qi ^ ((qi >> 5) & 7), vabatch.cu)
                 const size_t qs = qi ^ ((qi >> 5) & 7u);
                 qbv[pv ? (size_t(u / 2) * 1024 + qs) * 2 + u % 2 : size_t(qi) * qstride + u] = make_float2(p.lo, p.hi);
-                if (pv) {
-                    cbl[qs * 16 + u] = uint8_t(std::min<uint32_t>(p.cl, maxcode));
-                    cbh[qs * 16 + u] = uint8_t(std::min<uint32_t>(p.ch, maxcode));
-                    qfv[qs * qstride + u] = make_float2(p.lo, p.hi);
-                }
                 if (p.lo > p.hi) continue;   // empty interval (kernel level only): no cell overlaps
                 // overlap cells [lo_c, hi_c]; containment drops the edge cells
                 const int lo_c = int(p.cl) >> ps.shift, hi_c = int(p.ch) >> ps.shift, top = int(cells) - 1;
@@ -611,25 +589,6 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         b->vb_tables.insert(b->vb_tables.end(), tab.begin(), tab.end());
         b->vb_qb.insert(b->vb_qb.end(), qbv.begin(), qbv.end());
         b->vb_cm.insert(b->vb_cm.end(), cmv.begin(), cmv.end());
-        if (pv) {
-            // per slot: cbw uint4 = (lo dims 0-7, hi dims 0-7) or (lo 0-15, hi 0-15)
-            auto word = [](const uint8_t* p4) {
-                return uint32_t(p4[0]) | uint32_t(p4[1]) << 8 | uint32_t(p4[2]) << 16 | uint32_t(p4[3]) << 24;
-            };
-            for (size_t sl = 0; sl < 1024; ++sl) {
-                const uint8_t* l = &cbl[sl * 16];
-                const uint8_t* h = &cbh[sl * 16];
-                if (cbw == 1) {
-                    const uint32_t w4[4] = {word(l), word(l + 4), word(h), word(h + 4)};
-                    b->vb_qcb.insert(b->vb_qcb.end(), w4, w4 + 4);
-                } else {
-                    const uint32_t w8[8] = {word(l), word(l + 4), word(l + 8), word(l + 12),
-                                            word(h), word(h + 4), word(h + 8), word(h + 12)};
-                    b->vb_qcb.insert(b->vb_qcb.end(), w8, w8 + 8);
-                }
-            }
-            b->vb_qfb.insert(b->vb_qfb.end(), qfv.begin(), qfv.end());
-        }
         b->vb_passes.push_back(ps);
     }
 }
@@ -777,8 +736,6 @@ void upload_batch(mdrq_store* s, mdrq_batch* b, bool sync = true) {
     upload(b->d_vb_tables, b->vb_tables, s->stream);
     upload(b->d_vb_qb, b->vb_qb, s->stream);
     upload(b->d_vb_cm, b->vb_cm, s->stream);
-    upload(b->d_vb_qcb, b->vb_qcb, s->stream);
-    upload(b->d_vb_qfb, b->vb_qfb, s->stream);
     upload(b->d_vb_perm, b->vb_perm, s->stream);
     const size_t nq = b->nq;
     b->d_scratch.reserve(scratch_words(b->nq));
@@ -801,8 +758,7 @@ uint64_t upload_bytes(const mdrq_batch* b) {
            b->udims.size() * sizeof(uint16_t) + b->bounds.size() * sizeof(float2) +
            b->cmask.size() * sizeof(unsigned long long) + b->vb_udims.size() * sizeof(uint16_t) +
            b->vb_tables.size() * sizeof(uint32_t) + b->vb_qb.size() * sizeof(float2) +
-           b->vb_cm.size() * sizeof(uint32_t) + b->vb_perm.size() * sizeof(uint32_t) +
-           b->vb_qcb.size() * sizeof(uint32_t) + b->vb_qfb.size() * sizeof(float2);
+           b->vb_cm.size() * sizeof(uint32_t) + b->vb_perm.size() * sizeof(uint32_t);
 }
 
 uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
@@ -884,8 +840,6 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.tables = b->d_vb_tables.p + ps.table_off;
     a.qbounds = b->d_vb_qb.p + ps.qb_off;
     a.qcmask = b->d_vb_cm.p + ps.cm_off;
-    a.qcb = reinterpret_cast<const uint4*>(b->d_vb_qcb.p) + ps.qcb_off;
-    a.qfb = b->d_vb_qfb.p + ps.qfb_off;
     // one CTA per SM (the tables take most of the shared memory); chunks of
     // < 65536 tuples (16-bit per-warp counters), identical in every mode
     a.grid = uint32_t(s->num_sms);

@@ -56,6 +56,13 @@ __device__ __forceinline__ float f4_get(const float4& w, uint32_t i) {
     return i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w;
 }
 
+// staged-value slot of tuple t (in the block) and pair h in a warp's buffer:
+// h * 128 + (t & 3) * 32 + (t >> 2).  Lane l stages its tuples 4l .. 4l+3, so
+// every store instruction hits 32 consecutive slots (conflict-free; the
+// earlier tuple-major layout took 4 wavefronts per ideal one on C5)
+__device__ __forceinline__ uint32_t val_slot(uint32_t t, uint32_t h) {
+    return h * 128u + ((t & 3u) << 5) + (t >> 2);
+}
 
 // LW = lanes per tuple: 32 (a pass of up to 1 024 queries, lane w = query
 // word w), or 16 / 8 for passes of <= 512 / <= 256 queries, whose 16 / 8
@@ -82,6 +89,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     // memory (8 bytes per tuple): one LDS.64 hands the TPI lane groups of an
     // instruction their tuples' cells of all dims, instead of one SHFL per
     // dimension and code word (the SHFLs cost data-pipe wavefronts too)
+    constexpr bool SCODE = TPI > 1 && KB <= 8 && MODE != 2;
     extern __shared__ __align__(16) uint32_t sm[];
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
     constexpr bool PV = va_batch_pv(KB);           // values + bounds in smem, overlap-only table
@@ -89,34 +97,16 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     constexpr int VS = KBV % 4 == 0 ? 4 : 2;       // floats per staging slot (float4 / float2)
     constexpr int H = PV ? KBV / VS : 1;           // staging slots per tuple
     constexpr bool DENSE = MODE != 2;              // candidates refined lane-parallel from a queue
-    // CR ("code refinement"), the dense passes of unions of <= 16 dims: every
-    // block's 8-bit codes are staged tuple-major in shared memory (SCW words
-    // per tuple: 8 or 16 dims); the table rows are addressed from them (no
-    // shuffle per dimension and code word), and a candidate (tuple, query) is
-    // refined on the codes first -- a code strictly inside the query's code
-    // range [cl, ch] passes, one outside fails -- against the query's code
-    // bounds in shared memory (16 / 32 bytes per query); only the dims where
-    // the code equals cl or ch compare float32 (the staged value or the
-    // column, the query's bound from global memory, L1-resident).
-    constexpr bool CR = PV && DENSE;
-    constexpr int SCW = KBV <= 8 ? 2 : 4;          // CR: staged code words per tuple
-    constexpr int CBW = KBV <= 8 ? 1 : 2;          // CR: 16-byte code-bound words per query
-    // row addresses come from staged codes (CR) instead of shuffles
-    constexpr bool SCODE = CR;
     // values staged on chip; the recount fallback of 9/10-dim unions reads
     // them from global memory instead (its per-warp counters need the room)
     constexpr bool STAGE = PV && KB <= 10 && !(MODE == 2 && KB > 8);
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_end = sm + va_batch_table_words(KB, K);
-    // CR: per query slot its code bounds [1024][CBW] uint4 and constrained
-    // union dims [1024] u32; else (PV) the exact query bounds [KBV/2][1024]
-    // float4 (lo_u, hi_u, lo_u+1, hi_u+1 of dim pair u/2).  Then every warp's
-    // staged block values: [H][4][32] slots of VS floats (slot of tuple t, pair
-    // h: h*128 + (t & 3)*32 + (t >> 2) -- the lanes' stores hit consecutive slots)
-    uint4* s_cb = reinterpret_cast<uint4*>(s_end);
-    uint32_t* s_qcm = reinterpret_cast<uint32_t*>(s_cb + (CR ? 1024 * CBW : 0));
-    float4* s_qb = reinterpret_cast<float4*>(s_qcm + (CR ? 1024 : 0));
-    float* s_val = reinterpret_cast<float*>(s_qb + ((PV && !CR) ? 1024 * KBV / 2 : 0));
+    // PV: exact query bounds [KBV/2][1024] float4 (lo_u, hi_u, lo_u+1, hi_u+1
+    // of dim pair u/2) and every warp's staged block values [128 * H] slots of
+    // VS floats
+    float4* s_qb = reinterpret_cast<float4*>(s_end);
+    float* s_val = reinterpret_cast<float*>(s_qb + (PV ? 1024 * KBV / 2 : 0));
     uint32_t* s_rest = reinterpret_cast<uint32_t*>(s_val + (STAGE ? VB_WARPS * 128 * KBV : 0));
     // DENSE (modes 0, 3): CTA counters u32 [1024], then every warp's candidate
     // queue: entries uint2 [QCAP] = (overlap word, tuple-in-block << 5 | query
@@ -125,12 +115,12 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     uint32_t* s_cnt32 = s_rest;
     uint2* s_qe = reinterpret_cast<uint2*>(s_rest + 1024);
     uint32_t* s_qs = reinterpret_cast<uint32_t*>(s_qe + VB_WARPS * VB_QCAP);
-    // SCODE (PV, so no containment words): every warp's staged codes [128][SCW] u32
-    uint32_t* s_code = reinterpret_cast<uint32_t*>(s_qe + VB_WARPS * VB_QCAP);
+    // SCODE (PV, so no containment words): every warp's staged cells [128] uint2
+    uint2* s_code = reinterpret_cast<uint2*>(s_qe + VB_WARPS * VB_QCAP);
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_rest);
     // W2 (multi-word) dense passes: every warp's compacted list of the block's
-    // unpruned tuples [128] u8, after the queues and staged codes
-    uint8_t* s_alive = reinterpret_cast<uint8_t*>(s_qe + VB_WARPS * VB_QCAP) + (SCODE ? VB_WARPS * 128 * SCW * 4 : 0);
+    // unpruned tuples [128] u8, after the queues and staged cells
+    uint8_t* s_alive = reinterpret_cast<uint8_t*>(s_qe + VB_WARPS * VB_QCAP) + (SCODE ? VB_WARPS * 128 * 8 : 0);
 
     // the recount pass only runs when the single-pass staging overflowed
     if (MODE == 2 && *reinterpret_cast<volatile const uint32_t*>(a.overflow) == 0) return;
@@ -140,11 +130,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
         uint4* dst = reinterpret_cast<uint4*>(sm);
         const uint32_t n4 = va_batch_table_words(KB, K) / 4;
         for (uint32_t i = tid; i < n4; i += VB_THREADS) dst[i] = src[i];
-        if constexpr (CR) {
-            for (uint32_t i = tid; i < 1024 * CBW; i += VB_THREADS) s_cb[i] = a.qcb[i];
-            // (at the query's swizzled slot, like its code bounds)
-            for (uint32_t i = tid; i < 1024; i += VB_THREADS) s_qcm[i ^ ((i >> 5) & 7u)] = a.qcmask[i];
-        } else if constexpr (PV) {
+        if constexpr (PV) {
             const uint4* qsrc = reinterpret_cast<const uint4*>(a.qbounds);
             uint4* qdst = reinterpret_cast<uint4*>(s_qb);
             for (uint32_t i = tid; i < 1024 * KBV / 2; i += VB_THREADS) qdst[i] = qsrc[i];
@@ -156,7 +142,6 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     __syncthreads();
 
     const uint32_t shift = a.shift;
-    const uint32_t sh8 = 8u - shift;               // CR: code -> (cell << 8) is (code << sh8) & 0xFF00
     // byte offset of the lane's word in a table row:
     //   PV: overlap word (u, c, w) at byte (u/2*K + c)*256 + (u%2)*128 + w*4
     //   else (overlap, containment) uint2 (u, c, w) at byte (u*K + c)*256 + w*8
@@ -169,80 +154,16 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     const char* s_tab = reinterpret_cast<const char*>(sm);
     float* wval = s_val + warp * 128 * KBV;        // STAGE: this warp's staged values
     uint2* qe = s_qe + warp * VB_QCAP;
-    uint32_t* wcode = s_code + warp * 128 * SCW;   // SCODE: this warp's staged codes
+    uint2* wcode = s_code + warp * 128;            // SCODE: this warp's staged cells
     uint32_t* qs = s_qs + warp * VB_QCAP;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 2
     uint8_t* walive = s_alive + warp * 128;        // W2: compacted tuple list of the block
     const uint32_t lt = lanemask_lt();
 
-    // staged slots: tuple t of the block is slot (t & 3) * 32 + (t >> 2) --
-    // lane l stages its tuples 4l .. 4l+3, so every store instruction hits
-    // 32 consecutive slots (conflict-free); values: VS-float slot of pair h
-    // at h * 128 + that
-    auto tslot = [](uint32_t t) -> uint32_t { return ((t & 3u) << 5) | (t >> 2); };
-
     // Exact refinement of one query word for one tuple: bit b of the result
     // is set iff query wq + b (a candidate in `word`) contains the tuple.
     // tl = tuple within the staged block (PV), t = tuple index (wide unions).
     auto refine_word = [&](uint32_t word, uint32_t su, uint32_t tl, uint64_t t, uint32_t wq) -> uint32_t {
-      if constexpr (CR) {
-        uint32_t hits = 0u, r = word;
-        if (r) {
-            // the tuple's codes (dims 4w .. 4w+3 in word w)
-            uint32_t c[SCW];
-            if constexpr (SCW == 4) {
-                const uint4 x = reinterpret_cast<const uint4*>(wcode)[tslot(tl)];
-                c[0] = x.x; c[1] = x.y; c[2] = x.z; c[3] = x.w;
-            } else {
-                const uint2 x = reinterpret_cast<const uint2*>(wcode)[tslot(tl)];
-                c[0] = x.x; c[1] = x.y;
-            }
-            const uint32_t sw = (wq >> 5) & 7u;
-            while (r) {
-                const int b = __ffs(r) - 1;
-                r &= r - 1;
-                // query wq + b sits at slot wq + (b ^ (word & 7)) (bank spread)
-                const uint32_t j = wq + (uint32_t(b) ^ sw);
-                uint32_t lo[SCW], hi[SCW];
-                if constexpr (CBW == 1) {
-                    const uint4 x = s_cb[j];
-                    lo[0] = x.x; lo[1] = x.y; hi[0] = x.z; hi[1] = x.w;
-                } else {
-                    const uint4 x = s_cb[2 * j], y = s_cb[2 * j + 1];
-                    lo[0] = x.x; lo[1] = x.y; lo[2] = x.z; lo[3] = x.w;
-                    hi[0] = y.x; hi[1] = y.y; hi[2] = y.z; hi[3] = y.w;
-                }
-                bool ok = true;
-                uint32_t edge = 0;
-#pragma unroll
-                for (int u = 0; u < KB; ++u) {
-                    // code strictly inside [cl, ch]: in; outside: out; on cl or
-                    // ch: compare the float32 value (the quantile cell of the
-                    // code straddles the bound)
-                    const uint32_t sel = 0x4440u | uint32_t(u & 3);
-                    const uint32_t cu = __byte_perm(c[u >> 2], 0u, sel);
-                    const uint32_t lu = __byte_perm(lo[u >> 2], 0u, sel);
-                    const uint32_t hu = __byte_perm(hi[u >> 2], 0u, sel);
-                    ok = ok & (cu - lu <= hu - lu);
-                    edge |= uint32_t((cu == lu) | (cu == hu)) << u;
-                }
-                edge &= s_qcm[j];   // an unconstrained dim (codes 0 .. max) never needs floats
-                while (ok && edge) {
-                    const int u = __ffs(edge) - 1;
-                    edge &= edge - 1;
-                    float v;
-                    if constexpr (STAGE)
-                        v = wval[(uint32_t(u / VS) * 128 + tslot(tl)) * VS + uint32_t(u % VS)];
-                    else
-                        v = __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t);
-                    const float2 fb = __ldg(a.qfb + size_t(j) * KBV + u);
-                    ok = (fb.x <= v) && (v <= fb.y);
-                }
-                hits |= uint32_t(ok) << b;
-            }
-        }
-        return hits;
-      } else {
         uint32_t hits = PV ? 0u : su;
         uint32_t r = PV ? word : (word & ~su);
         if (r) {
@@ -250,7 +171,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             if constexpr (STAGE && VS == 4) {
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    const float4 w4 = reinterpret_cast<const float4*>(wval)[h * 128 + tslot(tl)];
+                    const float4 w4 = reinterpret_cast<const float4*>(wval)[val_slot(tl, h)];
                     v[4 * h] = w4.x;
                     v[4 * h + 1] = w4.y;
                     v[4 * h + 2] = w4.z;
@@ -259,7 +180,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             } else if constexpr (STAGE) {
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    const float2 w2 = reinterpret_cast<const float2*>(wval)[h * 128 + tslot(tl)];
+                    const float2 w2 = reinterpret_cast<const float2*>(wval)[val_slot(tl, h)];
                     v[2 * h] = w2.x;
                     v[2 * h + 1] = w2.y;
                 }
@@ -316,7 +237,6 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             }
         }
         return hits;
-      }
     };
 
     // Walk the tuples [start, end) of a subchunk in 128-tuple blocks (lane l
@@ -344,12 +264,11 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 // table cells of the 4 tuples of every word: (code >> shift) per byte
                 cw[u] = (cw_n[u] >> shift) & (0x01010101u * (K - 1));
             before_block(t0);
-            if constexpr (STAGE || SCODE) {
-                __syncwarp();
-            }
             if constexpr (STAGE) {
                 // stage the block's exact values (tuple t, dims VS*h ..
-                // VS*h+VS-1 at slot h * 128 + tslot(t), zero-padded dims)
+                // VS*h+VS-1 in slot val_slot(t, h), zero-padded dims) so a
+                // refinement reads a tuple with H LDS.128 / LDS.64
+                __syncwarp();
 #pragma unroll
                 for (uint32_t jj = 0; jj < 4; ++jj)
 #pragma unroll
@@ -360,36 +279,29 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             const int u = VS * h + e;
                             c[e] = u < KB ? f4_get(vv_n[u < KB ? u : 0], jj) : 0.0f;
                         }
-                        // tuple 4 lane + jj: slot h * 128 + jj * 32 + lane
                         if constexpr (VS == 4)
-                            reinterpret_cast<float4*>(wval)[h * 128 + jj * 32 + lane] =
+                            reinterpret_cast<float4*>(wval)[val_slot(4 * lane + jj, h)] =
                                 make_float4(c[0], c[1], c[2], c[3]);
                         else
-                            reinterpret_cast<float2*>(wval)[h * 128 + jj * 32 + lane] = make_float2(c[0], c[1]);
+                            reinterpret_cast<float2*>(wval)[val_slot(4 * lane + jj, h)] = make_float2(c[0], c[1]);
                     }
-            }
-            if constexpr (SCODE) {
-                // the raw 8-bit codes of tuples 4 lane + b (b = 0..3),
-                // byte-transposed into words of 4 dims (SCW words per tuple)
-                // at slot tslot(4 lane + b) = b * 32 + lane
-                uint32_t c16[4 * SCW];
+                if constexpr (SCODE) {
+                    // cells of tuples 4*lane + b (b = 0..3), dims 0..3 / 4..7
+                    // byte-transposed into (lo, hi) words
+                    uint32_t c8[8];
 #pragma unroll
-                for (int u = 0; u < 4 * SCW; ++u) c16[u] = u < KB ? cw_n[u < KB ? u : 0] : 0u;
+                    for (int u = 0; u < 8; ++u) c8[u] = u < KB ? cw[u < KB ? u : 0] : 0u;
+                    uint32_t lo[4], hi[4];
 #pragma unroll
-                for (uint32_t b = 0; b < 4; ++b) {
-                    const uint32_t sb = b | ((4u + b) << 4);   // byte b of x, byte b of y
-                    uint32_t wv[SCW];
-#pragma unroll
-                    for (int g = 0; g < SCW; ++g)
-                        wv[g] = __byte_perm(__byte_perm(c16[4 * g], c16[4 * g + 1], sb),
-                                            __byte_perm(c16[4 * g + 2], c16[4 * g + 3], sb), 0x5410);
-                    if constexpr (SCW == 4)
-                        reinterpret_cast<uint4*>(wcode)[b * 32 + lane] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                    else
-                        reinterpret_cast<uint2*>(wcode)[b * 32 + lane] = make_uint2(wv[0], wv[1]);
+                    for (uint32_t b = 0; b < 4; ++b) {
+                        const uint32_t sb = b | ((4u + b) << 4);   // byte b of x, byte b of y
+                        lo[b] = __byte_perm(__byte_perm(c8[0], c8[1], sb), __byte_perm(c8[2], c8[3], sb), 0x5410);
+                        hi[b] = __byte_perm(__byte_perm(c8[4], c8[5], sb), __byte_perm(c8[6], c8[7], sb), 0x5410);
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(wcode) + 2 * lane;
+                    dst[0] = make_uint4(lo[0], hi[0], lo[1], hi[1]);
+                    dst[1] = make_uint4(lo[2], hi[2], lo[3], hi[3]);
                 }
-            }
-            if constexpr (STAGE || SCODE) {
                 __syncwarp();
             }
             if (t0 + 128 < end) load_block(t0 + 128);
@@ -446,17 +358,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 // (W2: one word per sub-step, fetched for the lane's own tuple)
                 constexpr int NXW = W2 ? NS : CWS;
                 uint32_t xw[NXW][KB];
-                uint4 sc[SCODE ? NS : 1];   // SCODE: sub-step ss's tuple codes (dims 0-3, 4-7, 8-11, 12-15)
+                uint2 sc[SCODE ? NS : 1];   // SCODE: sub-step ss's tuple cells (dims 0-3, 4-7)
                 if constexpr (SCODE) {
 #pragma unroll
-                    for (int ss = 0; ss < NS; ++ss) {
-                        if constexpr (SCW == 4) {
-                            sc[ss] = reinterpret_cast<const uint4*>(wcode)[tslot(tix[ss])];
-                        } else {
-                            const uint2 x = reinterpret_cast<const uint2*>(wcode)[tslot(tix[ss])];
-                            sc[ss] = make_uint4(x.x, x.y, 0u, 0u);
-                        }
-                    }
+                    for (int ss = 0; ss < NS; ++ss) sc[ss] = wcode[tix[ss]];
                 } else if constexpr (W2) {
                     // sub-step ss = code word ss: each lane group fetches the
                     // word holding its own (compacted) tuple
@@ -488,14 +393,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         // row address of dim uu (SCODE: byte uu % 4 of the
                         // staged word, a compile-time selector)
                         auto addr = [&](int uu) -> uint32_t {
-                            if constexpr (SCODE) {
-                                // code byte uu -> (code >> shift) << 8 | lane offset
-                                const uint32_t wsel = uu < 4 ? sc[ss].x : uu < 8 ? sc[ss].y : uu < 12 ? sc[ss].z : sc[ss].w;
-                                const uint32_t code = __byte_perm(wsel, 0u, 0x4440u | (uint32_t(uu) & 3u));
-                                return ((code << sh8) & 0xFF00u) | lane_off;
-                            } else {
+                            if constexpr (SCODE)
+                                return __byte_perm(uu < 4 ? sc[ss].x : sc[ss].y, lane_off, 0x5504u | ((uint32_t(uu) & 3u) << 4));
+                            else
                                 return __byte_perm(x[uu], lane_off, sel);
-                            }
                         };
                         const uint32_t ca = addr(u);
                         if constexpr (W2) {
@@ -1399,18 +1300,16 @@ void dispatch(const VaBatchArgs& a, cudaStream_t st, std::integer_sequence<int, 
 size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
     // mirrors the layout at the top of va_batch_kernel
     const bool pv = va_batch_pv(kb);
-    const bool cr = pv && mode != 2;
     const size_t vd = va_batch_vdims(kb);
     size_t bytes = size_t(va_batch_table_words(kb, cells)) * 4;
-    if (cr) bytes += 1024 * (vd <= 8 ? 16 : 32) + 1024 * 4;              // code bounds + constrained dims
-    else if (pv) bytes += vd * 1024 * 8;                                 // float bounds
+    if (pv) bytes += vd * 1024 * 8;                                      // bounds
     if (pv && kb <= 10 && !(mode == 2 && kb > 8)) bytes += size_t(VB_WARPS) * 128 * vd * 4;   // staged values
     if (mode == 2)
         bytes += size_t(VB_WARPS) * 1024 * 2;
     else
         bytes += 1024 * 4 + size_t(VB_WARPS) * VB_QCAP * (8 + (pv ? 0 : 4));
-    if (cr) bytes += size_t(VB_WARPS) * 128 * (vd <= 8 ? 8 : 16);         // staged codes
-    if (cr) bytes += size_t(VB_WARPS) * 128;                              // compacted tuple lists
+    if (mode != 2 && pv && kb <= 8) bytes += size_t(VB_WARPS) * 128 * 8;   // staged cells (multi-word passes)
+    if (mode != 2 && pv) bytes += size_t(VB_WARPS) * 128;                 // compacted tuple lists
     return bytes;
 }
 
