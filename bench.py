@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--count-steps", type=int, default=None, help="timed steps of the count-mode batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-host-gather", action="store_true",
+                    help="skip the per-rank direct copy of the merged ids into one shared host buffer")
     return ap.parse_args()
 
 
@@ -397,6 +399,13 @@ def main():
                 "how": "NCCL all_gather of every rank's padded id slices + mdrq_copy_segments placement; "
                        "the step itself ends with the counts combine (global offsets on every rank)"}
 
+    # ---- the ids to the host without an NCCL exchange: every rank writes its
+    # own slices into ONE node-shared pinned host buffer at the rank-ordered
+    # offsets (its own PCIe link; parallel.gather_ids_to_host)
+    host_gather = None
+    if merge and not args.no_host_gather:
+        host_gather = measure_host_gather(batch, nq, total_ids, total_local, dev, world)
+
     # ---- dominant kernel of the step: one ids pass with events between
     # launch groups (mdrq_batch_profile), bytes from the kernels' counters
     peak, peak_kind = measured_peaks()
@@ -512,6 +521,7 @@ def main():
             "paths_us_per_query": paths,
             "e2e": e2e,
             "id_exchange": xchg,
+            "host_gather": host_gather,
             "c2": c2,
             "gpu_launches": launches_ids * args.steps,
             "clocks": clocks.summary(),
@@ -527,6 +537,46 @@ def main():
     if merge:
         dist.destroy_process_group()
     return 0
+
+
+def measure_host_gather(batch, nq, total_ids, total_local, dev, world):
+    """Wall time of parallel.gather_ids_to_host (counts all_gather + every
+    rank's placement kernel into the shared pinned buffer + barrier), max over
+    ranks; skipped when /dev/shm cannot hold the merged result."""
+    import torch
+    from paper_1801_03644_b200.parallel import SharedHostBuffer, gather_ids_to_host
+    need = 4 * total_ids
+    try:
+        st = os.statvfs("/dev/shm")
+        free = st.f_bavail * st.f_frsize
+    except OSError:
+        free = 0
+    ok = torch.tensor([1 if free > need * 1.05 + (1 << 30) else 0], device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if not int(ok.item()):
+        return {"skipped": f"/dev/shm holds {free / 1e9:.1f} GB, the merged ids need {need / 1e9:.1f} GB"}
+    d_ids, d_offs, tot = batch.result_device()
+    ids_t = _wrap(d_ids, tot, torch.int32, dev)
+    offs_t = _wrap(d_offs, nq + 1, torch.int64, dev)
+    buf = SharedHostBuffer(need, None, device=dev)
+    try:
+        o, i, _ = gather_ids_to_host(offs_t, ids_t, None, out=buf)   # warm (also touches the pages)
+        assert int(o[-1]) == total_ids
+        del o, i
+        t0 = time.perf_counter()
+        reps = 2
+        for _ in range(reps):
+            o, i, _ = gather_ids_to_host(offs_t, ids_t, None, out=buf)
+            del o, i
+        dt = max_over_ranks((time.perf_counter() - t0) / reps, world)
+    finally:
+        buf.close()
+    return {"ms_per_step": dt * 1e3, "bytes_per_rank": 4 * total_local, "ids_total": total_ids,
+            "gbs_per_rank": 4 * total_local / dt / 1e9,
+            "how": "counts all_gather, then every rank's mdrq_copy_segments kernel writes its slices into one "
+                   "POSIX-shared host buffer registered with CUDA (rank-ordered offsets), barrier; wall clock"}
 
 
 def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
