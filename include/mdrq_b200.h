@@ -95,6 +95,12 @@ typedef struct mdrq_search_stats {
 
 /* -- library ------------------------------------------------------------ */
 const char* mdrq_last_error(void);
+/* Debug / test entry point: the failed device-side bounds checks since the
+ * last call (bits per check kind, common.cuh), OR-ed over the library's units
+ * and cleared; bit 31 is set when the library was built with the checks
+ * (libmdrq_b200_checked.so, MDRQ_CHECKS).  Synchronises the device. */
+int mdrq_check_flags(uint32_t* flags);
+
 int mdrq_abi_version(void);
 int mdrq_device_count(int* count);
 /* Read-stream bandwidth probe (GB/s, best of iters) over a `bytes` buffer:

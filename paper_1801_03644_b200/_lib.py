@@ -15,7 +15,10 @@ import threading
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libmdrq_b200.so")
+# MDRQ_LIB=checked loads the build with device-side bounds checks
+# (build.py --checked, common.cuh MDRQ_CHECKS) -- for tests
+LIB_PATH = os.path.join(PKG, "libmdrq_b200_checked.so" if os.environ.get("MDRQ_LIB") == "checked"
+                        else "libmdrq_b200.so")
 
 MDRQ_OK = 0
 MDRQ_EINVAL = -1
@@ -49,7 +52,7 @@ MODE_BLOCKED = 1
 
 #: every symbol include/mdrq_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
-    "mdrq_last_error", "mdrq_abi_version", "mdrq_device_count", "mdrq_measure_read_bw", "mdrq_copy_segments",
+    "mdrq_last_error", "mdrq_abi_version", "mdrq_check_flags", "mdrq_device_count", "mdrq_measure_read_bw", "mdrq_copy_segments",
     "mdrq_match_rows", "mdrq_scan_rows", "mdrq_scan_column", "mdrq_and_masks",
     "mdrq_mask_popcount", "mdrq_mask_to_ids",
     "mdrq_store_create", "mdrq_store_destroy", "mdrq_store_get_info",
@@ -97,6 +100,7 @@ _int = ctypes.c_int
 _SIGS = {
     "mdrq_last_error": (ctypes.c_char_p, []),
     "mdrq_abi_version": (_int, []),
+    "mdrq_check_flags": (_int, [ctypes.POINTER(ctypes.c_uint32)]),
     "mdrq_device_count": (_int, [ctypes.POINTER(_int)]),
     "mdrq_measure_read_bw": (_int, [_int, _u64, _int, ctypes.POINTER(ctypes.c_double)]),
     "mdrq_copy_segments": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp]),

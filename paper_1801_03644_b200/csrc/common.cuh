@@ -7,9 +7,54 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace mdrq {
+
+// ---------------------------------------------------------------------------
+// Checked build (MDRQ_CHECKS, `build.py --checked` -> libmdrq_b200_checked.so):
+// device-side bounds checks on the shared-memory queues, staging blocks,
+// scatter windows, masks and result writes.  A failed check sets bit `bit`
+// of this translation unit's flag word (the first failure of a bit prints
+// its line) and the kernel carries on; the host reads every unit's flags
+// with mdrq_check_flags().  This stands in for compute-sanitizer, which is
+// not available on the GPU pool.  Release builds compile the checks away.
+#ifdef MDRQ_CHECKS
+static __device__ unsigned int g_check_flags;
+static __device__ __noinline__ void check_fail(unsigned bit, int line) {
+    if (!(atomicOr(&g_check_flags, 1u << bit) & (1u << bit))) printf("MDRQ_CHECK failed: bit %u line %d\n", bit, line);
+}
+#define MDRQ_CHECK(cond, bit)                              \
+    do {                                                   \
+        if (!(cond)) ::mdrq::check_fail((bit), __LINE__);  \
+    } while (0)
+#define MDRQ_CHECK_FLAGS_FN(name)                                            \
+    uint32_t name() {                                                        \
+        uint32_t v = 0;                                                      \
+        cudaMemcpyFromSymbol(&v, g_check_flags, sizeof(v));                  \
+        const uint32_t z = 0;                                                \
+        cudaMemcpyToSymbol(g_check_flags, &z, sizeof(z));                    \
+        return v;                                                            \
+    }
+#else
+#define MDRQ_CHECK(cond, bit) \
+    do {                      \
+    } while (0)
+#define MDRQ_CHECK_FLAGS_FN(name) \
+    uint32_t name() { return 0; }
+#endif
+// check bits
+enum : unsigned {
+    kChkQueue = 0,      // candidate queue slot beyond VB_QCAP
+    kChkRecBlock = 1,   // staged record beyond its 1 024-record block
+    kChkAlive = 2,      // compacted tuple list beyond 128
+    kChkCounter = 3,    // per-query counter index beyond 1 024
+    kChkWindow = 4,     // scatter window slot beyond its capacity
+    kChkMask = 5,       // mask word beyond the mask
+    kChkIds = 6,        // id write beyond the result pool
+    kChkTuple = 7,      // tuple index beyond the block / store
+};
 
 constexpr int kMaxDims = 256;      // dimensions a store may have
 constexpr int kWarp = 32;

@@ -173,6 +173,8 @@ __global__ void reduce_partials_kernel(const unsigned long long* __restrict__ pa
 
 }  // namespace
 
+MDRQ_CHECK_FLAGS_FN(expand_check_flags)
+
 void launch_reduce_partials(const unsigned long long* partials, uint32_t nq, bool add_counts,
                             unsigned long long* counts, unsigned long long* stats, cudaStream_t st) {
     if (!nq) return;

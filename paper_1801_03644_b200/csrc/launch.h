@@ -186,6 +186,11 @@ uint32_t col_batch_padded_dims(uint32_t kb);   // union dims the kernel evaluate
 uint32_t row_tile_rows(uint32_t m);
 size_t row_scan_smem(uint32_t m);
 
+// checked builds (MDRQ_CHECKS): every unit's failed-check bits, cleared on read
+uint32_t vabatch_check_flags();
+uint32_t columnar_check_flags();
+uint32_t expand_check_flags();
+
 // store construction
 void launch_transpose_rows_to_cols(const float* rows, uint64_t n, uint32_t m, float* cols,
                                    uint64_t stride, cudaStream_t st);

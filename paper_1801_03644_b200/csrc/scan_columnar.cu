@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(256) col_batch_ids_kernel(const BatchArgs a, u
 #pragma unroll
                 for (int t = 0; t < TPT; ++t)
                     if (t0 + 32 * t < a.n) {
+                        MDRQ_CHECK(t0 / 32 + t < mask_words, kChkMask);
                         masks[uint64_t(lane) * mask_words + t0 / 32 + t] = mine[t];
                         acc += __popc(mine[t]);
                     }
@@ -288,6 +289,8 @@ void launch_col_batch_ids(const BatchArgs& a, uint32_t* masks, uint64_t mask_wor
     else
         run_batch_ids<64>(a, masks, mask_words, chunk_counts, num_sms, st);
 }
+
+MDRQ_CHECK_FLAGS_FN(columnar_check_flags)
 
 void launch_col_scan(const ScanArgs& a, bool ids, cudaStream_t st) {
     if (a.num_tiles == 0) return;

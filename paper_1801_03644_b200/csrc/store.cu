@@ -1328,6 +1328,17 @@ const char* mdrq_last_error(void) { return g_err.c_str(); }
 
 int mdrq_abi_version(void) { return MDRQ_ABI_VERSION; }
 
+int mdrq_check_flags(uint32_t* flags) {
+    return guard([&] {
+        if (!flags) raise(MDRQ_EINVAL, "null flags");
+        CK(cudaDeviceSynchronize());
+        *flags = vabatch_check_flags() | columnar_check_flags() | expand_check_flags();
+#ifdef MDRQ_CHECKS
+        *flags |= 0x80000000u;   // this library was built with the checks
+#endif
+    });
+}
+
 int mdrq_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_off, const int64_t* dst_off,
                        const int64_t* len, uint64_t nseg, void* stream) {
     return guard([&] {

@@ -336,7 +336,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         uint32_t pos = incl - c;
 #pragma unroll
                         for (uint32_t bb = 0; bb < 4; ++bb)
-                            if (nib >> bb & 1u) walive[pos++] = uint8_t(4 * lane + bb);
+                            if (nib >> bb & 1u) {
+                                MDRQ_CHECK(pos < 128u, kChkAlive);
+                                walive[pos++] = uint8_t(4 * lane + bb);
+                            }
                         __syncwarp();
                     }
                 }
@@ -488,6 +491,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     while (hits) {
                         const int b = __ffs(hits) - 1;
                         hits &= hits - 1;
+                        MDRQ_CHECK(wq + b < 1024u, kChkCounter);
                         atomicAdd(&s_cnt32[wq + b], 1u);
                     }
                 } else {
@@ -539,6 +543,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             const int b = __ffs(hits) - 1;
                             hits &= hits - 1;
                             const uint32_t q = wq + b;
+                            MDRQ_CHECK(!stage_on || dst < a.rec + (uint64_t(blk) + 1) * kRecBlock, kChkRecBlock);
+                            MDRQ_CHECK(q < 1024u && t - gstart < (1ull << 22), kChkCounter);
                             if (stage_on) *dst++ = trel | q;
                             atomicAdd(&s_cnt32[q], 1u);
                         }
@@ -616,7 +622,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                                 const uint32_t mb = ((tix[ss] << 5) | (NW * (lane % LPT)));
 #pragma unroll
                                 for (int h = 0; h < NW; ++h)
-                                    if (nzm[ss] >> h & 1u) qe[slot++] = make_uint2(ov4[ss + NS * h], mb + h);
+                                    if (nzm[ss] >> h & 1u) {
+                                        MDRQ_CHECK(slot < VB_QCAP, kChkQueue);
+                                        qe[slot++] = make_uint2(ov4[ss + NS * h], mb + h);
+                                    }
                             }
                             qn += __popc(pl[ss][0] & lanes) + 2u * __popc(pl[ss][1] & lanes) +
                                   4u * __popc(pl[ss][2] & lanes);
@@ -655,6 +664,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         for (uint32_t s2 = 0; s2 < NB; ++s2) {
                             if (bal[s2] >> lane & 1u) {
                                 const uint32_t slot = qn + __popc(bal[s2] & lt);
+                                MDRQ_CHECK(slot < VB_QCAP, kChkQueue);
                                 qe[slot] = make_uint2(ov4[s2], meta[s2]);
                                 if constexpr (!PV) qs[slot] = su4[s2];
                             }
@@ -667,6 +677,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         for (uint32_t s2 = 0; s2 < NB; ++s2) {
                             if (bal[s2] >> lane & 1u) {
                                 const uint32_t slot = qn + __popc(bal[s2] & lt);
+                                MDRQ_CHECK(slot < VB_QCAP, kChkQueue);
                                 qe[slot] = make_uint2(ov4[s2], meta[s2]);
                                 if constexpr (!PV) qs[slot] = su4[s2];
                             }
@@ -1114,6 +1125,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                             rem &= ~grp;
                         }
                     }
+                    MDRQ_CHECK(off + c + __popc(same & lt) < SC_WIN, kChkWindow);
                     sts_u32(a_out + 4u * (off + c + __popc(same & lt)), r);
                     __syncwarp();   // every lane has read wc[q] before its leader bumps it
                     if ((same & lt) == 0) sts_u16(a_wc + 2u * q, c + __popc(same));
@@ -1136,6 +1148,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) vb_scatter_kernel(const VaBatch
                 const uint32_t same = __any_sync(0xFFFFFFFFu, dup) ? match_q10(q, act) : (1u << lane);
                 if (act) {
                     const uint32_t pp = s_off[q] + wc[q] + __popc(same & lt);
+                    MDRQ_CHECK(pp < SC_WIN, kChkWindow);
                     s_out[pp] = r;
                 }
                 __syncwarp();
@@ -1358,6 +1371,8 @@ uint32_t launch_va_batch_unpermute(const uint32_t* perm, const unsigned long lon
                                                                          src_cap, ids, cap, nq);
     return 3;
 }
+
+MDRQ_CHECK_FLAGS_FN(vabatch_check_flags)
 
 void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st) {
     vb_block_list_kernel<<<a.grid * 4, 256, 0, st>>>(a);

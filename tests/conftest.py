@@ -29,3 +29,18 @@ def gpu():
     if n < 1:
         raise RuntimeError("GPU test selected but no CUDA device is visible")
     return eng
+
+
+@pytest.fixture(autouse=True)
+def _device_checks(request):
+    """With MDRQ_LIB=checked (the build with device-side bounds checks,
+    common.cuh MDRQ_CHECKS) every GPU test ends with no failed check."""
+    yield
+    if os.environ.get("MDRQ_LIB") != "checked" or request.node.get_closest_marker("gpu") is None:
+        return
+    import ctypes
+    from paper_1801_03644_b200 import _lib
+    f = ctypes.c_uint32(0)
+    _lib.check(_lib.load().mdrq_check_flags(ctypes.byref(f)))
+    assert f.value & 0x80000000, "MDRQ_LIB=checked but the library was built without the checks"
+    assert f.value & 0x7FFFFFFF == 0, f"device-side bounds checks failed: bits {f.value & 0x7FFFFFFF:#x}"

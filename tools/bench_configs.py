@@ -1,6 +1,6 @@
 """Per-configuration measurements (BASELINE.json configs C1-C5) on one GPU.
 
-    python tools/bench_configs.py [c1 c2 c3 c4 c5] > profiles/r01_configs.json
+    python tools/bench_configs.py [c1 c2 c3 c4 c5] > profiles/r02_configs.json
 
 For every configuration: the table, its queries (the same seeded inputs the
 parity tests use), the device time per query of every path in count and ids
@@ -70,8 +70,6 @@ def measure(cfg):
         b = st.prepare(lo[:q], hi[:q], p)
         entry = {"queries_timed": q}
         for mode in ("count", "ids"):
-            if mode == "ids" and p == "columnar_batch":
-                continue
             if mode == "ids":
                 total = b.reserve()
                 entry["ids_per_query"] = total / q
