@@ -265,7 +265,9 @@ struct mdrq_store {
     DBuf<unsigned long long> vb_base, vb_total, vb_qoff;
     // single-pass ids staging (linked record blocks), grown when a pass overflows
     DBuf<uint32_t> vb_rec, vb_blk_count, vb_blk_chunk, vb_blk_seq, vb_blk_list;
-    DBuf<uint32_t> vb_chunk_nblk, vb_chunk_first, vb_flags;  // flags: cursor, overflow
+    // flags: cursor, overflow of the current pass, overflow of any pass of the
+    // batch (sticky: read after the batch to size the staging pool)
+    DBuf<uint32_t> vb_chunk_nblk, vb_chunk_first, vb_flags;
     uint32_t vb_max_blocks = 1u << 16;   // 64K blocks x 1024 records x 4 B = 256 MB
     DBuf<uint32_t> ids;              // result pool
     uint64_t last_total = 0;
@@ -881,7 +883,7 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     s->vb_blk_list.reserve(s->vb_max_blocks);
     s->vb_chunk_nblk.reserve(chunks);
     s->vb_chunk_first.reserve(chunks);
-    s->vb_flags.reserve(2);
+    s->vb_flags.reserve(3);
     a.rec = s->vb_rec.p;
     a.blk_count = s->vb_blk_count.p;
     a.blk_chunk = s->vb_blk_chunk.p;
@@ -1002,6 +1004,10 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
         }
     };
     if (path == MDRQ_PATH_VAFILE_BATCH) {
+        if (ids) {
+            s->vb_flags.reserve(3);
+            CK(cudaMemsetAsync(s->vb_flags.p + 2, 0, sizeof(uint32_t), st));
+        }
         const bool sorted = !b->vb_perm.empty();
         DBuf<uint32_t>& pool = pool_of(s, b);
         // slot-order ids, as large as the result pool (+ 4 words of slack
@@ -1031,6 +1037,14 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
                 mark(0, 1);
                 launch_va_batch(va, 3, st);
                 dsync("mode3");
+                static const bool vdbg = getenv("MDRQ_DEBUG_VB") != nullptr;
+                if (vdbg) {
+                    uint32_t fl[2] = {0, 0};
+                    CK(cudaMemcpyAsync(fl, va.cursor, sizeof(fl), cudaMemcpyDeviceToHost, st));
+                    CK(cudaStreamSynchronize(st));
+                    fprintf(stderr, "vb pass q0=%u nqp=%u kb=%u: staged blocks %u of %u, overflow %u\n", ps.q0, ps.nqp,
+                            ps.kb, fl[0], va.max_blocks, fl[1]);
+                }
                 mark(1, 3);
                 launch_va_batch_scans(va, ps.q0, st);
                 dsync("scans");
@@ -1136,8 +1150,10 @@ uint32_t count_launches(const mdrq_store* s, const mdrq_batch* b, bool ids) {
 void grow_vb_staging(mdrq_store* s, uint64_t total) {
     constexpr uint64_t kMaxBlocks = 1ull << 24;
     const uint64_t per_block = uint64_t(kRecBlock) * 4 + 4 * sizeof(uint32_t);
+    // blocks close when a refinement round's records do not fit: dense passes
+    // fill them to ~85-90 % (C2 1e-1: 5e9 records took 5.38 M blocks)
     uint64_t want = std::max<uint64_t>(2ull * s->vb_max_blocks,
-                                       total / kRecBlock + total / (10 * kRecBlock) + 2ull * 16 * s->num_sms + 64);
+                                       total / kRecBlock + total / (4 * kRecBlock) + 2ull * 16 * s->num_sms + 64);
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
         // the current pool is released first, so its bytes count as free
@@ -1157,26 +1173,28 @@ void grow_vb_staging(mdrq_store* s, uint64_t total) {
 
 uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
     s->bounce_ids = 0;
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    // until the result pool holds the batch AND no pass overflowed the
+    // staging pool (a reserved batch then never runs the recount pass)
+    for (int attempt = 0; attempt < 4; ++attempt) {
         enqueue(s, b, true, s->stream);
         unsigned long long total = 0;
         if (b->nq && s->n)
             CK(cudaMemcpyAsync(&total, b->d_offsets.p + b->nq, sizeof(total), cudaMemcpyDeviceToHost, s->stream));
         uint32_t overflowed = 0;
         if (b->path == MDRQ_PATH_VAFILE_BATCH && s->vb_flags.p)
-            CK(cudaMemcpyAsync(&overflowed, s->vb_flags.p + 1, sizeof(overflowed), cudaMemcpyDeviceToHost,
+            CK(cudaMemcpyAsync(&overflowed, s->vb_flags.p + 2, sizeof(overflowed), cudaMemcpyDeviceToHost,
                                s->stream));
         CK(cudaStreamSynchronize(s->stream));
         if (overflowed) grow_vb_staging(s, total);
         DBuf<uint32_t>& pool = pool_of(s, b);
-        if (total <= (pool.p ? pool.cap : 0)) {
+        if (total <= (pool.p ? pool.cap : 0) && (!overflowed || attempt == 3)) {
             s->last_total = total;
             s->last_nq = b->nq;
             s->last_path = b->path;
             s->last_batch = b;
             return total;
         }
-        pool.reserve(size_t(total + total / 8 + 4096));
+        if (total > (pool.p ? pool.cap : 0)) pool.reserve(size_t(total + total / 8 + 4096));
     }
     raise(MDRQ_ECUDA, "result pool did not converge");
 }
@@ -1276,7 +1294,7 @@ int query_ids_impl(mdrq_store* s, const float* lower, const float* upper, uint32
             if (have)
                 CK(cudaMemcpyAsync(h_off, b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
                                    s->stream));
-            if (vb) CK(cudaMemcpyAsync(h_flag, s->vb_flags.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
+            if (vb) CK(cudaMemcpyAsync(h_flag, s->vb_flags.p + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream));
             if (spec) CK(cudaMemcpyAsync(hb + head, pool.p, sizeof(uint32_t) * spec, cudaMemcpyDeviceToHost, s->stream));
             CK(cudaStreamSynchronize(s->stream));
             total = have ? h_off[nq] : 0;
@@ -1655,7 +1673,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
                 CK(cudaMemcpyAsync(sl.h_flags, b->d_offsets.p + nq, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                    s->stream));
                 if (b->path == MDRQ_PATH_VAFILE_BATCH && s->vb_flags.p)
-                    CK(cudaMemcpyAsync(sl.h_flags + 1, s->vb_flags.p + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                    CK(cudaMemcpyAsync(sl.h_flags + 1, s->vb_flags.p + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                        s->stream));
             }
             CK(cudaEventRecord(sl.comp, s->stream));

@@ -525,6 +525,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                                 nb = atomicAdd(a.cursor, 1u);
                                 if (nb >= a.max_blocks) {
                                     atomicExch(a.overflow, 1u);
+                                    atomicExch(a.overflow + 1, 1u);   // sticky: some pass of the batch overflowed
                                     nb = kNoBlock - 1;   // stop staging this subchunk
                                 } else {
                                     a.blk_chunk[nb] = chunk;
