@@ -116,6 +116,15 @@ int mdrq_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_of
                        const int64_t* dst_off, const int64_t* len, uint64_t nseg,
                        void* stream);
 
+/* The same segment placement with the copy engines, for a destination in
+ * pinned (or registered) host memory: one cudaMemcpyBatchAsync over the
+ * segments (host arrays src_off / dst_off / len, in elements), enqueued on
+ * `stream` (not the legacy default stream).  The multi-GPU host gather
+ * (parallel.gather_ids_to_host) uses it: each rank's ids go to their
+ * rank-ordered places over its own PCIe link at DMA speed. */
+int mdrq_copy_segments_dma(const uint32_t* src, uint32_t* dst, const int64_t* src_off, const int64_t* dst_off,
+                           const int64_t* len, uint64_t nseg, void* stream);
+
 /* -- kernel-backend level: host buffers in and out (parity / tests) ------ */
 /* match_row for `nrows` rows against one query: out[r] = 1 match / 0 not.  */
 int mdrq_match_rows(const float* rows, uint64_t nrows, uint32_t m,

@@ -53,6 +53,7 @@ MODE_BLOCKED = 1
 #: every symbol include/mdrq_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "mdrq_last_error", "mdrq_abi_version", "mdrq_check_flags", "mdrq_device_count", "mdrq_measure_read_bw", "mdrq_copy_segments",
+    "mdrq_copy_segments_dma",
     "mdrq_match_rows", "mdrq_scan_rows", "mdrq_scan_column", "mdrq_and_masks",
     "mdrq_mask_popcount", "mdrq_mask_to_ids",
     "mdrq_store_create", "mdrq_store_destroy", "mdrq_store_get_info",
@@ -99,6 +100,9 @@ _int = ctypes.c_int
 
 _SIGS = {
     "mdrq_last_error": (ctypes.c_char_p, []),
+    "mdrq_copy_segments_dma": (_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.c_uint64, ctypes.c_void_p]),
     "mdrq_abi_version": (_int, []),
     "mdrq_check_flags": (_int, [ctypes.POINTER(ctypes.c_uint32)]),
     "mdrq_device_count": (_int, [ctypes.POINTER(_int)]),

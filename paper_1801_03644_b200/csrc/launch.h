@@ -151,6 +151,7 @@ constexpr uint32_t kRecBlock = 1024;
 constexpr uint32_t kNoBlock = 0xFFFFFFFFu;
 size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode);
 int va_batch_max_dims();
+int va_batch_words(uint32_t kb);   // query words per lane of a full pass (4 / 2: the multi-word layouts)
 uint32_t va_batch_warps();
 // mode 0 count, 2 ids (recount pass after a staging overflow), 3 group counts + staged records
 void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st);

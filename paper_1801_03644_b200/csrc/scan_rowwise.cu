@@ -4,10 +4,11 @@
 // hot loop is scan_rows (_kernels_cy.pyx:58-86) calling _match_code
 // (_kernels_cy.pyx:23-46) once per row.  Each CTA claims row tiles in order
 // (atomic tile counter), stages them into shared memory with the TMA bulk
-// engine (cp.async.bulk + mbarrier, two stages: the next tile streams in
-// while the current one is evaluated), evaluates one row per thread, and
-// emits ascending ids through the same ballot / block-scan / decoupled
-// look-back compaction as the columnar path.
+// engine (cp.async.bulk + mbarrier, kRowStages stages of 32 KB: the next
+// tiles stream in while the current one is evaluated), evaluates one row per
+// thread, and in ids mode writes the verdicts as a bitmask + per-chunk counts
+// that expand.cu turns into ascending ids (the same two light kernels as the
+// columnar path; no look-back inside the bandwidth-bound scan).
 //
 // The early-break counter of the reference (`early`, pyx:84-85) is
 // reproduced exactly for both kernel modes from the first failing

@@ -465,11 +465,17 @@ void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
     static const bool no_sort = getenv("MDRQ_VB_NO_SORT") != nullptr;   // measurement / test switch
     b->vb_perm = no_sort ? std::vector<uint32_t>() : choose_vb_order(s, b);
     build_vb_passes_ordered(s, b);
-    bool fb = false;
-    for (const VbPass& ps : b->vb_passes) fb |= ps.fallback;
-    if (fb && !b->vb_perm.empty()) {
-        // a pass fell back to per-query scans, which write in query order:
-        // keep the batch order
+    bool fb = false, prunes = false;
+    for (const VbPass& ps : b->vb_passes) {
+        fb |= ps.fallback;
+        // only the multi-word layout (full passes of <= 10 union dims,
+        // vabatch.cu) drops pruned tuples
+        prunes |= !ps.fallback && ps.prune && ps.nqp > 512 && va_batch_pv(ps.kb) && va_batch_words(ps.kb) > 1;
+    }
+    if (!b->vb_perm.empty() && (fb || !prunes)) {
+        // a pass fell back to per-query scans, which write in query order, or
+        // no pass can use its cell masks: keep the batch order (the sorted
+        // order would only add the move back to query order)
         b->vb_perm.clear();
         build_vb_passes_ordered(s, b);
     }
@@ -1363,6 +1369,36 @@ int mdrq_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_of
         if (nseg && (!src || !dst || !src_off || !dst_off || !len)) raise(MDRQ_EINVAL, "null argument");
         launch_copy_segments(src, dst, src_off, dst_off, len, nseg, static_cast<cudaStream_t>(stream));
         CK(cudaGetLastError());
+    });
+}
+
+int mdrq_copy_segments_dma(const uint32_t* src, uint32_t* dst, const int64_t* src_off, const int64_t* dst_off,
+                           const int64_t* len, uint64_t nseg, void* stream) {
+    return guard([&] {
+        if (nseg && (!src || !dst || !src_off || !dst_off || !len)) raise(MDRQ_EINVAL, "null argument");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (!st) raise(MDRQ_EINVAL, "a non-default stream is required");
+        std::vector<void*> dsts, srcs;
+        std::vector<size_t> sizes;
+        dsts.reserve(nseg);
+        srcs.reserve(nseg);
+        sizes.reserve(nseg);
+        for (uint64_t i = 0; i < nseg; ++i) {
+            if (len[i] <= 0) continue;
+            dsts.push_back(dst + dst_off[i]);
+            srcs.push_back(const_cast<uint32_t*>(src) + src_off[i]);
+            sizes.push_back(size_t(len[i]) * sizeof(uint32_t));
+        }
+        if (dsts.empty()) return;
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        size_t idx0 = 0, fail = 0;
+        // one call, the copy engines take every segment (device -> host DMA)
+        for (size_t b0 = 0; b0 < dsts.size(); b0 += 65536) {   // bounded batches
+            const size_t cnt = std::min<size_t>(65536, dsts.size() - b0);
+            CK(cudaMemcpyBatchAsync(dsts.data() + b0, srcs.data() + b0, sizes.data() + b0, cnt, &attr, &idx0, 1,
+                                    &fail, st));
+        }
     });
 }
 

@@ -1329,6 +1329,8 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
 
 int va_batch_max_dims() { return kVaBatchMaxDims; }
 
+int va_batch_words(uint32_t kb) { return vb_words(kb); }
+
 uint32_t va_batch_warps() { return VB_WARPS; }
 
 void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st) {

@@ -288,7 +288,29 @@ class SharedHostBuffer:
         self._shm = None
 
 
-def gather_ids_to_host(local_offsets, local_ids, group=None, out: SharedHostBuffer | None = None):
+def _dma_segments(local_ids, buf_ptr: int, src_off, dst_off, seg) -> bool:
+    """Every segment device -> host with the copy engines (one
+    cudaMemcpyBatchAsync, mdrq_copy_segments_dma) on a side stream ordered
+    after the current one; False when the runtime / driver refuses it."""
+    import ctypes
+    import torch
+    from . import _lib
+    so = src_off.cpu().numpy().astype(np.int64)
+    do = dst_off.cpu().numpy().astype(np.int64)
+    sl = seg.cpu().numpy().astype(np.int64)
+    dev = local_ids.device
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    rc = _lib.load().mdrq_copy_segments_dma(ctypes.c_void_p(local_ids.data_ptr()), ctypes.c_void_p(buf_ptr),
+                                            so.ctypes.data_as(p64), do.ctypes.data_as(p64), sl.ctypes.data_as(p64),
+                                            so.size, ctypes.c_void_p(side.cuda_stream))
+    side.synchronize()
+    return rc == 0
+
+
+def gather_ids_to_host(local_offsets, local_ids, group=None, out: SharedHostBuffer | None = None,
+                       method: str = "dma"):
     """Merged ids of every rank in ONE host buffer, written by the ranks
     themselves: the per-query counts are all_gathered (8 B per query and
     rank), every rank computes where its slice of each query goes and copies
@@ -313,8 +335,11 @@ def gather_ids_to_host(local_offsets, local_ids, group=None, out: SharedHostBuff
         raise ValueError(f"host buffer holds {buf.nbytes // 4} ids, the merge needs {total}")
     src_off, dst_off, seg = rank_segments(all_counts, rank, out_offsets, rank_prefix)
     if dev.type == "cuda":
-        _place_segments(local_ids, buf.ptr, src_off, dst_off, seg)
-        torch.cuda.current_stream(dev).synchronize()
+        # the copy engines (DMA, ~the pinned-copy bandwidth of the link), else
+        # the placement kernel writing through the mapping
+        if method != "dma" or not _dma_segments(local_ids, buf.ptr, src_off, dst_off, seg):
+            _place_segments(local_ids, buf.ptr, src_off, dst_off, seg)
+            torch.cuda.current_stream(dev).synchronize()
     else:
         host = torch.from_numpy(buf.view(_np.int32, total)) if total else torch.empty(0, dtype=torch.int32)
         _place_segments(local_ids.to(torch.int32), host, src_off, dst_off, seg)
