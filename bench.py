@@ -579,7 +579,7 @@ def measure_host_gather(batch, nq, total_ids, total_local, dev, world):
     return {"ms_per_step": dt * 1e3, "bytes_per_rank": 4 * total_local, "ids_total": total_ids,
             "gbs_per_rank": 4 * total_local / dt / 1e9, "kernel_ms_per_step": res["kernel"] * 1e3,
             "how": "counts all_gather, then every rank copies its slices into one POSIX-shared host buffer "
-                   "registered with CUDA at the rank-ordered offsets (one batched DMA memcpy of the segments; "
+                   "registered with CUDA at the rank-ordered offsets (one DMA copy per query segment; "
                    "kernel_ms_per_step: the placement kernel writing through the mapping instead), barrier; "
                    "wall clock"}
 

@@ -117,8 +117,8 @@ int mdrq_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_of
                        void* stream);
 
 /* The same segment placement with the copy engines, for a destination in
- * pinned (or registered) host memory: one cudaMemcpyBatchAsync over the
- * segments (host arrays src_off / dst_off / len, in elements), enqueued on
+ * pinned (or registered) host memory: one asynchronous device-to-host copy
+ * per segment (host arrays src_off / dst_off / len, in elements), enqueued on
  * `stream` (not the legacy default stream).  The multi-GPU host gather
  * (parallel.gather_ids_to_host) uses it: each rank's ids go to their
  * rank-ordered places over its own PCIe link at DMA speed. */

@@ -289,9 +289,9 @@ class SharedHostBuffer:
 
 
 def _dma_segments(local_ids, buf_ptr: int, src_off, dst_off, seg) -> bool:
-    """Every segment device -> host with the copy engines (one
-    cudaMemcpyBatchAsync, mdrq_copy_segments_dma) on a side stream ordered
-    after the current one; False when the runtime / driver refuses it."""
+    """Every segment device -> host with the copy engines (one async copy per
+    segment, mdrq_copy_segments_dma) on a side stream ordered after the
+    current one; False when the runtime refuses it."""
     import ctypes
     import torch
     from . import _lib
