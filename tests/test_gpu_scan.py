@@ -532,3 +532,86 @@ def test_sorted_multi_pass_batches_vs_oracle(gpu, m, nq, width):
         offs, ids = st_.ids(lo[:1500], hi[:1500], "vafile_batch")   # the synchronous path too
         assert np.array_equal(np.diff(offs), exp_c[:1500])
         assert np.array_equal(oracle.set_hash(offs, ids), exp_h[:1500])
+
+
+def test_prepared_batch_lifecycle_and_async_contract(gpu):
+    """a batch outliving its store is detached (destroying it
+    later is safe, using it raises); ids_async refuses an unreserved batch;
+    after reserve() it runs on the caller's stream and a synchronous call on
+    the store's own stream right after it sees a consistent state."""
+    import ctypes
+    import torch
+    from paper_1801_03644_b200 import _lib
+    rng = np.random.default_rng(9)
+    values = rng.random((50_003, 4), dtype=np.float32)
+    lo = rng.uniform(0, 0.5, (40, 4)).astype(np.float32)
+    hi = (lo + 0.5).astype(np.float32)
+    exp_offs, exp_ids = oracle.ids_batch(values, lo, hi)
+    st_ = gpu.DeviceStore(values, layouts=1 | 4, va_bits=8)
+    b = st_.prepare(lo, hi, "vafile_batch")
+    with pytest.raises(ValueError):
+        b.ids_async(0)                      # not reserved
+    assert b.reserve() == exp_offs[-1]
+    s = torch.cuda.Stream()
+    b.ids_async(s.cuda_stream)              # caller stream
+    # a synchronous pass on the store's stream, ordered after the async one
+    offs, ids = st_.ids(lo[:5], hi[:5], "columnar")
+    assert np.array_equal(offs, exp_offs[:6]) and np.array_equal(ids.astype(np.int64), exp_ids[:exp_offs[5]])
+    b.ids_async(s.cuda_stream)
+    d_ids, d_offs, tot = b.result_device()
+    s.synchronize()
+    assert tot == exp_offs[-1]
+    # DeviceStore.close closes its prepared batches first ...
+    b2 = st_.prepare(lo, hi, "columnar_batch")
+    # ... and a batch the Python side does not track (raw C handle) is
+    # detached by mdrq_store_destroy: destroying it afterwards is safe
+    lib = _lib.load()
+    raw = ctypes.c_void_p()
+    f32p = ctypes.POINTER(ctypes.c_float)
+    lo_c, hi_c = np.ascontiguousarray(lo), np.ascontiguousarray(hi)
+    _lib.check(lib.mdrq_batch_prepare(st_.handle, lo_c.ctypes.data_as(f32p), hi_c.ctypes.data_as(f32p),
+                                      lo.shape[0], _lib.PATHS["vafile_batch"], ctypes.byref(raw)))
+    st_.close()
+    assert b2._h is None
+    assert lib.mdrq_batch_destroy(raw) == 0
+
+
+def test_store_bounds_for_every_layout(gpu):
+    """DeviceStore.bounds() is the observed per-dim [min, max]
+    (core.py:99-105) for a row-wise-only store too."""
+    rng = np.random.default_rng(4)
+    values = (rng.random((10_007, 6), dtype=np.float32) * 5 - 2).astype(np.float32)
+    exp = np.stack([values.min(0), values.max(0)], 1)
+    for layouts in (1, 2, 4, 2 | 4):
+        with gpu.DeviceStore(values, layouts=layouts, va_bits=8) as st_:
+            assert np.array_equal(st_.bounds(), exp), layouts
+
+
+def test_reference_api_batches_use_the_multi_query_passes(gpu):
+    """VaFile.search_batch / count_batch go through the planner
+    (the bit-sliced pass from 10 queries); VerticalScan.search_batch through
+    the multi-query columnar pass; results equal the oracle."""
+    from paper_1801_03644_b200 import workload
+    rng = np.random.default_rng(12)
+    values = rng.random((30_011, 5), dtype=np.float32)
+    lo = rng.uniform(0, 0.6, (50, 5)).astype(np.float32)
+    hi = (lo + 0.4).astype(np.float32)
+    queries = workload.queries_from_arrays(lo, hi)
+    exp_offs, exp_ids = oracle.ids_batch(values, lo, hi)
+    data = gpu.DataSet(values)
+    for name in ("vafile", "vertical"):
+        m = gpu.build_method(name, data)
+        try:
+            res = m.search_batch(queries)
+            assert np.array_equal(res.offsets, exp_offs), name
+            assert np.array_equal(res.ids.astype(np.int64), exp_ids), name
+            assert np.array_equal(m.count_batch(queries), np.diff(exp_offs)), name
+            # the batch ran the multi-query path the planner picks
+            b = m.store.prepare(lo, hi, "auto")
+            assert b.info()["path"] == ("vafile_batch" if name == "vafile" else "columnar_batch"), name
+            b.close()
+            streamed = m.search_stream([queries, queries[:7]])
+            assert np.array_equal(streamed[0].offsets, exp_offs)
+            assert np.array_equal(streamed[1].ids.astype(np.int64), exp_ids[:exp_offs[7]])
+        finally:
+            m.close()
