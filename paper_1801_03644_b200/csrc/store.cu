@@ -269,6 +269,7 @@ struct mdrq_store {
     // batch (sticky: read after the batch to size the staging pool)
     DBuf<uint32_t> vb_chunk_nblk, vb_chunk_first, vb_flags;
     uint32_t vb_max_blocks = 1u << 16;   // 64K blocks x 1024 records x 4 B = 256 MB
+    bool vb_sized = false;               // the staging pool was sized from a counted batch
     DBuf<uint32_t> ids;              // result pool
     uint64_t last_total = 0;
     uint32_t last_nq = 0;
@@ -1177,8 +1178,24 @@ void grow_vb_staging(mdrq_store* s, uint64_t total) {
     s->vb_blk_list.release();
 }
 
+// The first bit-sliced ids batch of a store: count it first and size the
+// staging pool from its total, so the batch does not overflow the default pool
+// and take the recount pass (~6x a filter pass) on every overflowing pass.
+void presize_vb_staging(mdrq_store* s, mdrq_batch* b) {
+    if (s->vb_sized || b->path != MDRQ_PATH_VAFILE_BATCH || !b->nq || !s->n) return;
+    enqueue(s, b, false, s->stream);
+    std::vector<unsigned long long> c(b->nq);
+    CK(cudaMemcpyAsync(c.data(), b->d_counts.p, sizeof(unsigned long long) * b->nq, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    uint64_t total = 0;
+    for (unsigned long long v : c) total += v;
+    if (total > uint64_t(s->vb_max_blocks) * kRecBlock / 2) grow_vb_staging(s, total);
+    s->vb_sized = true;
+}
+
 uint64_t run_ids_sync(mdrq_store* s, mdrq_batch* b) {
     s->bounce_ids = 0;
+    presize_vb_staging(s, b);
     // until the result pool holds the batch AND no pass overflowed the
     // staging pool (a reserved batch then never runs the recount pass)
     for (int attempt = 0; attempt < 4; ++attempt) {
@@ -1282,6 +1299,7 @@ int query_ids_impl(mdrq_store* s, const float* lower, const float* upper, uint32
         if (head > kBounceMaxBytes) raise(MDRQ_EINVAL, "too many queries in one call");
         uint64_t total = 0, spec = 0;
         uint8_t* hb = nullptr;
+        presize_vb_staging(s, b);
         for (int attempt = 0;; ++attempt) {
             if (attempt == 2) raise(MDRQ_ECUDA, "result pool did not converge");
             enqueue(s, b, true, s->stream);
@@ -1688,6 +1706,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             // far: a fresh slot must not run its first batch twice
             if (s->stream_hint && (!b->own_ids.p || b->own_ids.cap < s->stream_hint))
                 b->own_ids.reserve(size_t(s->stream_hint + s->stream_hint / 8 + 4096));
+            presize_vb_staging(s, b);   // a store's first bit-sliced batch (synchronous, once)
             up += upload_bytes(b);
             enqueue(s, b, true, s->stream);
             sl.h_flags[0] = sl.h_flags[1] = 0;
