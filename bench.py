@@ -608,7 +608,7 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
     pinned = [torch.empty(max(1, total_local + 1024), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
               for _ in range(nbuf)]
     pin_s = time.perf_counter() - t0
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e_steps = max(3, min(args.steps, 20))   # the first step's device pass is the only unhidden part
     # warm: every slot of the stream (3) sizes its result pool once
     method.search_stream([queries] * 3, outs=[pinned[k % nbuf] for k in range(3)])
     if world > 1:

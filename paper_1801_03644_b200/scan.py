@@ -153,12 +153,14 @@ class _GpuScan:
         BatchResult per batch; batch k's device->host copy runs under batch
         k+1's device pass (DeviceStore.ids_stream).  ``outs`` optionally
         gives one caller-owned (pinned) uint32 buffer per batch."""
-        pairs = []
+        pairs, seen = [], {}
         for queries in batches:
-            queries = list(queries)
-            for q in queries:
-                self._check(q)
-            pairs.append(stack_queries(queries, self.m))
+            if id(queries) not in seen:   # a repeated batch object is stacked once
+                qs = list(queries)
+                for q in qs:
+                    self._check(q)
+                seen[id(queries)] = stack_queries(qs, self.m)
+            pairs.append(seen[id(queries)])
         return [BatchResult(o, i) for o, i in self.store.ids_stream(pairs, self._batch_path, outs=outs, info=info)]
 
     def search_batch(self, queries) -> BatchResult:

@@ -153,13 +153,15 @@ class VaFile:
     def search_stream(self, batches, outs=None, info: dict | None = None) -> list:
         """Pipelined ids of a sequence of query batches (see
         _GpuScan.search_stream)."""
-        pairs = []
+        pairs, seen = [], {}
         for queries in batches:
-            queries = list(queries)
-            for q in queries:
-                if q.m != self.m:
-                    raise ValueError(f"query has {q.m} dimensions, grid has {self.m}")
-            pairs.append(stack_queries(queries, self.m))
+            if id(queries) not in seen:   # a repeated batch object is stacked once
+                qs = list(queries)
+                for q in qs:
+                    if q.m != self.m:
+                        raise ValueError(f"query has {q.m} dimensions, grid has {self.m}")
+                seen[id(queries)] = stack_queries(qs, self.m)
+            pairs.append(seen[id(queries)])
         res = self.store.ids_stream(pairs, "auto", outs=outs, info=info)
         if self._ids is not None:
             out = []
