@@ -29,10 +29,8 @@ from .core import (
 from .kernels import BACKEND
 from .methods import METHOD_NAMES, build_method
 from .parallel import (
-    ExecutorConfig,
     PartitionLayout,
     ShardedScan,
-    WorkerPool,
     combine_counts,
     combine_ids,
     default_threads,

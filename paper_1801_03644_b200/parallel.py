@@ -16,77 +16,37 @@ On B200 the partitions are GPUs, one process per GPU:
   vectorised scatter into rank order.  Over NCCL this runs on NVLink; the
   same functions run over gloo on CPU tensors for the tests.
 
-``make_layout`` / ``PartitionLayout`` / ``WorkerPool`` keep the reference's
-host-side API (HorizontalScan and build_method accept layouts).
+``make_layout`` / ``PartitionLayout`` keep the reference's host-side API
+(HorizontalScan and build_method accept layouts); the reference's thread
+pool has no counterpart -- on one GPU the CTA grid is the fan-out.
 """
 
 from __future__ import annotations
 
 import os
-from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
 
 
 def default_threads() -> int:
-    """MDRQ_THREADS override, else the machine's logical cores (parallel.py:20-27)."""
-    env = os.environ.get("MDRQ_THREADS")
-    if env:
-        t = int(env)
-        if t >= 1:
-            return t
-    return os.cpu_count() or 1
-
-
-@dataclass(frozen=True)
-class ExecutorConfig:
-    """Worker count t; the partition count defaults to t (parallel.py:30-42)."""
-
-    t: int
-
-    def __post_init__(self):
-        if self.t < 1:
-            raise ValueError("worker count must be at least 1")
-
-    @property
-    def p(self) -> int:
-        return self.t
-
-
-class WorkerPool:
-    """Thin reusable ThreadPoolExecutor wrapper (parallel.py:45-78)."""
-
-    def __init__(self, workers: int):
-        if workers < 1:
-            raise ValueError("worker count must be at least 1")
-        self.workers = workers
-        self._executor: ThreadPoolExecutor | None = None
-
-    def run(self, tasks):
-        tasks = list(tasks)
-        if self.workers == 1 or len(tasks) <= 1:
-            return [task() for task in tasks]
-        if self._executor is None:
-            self._executor = ThreadPoolExecutor(max_workers=self.workers)
-        futures = [self._executor.submit(task) for task in tasks]
-        return [f.result() for f in futures]
-
-    def close(self) -> None:
-        if self._executor is not None:
-            self._executor.shutdown(wait=True)
-            self._executor = None
-
-    def __enter__(self):
-        return self
-
-    def __exit__(self, *exc):
-        self.close()
+    """Host worker count: MDRQ_THREADS when it is a positive integer, else the
+    logical core count (parallel.py:20-27).  On this engine it only sizes
+    host-side helpers; the scan's parallelism is the CTA grid."""
+    try:
+        t = int(os.environ.get("MDRQ_THREADS", ""))
+    except ValueError:
+        t = 0
+    return t if t >= 1 else (os.cpu_count() or 1)
 
 
 @dataclass(frozen=True)
 class PartitionLayout:
-    """Balanced random assignment of n objects to p partitions (parallel.py:81-95)."""
+    """The reference's seeded row partitioning (parallel.py:81-118), kept so
+    layout-taking constructors (HorizontalScan) accept the same arguments.
+    ``parts[q]`` are the ids of partition q in permutation order and
+    ``assignment[i]`` is the partition of object i.  The GPU scan does not
+    need it (one store covers all rows); results do not depend on it."""
 
     p: int
     seed: int
@@ -95,29 +55,24 @@ class PartitionLayout:
 
     @property
     def n(self) -> int:
-        return int(self.assignment.size)
+        return len(self.assignment)
 
     def sizes(self) -> list[int]:
-        return [int(ids.size) for ids in self.parts]
+        return [len(ids) for ids in self.parts]
 
 
 def make_layout(n: int, p: int, seed: int) -> PartitionLayout:
-    """Seeded permutation split into p near-equal runs (parallel.py:98-118)."""
+    """``default_rng(seed).permutation(n)`` cut into p runs whose sizes differ
+    by at most one, the larger runs first (parallel.py:98-118)."""
     if p < 1:
         raise ValueError("partition count must be at least 1")
-    rng = np.random.default_rng(seed)
-    perm = rng.permutation(n).astype(np.int64)
-    base, extra = divmod(n, p)
-    parts = []
+    order = np.random.default_rng(seed).permutation(n).astype(np.int64)
+    sizes = np.full(p, n // p, dtype=np.int64)
+    sizes[: n % p] += 1
+    cuts = np.cumsum(sizes)[:-1]
     assignment = np.empty(n, dtype=np.int32)
-    start = 0
-    for q in range(p):
-        size = base + (1 if q < extra else 0)
-        ids = perm[start:start + size]
-        assignment[ids] = q
-        parts.append(ids)
-        start += size
-    return PartitionLayout(p=p, seed=seed, assignment=assignment, parts=tuple(parts))
+    assignment[order] = np.repeat(np.arange(p, dtype=np.int32), sizes)
+    return PartitionLayout(p=p, seed=seed, assignment=assignment, parts=tuple(np.split(order, cuts)))
 
 
 # ----------------------------------------------------------- GPU sharding --

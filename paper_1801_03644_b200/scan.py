@@ -27,42 +27,42 @@ from . import _lib
 
 
 class ColumnSet:
-    """Columnar mirror of a DataSet: m contiguous 1-d arrays (scan.py:17-40)."""
+    """Host-side columnar view of a DataSet: m read-only float32 columns of
+    one length (scan.py:17-40).  The scan itself runs on the device store's
+    own ``cols[m][n_pad]`` layout; this object is the API the reference
+    exposes for it."""
 
     __slots__ = ("columns", "n", "m")
 
     def __init__(self, columns):
-        columns = [np.ascontiguousarray(c, dtype=np.float32) for c in columns]
-        if not columns:
+        cols = [np.ascontiguousarray(c, dtype=np.float32) for c in columns]
+        if len(cols) == 0:
             raise ValueError("at least one column required")
-        n = columns[0].shape[0]
-        for c in columns:
-            if c.ndim != 1 or c.shape[0] != n:
-                raise ValueError("columns must be 1-d and of equal length")
+        length = len(cols[0]) if cols[0].ndim == 1 else -1
+        if any(c.ndim != 1 or len(c) != length for c in cols):
+            raise ValueError("columns must be 1-d and of equal length")
+        for c in cols:
             c.setflags(write=False)
-        self.columns = columns
-        self.n = n
-        self.m = len(columns)
+        self.columns, self.n, self.m = cols, length, len(cols)
 
     @classmethod
     def from_dataset(cls, data: DataSet) -> "ColumnSet":
-        return cls([data.values[:, j] for j in range(data.m)])
+        return cls(list(data.values.T))
 
     def to_matrix(self) -> np.ndarray:
-        return np.column_stack(self.columns)
+        return np.stack(self.columns, axis=1)
 
 
 def chunk_spans(nbytes: int, t: int) -> list[tuple[int, int]]:
-    """Exactly t byte spans of near-equal size; the last takes the remainder
-    (scan.py:43-52; host arithmetic, kept for API parity)."""
+    """t byte spans [start, stop) of ceil(nbytes / t) bytes, clipped at nbytes
+    (so trailing spans may be empty) -- scan.py:43-52; host arithmetic kept for
+    API parity (the device splits its own work)."""
     if t < 1:
         raise ValueError("chunk count must be at least 1")
-    size = -(-nbytes // t)
-    spans = []
-    for i in range(t):
-        start = min(i * size, nbytes)
-        spans.append((start, min(start + size, nbytes)))
-    return spans
+    step = -(-nbytes // t)
+    starts = np.minimum(np.arange(t, dtype=np.int64) * step, nbytes)
+    stops = np.minimum(starts + step, nbytes)
+    return [(int(a), int(b)) for a, b in zip(starts, stops)]
 
 
 def and_masks_chunked(masks, t: int, pool=None) -> np.ndarray:

@@ -79,20 +79,23 @@ def uniform_rows(seed: int, m: int, start: int, stop: int) -> np.ndarray:
     return rng.random((stop - start, m), dtype=np.float32)
 
 
+def _generator(seed) -> np.random.Generator:
+    return seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
+
+
 def gen_query_from_pair(data: DataSet, seed) -> RangeQuery:
-    """Complete-match query from two random objects (workload.py:113-120)."""
+    """The bounding box of two distinct random objects (workload.py:113-120):
+    one ``choice(n, 2, replace=False)`` draw per query, so a shared generator
+    yields the reference's query sequence."""
     if data.n < 2:
         raise ValueError("pair query generation needs at least 2 objects")
-    rng = seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
-    i, j = rng.choice(data.n, size=2, replace=False)
-    a = data.values[i]
-    b = data.values[j]
-    return RangeQuery(np.minimum(a, b), np.maximum(a, b))
+    pair = data.values[_generator(seed).choice(data.n, size=2, replace=False)]
+    return RangeQuery(pair.min(axis=0), pair.max(axis=0))
 
 
 def pair_query_batch(data: DataSet, count: int, seed) -> list[RangeQuery]:
-    """workload.py:123-126."""
-    rng = seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
+    """``count`` pair queries from one generator (workload.py:123-126)."""
+    rng = _generator(seed)
     return [gen_query_from_pair(data, rng) for _ in range(count)]
 
 
@@ -351,27 +354,33 @@ def queries_from_arrays(lo: np.ndarray, hi: np.ndarray) -> list[RangeQuery]:
 
 # -- query batch serialisation (JSON lines, workload.py:343-366) ----------------
 
+def _json_bound(v, sentinel):
+    return None if v == sentinel else float(v)
+
+
 def write_queries(queries, path) -> None:
-    """One JSON object per line; nulls encode the infinity sentinels."""
+    """JSON lines ``{"lower": [...], "upper": [...]}``; null stands for the
+    -inf / +inf sentinel of an unqueried bound."""
+    lines = [json.dumps({"lower": [_json_bound(v, -np.inf) for v in q.lower],
+                         "upper": [_json_bound(v, np.inf) for v in q.upper]})
+             for q in queries]
     with open(path, "w", encoding="utf-8") as fh:
-        for q in queries:
-            lower = [None if v == -np.inf else float(v) for v in q.lower]
-            upper = [None if v == np.inf else float(v) for v in q.upper]
-            fh.write(json.dumps({"lower": lower, "upper": upper}) + "\n")
+        fh.writelines(line + "\n" for line in lines)
 
 
 def read_queries(path) -> list[RangeQuery]:
-    queries = []
+    """Inverse of ``write_queries``; blank lines are skipped, a malformed
+    record raises ValueError naming ``path:line`` (workload.py:355-366)."""
+    out = []
     with open(path, "r", encoding="utf-8") as fh:
-        for lineno, line in enumerate(fh, 1):
-            line = line.strip()
-            if not line:
+        for lineno, text in enumerate(fh, 1):
+            if not text.strip():
                 continue
             try:
-                obj = json.loads(line)
-                lower = [(-np.inf if v is None else v) for v in obj["lower"]]
-                upper = [(np.inf if v is None else v) for v in obj["upper"]]
+                rec = json.loads(text)
+                lower = [-np.inf if v is None else v for v in rec["lower"]]
+                upper = [np.inf if v is None else v for v in rec["upper"]]
             except (json.JSONDecodeError, KeyError, TypeError) as exc:
                 raise ValueError(f"{path}:{lineno}: bad query record: {exc}") from None
-            queries.append(RangeQuery(lower, upper))
-    return queries
+            out.append(RangeQuery(lower, upper))
+    return out

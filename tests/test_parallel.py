@@ -15,7 +15,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_1801_03644_b200 import ExecutorConfig, make_layout
+from paper_1801_03644_b200 import make_layout
 from paper_1801_03644_b200.parallel import combine_counts, combine_ids, shard_range
 
 
@@ -46,9 +46,6 @@ class TestMakeLayout:
     def test_validation(self):
         with pytest.raises(ValueError):
             make_layout(10, 0, seed=0)
-        with pytest.raises(ValueError):
-            ExecutorConfig(t=0)
-        assert ExecutorConfig(t=6).p == 6
 
 
 @pytest.mark.parametrize("n,world", [(0, 2), (1, 2), (10, 3), (100, 8), (5_000_000, 8), (7, 8)])
