@@ -17,7 +17,8 @@ import numpy as np
 PKG = os.path.dirname(os.path.abspath(__file__))
 # MDRQ_LIB=checked loads the build with device-side bounds checks
 # (build.py --checked, common.cuh MDRQ_CHECKS) -- for tests
-LIB_PATH = os.path.join(PKG, "libmdrq_b200_checked.so" if os.environ.get("MDRQ_LIB") == "checked"
+# (any other MDRQ_LIB=<name>: an experiment build, build.py --variant <name>)
+LIB_PATH = os.path.join(PKG, f"libmdrq_b200_{os.environ['MDRQ_LIB']}.so" if os.environ.get("MDRQ_LIB")
                         else "libmdrq_b200.so")
 
 MDRQ_OK = 0

@@ -50,7 +50,8 @@ def _stale(target: str, deps) -> bool:
 LIB_CHECKED = os.path.join(PKG, "libmdrq_b200_checked.so")
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False,
+          variant: str = "", defines=()) -> str:
     """Build libmdrq_b200.so; ``checked`` builds libmdrq_b200_checked.so with
     the device-side bounds checks (MDRQ_CHECKS, common.cuh) into its own
     object directory.  The product loads the release library; the checked one
@@ -58,6 +59,12 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     build_dir = BUILD + ("_checked" if checked else "")
     lib_path = LIB_CHECKED if checked else LIB
     extra = ["-DMDRQ_CHECKS"] if checked else []
+    if variant:
+        # experiment builds (tools/): libmdrq_b200_<variant>.so with extra
+        # defines, loaded with MDRQ_LIB=<variant>; never the product library
+        build_dir = BUILD + "_" + variant
+        lib_path = os.path.join(PKG, f"libmdrq_b200_{variant}.so")
+        extra = [f"-D{d}" for d in defines]
     os.makedirs(build_dir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "mdrq_b200.h")]
     objs = []
@@ -91,5 +98,8 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     return lib_path
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--variant" in sys.argv:
+    i = sys.argv.index("--variant")
+    print(build(variant=sys.argv[i + 1], defines=sys.argv[i + 2:]))
+elif __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

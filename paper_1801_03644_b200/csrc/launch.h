@@ -79,7 +79,12 @@ struct BatchArgs {
 constexpr int kVaBatchMaxDims = 24;
 // table cells per dimension for a pass with kb union dims (fits 227 KB smem)
 // (9..16-dim unions use 32 cells so their on-chip values / bounds fit)
-__host__ __device__ constexpr uint32_t va_batch_cells(uint32_t kb) { return kb <= 8 ? 64u : 32u; }
+#ifndef MDRQ_VB_CELLS_WIDE
+#define MDRQ_VB_CELLS_WIDE 32
+#endif
+__host__ __device__ constexpr uint32_t va_batch_cells(uint32_t kb) {
+    return kb <= 8 ? 64u : kb <= 10 ? uint32_t(MDRQ_VB_CELLS_WIDE) : 32u;
+}
 // Unions of kb <= kVbPvDims keep the exact query bounds in shared memory (and,
 // up to 10 dims, the block's exact values) and refine every overlap candidate
 // exactly, so their table is overlap-only: rows of dims (2p, 2p+1) at cell c

@@ -46,7 +46,13 @@ namespace mdrq {
 
 namespace {
 
-constexpr int VB_THREADS = 512;
+#ifndef MDRQ_VB_THREADS
+#define MDRQ_VB_THREADS 512
+#endif
+#ifndef MDRQ_VB_ACODE
+#define MDRQ_VB_ACODE 1
+#endif
+constexpr int VB_THREADS = MDRQ_VB_THREADS;
 constexpr int VB_WARPS = VB_THREADS / 32;
 // candidate queue per warp: < 32 left over + 2 ballots x 32 lanes (a step
 // drains the queue after its second and its last ballot)
@@ -57,11 +63,19 @@ __device__ __forceinline__ float f4_get(const float4& w, uint32_t i) {
 }
 
 // staged-value slot of tuple t (in the block) and pair h in a warp's buffer:
-// h * 128 + (t & 3) * 32 + (t >> 2).  Lane l stages its tuples 4l .. 4l+3, so
-// every store instruction hits 32 consecutive slots (conflict-free; the
-// earlier tuple-major layout took 4 wavefronts per ideal one on C5)
+// h * 128 + (t & 3) * 32 + ((t >> 2) ^ ((t & 3) << SW)).  Lane l stages its
+// tuples 4l .. 4l+3, so every store instruction hits 32 consecutive slots in a
+// permuted order (conflict-free; the earlier tuple-major layout took 4
+// wavefronts per ideal one on C5).  The XOR spreads the four tuples of a lane
+// over the bank groups: a refinement round reads a handful of neighbouring
+// tuples (queue order is tuple order), and without it tuples 4k .. 4k+3 shared
+// one bank group (2-3 wavefronts per ideal one on C5's value reads).  SW = 2
+// for 8-byte slots (16 bank pairs per half warp: tuples 4k .. 4k+15 distinct
+// for k % 4 == 0), 1 for 16-byte slots (8 bank groups per quarter warp)
+template <int VS>
 __device__ __forceinline__ uint32_t val_slot(uint32_t t, uint32_t h) {
-    return h * 128u + ((t & 3u) << 5) + (t >> 2);
+    constexpr uint32_t SW = VS == 4 ? 1u : 2u;
+    return h * 128u + ((t & 3u) << 5) + ((t >> 2) ^ ((t & 3u) << SW));
 }
 
 // LW = lanes per tuple: 32 (a pass of up to 1 024 queries, lane w = query
@@ -90,6 +104,13 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     // instruction their tuples' cells of all dims, instead of one SHFL per
     // dimension and code word (the SHFLs cost data-pipe wavefronts too)
     constexpr bool SCODE = TPI > 1 && KB <= 8 && MODE != 2;
+    // multi-word passes of 9 / 10 union dims have no room for staged cells;
+    // their compacted tuple list carries, per unpruned tuple, the tuple index
+    // (7 bits) and the table cells of the first AND dims (CB bits each) in one
+    // word, so the sub-step's one list load replaces AND of its KB shuffles
+    constexpr bool ACODE = MDRQ_VB_ACODE && W2 && !SCODE && MODE != 2;
+    constexpr uint32_t CB = va_batch_cells(KB) == 64 ? 6u : 5u;   // bits per cell
+    constexpr int AND = ACODE ? (int(25u / CB) < KB ? int(25u / CB) : KB) : 0;
     extern __shared__ __align__(16) uint32_t sm[];
     constexpr uint32_t K = va_batch_cells(KB);     // cells per dimension (64 / 32)
     constexpr bool PV = va_batch_pv(KB);           // values + bounds in smem, overlap-only table
@@ -120,6 +141,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     uint16_t* s_cnt16 = reinterpret_cast<uint16_t*>(s_rest);
     // W2 (multi-word) dense passes: every warp's compacted list of the block's
     // unpruned tuples [128] u8, after the queues and staged cells
+    // (ACODE: a word per tuple, see above)
     uint8_t* s_alive = reinterpret_cast<uint8_t*>(s_qe + VB_WARPS * VB_QCAP) + (SCODE ? VB_WARPS * 128 * 8 : 0);
 
     // the recount pass only runs when the single-pass staging overflowed
@@ -158,6 +180,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     uint32_t* qs = s_qs + warp * VB_QCAP;
     uint16_t* wcnt = s_cnt16 + warp * 1024;        // MODE 2
     uint8_t* walive = s_alive + warp * 128;        // W2: compacted tuple list of the block
+    uint32_t* walive32 = reinterpret_cast<uint32_t*>(s_alive) + warp * 128;   // ACODE
     const uint32_t lt = lanemask_lt();
 
     // Exact refinement of one query word for one tuple: bit b of the result
@@ -171,7 +194,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             if constexpr (STAGE && VS == 4) {
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    const float4 w4 = reinterpret_cast<const float4*>(wval)[val_slot(tl, h)];
+                    const float4 w4 = reinterpret_cast<const float4*>(wval)[val_slot<VS>(tl, h)];
                     v[4 * h] = w4.x;
                     v[4 * h + 1] = w4.y;
                     v[4 * h + 2] = w4.z;
@@ -180,7 +203,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             } else if constexpr (STAGE) {
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    const float2 w2 = reinterpret_cast<const float2*>(wval)[val_slot(tl, h)];
+                    const float2 w2 = reinterpret_cast<const float2*>(wval)[val_slot<VS>(tl, h)];
                     v[2 * h] = w2.x;
                     v[2 * h + 1] = w2.y;
                 }
@@ -280,10 +303,10 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                             c[e] = u < KB ? f4_get(vv_n[u < KB ? u : 0], jj) : 0.0f;
                         }
                         if constexpr (VS == 4)
-                            reinterpret_cast<float4*>(wval)[val_slot(4 * lane + jj, h)] =
+                            reinterpret_cast<float4*>(wval)[val_slot<VS>(4 * lane + jj, h)] =
                                 make_float4(c[0], c[1], c[2], c[3]);
                         else
-                            reinterpret_cast<float2*>(wval)[val_slot(4 * lane + jj, h)] = make_float2(c[0], c[1]);
+                            reinterpret_cast<float2*>(wval)[val_slot<VS>(4 * lane + jj, h)] = make_float2(c[0], c[1]);
                     }
                 if constexpr (SCODE) {
                     // cells of tuples 4*lane + b (b = 0..3), dims 0..3 / 4..7
@@ -312,7 +335,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
             uint32_t nalive = jmax;
             bool compact = false;
             if constexpr (W2 && MODE != 2) {
-                if (a.prune_dims) {
+                if (ACODE || a.prune_dims) {
                     uint32_t nib = 0xFu;
 #pragma unroll
                     for (int u = 0; u < KB; ++u)
@@ -331,14 +354,22 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         if (lane >= uint32_t(o)) incl += x2;
                     }
                     nalive = __shfl_sync(0xFFFFFFFFu, incl, 31);
-                    compact = nalive < jmax;
+                    compact = ACODE || nalive < jmax;
                     if (compact) {
                         uint32_t pos = incl - c;
 #pragma unroll
                         for (uint32_t bb = 0; bb < 4; ++bb)
                             if (nib >> bb & 1u) {
                                 MDRQ_CHECK(pos < 128u, kChkAlive);
-                                walive[pos++] = uint8_t(4 * lane + bb);
+                                if constexpr (ACODE) {
+                                    // tuple index << 25 | cells of dims 0 .. AND-1
+                                    uint32_t e = (4 * lane + bb) << 25;
+#pragma unroll
+                                    for (int u = 0; u < AND; ++u) e |= ((cw[u] >> (8 * bb)) & 0xFFu) << (CB * u);
+                                    walive32[pos++] = e;
+                                } else {
+                                    walive[pos++] = uint8_t(4 * lane + bb);
+                                }
                             }
                         __syncwarp();
                     }
@@ -348,13 +379,19 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 // this lane's tuple (index in the block) of every sub-step and
                 // whether it exists: tix / tvm
                 uint32_t tix[NS];
+                uint32_t pk[ACODE ? NS : 1];   // ACODE: the list word (tuple index, packed cells)
                 uint32_t tvm = 0;
 #pragma unroll
                 for (int ss = 0; ss < NS; ++ss) {
                     const uint32_t pos = j4 + ss * TPI + (LW == 32 ? 0u : lane_tup);
                     const bool ok = pos < nalive;
                     tvm |= uint32_t(ok) << ss;
-                    tix[ss] = (W2 && compact) ? (ok ? uint32_t(walive[pos]) : 0u) : pos;
+                    if constexpr (ACODE) {
+                        pk[ss] = ok ? walive32[pos] : 0u;
+                        tix[ss] = pk[ss] >> 25;
+                    } else {
+                        tix[ss] = (W2 && compact) ? (ok ? uint32_t(walive[pos]) : 0u) : pos;
+                    }
                 }
                 // the step's CWS code words of every union dim (narrow passes
                 // take 8 tuples per step for more independent work)
@@ -371,7 +408,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
 #pragma unroll
                     for (int c = 0; c < NS; ++c)
 #pragma unroll
-                        for (int u = 0; u < KB; ++u) xw[c][u] = __shfl_sync(0xFFFFFFFFu, cw[u], tix[c] >> 2);
+                        for (int u = AND; u < KB; ++u) xw[c][u] = __shfl_sync(0xFFFFFFFFu, cw[u], tix[c] >> 2);
                 } else {
 #pragma unroll
                     for (int c = 0; c < CWS; ++c)
@@ -396,10 +433,19 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                         // row address of dim uu (SCODE: byte uu % 4 of the
                         // staged word, a compile-time selector)
                         auto addr = [&](int uu) -> uint32_t {
-                            if constexpr (SCODE)
+                            if constexpr (SCODE) {
                                 return __byte_perm(uu < 4 ? sc[ss].x : sc[ss].y, lane_off, 0x5504u | ((uint32_t(uu) & 3u) << 4));
-                            else
+                            } else if constexpr (ACODE) {
+                                if (uu < AND) {
+                                    // (cell << 8) | lane offset from the packed list word
+                                    const int sh = int(CB) * uu - 8;
+                                    const uint32_t c8 = sh < 0 ? pk[ss] << (sh < 0 ? -sh : 0) : pk[ss] >> (sh < 0 ? 0 : sh);
+                                    return (c8 & ((K - 1u) << 8)) | lane_off;
+                                }
                                 return __byte_perm(x[uu], lane_off, sel);
+                            } else {
+                                return __byte_perm(x[uu], lane_off, sel);
+                            }
                         };
                         const uint32_t ca = addr(u);
                         if constexpr (W2) {
@@ -1323,7 +1369,8 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
     else
         bytes += 1024 * 4 + size_t(VB_WARPS) * VB_QCAP * (8 + (pv ? 0 : 4));
     if (mode != 2 && pv && kb <= 8) bytes += size_t(VB_WARPS) * 128 * 8;   // staged cells (multi-word passes)
-    if (mode != 2 && pv) bytes += size_t(VB_WARPS) * 128;                 // compacted tuple lists
+    // compacted tuple lists (a word per tuple where they carry packed cells)
+    if (mode != 2 && pv) bytes += size_t(VB_WARPS) * 128 * ((MDRQ_VB_ACODE && kb > 8 && vb_words(kb) > 1) ? 4 : 1);
     return bytes;
 }
 
