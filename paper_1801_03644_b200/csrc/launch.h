@@ -78,9 +78,13 @@ struct BatchArgs {
 // bit-sliced multi-query VA pass (vabatch.cu), <= 1024 queries per pass
 constexpr int kVaBatchMaxDims = 24;
 // table cells per dimension for a pass with kb union dims (fits 227 KB smem)
-// (9..16-dim unions use 32 cells so their on-chip values / bounds fit)
+// (11..16-dim unions use 32 cells so their on-chip bounds fit; 9 / 10 dims
+// have room for 64 since their bounds are 15-bit codes)
+#ifndef MDRQ_VB_Q15
+#define MDRQ_VB_Q15 1
+#endif
 #ifndef MDRQ_VB_CELLS_WIDE
-#define MDRQ_VB_CELLS_WIDE 32
+#define MDRQ_VB_CELLS_WIDE (MDRQ_VB_Q15 ? 64 : 32)
 #endif
 __host__ __device__ constexpr uint32_t va_batch_cells(uint32_t kb) {
     return kb <= 8 ? 64u : kb <= 10 ? uint32_t(MDRQ_VB_CELLS_WIDE) : 32u;
@@ -102,6 +106,25 @@ __host__ __device__ constexpr uint32_t va_batch_vdims(uint32_t kb) {
 __host__ __device__ constexpr uint32_t va_batch_table_words(uint32_t kb, uint32_t cells) {
     return va_batch_pv(kb) ? (kb + 1) / 2 * cells * 64 : kb * cells * 64;
 }
+// Staged unions (<= kVbStageDims dims, values on chip) refine on 15-bit
+// monotone codes first (MDRQ_VB_Q15): value code c(v) = bits 8..22 of
+// clamp(fma(v - vmin[u], vscale[u], 2)) in [1, 32766]; a query bound is the
+// code of its lo / hi (0 / 32767 when it lies below / above every value), two
+// dims per word with a guard bit per half.  c > L and c < H in every dim
+// decides a candidate exactly (matches), c < L or c > H in some dim rejects
+// it; only a code equal to a bound's falls back to the float32 compare
+// against the exact bounds in global memory.  Per query the codes take
+// vdims(kb) words (LN = 0x8000 - L per half for the vdims/2 dim pairs, then
+// HG = 0x8000 + H): 40 bytes for 10 dims against 80 bytes of float bounds.
+constexpr uint32_t kVbStageDims = 10;
+__host__ __device__ constexpr bool va_batch_q15(uint32_t kb) { return MDRQ_VB_Q15 && kb <= kVbStageDims; }
+constexpr float kVbQ15Min = 2.00006103515625f;    // 2 + 2^-14: code 1
+constexpr float kVbQ15Max = 3.9998779296875f;     // 2 + 32766 * 2^-14: code 32766
+// the code function, identical on host and device (monotone non-decreasing
+// in v for scale > 0; NaN from inf - inf clamps to code 1 on both sides)
+__host__ __device__ __forceinline__ float va_batch_q15_t(float v, float vmin, float scale) {
+    return fminf(fmaxf(fmaf(v - vmin, scale, 2.0f), kVbQ15Min), kVbQ15Max);
+}
 struct VaBatchArgs {
     const uint8_t* codes;        // VA code planes [m][stride]
     const float* cols;           // exact columns [m][stride] (refinement)
@@ -116,6 +139,11 @@ struct VaBatchArgs {
     const uint32_t* tables;      // query-mask words, layout per va_batch_pv(kb) (above)
     const float2* qbounds;       // exact (lo, hi), +-inf where unconstrained; layout per va_batch_pv(kb)
     const uint32_t* qcmask;      // [1024] constrained union dims per query (bit u)
+    // Q15 refinement (staged unions): per query vdims words (LN pairs, HG
+    // pairs) in 16-byte chunks [chunk][1024 slots] + an 8-byte tail
+    // [1024 slots]; the code function's per-dim origin and scale
+    const uint32_t* qb16;
+    float vmin[kVbStageDims], vscale[kVbStageDims];
     uint32_t grid;               // CTAs (chunks = grid * warps)
     uint64_t chunk_tuples;       // tuples per chunk (multiple of 128, < 65536: u16 counters)
     uint32_t nchunks;            // subchunks: ceil(n / chunk_tuples), one warp each

@@ -10,6 +10,7 @@
 //   VaFile filter + refine                                 vafile.py:88-219
 //   SearchStats counters                                   core.py:218-237
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 #include <cstring>
 #include <chrono>
@@ -166,7 +167,9 @@ struct Pass {
 struct VbPass {
     uint32_t q0 = 0, nqp = 0, kb = 0, cells = 0, shift = 0;
     bool fallback = false;   // union wider than kVaBatchMaxDims: per-query VA
-    size_t udim_off = 0, table_off = 0, qb_off = 0, cm_off = 0;
+    size_t udim_off = 0, table_off = 0, qb_off = 0, cm_off = 0, q16_off = 0;
+    // staged unions (va_batch_q15): the 15-bit code function of every union dim
+    float vmin[kVbStageDims] = {}, vscale[kVbStageDims] = {};
     uint32_t prune = 0;                  // union dims whose cell mask is not full
     unsigned long long cellmask[kVaBatchMaxDims] = {};
 };
@@ -194,6 +197,8 @@ struct mdrq_batch {
     std::vector<uint32_t> vb_tables;
     std::vector<float2> vb_qb;
     std::vector<uint32_t> vb_cm;   // per query of a pass: constrained union dims
+    std::vector<uint32_t> vb_q16;  // staged unions: the queries' 15-bit bound codes (launch.h)
+    DBuf<uint32_t> d_vb_q16;
     // sorted batch: slot i of the passes holds query vb_perm[i] (empty: slot = query)
     std::vector<uint32_t> vb_perm;
     DBuf<uint32_t> d_vb_perm;
@@ -222,7 +227,7 @@ struct mdrq_batch {
     // device buffers freed (the owning store was destroyed first)
     void release_device() {
         d_descs.release(); d_preds.release(); d_udims.release(); d_bounds.release(); d_cmask.release();
-        d_vb_udims.release(); d_vb_tables.release(); d_vb_qb.release(); d_vb_cm.release();
+        d_vb_udims.release(); d_vb_tables.release(); d_vb_qb.release(); d_vb_cm.release(); d_vb_q16.release();
         d_scratch.release(); own_ids.release();
     }
 };
@@ -462,6 +467,13 @@ std::vector<uint32_t> choose_vb_order(const mdrq_store* s, const mdrq_batch* b) 
 
 void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b);
 
+// word j (of vd) of query slot qs in a pass's 15-bit bound codes: 16-byte
+// chunks [vd / 4][1024 slots], then the 8-byte tail [1024 slots] (vabatch.cu)
+inline size_t vb_q16_index(uint32_t vd, uint32_t j, uint32_t qs) {
+    const uint32_t c4 = vd / 4;
+    return j < 4 * c4 ? (size_t(j / 4) * 1024 + qs) * 4 + j % 4 : size_t(c4) * 4096 + size_t(qs) * 2 + (j - 4 * c4);
+}
+
 void build_vb_passes(const mdrq_store* s, mdrq_batch* b) {
     static const bool no_sort = getenv("MDRQ_VB_NO_SORT") != nullptr;   // measurement / test switch
     b->vb_perm = no_sort ? std::vector<uint32_t>() : choose_vb_order(s, b);
@@ -488,6 +500,7 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
     b->vb_tables.clear();
     b->vb_qb.clear();
     b->vb_cm.clear();
+    b->vb_q16.clear();
     const uint32_t m = s->m, bits = s->va_bits;
     const bool sorted = !b->vb_perm.empty();
     auto query_of = [&](uint32_t slot) { return sorted ? b->vb_perm[slot] : slot; };
@@ -531,6 +544,38 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         const uint32_t cells = ps.cells;
         std::vector<uint32_t> tab(va_batch_table_words(ps.kb, cells), 0u);
         std::vector<float2> qbv(size_t(1024) * qstride, make_float2(-INFINITY, INFINITY));
+        // staged unions: the 15-bit code function per union dim (monotone; any
+        // positive scale is sound, a degenerate range only sends more
+        // candidates to the exact compare) and the queries' bound codes, two
+        // dims per word: LN = 0x8000 - L, HG = 0x8000 + H per half; a free dim
+        // is (L, H) = (0, 32767), strictly outside every value code
+        const bool q15 = va_batch_q15(ps.kb);
+        const uint32_t vd = va_batch_vdims(ps.kb);
+        std::vector<uint32_t> q16;
+        if (q15) {
+            for (uint32_t u = 0; u < kVbStageDims; ++u) {
+                ps.vmin[u] = 0.f;
+                ps.vscale[u] = FLT_MIN;
+                if (u >= ps.kb || s->h_minmax.size() < size_t(2) * m) continue;
+                const float mn = s->h_minmax[2 * ud[u]], mx = s->h_minmax[2 * ud[u] + 1];
+                const float range = mx - mn;
+                if (std::isfinite(mn)) ps.vmin[u] = mn;
+                if (range > 0.f && std::isfinite(range)) {
+                    const float sc = float(2.0 * (1.0 - 1.0 / 4096) / double(range));
+                    if (sc > 0.f && std::isfinite(sc)) ps.vscale[u] = sc;
+                }
+            }
+            q16.assign(size_t(1024) * vd, 0u);
+            for (uint32_t j = 0; j < vd; ++j)
+                for (uint32_t qs = 0; qs < 1024; ++qs)
+                    q16[vb_q16_index(vd, j, qs)] = j < vd / 2 ? 0x80008000u : 0xFFFFFFFFu;
+        }
+        auto q15_code = [&](float x, uint32_t u) -> uint32_t {
+            const float t = va_batch_q15_t(x, ps.vmin[u], ps.vscale[u]);
+            uint32_t bits32;
+            std::memcpy(&bits32, &t, 4);
+            return (bits32 >> 8) & 0x7FFFu;
+        };
         // word index of (u, c, w): overlap word, and (wide unions) the
         // containment word right after it
         auto ov_idx = [&](uint32_t u, uint32_t c, uint32_t w) -> size_t {
@@ -555,6 +600,18 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
                 // (narrow: query qi at slot qi ^ ((qi >> 5) & 7), vabatch.cu)
                 const size_t qs = qi ^ ((qi >> 5) & 7u);
                 qbv[pv ? (size_t(u / 2) * 1024 + qs) * 2 + u % 2 : size_t(qi) * qstride + u] = make_float2(p.lo, p.hi);
+                if (q15) {
+                    // a bound outside the observed [min, max] of the dimension
+                    // decides every tuple: code 0 / 32767
+                    const bool have = s->h_minmax.size() >= size_t(2) * m;
+                    const uint32_t L = (have && p.lo < s->h_minmax[2 * p.dim]) ? 0u : q15_code(p.lo, u);
+                    const uint32_t H = (have && p.hi > s->h_minmax[2 * p.dim + 1]) ? 32767u : q15_code(p.hi, u);
+                    const uint32_t sh = 16 * (u % 2), keep = ~(0xFFFFu << sh);
+                    uint32_t& ln = q16[vb_q16_index(vd, u / 2, uint32_t(qs))];
+                    uint32_t& hg = q16[vb_q16_index(vd, vd / 2 + u / 2, uint32_t(qs))];
+                    ln = (ln & keep) | ((0x8000u - L) << sh);
+                    hg = (hg & keep) | ((0x8000u + H) << sh);
+                }
                 if (p.lo > p.hi) continue;   // empty interval (kernel level only): no cell overlaps
                 // overlap cells [lo_c, hi_c]; containment drops the edge cells
                 const int lo_c = int(p.cl) >> ps.shift, hi_c = int(p.ch) >> ps.shift, top = int(cells) - 1;
@@ -598,6 +655,8 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         b->vb_tables.insert(b->vb_tables.end(), tab.begin(), tab.end());
         b->vb_qb.insert(b->vb_qb.end(), qbv.begin(), qbv.end());
         b->vb_cm.insert(b->vb_cm.end(), cmv.begin(), cmv.end());
+        ps.q16_off = b->vb_q16.size();
+        b->vb_q16.insert(b->vb_q16.end(), q16.begin(), q16.end());
         b->vb_passes.push_back(ps);
     }
 }
@@ -745,6 +804,7 @@ void upload_batch(mdrq_store* s, mdrq_batch* b, bool sync = true) {
     upload(b->d_vb_tables, b->vb_tables, s->stream);
     upload(b->d_vb_qb, b->vb_qb, s->stream);
     upload(b->d_vb_cm, b->vb_cm, s->stream);
+    upload(b->d_vb_q16, b->vb_q16, s->stream);
     upload(b->d_vb_perm, b->vb_perm, s->stream);
     const size_t nq = b->nq;
     b->d_scratch.reserve(scratch_words(b->nq));
@@ -767,7 +827,8 @@ uint64_t upload_bytes(const mdrq_batch* b) {
            b->udims.size() * sizeof(uint16_t) + b->bounds.size() * sizeof(float2) +
            b->cmask.size() * sizeof(unsigned long long) + b->vb_udims.size() * sizeof(uint16_t) +
            b->vb_tables.size() * sizeof(uint32_t) + b->vb_qb.size() * sizeof(float2) +
-           b->vb_cm.size() * sizeof(uint32_t) + b->vb_perm.size() * sizeof(uint32_t);
+           b->vb_cm.size() * sizeof(uint32_t) + b->vb_perm.size() * sizeof(uint32_t) +
+           b->vb_q16.size() * sizeof(uint32_t);
 }
 
 uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
@@ -849,6 +910,11 @@ VaBatchArgs vb_args(mdrq_store* s, mdrq_batch* b, const VbPass& ps) {
     a.tables = b->d_vb_tables.p + ps.table_off;
     a.qbounds = b->d_vb_qb.p + ps.qb_off;
     a.qcmask = b->d_vb_cm.p + ps.cm_off;
+    a.qb16 = b->d_vb_q16.p ? b->d_vb_q16.p + ps.q16_off : nullptr;
+    for (uint32_t u = 0; u < kVbStageDims; ++u) {
+        a.vmin[u] = ps.vmin[u];
+        a.vscale[u] = ps.vscale[u];
+    }
     // one CTA per SM (the tables take most of the shared memory); chunks of
     // < 65536 tuples (16-bit per-warp counters), identical in every mode
     a.grid = uint32_t(s->num_sms);

@@ -121,13 +121,21 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     // values staged on chip; the recount fallback of 9/10-dim unions reads
     // them from global memory instead (its per-warp counters need the room)
     constexpr bool STAGE = PV && KB <= 10 && !(MODE == 2 && KB > 8);
+    // staged unions refine on 15-bit codes (launch.h): KBV words per query in
+    // shared memory instead of KBV float2 bounds
+    constexpr bool Q15 = STAGE && va_batch_q15(KB);
+    constexpr int QC4 = KBV / 4;                   // Q15: 16-byte chunks per query (+ an 8-byte tail)
+    constexpr bool QT2 = KBV % 4 == 2;
     __shared__ uint32_t s_dim[KB];
     uint32_t* s_end = sm + va_batch_table_words(KB, K);
     // PV: exact query bounds [KBV/2][1024] float4 (lo_u, hi_u, lo_u+1, hi_u+1
     // of dim pair u/2) and every warp's staged block values [128 * H] slots of
     // VS floats
     float4* s_qb = reinterpret_cast<float4*>(s_end);
-    float* s_val = reinterpret_cast<float*>(s_qb + (PV ? 1024 * KBV / 2 : 0));
+    // (Q15: the code words instead, [QC4][1024] uint4 then [1024] uint2)
+    const uint4* s_q16 = reinterpret_cast<const uint4*>(s_end);
+    const uint2* s_q16t = reinterpret_cast<const uint2*>(s_q16 + QC4 * 1024);
+    float* s_val = reinterpret_cast<float*>(s_qb + (PV ? (Q15 ? 1024 * KBV / 4 : 1024 * KBV / 2) : 0));
     uint32_t* s_rest = reinterpret_cast<uint32_t*>(s_val + (STAGE ? VB_WARPS * 128 * KBV : 0));
     // DENSE (modes 0, 3): CTA counters u32 [1024], then every warp's candidate
     // queue: entries uint2 [QCAP] = (overlap word, tuple-in-block << 5 | query
@@ -152,7 +160,11 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
         uint4* dst = reinterpret_cast<uint4*>(sm);
         const uint32_t n4 = va_batch_table_words(KB, K) / 4;
         for (uint32_t i = tid; i < n4; i += VB_THREADS) dst[i] = src[i];
-        if constexpr (PV) {
+        if constexpr (Q15) {
+            const uint4* qsrc = reinterpret_cast<const uint4*>(a.qb16);
+            uint4* qdst = reinterpret_cast<uint4*>(s_qb);
+            for (uint32_t i = tid; i < 1024 * KBV / 4; i += VB_THREADS) qdst[i] = qsrc[i];
+        } else if constexpr (PV) {
             const uint4* qsrc = reinterpret_cast<const uint4*>(a.qbounds);
             uint4* qdst = reinterpret_cast<uint4*>(s_qb);
             for (uint32_t i = tid; i < 1024 * KBV / 2; i += VB_THREADS) qdst[i] = qsrc[i];
@@ -224,6 +236,62 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
 #pragma unroll
                 for (int u = 0; u < KB; ++u)
                     v[u] = (need >> u & 1u) ? __ldg(a.cols + uint64_t(s_dim[u]) * a.stride + t) : 0.0f;
+            }
+            if constexpr (Q15) {
+                // the tuple's codes, two dims per word (bytes 1-2 of the
+                // clamped transform: 15 code bits under a clear bit 15)
+                constexpr int P = KBV / 2;
+                uint32_t c[P];
+#pragma unroll
+                for (int p2 = 0; p2 < P; ++p2) {
+                    const float ta = va_batch_q15_t(v[2 * p2], a.vmin[2 * p2], a.vscale[2 * p2]);
+                    const float tb = va_batch_q15_t(v[2 * p2 + 1], a.vmin[2 * p2 + 1], a.vscale[2 * p2 + 1]);
+                    c[p2] = __byte_perm(__float_as_uint(ta), __float_as_uint(tb), 0x6521);
+                }
+                constexpr uint32_t G2 = 0x80008000u, ONE2 = 0x00010001u;
+                uint32_t amb = 0;
+                while (r) {
+                    const int b = __ffs(r) - 1;
+                    r &= r - 1;
+                    const uint32_t slot = wq + (uint32_t(b) ^ ((wq >> 5) & 7u));
+                    uint32_t w[KBV];   // LN[0..P-1], HG[0..P-1]
+#pragma unroll
+                    for (int k4 = 0; k4 < QC4; ++k4) {
+                        const uint4 x = s_q16[k4 * 1024 + slot];
+                        w[4 * k4] = x.x, w[4 * k4 + 1] = x.y, w[4 * k4 + 2] = x.z, w[4 * k4 + 3] = x.w;
+                    }
+                    if constexpr (QT2) {
+                        const uint2 y = s_q16t[slot];
+                        w[4 * QC4] = y.x, w[4 * QC4 + 1] = y.y;
+                    }
+                    uint32_t nf = G2, sr = G2;
+#pragma unroll
+                    for (int p2 = 0; p2 < P; ++p2) {
+                        const uint32_t d1 = c[p2] + w[p2];        // bit 15 per half: c >= L
+                        const uint32_t d2 = w[P + p2] - c[p2];    //                  c <= H
+                        nf &= d1 & d2;
+                        sr &= (d1 - ONE2) & (d2 - ONE2);          // c > L, c < H
+                    }
+                    const bool sure = (sr & G2) == G2;
+                    hits |= uint32_t(sure) << b;
+                    amb |= uint32_t(!sure && (nf & G2) == G2) << b;
+                }
+                // a code on a bound's: the exact float32 compare against the
+                // bounds in global memory (rare)
+                while (amb) {
+                    const int b = __ffs(amb) - 1;
+                    amb &= amb - 1;
+                    const float4* qq = reinterpret_cast<const float4*>(a.qbounds) + (wq + (uint32_t(b) ^ ((wq >> 5) & 7u)));
+                    bool ok = true;
+#pragma unroll
+                    for (int u2 = 0; u2 < KBV / 2; ++u2) {
+                        const float4 bb = __ldg(qq + u2 * 1024);
+                        ok = ok & (bb.x <= v[2 * u2]) & (v[2 * u2] <= bb.y) & (bb.z <= v[2 * u2 + 1]) &
+                             (v[2 * u2 + 1] <= bb.w);
+                    }
+                    hits |= uint32_t(ok) << b;
+                }
+                return hits;
             }
             while (r) {
                 const int b = __ffs(r) - 1;
@@ -1362,8 +1430,9 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
     const bool pv = va_batch_pv(kb);
     const size_t vd = va_batch_vdims(kb);
     size_t bytes = size_t(va_batch_table_words(kb, cells)) * 4;
-    if (pv) bytes += vd * 1024 * 8;                                      // bounds
-    if (pv && kb <= 10 && !(mode == 2 && kb > 8)) bytes += size_t(VB_WARPS) * 128 * vd * 4;   // staged values
+    const bool stage = pv && kb <= 10 && !(mode == 2 && kb > 8);
+    if (pv) bytes += vd * 1024 * ((stage && va_batch_q15(kb)) ? 4 : 8);  // bounds (15-bit codes / float32)
+    if (stage) bytes += size_t(VB_WARPS) * 128 * vd * 4;                 // staged values
     if (mode == 2)
         bytes += size_t(VB_WARPS) * 1024 * 2;
     else
