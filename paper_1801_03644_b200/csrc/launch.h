@@ -106,7 +106,8 @@ __host__ __device__ constexpr uint32_t va_batch_vdims(uint32_t kb) {
 __host__ __device__ constexpr uint32_t va_batch_table_words(uint32_t kb, uint32_t cells) {
     return va_batch_pv(kb) ? (kb + 1) / 2 * cells * 64 : kb * cells * 64;
 }
-// Staged unions (<= kVbStageDims dims, values on chip) refine on 15-bit
+// Staged unions (<= kVbStageDims dims: float32 values on chip up to 10 dims,
+// their 15-bit codes above) refine on 15-bit
 // monotone codes first (MDRQ_VB_Q15): value code c(v) = bits 8..22 of
 // clamp(fma(v - vmin[u], vscale[u], 2)) in [1, 32766]; a query bound is the
 // code of its lo / hi (0 / 32767 when it lies below / above every value), two
@@ -116,7 +117,7 @@ __host__ __device__ constexpr uint32_t va_batch_table_words(uint32_t kb, uint32_
 // against the exact bounds in global memory.  Per query the codes take
 // vdims(kb) words (LN = 0x8000 - L per half for the vdims/2 dim pairs, then
 // HG = 0x8000 + H): 40 bytes for 10 dims against 80 bytes of float bounds.
-constexpr uint32_t kVbStageDims = 10;
+constexpr uint32_t kVbStageDims = 16;   // = kVbPvDims
 __host__ __device__ constexpr bool va_batch_q15(uint32_t kb) { return MDRQ_VB_Q15 && kb <= kVbStageDims; }
 constexpr float kVbQ15Min = 2.00006103515625f;    // 2 + 2^-14: code 1
 constexpr float kVbQ15Max = 3.9998779296875f;     // 2 + 32766 * 2^-14: code 32766

@@ -123,7 +123,12 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     constexpr bool STAGE = PV && KB <= 10 && !(MODE == 2 && KB > 8);
     // staged unions refine on 15-bit codes (launch.h): KBV words per query in
     // shared memory instead of KBV float2 bounds
-    constexpr bool Q15 = STAGE && va_batch_q15(KB);
+    // 11..16-dim unions stage the block's 15-bit value codes instead (two
+    // dims per word, PP words per tuple in 8-byte slots): their refinement
+    // runs on chip too, only a code on a bound's reads float32 from global
+    constexpr bool STAGEC = MDRQ_VB_Q15 && PV && KB > 10 && MODE != 2;
+    constexpr int PP = (KBV / 2 + 1) / 2 * 2;       // STAGEC: code words per tuple (even)
+    constexpr bool Q15 = (STAGE || STAGEC) && va_batch_q15(KB);
     constexpr int QC4 = KBV / 4;                   // Q15: 16-byte chunks per query (+ an 8-byte tail)
     constexpr bool QT2 = KBV % 4 == 2;
     __shared__ uint32_t s_dim[KB];
@@ -136,7 +141,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     const uint4* s_q16 = reinterpret_cast<const uint4*>(s_end);
     const uint2* s_q16t = reinterpret_cast<const uint2*>(s_q16 + QC4 * 1024);
     float* s_val = reinterpret_cast<float*>(s_qb + (PV ? (Q15 ? 1024 * KBV / 4 : 1024 * KBV / 2) : 0));
-    uint32_t* s_rest = reinterpret_cast<uint32_t*>(s_val + (STAGE ? VB_WARPS * 128 * KBV : 0));
+    constexpr int WV = STAGE ? 128 * KBV : STAGEC ? 128 * PP : 0;   // staged words per warp
+    uint32_t* s_rest = reinterpret_cast<uint32_t*>(s_val + VB_WARPS * WV);
     // DENSE (modes 0, 3): CTA counters u32 [1024], then every warp's candidate
     // queue: entries uint2 [QCAP] = (overlap word, tuple-in-block << 5 | query
     // word), (wide unions) containment words u32 [QCAP].
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
     const uint32_t lane_off = W2 ? (lane % LPT) * (4u * NW) : lane * (PV ? 4 : 8);
     const uint32_t lane_tup = lane / LPT;          // this lane's tuple within a sub-step
     const char* s_tab = reinterpret_cast<const char*>(sm);
-    float* wval = s_val + warp * 128 * KBV;        // STAGE: this warp's staged values
+    float* wval = s_val + warp * WV;               // STAGE / STAGEC: this warp's staged values / codes
     uint2* qe = s_qe + warp * VB_QCAP;
     uint2* wcode = s_code + warp * 128;            // SCODE: this warp's staged cells
     uint32_t* qs = s_qs + warp * VB_QCAP;
@@ -219,6 +225,8 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     v[2 * h] = w2.x;
                     v[2 * h + 1] = w2.y;
                 }
+            } else if constexpr (STAGEC) {
+                // codes only (below); float32 values are read when needed
             } else if constexpr (PV) {
                 // unions too wide to stage: the values of the dims some
                 // candidate of the word constrains, from global memory
@@ -241,12 +249,21 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 // the tuple's codes, two dims per word (bytes 1-2 of the
                 // clamped transform: 15 code bits under a clear bit 15)
                 constexpr int P = KBV / 2;
-                uint32_t c[P];
+                uint32_t c[STAGEC ? PP : P];
+                if constexpr (STAGEC) {
 #pragma unroll
-                for (int p2 = 0; p2 < P; ++p2) {
-                    const float ta = va_batch_q15_t(v[2 * p2], a.vmin[2 * p2], a.vscale[2 * p2]);
-                    const float tb = va_batch_q15_t(v[2 * p2 + 1], a.vmin[2 * p2 + 1], a.vscale[2 * p2 + 1]);
-                    c[p2] = __byte_perm(__float_as_uint(ta), __float_as_uint(tb), 0x6521);
+                    for (int h = 0; h < PP / 2; ++h) {
+                        const uint2 w2 = reinterpret_cast<const uint2*>(wval)[val_slot<2>(tl, h)];
+                        c[2 * h] = w2.x;
+                        c[2 * h + 1] = w2.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int p2 = 0; p2 < P; ++p2) {
+                        const float ta = va_batch_q15_t(v[2 * p2], a.vmin[2 * p2], a.vscale[2 * p2]);
+                        const float tb = va_batch_q15_t(v[2 * p2 + 1], a.vmin[2 * p2 + 1], a.vscale[2 * p2 + 1]);
+                        c[p2] = __byte_perm(__float_as_uint(ta), __float_as_uint(tb), 0x6521);
+                    }
                 }
                 constexpr uint32_t G2 = 0x80008000u, ONE2 = 0x00010001u;
                 uint32_t amb = 0;
@@ -278,6 +295,13 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                 }
                 // a code on a bound's: the exact float32 compare against the
                 // bounds in global memory (rare)
+                if constexpr (STAGEC) {
+                    if (amb) {
+#pragma unroll
+                        for (int u = 0; u < KBV; ++u)
+                            v[u] = u < KB ? __ldg(a.cols + uint64_t(s_dim[u < KB ? u : 0]) * a.stride + t) : 0.0f;
+                    }
+                }
                 while (amb) {
                     const int b = __ffs(amb) - 1;
                     amb &= amb - 1;
@@ -392,6 +416,34 @@ __global__ void __launch_bounds__(VB_THREADS, 1) va_batch_kernel(const VaBatchAr
                     uint4* dst = reinterpret_cast<uint4*>(wcode) + 2 * lane;
                     dst[0] = make_uint4(lo[0], hi[0], lo[1], hi[1]);
                     dst[1] = make_uint4(lo[2], hi[2], lo[3], hi[3]);
+                }
+                __syncwarp();
+            }
+            if constexpr (STAGEC) {
+                // the block's value codes, four dims (one 8-byte slot per
+                // tuple) at a time: lane l converts its tuples 4l .. 4l+3
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < PP / 2; ++h) {
+                    float4 x[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int u = 4 * h + e;
+                        x[e] = u < KB ? __ldcs(reinterpret_cast<const float4*>(
+                                                   a.cols + uint64_t(s_dim[u < KB ? u : 0]) * a.stride + t0) + lane)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (uint32_t jj = 0; jj < 4; ++jj) {
+                        uint32_t tb[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int u = 4 * h + e < int(kVbStageDims) ? 4 * h + e : 0;
+                            tb[e] = __float_as_uint(va_batch_q15_t(f4_get(x[e], jj), a.vmin[u], a.vscale[u]));
+                        }
+                        reinterpret_cast<uint2*>(wval)[val_slot<2>(4 * lane + jj, h)] =
+                            make_uint2(__byte_perm(tb[0], tb[1], 0x6521), __byte_perm(tb[2], tb[3], 0x6521));
+                    }
                 }
                 __syncwarp();
             }
@@ -1390,11 +1442,12 @@ void run_kb_lw(const VaBatchArgs& a, cudaStream_t st) {
     va_batch_kernel<MODE, KB, LW><<<a.grid, VB_THREADS, smem, st>>>(a);
 }
 
-// query words per lane of a full pass over a union of kb dims: 4 where the
-// values are staged on chip (<= 10 dims), 1 where the refinement reads them
-// from global memory (11..16 dims: the four-word order measured 20 % slower
-// in ids mode on C3); MDRQ_VB_WORDS (1, 2 or 4) overrides it for every union,
-// for comparison and tests
+// query words per lane of a full pass over a union of kb dims: 4 up to 10
+// dims, 1 above (11..16 dims, C3: the one-word order measured 27.9 / 40.6 us
+// per query count / ids against 29.6 / 50.8 for four words -- its passes are
+// dense, ~25 candidates per tuple, and the refinement dominates);
+// MDRQ_VB_WORDS (1, 2 or 4) overrides it for every union, for comparison and
+// tests
 int vb_words(uint32_t kb) {
     static const int v = [] {
         const char* e = std::getenv("MDRQ_VB_WORDS");
@@ -1431,15 +1484,17 @@ size_t va_batch_smem(uint32_t kb, uint32_t cells, int mode) {
     const size_t vd = va_batch_vdims(kb);
     size_t bytes = size_t(va_batch_table_words(kb, cells)) * 4;
     const bool stage = pv && kb <= 10 && !(mode == 2 && kb > 8);
-    if (pv) bytes += vd * 1024 * ((stage && va_batch_q15(kb)) ? 4 : 8);  // bounds (15-bit codes / float32)
+    const bool stagec = MDRQ_VB_Q15 && pv && kb > 10 && mode != 2;       // staged 15-bit value codes
+    if (pv) bytes += vd * 1024 * (((stage || stagec) && va_batch_q15(kb)) ? 4 : 8);  // bounds (15-bit codes / float32)
     if (stage) bytes += size_t(VB_WARPS) * 128 * vd * 4;                 // staged values
+    if (stagec) bytes += size_t(VB_WARPS) * 128 * ((vd / 2 + 1) / 2 * 2) * 4;
     if (mode == 2)
         bytes += size_t(VB_WARPS) * 1024 * 2;
     else
         bytes += 1024 * 4 + size_t(VB_WARPS) * VB_QCAP * (8 + (pv ? 0 : 4));
     if (mode != 2 && pv && kb <= 8) bytes += size_t(VB_WARPS) * 128 * 8;   // staged cells (multi-word passes)
     // compacted tuple lists (a word per tuple where they carry packed cells)
-    if (mode != 2 && pv) bytes += size_t(VB_WARPS) * 128 * ((MDRQ_VB_ACODE && kb > 8 && vb_words(kb) > 1) ? 4 : 1);
+    if (mode != 2 && pv) bytes += size_t(VB_WARPS) * 128 * ((MDRQ_VB_ACODE && kb > 8 && pv && vb_words(kb) > 1) ? 4 : 1);
     return bytes;
 }
 
