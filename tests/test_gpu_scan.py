@@ -404,6 +404,53 @@ def test_vafile_batch_multi_pass_vs_oracle(gpu, m):
     check_store(gpu, v, lo, hi, paths=("vafile_batch",))
 
 
+@pytest.mark.parametrize("m", [4, 8, 10, 12, 13, 16])
+def test_vafile_batch_code_refinement_edges(gpu, m):
+    """The bit-sliced pass refines staged unions on 15-bit monotone codes
+    (launch.h va_batch_q15_t: float32 values staged up to 10 dims, their
+    codes above) and falls back to the float32 compare only when a code
+    equals a bound's.  Data and bounds built to sit on that edge: integer
+    categoricals with equality predicates, bounds one ulp either side of
+    data values, a column with a huge offset (every value shares one code),
+    a constant column, columns holding +-inf and +-FLT_MAX; two passes of
+    full-match, partial-match and point queries against the oracle."""
+    rng = np.random.default_rng(700 + m)
+    n, nq = 120_000, 1100
+    v = rng.random((n, m), dtype=np.float32)
+    v[:, 0] = rng.integers(0, 10, n)                       # categorical
+    v[:, 1] = np.float32(1e9) + rng.integers(0, 64, n) * np.float32(64)   # tiny range on a huge offset
+    if m > 4:
+        v[:, 2] = 7.25                                     # constant
+        v[:, 3] = rng.normal(0, 1e30, n).astype(np.float32)
+        v[::1001, 3] = np.inf
+        v[1::1001, 3] = -np.inf
+        v[2::1001, 3] = np.finfo(np.float32).max
+        v[3::1001, 4] = -np.finfo(np.float32).max
+    lo = np.full((nq, m), -np.inf, np.float32)
+    hi = np.full((nq, m), np.inf, np.float32)
+    rows = rng.integers(0, n, nq)
+    for q in range(nq):
+        dims = rng.choice(m, size=int(rng.integers(1, min(m, 6) + 1)), replace=False)
+        for j in dims:
+            a = v[rows[q], j]
+            kind = rng.integers(0, 5)
+            if kind == 0 or not np.isfinite(a):   # point predicate on a data value
+                lo[q, j] = hi[q, j] = a
+            elif kind == 1:                       # one ulp inside / outside
+                lo[q, j] = np.nextafter(a, np.float32(np.inf))
+                hi[q, j] = np.nextafter(v[rows[(q + 1) % nq], j], np.float32(-np.inf))
+                if lo[q, j] > hi[q, j]:
+                    lo[q, j], hi[q, j] = hi[q, j], lo[q, j]
+            elif kind == 2:                       # a data value as the lower bound
+                lo[q, j] = a
+            elif kind == 3:                       # ... as the upper bound
+                hi[q, j] = a
+            else:
+                b = v[rows[(q + 7) % nq], j]
+                lo[q, j], hi[q, j] = (a, b) if a <= b else (b, a)
+    check_store(gpu, v, lo, hi, paths=("vafile_batch",))
+
+
 @pytest.mark.parametrize("nq", [1, 33, 200, 256, 257, 400, 512, 513])
 def test_vafile_batch_lanes_per_tuple_vs_oracle(gpu, nq):
     """Passes of <= 256 / <= 512 queries pack 4 / 2 tuples per warp
