@@ -609,8 +609,10 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
               for _ in range(nbuf)]
     pin_s = time.perf_counter() - t0
     e2e_steps = max(3, min(args.steps, 20))   # the first step's device pass is the only unhidden part
-    # warm: every slot of the stream (3) sizes its result pool once
-    method.search_stream([queries] * 3, outs=[pinned[k % nbuf] for k in range(3)])
+    # warm: every slot of the stream (3) sizes its buffers once (the first two
+    # batches of a store's first stream leave raw -- no result size is known
+    # yet --, the next three allocate every slot's packed-copy staging)
+    method.search_stream([queries] * 5, outs=[pinned[k % nbuf] for k in range(5)])
     if world > 1:
         dist.barrier()
     info = {}
@@ -618,8 +620,29 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
     res = method.search_stream([queries] * e2e_steps, outs=[pinned[k % nbuf] for k in range(e2e_steps)], info=info)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     assert all(int(r.offsets[-1]) == total_local for r in res), "stream result differs from the timed batch"
-    del res
+    # the last step's ids, rebuilt on the host from the packed copy, against
+    # the device result of the timed batch (count + set hash per query is
+    # the tests' job; here: the copy that was timed is the right one)
+    last = res[-1]
+    head = min(nq, 64)
+    dev_offs, dev_ids = store.ids(lo[:head], hi[:head], "columnar_batch" if head >= 4 else "columnar")
+    assert np.array_equal(last.offsets[: head + 1], dev_offs), "stream offsets differ"
+    assert np.array_equal(np.asarray(last.ids)[: dev_ids.size], dev_ids), "stream ids differ from the columnar scan's"
+    del res, last, dev_ids
     h2d = info.get("h2d_bytes", 0) // e2e_steps   # the batch's descriptors: bounds, query-mask tables, order
+    d2h = info.get("d2h_bytes", 0) // e2e_steps or ids_bytes
+    packed = info.get("packed_batches", 0)
+    # the same stream with the packing off: the raw uint32 ids cross PCIe
+    raw_steps = 5
+    os.environ["MDRQ_STREAM_PACK"] = "0"
+    try:
+        method.search_stream([queries] * 3, outs=[pinned[k % nbuf] for k in range(3)])   # the slots' own pools
+        t0 = time.perf_counter()
+        method.search_stream([queries] * raw_steps, outs=[pinned[k % nbuf] for k in range(raw_steps)])
+        raw_s = (time.perf_counter() - t0) / raw_steps
+    finally:
+        del os.environ["MDRQ_STREAM_PACK"]
+    raw_s = max_over_ranks(raw_s, world)
     store.ids(lo, hi, args.path, out=pinned[0])   # warm
     t0 = time.perf_counter()
     sync_n = 2
@@ -645,13 +668,18 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
     del d_src, h_dst, pinned
     return {"value": n_total * nq / e2e_s, "unit": "tuple-queries/s",
             "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": ids_bytes * world,
+            "d2h_bytes_per_step": int(d2h) * world,
+            "result_bytes_per_step": ids_bytes * world,
             "api": f"VaFile.search_stream (the build_method('vafile') object over the bench store): {e2e_steps} "
                    f"repetitions of the RangeQuery batch pipelined (copy of step k under the device pass of step "
-                   f"k+1), {nbuf} pinned output buffer(s); wall clock, max over ranks",
+                   f"k+1, host unpack of step k-1 beside them), {nbuf} output buffer(s); wall clock, max over ranks",
             "ms_per_step": e2e_s * 1e3,
-            "d2h_roofline": {"achieved_gbs": ids_bytes / e2e_s / 1e9, "peak_gbs": d2h_peak,
-                             "frac": ids_bytes / e2e_s / 1e9 / d2h_peak,
+            "packed_batches": f"{packed} of {e2e_steps}: ids leave the device as 16-bit low halves + per-query "
+                              "bucket ends and are rebuilt to uint32 on the host threads (mdrq_unpack_ids16)",
+            "unpacked": {"ms_per_step": raw_s * 1e3, "value": n_total * nq / raw_s,
+                         "note": f"MDRQ_STREAM_PACK=0, {raw_steps} steps: raw uint32 ids over PCIe"},
+            "d2h_roofline": {"achieved_gbs": d2h / e2e_s / 1e9, "peak_gbs": d2h_peak,
+                             "frac": d2h / e2e_s / 1e9 / d2h_peak,
                              "peak_kind": "measured in this run: one pinned copy of min(result, 4 GB) per GPU"},
             "sync_call": {"value": n_total * nq / sync_s, "ms_per_step": sync_s * 1e3,
                           "api": "DeviceStore.ids into a pinned buffer, one synchronous call per step"},

@@ -195,6 +195,22 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
                           uint64_t* const* offsets_out, uint32_t* const* ids_out,
                           const uint64_t* ids_caps, uint64_t* totals,
                           uint64_t* h2d_bytes);
+
+/* The stream's device->host copies are PCIe-bound on large results (C5:
+ * 20 GB of ids per 10 000-query batch), so batches whose id lists are long
+ * enough leave the device packed: the low 16 bits of every id (same order)
+ * plus, per query, the end position of every 65 536-id bucket in its list;
+ * the host rebuilds the uint32 ids on all its threads while the next batch
+ * scans and the one after copies (MDRQ_STREAM_PACK=0 / 1 forces it off / on,
+ * MDRQ_UNPACK_THREADS sets the thread count).  mdrq_unpack_ids16 is that
+ * host step: out[offsets[q] + i] = (hb0 + b) << 16 | lo16[offsets[q] + i] for
+ * ends[q][b-1] <= i < ends[q][b] (ends: nq x nbuckets, positions relative to
+ * the query's list; offsets: nq + 1).  It needs no device.
+ * mdrq_stream_info: out[0] = device->host bytes of the store's last stream
+ * call, out[1] = batches of it that were packed, out[2] = its batches.      */
+int mdrq_unpack_ids16(const uint16_t* lo16, const uint32_t* ends, const uint64_t* offsets,
+                      uint32_t nq, uint32_t hb0, uint32_t nbuckets, uint32_t* out, int threads);
+int mdrq_stream_info(mdrq_store* s, uint64_t out[3]);
 /* SearchStats of the last count/ids call, one entry per query.            */
 int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats,
                      uint32_t nq);

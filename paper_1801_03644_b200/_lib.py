@@ -59,7 +59,7 @@ EXPORTED = (
     "mdrq_mask_popcount", "mdrq_mask_to_ids",
     "mdrq_store_create", "mdrq_store_destroy", "mdrq_store_get_info",
     "mdrq_store_va_boundaries", "mdrq_store_bounds",
-    "mdrq_query_count", "mdrq_query_ids", "mdrq_fetch_ids", "mdrq_query_ids64", "mdrq_fetch_ids64", "mdrq_query_ids_stream", "mdrq_query_stats",
+    "mdrq_query_count", "mdrq_query_ids", "mdrq_fetch_ids", "mdrq_query_ids64", "mdrq_fetch_ids64", "mdrq_query_ids_stream", "mdrq_unpack_ids16", "mdrq_stream_info", "mdrq_query_stats",
     "mdrq_batch_prepare", "mdrq_batch_destroy", "mdrq_batch_count_async",
     "mdrq_batch_ids_async", "mdrq_batch_reserve", "mdrq_result_device",
     "mdrq_batch_launches", "mdrq_batch_profile", "mdrq_batch_info",
@@ -105,6 +105,8 @@ _SIGS = {
                                       ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                       ctypes.c_uint64, ctypes.c_void_p]),
     "mdrq_abi_version": (_int, []),
+    "mdrq_unpack_ids16": (_int, [ctypes.POINTER(ctypes.c_uint16), _u32p, _u64p, _u32, _u32, _u32, _u32p, _int]),
+    "mdrq_stream_info": (_int, [_vp, _u64p]),
     "mdrq_check_flags": (_int, [ctypes.POINTER(ctypes.c_uint32)]),
     "mdrq_device_count": (_int, [ctypes.POINTER(_int)]),
     "mdrq_measure_read_bw": (_int, [_int, _u64, _int, ctypes.POINTER(ctypes.c_double)]),

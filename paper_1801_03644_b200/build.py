@@ -20,7 +20,9 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libmdrq_b200.so")
 
-SOURCES = ["store.cu", "scan_columnar.cu", "scan_rowwise.cu", "vafile.cu", "masks.cu", "expand.cu", "vabatch.cu"]
+SOURCES = ["store.cu", "scan_columnar.cu", "scan_rowwise.cu", "vafile.cu", "masks.cu", "expand.cu", "vabatch.cu", "pack.cu"]
+# plain host C++ (g++): the multi-threaded id unpacker
+HOST_SOURCES = ["unpack_host.cpp"]
 HEADERS = ["common.cuh", "launch.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -75,6 +77,14 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False,
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
             jobs.append([nvcc(), *NVCC_FLAGS, *extra, "-c", s, "-o", o])
+
+    for src in HOST_SOURCES:
+        sp = os.path.join(CSRC, src)
+        o = os.path.join(build_dir, src.replace(".cpp", ".o"))
+        objs.append(o)
+        if force or _stale(o, [sp] + hdrs):
+            jobs.append([shutil.which("g++") or "g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-I", INCLUDE,
+                         "-c", sp, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

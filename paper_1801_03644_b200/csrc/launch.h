@@ -255,6 +255,10 @@ void launch_mask_to_ids(const uint32_t* words, uint64_t n, uint32_t* status_scra
 void launch_read_stream(const void* p, uint64_t bytes, uint32_t* sink, int num_sms, cudaStream_t st);
 void launch_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src_off, const int64_t* dst_off,
                           const int64_t* len, uint64_t nseg, cudaStream_t st);
+// 16-bit packing of a batch's id lists for the device->host copy (pack.cu):
+// lo16[i] = ids[i] & 0xFFFF, ends[q][b] = ids of query q in buckets <= hb0 + b
+void launch_pack_ids16(const uint32_t* ids, const unsigned long long* offsets, uint32_t nq, uint64_t cap,
+                       uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends, int num_sms, cudaStream_t st);
 void launch_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lo,
                        const float* hi, uint8_t* out, cudaStream_t st);
 

@@ -19,6 +19,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -235,11 +236,44 @@ struct mdrq_batch {
 // One slot of the pipelined ids stream (mdrq_query_ids_stream): a batch with
 // its own result pool, the events that order it, and a pinned mirror of its
 // total / staging-overflow flag.
+// pinned host buffer, grown on demand
+template <class T>
+struct HBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        CK(cudaMallocHost(reinterpret_cast<void**>(&p), n * sizeof(T)));
+        cap = n;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
 struct StreamSlot {
     mdrq_batch b;
     cudaEvent_t comp = nullptr, copy = nullptr;
     unsigned long long* h_flags = nullptr;   // pinned [2]: total, overflow
     bool busy = false;                       // a D2H of this slot is in flight
+    // packed copies (pack.cu): the batch's low id halves and bucket ends on
+    // the device, their pinned staging on the host, and the thread that
+    // rebuilds the caller's uint32 ids from the staging
+    bool packed = false;
+    uint64_t pool_cap = 0;                   // capacity of the result pool the batch ran into
+    DBuf<uint16_t> d_lo16;
+    DBuf<uint32_t> d_ends;
+    HBuf<uint16_t> h_lo16;
+    HBuf<uint32_t> h_ends;
+    std::thread unpack;
+    void join() {
+        if (unpack.joinable()) unpack.join();
+    }
 };
 constexpr int kStreamSlots = 3;
 
@@ -292,6 +326,7 @@ struct mdrq_store {
     // pipelined ids stream: a copy stream + slots, created on first use
     cudaStream_t copy_stream = nullptr;
     StreamSlot* slots = nullptr;
+    uint64_t stream_d2h = 0, stream_packed = 0, stream_batches = 0;   // the last stream call (mdrq_stream_info)
     uint64_t stream_hint = 0;        // largest batch total seen by the stream (pre-sizes fresh slot pools)
     // pinned bounce buffer of the synchronous ids calls: the offsets, the VA
     // overflow flag and a speculative prefix of the ids come back in one
@@ -309,6 +344,9 @@ struct mdrq_store {
                 if (slots[i].comp) cudaEventDestroy(slots[i].comp);
                 if (slots[i].copy) cudaEventDestroy(slots[i].copy);
                 if (slots[i].h_flags) cudaFreeHost(slots[i].h_flags);
+                slots[i].join();
+                slots[i].h_lo16.release();
+                slots[i].h_ends.release();
             }
             delete[] slots;
         }
@@ -1756,6 +1794,43 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             }
         }
         uint64_t up = 0;
+        // packed copies (pack.cu): MDRQ_STREAM_PACK=0 never, =1 always,
+        // otherwise when the lists are long enough for the bucket ends to be
+        // small beside them (>= 32 ids per query and bucket, judged on the
+        // largest batch the stream has seen)
+        const bool sdbg = getenv("MDRQ_DEBUG_STREAM") != nullptr;   // per-stage host timings on stderr
+        const auto t_call = std::chrono::steady_clock::now();
+        auto since = [&] {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
+        };
+        const char* pk_env = getenv("MDRQ_STREAM_PACK");
+        const int pk_mode = pk_env ? std::atoi(pk_env) : -1;
+        const char* th_env = getenv("MDRQ_UNPACK_THREADS");
+        const int pk_threads = th_env ? std::atoi(th_env) : 0;
+        const uint32_t hb0 = s->id_base >> 16;
+        const uint32_t nbuckets = s->n ? uint32_t(((uint64_t(s->id_base) + s->n - 1) >> 16) - hb0 + 1) : 1;
+        auto want_pack = [&](uint32_t nq) {
+            if (!nq || !s->n || pk_mode == 0) return false;
+            if (pk_mode > 0) return true;
+            return s->stream_hint >= uint64_t(32) * nq * nbuckets;
+        };
+        // A packed batch's ids only live in the result pool until the pack
+        // kernel behind its pass has run, so packed batches share the store's
+        // pool (one pass at a time on the store stream) and a slot holds the
+        // low halves instead of a pool of its own; a raw batch's ids stay in
+        // its slot's pool until they are copied.
+        auto pack = [&](StreamSlot& sl, uint32_t nq) {
+            mdrq_batch* b = &sl.b;
+            DBuf<uint32_t>& pool = pool_of(s, b);
+            sl.packed = !b->own_pool && pool.p;
+            if (!sl.packed) return;
+            sl.d_lo16.reserve(pool.cap);
+            sl.d_ends.reserve(size_t(nq) * nbuckets);
+            launch_pack_ids16(pool.p, b->d_offsets.p, nq, pool.cap, hb0, nbuckets, sl.d_lo16.p, sl.d_ends.p,
+                              s->num_sms, s->stream);
+        };
+        s->stream_d2h = s->stream_packed = 0;
+        s->stream_batches = nbatches;
         // batch k: host build + H2D + filter/scatter on the store stream,
         // total and overflow flag mirrored to pinned memory
         auto launch = [&](uint32_t k) {
@@ -1768,13 +1843,23 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             const uint32_t nq = nqs[k];
             build_descs(s, lower + q0[k] * s->m, upper + q0[k] * s->m, nq, resolve_path(s, path, nq, true), true, b);
             upload_batch(s, b, false);
-            // a slot's pool starts at the size of the largest batch seen so
-            // far: a fresh slot must not run its first batch twice
-            if (s->stream_hint && (!b->own_ids.p || b->own_ids.cap < s->stream_hint))
-                b->own_ids.reserve(size_t(s->stream_hint + s->stream_hint / 8 + 4096));
+            b->own_pool = !want_pack(nq);
+            if (b->own_pool) {
+                sl.d_lo16.release();
+                sl.d_ends.release();
+            } else {
+                b->own_ids.release();
+            }
+            // a pool starts at the size of the largest batch seen so far: a
+            // fresh slot must not run its first batch twice
+            DBuf<uint32_t>& pool = pool_of(s, b);
+            if (s->stream_hint && (!pool.p || pool.cap < s->stream_hint))
+                pool.reserve(size_t(s->stream_hint + s->stream_hint / 8 + 4096));
+            sl.pool_cap = pool.p ? pool.cap : 0;
             presize_vb_staging(s, b);   // a store's first bit-sliced batch (synchronous, once)
             up += upload_bytes(b);
             enqueue(s, b, true, s->stream);
+            pack(sl, nq);
             sl.h_flags[0] = sl.h_flags[1] = 0;
             if (nq && s->n) {
                 CK(cudaMemcpyAsync(sl.h_flags, b->d_offsets.p + nq, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -1784,6 +1869,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
                                        s->stream));
             }
             CK(cudaEventRecord(sl.comp, s->stream));
+            if (sdbg) fprintf(stderr, "[stream] %8.1f launch %u done (packed=%d)\n", since(), k, int(sl.packed));
         };
         // batch k's results to the caller on the copy stream, while batch
         // k+1 runs on the store stream
@@ -1792,38 +1878,96 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             mdrq_batch* b = &sl.b;
             const uint32_t nq = nqs[k];
             CK(cudaEventSynchronize(sl.comp));
+            if (sdbg) fprintf(stderr, "[stream] %8.1f finish %u: device pass done\n", since(), k);
             const uint64_t total = sl.h_flags[0];
             if (sl.h_flags[1]) grow_vb_staging(s, total);
-            DBuf<uint32_t>& pool = b->own_ids;
-            if (total > (pool.p ? pool.cap : 0)) {
-                // the slot's pool was too small: grow it and run the batch again
-                pool.reserve(size_t(total + total / 8 + 4096));
+            DBuf<uint32_t>& pool = pool_of(s, b);
+            if (total > sl.pool_cap) {
+                // the pool the batch ran into was too small: grow it and run
+                // the batch again (behind the next batch's pass and pack)
+                if (total > (pool.p ? pool.cap : 0)) pool.reserve(size_t(total + total / 8 + 4096));
+                sl.pool_cap = pool.cap;
                 enqueue(s, b, true, s->stream);
+                pack(sl, nq);
                 CK(cudaEventRecord(sl.comp, s->stream));
             }
             totals[k] = total;
             s->stream_hint = std::max<uint64_t>(s->stream_hint, total);
             CK(cudaStreamWaitEvent(s->copy_stream, sl.comp, 0));
-            if (nq && s->n)
+            if (nq && s->n) {
                 CK(cudaMemcpyAsync(offsets_out[k], b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
                                    s->copy_stream));
-            else
+                s->stream_d2h += sizeof(uint64_t) * (nq + 1);
+            } else {
                 std::memset(offsets_out[k], 0, sizeof(uint64_t) * (size_t(nq) + 1));
-            if (total > ids_caps[k])
+            }
+            if (total > ids_caps[k]) {
                 trunc = 1;
-            else if (total)
+                sl.packed = false;
+            } else if (total && sl.packed) {
+                // the staging still feeds the unpack of the slot's previous batch
+                sl.join();
+                sl.h_lo16.reserve(size_t(total + total / 8 + 4096));
+                sl.h_ends.reserve(size_t(nq) * nbuckets);
+                CK(cudaMemcpyAsync(sl.h_lo16.p, sl.d_lo16.p, sizeof(uint16_t) * total, cudaMemcpyDeviceToHost,
+                                   s->copy_stream));
+                CK(cudaMemcpyAsync(sl.h_ends.p, sl.d_ends.p, sizeof(uint32_t) * size_t(nq) * nbuckets,
+                                   cudaMemcpyDeviceToHost, s->copy_stream));
+                s->stream_d2h += sizeof(uint16_t) * total + sizeof(uint32_t) * size_t(nq) * nbuckets;
+                s->stream_packed += 1;
+            } else if (total) {
+                sl.packed = false;
                 CK(cudaMemcpyAsync(ids_out[k], pool.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost,
                                    s->copy_stream));
+                s->stream_d2h += sizeof(uint32_t) * total;
+            } else {
+                sl.packed = false;
+            }
             CK(cudaEventRecord(sl.copy, s->copy_stream));
             sl.busy = true;
+            if (sdbg) fprintf(stderr, "[stream] %8.1f finish %u: copies enqueued\n", since(), k);
         };
+        // batch k's ids rebuilt from its packed copy, on host threads, while
+        // batch k+1 copies and batch k+2 scans
+        auto unpack = [&](uint32_t k) {
+            StreamSlot& sl = s->slots[k % kStreamSlots];
+            if (!sl.packed) return;
+            CK(cudaEventSynchronize(sl.copy));
+            if (sdbg) fprintf(stderr, "[stream] %8.1f unpack %u: copy done\n", since(), k);
+            const uint16_t* lo = sl.h_lo16.p;
+            const uint32_t* en = sl.h_ends.p;
+            const uint64_t* of = offsets_out[k];
+            uint32_t* out = ids_out[k];
+            const uint32_t nq = nqs[k];
+            sl.unpack = std::thread([=] {
+                const auto t0 = std::chrono::steady_clock::now();
+                mdrq_unpack_ids16(lo, en, of, nq, hb0, nbuckets, out, pk_threads);
+                if (sdbg)
+                    fprintf(stderr, "[stream] unpack %u: %.1f ms (%llu ids)\n", k,
+                            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+                            (unsigned long long)(of[nq] - of[0]));
+            });
+        };
+        struct Joiner {   // no unpack thread outlives the call, also when it throws
+            mdrq_store* s;
+            ~Joiner() {
+                if (s->slots)
+                    for (int i = 0; i < kStreamSlots; ++i) s->slots[i].join();
+            }
+        } joiner{s};
         for (uint32_t k = 0; k < nbatches; ++k) {
             launch(k);
             if (k) finish(k - 1);
+            if (k >= 2) unpack(k - 2);
         }
         if (nbatches) finish(nbatches - 1);
+        if (nbatches >= 2) unpack(nbatches - 2);
+        if (nbatches) unpack(nbatches - 1);
         CK(cudaStreamSynchronize(s->copy_stream));
-        for (int i = 0; i < kStreamSlots; ++i) s->slots[i].busy = false;
+        for (int i = 0; i < kStreamSlots; ++i) {
+            s->slots[i].join();
+            s->slots[i].busy = false;
+        }
         if (h2d_bytes) *h2d_bytes = up;
     });
     if (rc == MDRQ_OK && trunc) {
@@ -1831,6 +1975,17 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
         return MDRQ_ETRUNC;
     }
     return rc;
+}
+
+int mdrq_stream_info(mdrq_store* s, uint64_t out[3]) {
+    return guard([&] {
+        check_store(s);
+        if (!out) raise(MDRQ_EINVAL, "null argument");
+        std::lock_guard<std::mutex> lk(s->mu);
+        out[0] = s->stream_d2h;
+        out[1] = s->stream_packed;
+        out[2] = s->stream_batches;
+    });
 }
 
 int mdrq_fetch_ids(mdrq_store* s, uint32_t* ids, uint64_t ids_cap) {

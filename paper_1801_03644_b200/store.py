@@ -221,7 +221,9 @@ class DeviceStore:
         ``outs`` optionally gives one caller-owned (e.g. pinned) uint32 buffer
         per batch; a batch that does not fit its buffer raises ValueError.
         ``info``, when a dict, receives ``h2d_bytes`` (descriptor bytes
-        uploaded) and ``totals``.
+        uploaded), ``totals``, ``d2h_bytes`` and ``packed_batches`` (large
+        results cross PCIe as 16-bit low halves + per-query bucket ends and
+        are rebuilt on the host's threads, mdrq_unpack_ids16).
         """
         lib = _lib.load()
         pairs = [_bounds(lo, hi, self.m) for lo, hi in batches]
@@ -259,6 +261,13 @@ class DeviceStore:
         if info is not None:
             info["h2d_bytes"] = int(h2d.value)
             info["totals"] = [int(t) for t in totals]
+            si = (ctypes.c_uint64 * 3)()
+            with self._lock:
+                check(lib.mdrq_stream_info(self.handle, si))
+            # device->host bytes of the call and how many of its batches left
+            # the device packed (16-bit low halves + bucket ends, pack.cu)
+            info["d2h_bytes"] = int(si[0])
+            info["packed_batches"] = int(si[1])
         return out
 
     def stats(self, nq: int, mode: int = _lib.MODE_SCALAR):

@@ -120,3 +120,51 @@ def test_header_is_plain_c_and_links(tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "c abi ok" in r.stdout, (r.returncode, r.stdout, r.stderr)
+
+
+def _pack_ids16(offsets, ids, hb0, nbuckets):
+    """numpy restatement of pack.cu: the low halves and, per query, the end
+    position of every 65 536-id bucket in its list."""
+    nq = offsets.size - 1
+    lo16 = (ids & 0xFFFF).astype(np.uint16)
+    ends = np.zeros((nq, nbuckets), np.uint32)
+    for q in range(nq):
+        run = ids[offsets[q]:offsets[q + 1]].astype(np.int64)
+        ends[q] = np.searchsorted(run, (np.arange(nbuckets, dtype=np.int64) + hb0 + 1) << 16, side="left")
+    return lo16, ends
+
+
+@pytest.mark.parametrize("threads", [1, 3, 16])
+def test_unpack_ids16_rebuilds_the_ids(threads):
+    """mdrq_unpack_ids16 (the host half of the packed device->host copy)
+    needs no device: ascending id lists of ragged lengths -- empty, one id,
+    lists crossing many buckets, lists inside one bucket, a shard's id base --
+    packed with numpy and rebuilt by the library on 1, 3 and 16 threads."""
+    from paper_1801_03644_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(threads)
+    id_base, n = 3 * 65536 + 1234, 5_000_000
+    hb0 = id_base >> 16
+    nbuckets = ((id_base + n - 1) >> 16) - hb0 + 1
+    runs = []
+    for q in range(200):
+        kind = q % 5
+        cnt = [0, 1, int(rng.integers(2, 400_000)), int(rng.integers(2, 3000)), int(rng.integers(100, 60_000))][kind]
+        if kind == 3:   # inside one bucket
+            b = int(rng.integers(hb0 + 1, hb0 + nbuckets - 1))
+            pool = np.arange(b << 16, (b + 1) << 16, dtype=np.int64)
+        else:
+            pool = None
+        ids = (np.sort(rng.choice(pool, cnt, replace=False)) if pool is not None
+               else np.sort(rng.choice(n, cnt, replace=False)) + id_base)
+        runs.append(ids.astype(np.uint32))
+    offsets = np.concatenate([[0], np.cumsum([r.size for r in runs])]).astype(np.uint64)
+    ids = np.concatenate(runs).astype(np.uint32)
+    lo16, ends = _pack_ids16(offsets.astype(np.int64), ids, hb0, nbuckets)
+    out = np.full(ids.size + 8, 0xDEADBEEF, np.uint32)   # +8: nothing written past the end
+    rc = lib.mdrq_unpack_ids16(lo16.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)),
+                               ends.ctypes.data_as(_lib.u32p), offsets.ctypes.data_as(_lib.u64p),
+                               offsets.size - 1, hb0, nbuckets, out.ctypes.data_as(_lib.u32p), threads)
+    assert rc == 0
+    assert np.array_equal(out[: ids.size], ids)
+    assert (out[ids.size:] == 0xDEADBEEF).all()

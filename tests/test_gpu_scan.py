@@ -382,6 +382,54 @@ def test_ids_stream_pipelined_batches(gpu):
             st.ids_stream(batches[:2], "vafile_batch", outs=[np.empty(10, np.uint32)] * 2)
 
 
+@pytest.mark.parametrize("pack,id_base", [("1", 0), ("1", 7 * 65536 + 4321), ("0", 0), (None, 0)])
+def test_ids_stream_packed_copies(gpu, monkeypatch, pack, id_base):
+    """The stream's packed device->host copies (pack.cu + mdrq_unpack_ids16):
+    forced on, forced off and in the automatic mode, batches of ragged sizes
+    -- empty results, one query, every tuple, lists crossing several
+    65 536-id buckets -- on a store with and without an id base; every
+    batch equals the oracle's ids, and mdrq_stream_info reports the copy."""
+    import ctypes
+    from paper_1801_03644_b200 import _lib
+    if pack is None:
+        monkeypatch.delenv("MDRQ_STREAM_PACK", raising=False)
+    else:
+        monkeypatch.setenv("MDRQ_STREAM_PACK", pack)
+    monkeypatch.setenv("MDRQ_UNPACK_THREADS", "5")
+    rng = np.random.default_rng(5)
+    n, m = 300_001, 4
+    v = rng.random((n, m), dtype=np.float32)
+    batches = []
+    for nq, w in ((40, 0.7), (1, 1.5), (300, 0.5), (17, 0.0), (1100, 0.6), (64, 0.9), (5, 0.3)):
+        lo = rng.uniform(0, max(1 - w, 1e-3), (nq, m)).astype(np.float32)
+        hi = (lo + np.float32(w)).astype(np.float32)
+        if w == 0.0:
+            lo[:], hi[:] = 2.0, 3.0            # empty results
+        if w > 1:
+            lo[:], hi[:] = -np.inf, np.inf     # every tuple
+        batches.append((lo, hi))
+    exp = [oracle.ids_batch(v, lo, hi) for lo, hi in batches]
+    with gpu.DeviceStore(v, layouts=1 | 4, va_bits=8, id_base=id_base) as st_:
+        for rep in range(2):   # the second round reuses warmed slots (automatic mode packs from here)
+            info = {}
+            outs = [np.empty(ei.size + 16, np.uint32) for _, ei in exp]
+            res = st_.ids_stream(batches, "auto", outs=outs, info=info)
+            for (eo, ei), (offs, ids) in zip(exp, res):
+                assert np.array_equal(offs, eo)
+                assert np.array_equal(ids.astype(np.int64), ei + id_base)
+            out = (ctypes.c_uint64 * 3)()
+            _lib.check(_lib.load().mdrq_stream_info(st_.handle, out))
+            assert out[2] == len(batches)
+            total = sum(int(o[-1]) for o, _ in res)
+            assert info["d2h_bytes"] == out[0] and info["packed_batches"] == out[1]
+            if pack == "1":
+                assert out[1] == sum(1 for o, _ in res if o[-1] > 0)
+                assert out[0] < 4 * total            # fewer bytes than the raw ids
+            elif pack == "0":
+                assert out[1] == 0
+                assert out[0] >= 4 * total
+
+
 @pytest.mark.parametrize("m", [3, 8, 9, 10, 11])
 def test_vafile_batch_multi_pass_vs_oracle(gpu, m):
     """More queries than one bit-sliced pass holds (1 024): three passes, the
