@@ -257,8 +257,11 @@ void launch_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src
                           const int64_t* len, uint64_t nseg, cudaStream_t st);
 // 16-bit packing of a batch's id lists for the device->host copy (pack.cu):
 // lo16[i] = ids[i] & 0xFFFF, ends[q][b] = ids of query q in buckets <= hb0 + b
+// (perm / src_off / src_cap: the lists still in the slot order of a sorted
+// bit-sliced batch -- list i at ids + src_off[i] is query perm[i]'s; else null)
 void launch_pack_ids16(const uint32_t* ids, const unsigned long long* offsets, uint32_t nq, uint64_t cap,
-                       uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends, int num_sms, cudaStream_t st);
+                       uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends, const uint32_t* perm,
+                       const unsigned long long* src_off, uint64_t src_cap, int num_sms, cudaStream_t st);
 void launch_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lo,
                        const float* hi, uint8_t* out, cudaStream_t st);
 

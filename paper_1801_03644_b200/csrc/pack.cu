@@ -18,20 +18,28 @@ namespace {
 
 // One CTA per query run (grid-strided).  ends[q][b] = number of ids of query
 // q in buckets <= b (positions relative to the run), b relative to hb0.
+// Sorted bit-sliced batches (vabatch.cu) hold their lists in slot order: list
+// i (at src_off[i]) is query perm[i]'s; packing straight from there saves the
+// move of the uint32 ids to query order.
 __global__ void __launch_bounds__(256) pack_ids16_kernel(const uint32_t* __restrict__ ids,
                                                          const unsigned long long* __restrict__ offsets, uint32_t nq,
                                                          uint64_t cap, uint32_t hb0, uint32_t nbuckets,
-                                                         uint16_t* __restrict__ lo16, uint32_t* __restrict__ ends) {
-    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
+                                                         uint16_t* __restrict__ lo16, uint32_t* __restrict__ ends,
+                                                         const uint32_t* __restrict__ perm,
+                                                         const unsigned long long* __restrict__ src_off,
+                                                         uint64_t src_cap) {
+    for (uint32_t i0 = blockIdx.x; i0 < nq; i0 += gridDim.x) {
+        const uint32_t q = perm ? perm[i0] : i0;
         const uint64_t o0 = offsets[q], o1 = offsets[q + 1];
         if (o1 > cap) continue;   // truncated result: the caller grows the pool and reruns
         const uint64_t cnt = o1 - o0;
+        if (perm && src_off[i0] + cnt > src_cap) continue;
         uint32_t* e = ends + uint64_t(q) * nbuckets;
         if (cnt == 0) {
             for (uint32_t b = threadIdx.x; b < nbuckets; b += blockDim.x) e[b] = 0;
             continue;
         }
-        const uint32_t* s = ids + o0;
+        const uint32_t* s = ids + (perm ? src_off[i0] : o0);
         uint16_t* d = lo16 + o0;
         for (uint64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
             const uint32_t id = __ldcs(s + i);
@@ -50,10 +58,11 @@ __global__ void __launch_bounds__(256) pack_ids16_kernel(const uint32_t* __restr
 }  // namespace
 
 void launch_pack_ids16(const uint32_t* ids, const unsigned long long* offsets, uint32_t nq, uint64_t cap,
-                       uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends, int num_sms, cudaStream_t st) {
+                       uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends, const uint32_t* perm,
+                       const unsigned long long* src_off, uint64_t src_cap, int num_sms, cudaStream_t st) {
     if (!nq) return;
     const uint32_t grid = std::min<uint32_t>(nq, uint32_t(num_sms) * 8);
-    pack_ids16_kernel<<<grid, 256, 0, st>>>(ids, offsets, nq, cap, hb0, nbuckets, lo16, ends);
+    pack_ids16_kernel<<<grid, 256, 0, st>>>(ids, offsets, nq, cap, hb0, nbuckets, lo16, ends, perm, src_off, src_cap);
 }
 
 }  // namespace mdrq

@@ -225,6 +225,10 @@ struct mdrq_batch {
     // into a pool that has since been replaced by a smaller one)
     bool reserved = false;
     uint64_t reserved_total = 0;
+    // packed stream batches (pack.cu): a sorted bit-sliced batch leaves its
+    // ids in slot order (counts and offsets still move to query order); the
+    // pack kernel reads them from there
+    bool keep_slot_order = false;
     // device buffers freed (the owning store was destroyed first)
     void release_device() {
         d_descs.release(); d_preds.release(); d_udims.release(); d_bounds.release(); d_cmask.release();
@@ -1174,7 +1178,8 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
             launches += launch_va_batch_unpermute(b->d_vb_perm.p, b->d_counts_p.p, b->d_offsets_p.p, b->d_counts.p,
                                                   b->d_offsets.p, s->vb_ids_slot.p,
                                                   s->vb_ids_slot.cap > 4 ? s->vb_ids_slot.cap - 4 : 0, pool.p,
-                                                  pool.p ? pool.cap : 0, nq, ids && pool.p && s->vb_ids_slot.p, st);
+                                                  pool.p ? pool.cap : 0, nq,
+                                                  ids && pool.p && s->vb_ids_slot.p && !b->keep_slot_order, st);
         }
     } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
         // ids: query-major masks (word count a multiple of 4: 16-byte rows)
@@ -1826,8 +1831,13 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             if (!sl.packed) return;
             sl.d_lo16.reserve(pool.cap);
             sl.d_ends.reserve(size_t(nq) * nbuckets);
-            launch_pack_ids16(pool.p, b->d_offsets.p, nq, pool.cap, hb0, nbuckets, sl.d_lo16.p, sl.d_ends.p,
-                              s->num_sms, s->stream);
+            if (b->keep_slot_order && b->path == MDRQ_PATH_VAFILE_BATCH && !b->vb_perm.empty() && s->vb_ids_slot.p)
+                launch_pack_ids16(s->vb_ids_slot.p, b->d_offsets.p, nq, pool.cap, hb0, nbuckets, sl.d_lo16.p,
+                                  sl.d_ends.p, b->d_vb_perm.p, b->d_offsets_p.p,
+                                  s->vb_ids_slot.cap > 4 ? s->vb_ids_slot.cap - 4 : 0, s->num_sms, s->stream);
+            else
+                launch_pack_ids16(pool.p, b->d_offsets.p, nq, pool.cap, hb0, nbuckets, sl.d_lo16.p, sl.d_ends.p,
+                                  nullptr, nullptr, 0, s->num_sms, s->stream);
         };
         s->stream_d2h = s->stream_packed = 0;
         s->stream_batches = nbatches;
@@ -1844,6 +1854,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             build_descs(s, lower + q0[k] * s->m, upper + q0[k] * s->m, nq, resolve_path(s, path, nq, true), true, b);
             upload_batch(s, b, false);
             b->own_pool = !want_pack(nq);
+            b->keep_slot_order = !b->own_pool;
             if (b->own_pool) {
                 sl.d_lo16.release();
                 sl.d_ends.release();

@@ -400,7 +400,8 @@ def test_ids_stream_packed_copies(gpu, monkeypatch, pack, id_base):
     n, m = 300_001, 4
     v = rng.random((n, m), dtype=np.float32)
     batches = []
-    for nq, w in ((40, 0.7), (1, 1.5), (300, 0.5), (17, 0.0), (1100, 0.6), (64, 0.9), (5, 0.3)):
+    # (2100 queries: three sorted passes, packed straight from slot order)
+    for nq, w in ((40, 0.7), (1, 1.5), (300, 0.5), (17, 0.0), (1100, 0.6), (64, 0.9), (2100, 0.35), (5, 0.3)):
         lo = rng.uniform(0, max(1 - w, 1e-3), (nq, m)).astype(np.float32)
         hi = (lo + np.float32(w)).astype(np.float32)
         if w == 0.0:
