@@ -633,7 +633,7 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
     d2h = info.get("d2h_bytes", 0) // e2e_steps or ids_bytes
     packed = info.get("packed_batches", 0)
     # the same stream with the packing off: the raw uint32 ids cross PCIe
-    raw_steps = 5
+    raw_steps = e2e_steps
     os.environ["MDRQ_STREAM_PACK"] = "0"
     try:
         method.search_stream([queries] * 3, outs=[pinned[k % nbuf] for k in range(3)])   # the slots' own pools
