@@ -332,6 +332,7 @@ struct mdrq_store {
     StreamSlot* slots = nullptr;
     uint64_t stream_d2h = 0, stream_packed = 0, stream_batches = 0;   // the last stream call (mdrq_stream_info)
     uint64_t stream_hint = 0;        // largest batch total seen by the stream (pre-sizes fresh slot pools)
+    uint64_t stream_per_query = 0;   // largest ids-per-query average of a stream batch (packed copies or not)
     // pinned bounce buffer of the synchronous ids calls: the offsets, the VA
     // overflow flag and a speculative prefix of the ids come back in one
     // copy + one synchronisation; bounce_ids = ids of the last call held in
@@ -1802,7 +1803,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
         // packed copies (pack.cu): MDRQ_STREAM_PACK=0 never, =1 always,
         // otherwise when the lists are long enough for the bucket ends to be
         // small beside them (>= 32 ids per query and bucket, judged on the
-        // largest batch the stream has seen)
+        // longest lists a batch of this store's streams has produced)
         const bool sdbg = getenv("MDRQ_DEBUG_STREAM") != nullptr;   // per-stage host timings on stderr
         const auto t_call = std::chrono::steady_clock::now();
         auto since = [&] {
@@ -1811,13 +1812,19 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
         const char* pk_env = getenv("MDRQ_STREAM_PACK");
         const int pk_mode = pk_env ? std::atoi(pk_env) : -1;
         const char* th_env = getenv("MDRQ_UNPACK_THREADS");
-        const int pk_threads = th_env ? std::atoi(th_env) : 0;
+        int pk_threads = th_env ? std::atoi(th_env) : 0;
+        if (pk_threads <= 0) {
+            // one process per GPU: the node's ranks share the host threads
+            const char* lw = getenv("LOCAL_WORLD_SIZE");
+            const int ranks = lw ? std::max(1, std::atoi(lw)) : 1;
+            pk_threads = std::max(1, int(std::thread::hardware_concurrency()) / ranks);
+        }
         const uint32_t hb0 = s->id_base >> 16;
         const uint32_t nbuckets = s->n ? uint32_t(((uint64_t(s->id_base) + s->n - 1) >> 16) - hb0 + 1) : 1;
         auto want_pack = [&](uint32_t nq) {
             if (!nq || !s->n || pk_mode == 0) return false;
             if (pk_mode > 0) return true;
-            return s->stream_hint >= uint64_t(32) * nq * nbuckets;
+            return s->stream_per_query >= uint64_t(32) * nbuckets;
         };
         // A packed batch's ids only live in the result pool until the pack
         // kernel behind its pass has run, so packed batches share the store's
@@ -1904,6 +1911,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             }
             totals[k] = total;
             s->stream_hint = std::max<uint64_t>(s->stream_hint, total);
+            if (nq) s->stream_per_query = std::max<uint64_t>(s->stream_per_query, total / nq);
             CK(cudaStreamWaitEvent(s->copy_stream, sl.comp, 0));
             if (nq && s->n) {
                 CK(cudaMemcpyAsync(offsets_out[k], b->d_offsets.p, sizeof(uint64_t) * (nq + 1), cudaMemcpyDeviceToHost,
