@@ -18,6 +18,8 @@
 #include <mutex>
 #include <new>
 #include <stdexcept>
+#include <atomic>
+#include <exception>
 #include <string>
 #include <thread>
 #include <unordered_set>
@@ -409,6 +411,39 @@ uint16_t host_code(const float* b, uint32_t nb, float v) {
     return uint16_t(pos);
 }
 
+// Host-side fan-out for a batch's descriptor work (candidate pass orders, the
+// passes' tables): fn(i) for i in [0, n) on up to 8 threads, fewer when the
+// node's ranks share the host (LOCAL_WORLD_SIZE).  Exceptions are rethrown.
+template <class F>
+void host_parallel_for(size_t n, F&& fn) {
+    static const size_t max_threads = [] {
+        const char* lw = getenv("LOCAL_WORLD_SIZE");
+        const size_t ranks = lw ? size_t(std::max(1, std::atoi(lw))) : 1;
+        return std::max<size_t>(1, std::min<size_t>(8, std::thread::hardware_concurrency() / ranks));
+    }();
+    const size_t T = std::min(n, max_threads);
+    if (T <= 1) {
+        for (size_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::atomic<size_t> next{0};
+    std::exception_ptr err;
+    std::mutex emu;
+    auto work = [&] {
+        try {
+            for (size_t i = next.fetch_add(1); i < n; i = next.fetch_add(1)) fn(i);
+        } catch (...) {
+            std::lock_guard<std::mutex> lk(emu);
+            if (!err) err = std::current_exception();
+        }
+    };
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < T; ++t) th.emplace_back(work);
+    work();
+    for (auto& x : th) x.join();
+    if (err) std::rethrow_exception(err);
+}
+
 // Passes of the bit-sliced VA batch: <= 1024 queries each; per union
 // dimension u and table cell c the overlap / containment masks of the pass's
 // queries (vabatch.cu).  Table cells are the stored 8-bit codes >> shift.
@@ -471,40 +506,52 @@ std::vector<uint32_t> choose_vb_order(const mdrq_store* s, const mdrq_batch* b) 
         }
         return sum / nq;
     };
-    double best = 0.85;
-    std::vector<uint32_t> best_order, order(nq);
-    std::vector<std::pair<double, uint32_t>> one;
-    for (uint32_t d = 0; d < m; ++d) {
-        if (!used[d]) continue;
-        for (uint32_t q = 0; q < nq; ++q) order[q] = q;
-        by_dim(order, d, 0, nq);
-        const double sc = score(order, {d});
-        one.push_back({sc, d});
-        if (sc < best) {
-            best = sc;
-            best_order = order;
+    // every candidate order is scored on its own thread
+    struct Cand {
+        uint32_t da, db, ga;   // ga == 0: dimension da alone
+        double sc = 2.0;
+        std::vector<uint32_t> order;
+    };
+    auto eval = [&](Cand& c) {
+        c.order.resize(nq);
+        for (uint32_t q = 0; q < nq; ++q) c.order[q] = q;
+        by_dim(c.order, c.da, 0, nq);
+        if (c.ga == 0) {
+            c.sc = score(c.order, {c.da});
+        } else {
+            const uint32_t gb = (((nq + 1023) / 1024) + c.ga - 1) / c.ga;   // passes per group
+            for (size_t g0 = 0; g0 < nq; g0 += size_t(gb) * 1024)
+                by_dim(c.order, c.db, g0, std::min<size_t>(nq, g0 + size_t(gb) * 1024));
+            c.sc = score(c.order, {c.da, c.db});
         }
-    }
+        if (c.sc >= 0.85) std::vector<uint32_t>().swap(c.order);   // never chosen
+    };
+    std::vector<Cand> singles;
+    for (uint32_t d = 0; d < m; ++d)
+        if (used[d]) singles.push_back(Cand{d, d, 0});
+    host_parallel_for(singles.size(), [&](size_t i) { eval(singles[i]); });
+    std::vector<std::pair<double, uint32_t>> one;
+    for (const Cand& c : singles) one.push_back({c.sc, c.da});
     std::sort(one.begin(), one.end());
     const uint32_t passes = (nq + 1023) / 1024;
     const size_t top = std::min<size_t>(one.size(), 4);
+    std::vector<Cand> pairs;
     for (size_t ia = 0; ia < top; ++ia)
         for (size_t ib = 0; ib < top; ++ib) {
             if (ia == ib) continue;
-            const uint32_t da = one[ia].second, db = one[ib].second;
-            for (uint32_t ga = 2; ga <= passes / 2; ++ga) {
-                const uint32_t gb = (passes + ga - 1) / ga;   // passes per group
-                for (uint32_t q = 0; q < nq; ++q) order[q] = q;
-                by_dim(order, da, 0, nq);
-                for (size_t g0 = 0; g0 < nq; g0 += size_t(gb) * 1024)
-                    by_dim(order, db, g0, std::min<size_t>(nq, g0 + size_t(gb) * 1024));
-                const double sc = score(order, {da, db});
-                if (sc < best) {
-                    best = sc;
-                    best_order = order;
-                }
-            }
+            for (uint32_t ga = 2; ga <= passes / 2; ++ga) pairs.push_back(Cand{one[ia].second, one[ib].second, ga});
         }
+    host_parallel_for(pairs.size(), [&](size_t i) { eval(pairs[i]); });
+    // the first best in the sequential order of the candidates (singles by
+    // dimension, then the pairs), as the one-thread version chose
+    double best = 0.85;
+    std::vector<uint32_t> best_order;
+    for (std::vector<Cand>* v : {&singles, &pairs})
+        for (Cand& c : *v)
+            if (c.sc < best) {
+                best = c.sc;
+                best_order = std::move(c.order);
+            }
     return best_order;
 }
 
@@ -547,12 +594,23 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
     const uint32_t m = s->m, bits = s->va_bits;
     const bool sorted = !b->vb_perm.empty();
     auto query_of = [&](uint32_t slot) { return sorted ? b->vb_perm[slot] : slot; };
-    for (uint32_t q0 = 0; q0 < b->nq; q0 += 1024) {
+    // every pass's tables on its own thread, appended in pass order afterwards
+    struct PassOut {
         VbPass ps;
+        std::vector<uint16_t> ud;
+        std::vector<uint32_t> tab, cmv, q16;
+        std::vector<float2> qbv;
+    };
+    const uint32_t npasses = (b->nq + 1023) / 1024;
+    std::vector<PassOut> outs(npasses);
+    host_parallel_for(npasses, [&](size_t pi) {
+        PassOut& po = outs[pi];
+        VbPass& ps = po.ps;
+        const uint32_t q0 = uint32_t(pi) * 1024;
         ps.q0 = q0;
         ps.nqp = std::min<uint32_t>(1024, b->nq - q0);
         std::vector<int> uidx(m, -1);
-        std::vector<uint16_t> ud;
+        std::vector<uint16_t>& ud = po.ud;
         for (uint32_t sl = q0; sl < q0 + ps.nqp; ++sl)
             for (uint32_t i = 0; i < b->descs[query_of(sl)].k; ++i) {
                 const uint32_t d = b->preds[b->descs[query_of(sl)].off + i].dim;
@@ -567,8 +625,7 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         ps.kb = uint32_t(ud.size());
         if (int(ps.kb) > va_batch_max_dims()) {
             ps.fallback = true;
-            b->vb_passes.push_back(ps);
-            continue;
+            return;
         }
         // table cells: va_batch_cells(kb) (the kernel's constant); a store
         // with fewer code bits uses only the first 2^bits cells
@@ -577,16 +634,13 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         while ((1u << (tb + 1)) <= ps.cells) ++tb;
         tb = std::min(bits, tb);
         ps.shift = bits - tb;
-        ps.udim_off = b->vb_udims.size();
-        ps.table_off = b->vb_tables.size();
-        ps.qb_off = b->vb_qb.size();
-        ps.cm_off = b->vb_cm.size();
-        b->vb_udims.insert(b->vb_udims.end(), ud.begin(), ud.end());
         const bool pv = va_batch_pv(ps.kb);
         const uint32_t qstride = pv ? va_batch_vdims(ps.kb) : ps.kb;
         const uint32_t cells = ps.cells;
-        std::vector<uint32_t> tab(va_batch_table_words(ps.kb, cells), 0u);
-        std::vector<float2> qbv(size_t(1024) * qstride, make_float2(-INFINITY, INFINITY));
+        std::vector<uint32_t>& tab = po.tab;
+        tab.assign(va_batch_table_words(ps.kb, cells), 0u);
+        std::vector<float2>& qbv = po.qbv;
+        qbv.assign(size_t(1024) * qstride, make_float2(-INFINITY, INFINITY));
         // staged unions: the 15-bit code function per union dim (monotone; any
         // positive scale is sound, a degenerate range only sends more
         // candidates to the exact compare) and the queries' bound codes, two
@@ -594,7 +648,7 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         // is (L, H) = (0, 32767), strictly outside every value code
         const bool q15 = va_batch_q15(ps.kb);
         const uint32_t vd = va_batch_vdims(ps.kb);
-        std::vector<uint32_t> q16;
+        std::vector<uint32_t>& q16 = po.q16;
         if (q15) {
             for (uint32_t u = 0; u < kVbStageDims; ++u) {
                 ps.vmin[u] = 0.f;
@@ -626,7 +680,8 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         };
         // queries unconstrained in dimension u: every cell, set once per word below
         std::vector<uint32_t> free_mask(size_t(ps.kb) * 32, 0u);
-        std::vector<uint32_t> cmv(1024, 0u);
+        std::vector<uint32_t>& cmv = po.cmv;
+        cmv.assign(1024, 0u);
         std::vector<unsigned long long> cmask(ps.kb, 0ull);
         const unsigned long long cfull = cells == 64 ? ~0ull : ((1ull << cells) - 1);
         for (uint32_t qi = 0; qi < ps.nqp; ++qi) {
@@ -695,11 +750,21 @@ void build_vb_passes_ordered(const mdrq_store* s, mdrq_batch* b) {
         if (lw < 32)
             for (size_t row = 0; row < tab.size() / 32; ++row)
                 for (uint32_t w = lw; w < 32; ++w) tab[row * 32 + w] = tab[row * 32 + w % lw];
-        b->vb_tables.insert(b->vb_tables.end(), tab.begin(), tab.end());
-        b->vb_qb.insert(b->vb_qb.end(), qbv.begin(), qbv.end());
-        b->vb_cm.insert(b->vb_cm.end(), cmv.begin(), cmv.end());
-        ps.q16_off = b->vb_q16.size();
-        b->vb_q16.insert(b->vb_q16.end(), q16.begin(), q16.end());
+    });
+    for (PassOut& po : outs) {
+        VbPass& ps = po.ps;
+        if (!ps.fallback) {
+            ps.udim_off = b->vb_udims.size();
+            ps.table_off = b->vb_tables.size();
+            ps.qb_off = b->vb_qb.size();
+            ps.cm_off = b->vb_cm.size();
+            ps.q16_off = b->vb_q16.size();
+            b->vb_udims.insert(b->vb_udims.end(), po.ud.begin(), po.ud.end());
+            b->vb_tables.insert(b->vb_tables.end(), po.tab.begin(), po.tab.end());
+            b->vb_qb.insert(b->vb_qb.end(), po.qbv.begin(), po.qbv.end());
+            b->vb_cm.insert(b->vb_cm.end(), po.cmv.begin(), po.cmv.end());
+            b->vb_q16.insert(b->vb_q16.end(), po.q16.begin(), po.q16.end());
+        }
         b->vb_passes.push_back(ps);
     }
 }
