@@ -206,11 +206,15 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
  * host step: out[offsets[q] + i] = (hb0 + b) << 16 | lo16[offsets[q] + i] for
  * ends[q][b-1] <= i < ends[q][b] (ends: nq x nbuckets, positions relative to
  * the query's list; offsets: nq + 1).  It needs no device.
+ * A packed batch sends only a share of its queries packed and the rest raw,
+ * the share steered so the PCIe copy and the host unpack of a batch take
+ * about as long (MDRQ_STREAM_PACK_SHARE fixes it, 0..1).
  * mdrq_stream_info: out[0] = device->host bytes of the store's last stream
- * call, out[1] = batches of it that were packed, out[2] = its batches.      */
+ * call, out[1] = batches of it that were packed, out[2] = its batches,
+ * out[3] = the current packed share of a batch's queries, in 1/1000.        */
 int mdrq_unpack_ids16(const uint16_t* lo16, const uint32_t* ends, const uint64_t* offsets,
                       uint32_t nq, uint32_t hb0, uint32_t nbuckets, uint32_t* out, int threads);
-int mdrq_stream_info(mdrq_store* s, uint64_t out[3]);
+int mdrq_stream_info(mdrq_store* s, uint64_t out[4]);
 /* SearchStats of the last count/ids call, one entry per query.            */
 int mdrq_query_stats(mdrq_store* s, int mode, mdrq_search_stats* stats,
                      uint32_t nq);

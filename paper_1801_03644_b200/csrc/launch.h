@@ -192,12 +192,13 @@ void launch_va_batch(const VaBatchArgs& a, int mode, cudaStream_t st);
 void launch_va_batch_scatter(const VaBatchArgs& a, cudaStream_t st);
 void launch_va_batch_scans(const VaBatchArgs& a, uint32_t q0, cudaStream_t st);
 void launch_va_batch_block_list(const VaBatchArgs& a, cudaStream_t st);
-// sorted batches: slot-order counts / offsets / ids back to query order;
-// returns the number of kernels launched
+// sorted batches: slot-order counts / offsets / ids back to query order (the
+// ids of queries >= q_from only); returns the number of kernels launched
 uint32_t launch_va_batch_unpermute(const uint32_t* perm, const unsigned long long* counts_p,
                                    const unsigned long long* offsets_p, unsigned long long* counts,
                                    unsigned long long* offsets, const uint32_t* ids_p, uint64_t src_cap,
-                                   uint32_t* ids, uint64_t cap, uint32_t nq, bool with_ids, cudaStream_t st);
+                                   uint32_t* ids, uint64_t cap, uint32_t nq, bool with_ids, uint32_t q_from,
+                                   cudaStream_t st);
 
 constexpr int kColTile = 4096;     // tuples per CTA tile, single-query columnar
 constexpr int kVaTile = 8192;      // tuples per CTA tile, VA-file filter
@@ -259,9 +260,11 @@ void launch_copy_segments(const uint32_t* src, uint32_t* dst, const int64_t* src
 // lo16[i] = ids[i] & 0xFFFF, ends[q][b] = ids of query q in buckets <= hb0 + b
 // (perm / src_off / src_cap: the lists still in the slot order of a sorted
 // bit-sliced batch -- list i at ids + src_off[i] is query perm[i]'s; else null)
-void launch_pack_ids16(const uint32_t* ids, const unsigned long long* offsets, uint32_t nq, uint64_t cap,
-                       uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends, const uint32_t* perm,
-                       const unsigned long long* src_off, uint64_t src_cap, int num_sms, cudaStream_t st);
+// queries < q_to are packed (ends holds q_to rows); nq = lists to walk
+void launch_pack_ids16(const uint32_t* ids, const unsigned long long* offsets, uint32_t nq, uint32_t q_to,
+                       uint64_t cap, uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends,
+                       const uint32_t* perm, const unsigned long long* src_off, uint64_t src_cap, int num_sms,
+                       cudaStream_t st);
 void launch_match_rows(const float* rows, uint64_t nrows, uint32_t m, const float* lo,
                        const float* hi, uint8_t* out, cudaStream_t st);
 

@@ -7,7 +7,9 @@
 // their high half: the device writes the low halves (2 bytes per id, same
 // order) and, per query, the end position of every bucket in its run; the
 // host rebuilds id = bucket << 16 | low (unpack_host.cpp, multi-threaded).
-// The copy shrinks to half plus nq x nbuckets words.
+// The copy shrinks to half plus nq x nbuckets words.  The stream packs the
+// first q_to queries of a batch and sends the rest raw, q_to chosen so the
+// copy and the host unpack take about as long (store.cu).
 #include <algorithm>
 
 #include "launch.h"
@@ -23,13 +25,14 @@ namespace {
 // move of the uint32 ids to query order.
 __global__ void __launch_bounds__(256) pack_ids16_kernel(const uint32_t* __restrict__ ids,
                                                          const unsigned long long* __restrict__ offsets, uint32_t nq,
-                                                         uint64_t cap, uint32_t hb0, uint32_t nbuckets,
+                                                         uint32_t q_to, uint64_t cap, uint32_t hb0, uint32_t nbuckets,
                                                          uint16_t* __restrict__ lo16, uint32_t* __restrict__ ends,
                                                          const uint32_t* __restrict__ perm,
                                                          const unsigned long long* __restrict__ src_off,
                                                          uint64_t src_cap) {
     for (uint32_t i0 = blockIdx.x; i0 < nq; i0 += gridDim.x) {
         const uint32_t q = perm ? perm[i0] : i0;
+        if (q >= q_to) continue;   // this query's ids travel raw
         const uint64_t o0 = offsets[q], o1 = offsets[q + 1];
         if (o1 > cap) continue;   // truncated result: the caller grows the pool and reruns
         const uint64_t cnt = o1 - o0;
@@ -57,12 +60,15 @@ __global__ void __launch_bounds__(256) pack_ids16_kernel(const uint32_t* __restr
 
 }  // namespace
 
-void launch_pack_ids16(const uint32_t* ids, const unsigned long long* offsets, uint32_t nq, uint64_t cap,
-                       uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends, const uint32_t* perm,
-                       const unsigned long long* src_off, uint64_t src_cap, int num_sms, cudaStream_t st) {
-    if (!nq) return;
+void launch_pack_ids16(const uint32_t* ids, const unsigned long long* offsets, uint32_t nq, uint32_t q_to,
+                       uint64_t cap, uint32_t hb0, uint32_t nbuckets, uint16_t* lo16, uint32_t* ends,
+                       const uint32_t* perm, const unsigned long long* src_off, uint64_t src_cap, int num_sms,
+                       cudaStream_t st) {
+    if (!nq || !q_to) return;
+    if (!perm) nq = std::min(nq, q_to);   // lists in query order: only the packed ones
     const uint32_t grid = std::min<uint32_t>(nq, uint32_t(num_sms) * 8);
-    pack_ids16_kernel<<<grid, 256, 0, st>>>(ids, offsets, nq, cap, hb0, nbuckets, lo16, ends, perm, src_off, src_cap);
+    pack_ids16_kernel<<<grid, 256, 0, st>>>(ids, offsets, nq, q_to, cap, hb0, nbuckets, lo16, ends, perm, src_off,
+                                            src_cap);
 }
 
 }  // namespace mdrq

@@ -227,10 +227,15 @@ struct mdrq_batch {
     // into a pool that has since been replaced by a smaller one)
     bool reserved = false;
     uint64_t reserved_total = 0;
-    // packed stream batches (pack.cu): a sorted bit-sliced batch leaves its
-    // ids in slot order (counts and offsets still move to query order); the
-    // pack kernel reads them from there
-    bool keep_slot_order = false;
+    // packed stream batches (pack.cu): the ids of queries < packed_to are
+    // packed straight from the slot-order lists of a sorted bit-sliced batch
+    // (counts and offsets still move to query order), only the ids of the
+    // queries from packed_to on are moved to query order
+    uint32_t packed_to = 0;
+    // which of the store's two shared result pools a packed stream batch
+    // writes (its raw tail is copied out of it while the next batch runs
+    // into the other one)
+    uint8_t shared_pool = 0;
     // device buffers freed (the owning store was destroyed first)
     void release_device() {
         d_descs.release(); d_preds.release(); d_udims.release(); d_bounds.release(); d_cmask.release();
@@ -265,12 +270,16 @@ struct HBuf {
 struct StreamSlot {
     mdrq_batch b;
     cudaEvent_t comp = nullptr, copy = nullptr;
-    unsigned long long* h_flags = nullptr;   // pinned [2]: total, overflow
+    unsigned long long* h_flags = nullptr;   // pinned [3]: total, overflow, ids of the packed queries
     bool busy = false;                       // a D2H of this slot is in flight
     // packed copies (pack.cu): the batch's low id halves and bucket ends on
     // the device, their pinned staging on the host, and the thread that
     // rebuilds the caller's uint32 ids from the staging
     bool packed = false;
+    uint32_t q_split = 0;                    // packed batches: queries below travel packed, the rest raw
+    cudaEvent_t cp0 = nullptr, cp1 = nullptr;   // around the batch's copies (timed)
+    double unpack_ms = 0;                    // host unpack of the slot's last packed batch
+    bool measured = false;                   // cp0 / cp1 / unpack_ms belong to a finished packed batch
     uint64_t pool_cap = 0;                   // capacity of the result pool the batch ran into
     DBuf<uint16_t> d_lo16;
     DBuf<uint32_t> d_ends;
@@ -303,6 +312,8 @@ struct mdrq_store {
     DBuf<uint32_t> bmask, bchunk_counts, bchunk_offs;
     // sorted VA batches: ids in slot order before they move to query order
     DBuf<uint32_t> vb_ids_slot;
+    // second shared result pool of the packed stream (pool_of)
+    DBuf<uint32_t> ids_alt;
     DBuf<uint32_t> chunk_counts, chunk_offs;
     uint32_t nchunks = 0;
     // bit-sliced VA batch scratch ([chunks][1024] per pass)
@@ -335,6 +346,9 @@ struct mdrq_store {
     uint64_t stream_d2h = 0, stream_packed = 0, stream_batches = 0;   // the last stream call (mdrq_stream_info)
     uint64_t stream_hint = 0;        // largest batch total seen by the stream (pre-sizes fresh slot pools)
     uint64_t stream_per_query = 0;   // largest ids-per-query average of a stream batch (packed copies or not)
+    // share of a packed batch's queries that travel packed (the rest raw):
+    // steered so the PCIe copy and the host unpack of a batch take equally long
+    double stream_pack_share = 0.85;
     // pinned bounce buffer of the synchronous ids calls: the offsets, the VA
     // overflow flag and a speculative prefix of the ids come back in one
     // copy + one synchronisation; bounce_ids = ids of the last call held in
@@ -351,6 +365,8 @@ struct mdrq_store {
                 if (slots[i].comp) cudaEventDestroy(slots[i].comp);
                 if (slots[i].copy) cudaEventDestroy(slots[i].copy);
                 if (slots[i].h_flags) cudaFreeHost(slots[i].h_flags);
+                if (slots[i].cp0) cudaEventDestroy(slots[i].cp0);
+                if (slots[i].cp1) cudaEventDestroy(slots[i].cp1);
                 slots[i].join();
                 slots[i].h_lo16.release();
                 slots[i].h_ends.release();
@@ -973,7 +989,9 @@ uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids)
 }
 
 // the result pool a batch writes: its own (stream slots) or the store's
-DBuf<uint32_t>& pool_of(mdrq_store* s, mdrq_batch* b) { return b->own_pool ? b->own_ids : s->ids; }
+DBuf<uint32_t>& pool_of(mdrq_store* s, mdrq_batch* b) {
+    return b->own_pool ? b->own_ids : b->shared_pool ? s->ids_alt : s->ids;
+}
 
 ScanArgs base_args(mdrq_store* s, mdrq_batch* b, uint32_t path) {
     ScanArgs a{};
@@ -1245,7 +1263,8 @@ uint32_t enqueue_impl(mdrq_store* s, mdrq_batch* b, bool ids, cudaStream_t st, P
                                                   b->d_offsets.p, s->vb_ids_slot.p,
                                                   s->vb_ids_slot.cap > 4 ? s->vb_ids_slot.cap - 4 : 0, pool.p,
                                                   pool.p ? pool.cap : 0, nq,
-                                                  ids && pool.p && s->vb_ids_slot.p && !b->keep_slot_order, st);
+                                                  ids && pool.p && s->vb_ids_slot.p && b->packed_to < nq, b->packed_to,
+                                                  st);
         }
     } else if (path == MDRQ_PATH_COLUMNAR_BATCH) {
         // ids: query-major masks (word count a multiple of 4: 16-byte rows)
@@ -1859,7 +1878,9 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             for (int i = 0; i < kStreamSlots; ++i) {
                 CK(cudaEventCreateWithFlags(&s->slots[i].comp, cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&s->slots[i].copy, cudaEventDisableTiming));
-                CK(cudaMallocHost(reinterpret_cast<void**>(&s->slots[i].h_flags), 2 * sizeof(unsigned long long)));
+                CK(cudaMallocHost(reinterpret_cast<void**>(&s->slots[i].h_flags), 3 * sizeof(unsigned long long)));
+                CK(cudaEventCreate(&s->slots[i].cp0));
+                CK(cudaEventCreate(&s->slots[i].cp1));
                 s->slots[i].b.owner = s;
                 s->slots[i].b.own_pool = true;
             }
@@ -1902,14 +1923,35 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             sl.packed = !b->own_pool && pool.p;
             if (!sl.packed) return;
             sl.d_lo16.reserve(pool.cap);
-            sl.d_ends.reserve(size_t(nq) * nbuckets);
-            if (b->keep_slot_order && b->path == MDRQ_PATH_VAFILE_BATCH && !b->vb_perm.empty() && s->vb_ids_slot.p)
-                launch_pack_ids16(s->vb_ids_slot.p, b->d_offsets.p, nq, pool.cap, hb0, nbuckets, sl.d_lo16.p,
-                                  sl.d_ends.p, b->d_vb_perm.p, b->d_offsets_p.p,
+            sl.d_ends.reserve(size_t(nq) * nbuckets);   // (not q_split rows: the share moves, a regrowth synchronises)
+            if (b->path == MDRQ_PATH_VAFILE_BATCH && !b->vb_perm.empty() && s->vb_ids_slot.p)
+                launch_pack_ids16(s->vb_ids_slot.p, b->d_offsets.p, nq, sl.q_split, pool.cap, hb0, nbuckets,
+                                  sl.d_lo16.p, sl.d_ends.p, b->d_vb_perm.p, b->d_offsets_p.p,
                                   s->vb_ids_slot.cap > 4 ? s->vb_ids_slot.cap - 4 : 0, s->num_sms, s->stream);
             else
-                launch_pack_ids16(pool.p, b->d_offsets.p, nq, pool.cap, hb0, nbuckets, sl.d_lo16.p, sl.d_ends.p,
-                                  nullptr, nullptr, 0, s->num_sms, s->stream);
+                launch_pack_ids16(pool.p, b->d_offsets.p, nq, sl.q_split, pool.cap, hb0, nbuckets, sl.d_lo16.p,
+                                  sl.d_ends.p, nullptr, nullptr, 0, s->num_sms, s->stream);
+        };
+        // MDRQ_STREAM_PACK_SHARE fixes the packed share of a batch's queries
+        // (0..1); otherwise it follows the measured copy and unpack times
+        const char* sh_env = getenv("MDRQ_STREAM_PACK_SHARE");
+        if (sh_env) s->stream_pack_share = std::min(1.0, std::max(0.0, std::atof(sh_env)));
+        auto steer = [&](StreamSlot& sl) {
+            if (!sl.measured) return;
+            sl.measured = false;
+            float copy_ms = 0;
+            if (cudaEventElapsedTime(&copy_ms, sl.cp0, sl.cp1) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+            if (sdbg)
+                fprintf(stderr, "[stream] copy %.1f ms, unpack %.1f ms at packed share %.2f\n", copy_ms, sl.unpack_ms,
+                        s->stream_pack_share);
+            if (sh_env || copy_ms <= 0 || sl.unpack_ms <= 0) return;
+            if (sl.unpack_ms > 1.10 * copy_ms)
+                s->stream_pack_share = std::max(0.5, s->stream_pack_share - 0.02);
+            else if (copy_ms > 1.10 * sl.unpack_ms)
+                s->stream_pack_share = std::min(1.0, s->stream_pack_share + 0.02);
         };
         s->stream_d2h = s->stream_packed = 0;
         s->stream_batches = nbatches;
@@ -1926,12 +1968,22 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             build_descs(s, lower + q0[k] * s->m, upper + q0[k] * s->m, nq, resolve_path(s, path, nq, true), true, b);
             upload_batch(s, b, false);
             b->own_pool = !want_pack(nq);
-            b->keep_slot_order = !b->own_pool;
+            sl.q_split = b->own_pool ? 0u
+                                     : std::min<uint32_t>(nq, std::max<uint32_t>(1, uint32_t(s->stream_pack_share * nq + 0.5)));
+            b->packed_to = sl.q_split;
+            b->shared_pool = b->own_pool ? 0 : uint8_t(k & 1u);
             if (b->own_pool) {
                 sl.d_lo16.release();
                 sl.d_ends.release();
+                s->ids_alt.release();
             } else {
                 b->own_ids.release();
+                // batch k-2 ran into the same shared pool: its raw tail must
+                // have left it (its copies were enqueued an iteration ago)
+                if (k >= 2) {
+                    StreamSlot& prev = s->slots[(k - 2) % kStreamSlots];
+                    if (prev.busy) CK(cudaStreamWaitEvent(s->stream, prev.copy, 0));
+                }
             }
             // a pool starts at the size of the largest batch seen so far: a
             // fresh slot must not run its first batch twice
@@ -1943,10 +1995,12 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             up += upload_bytes(b);
             enqueue(s, b, true, s->stream);
             pack(sl, nq);
-            sl.h_flags[0] = sl.h_flags[1] = 0;
+            sl.h_flags[0] = sl.h_flags[1] = sl.h_flags[2] = 0;
             if (nq && s->n) {
                 CK(cudaMemcpyAsync(sl.h_flags, b->d_offsets.p + nq, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                    s->stream));
+                CK(cudaMemcpyAsync(sl.h_flags + 2, b->d_offsets.p + sl.q_split, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, s->stream));
                 if (b->path == MDRQ_PATH_VAFILE_BATCH && s->vb_flags.p)
                     CK(cudaMemcpyAsync(sl.h_flags + 1, s->vb_flags.p + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                        s->stream));
@@ -1991,13 +2045,23 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             } else if (total && sl.packed) {
                 // the staging still feeds the unpack of the slot's previous batch
                 sl.join();
+                steer(sl);
+                // ids [0, split) belong to the packed queries, [split, total) travel raw
+                const uint64_t split = std::min<uint64_t>(sl.h_flags[2], total);
                 sl.h_lo16.reserve(size_t(total + total / 8 + 4096));
                 sl.h_ends.reserve(size_t(nq) * nbuckets);
-                CK(cudaMemcpyAsync(sl.h_lo16.p, sl.d_lo16.p, sizeof(uint16_t) * total, cudaMemcpyDeviceToHost,
-                                   s->copy_stream));
-                CK(cudaMemcpyAsync(sl.h_ends.p, sl.d_ends.p, sizeof(uint32_t) * size_t(nq) * nbuckets,
+                CK(cudaEventRecord(sl.cp0, s->copy_stream));
+                if (split)
+                    CK(cudaMemcpyAsync(sl.h_lo16.p, sl.d_lo16.p, sizeof(uint16_t) * split, cudaMemcpyDeviceToHost,
+                                       s->copy_stream));
+                CK(cudaMemcpyAsync(sl.h_ends.p, sl.d_ends.p, sizeof(uint32_t) * size_t(sl.q_split) * nbuckets,
                                    cudaMemcpyDeviceToHost, s->copy_stream));
-                s->stream_d2h += sizeof(uint16_t) * total + sizeof(uint32_t) * size_t(nq) * nbuckets;
+                if (total > split)
+                    CK(cudaMemcpyAsync(ids_out[k] + split, pool.p + split, sizeof(uint32_t) * (total - split),
+                                       cudaMemcpyDeviceToHost, s->copy_stream));
+                CK(cudaEventRecord(sl.cp1, s->copy_stream));
+                s->stream_d2h += sizeof(uint16_t) * split + sizeof(uint32_t) * size_t(sl.q_split) * nbuckets +
+                                 sizeof(uint32_t) * (total - split);
                 s->stream_packed += 1;
             } else if (total) {
                 sl.packed = false;
@@ -2022,14 +2086,16 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             const uint32_t* en = sl.h_ends.p;
             const uint64_t* of = offsets_out[k];
             uint32_t* out = ids_out[k];
-            const uint32_t nq = nqs[k];
+            const uint32_t nq = sl.q_split;
+            StreamSlot* slp = &sl;
             sl.unpack = std::thread([=] {
                 const auto t0 = std::chrono::steady_clock::now();
                 mdrq_unpack_ids16(lo, en, of, nq, hb0, nbuckets, out, pk_threads);
+                slp->unpack_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                slp->measured = true;
                 if (sdbg)
-                    fprintf(stderr, "[stream] unpack %u: %.1f ms (%llu ids)\n", k,
-                            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
-                            (unsigned long long)(of[nq] - of[0]));
+                    fprintf(stderr, "[stream] unpack %u: %.1f ms (%llu ids of %u queries)\n", k, slp->unpack_ms,
+                            (unsigned long long)(of[nq] - of[0]), nq);
             });
         };
         struct Joiner {   // no unpack thread outlives the call, also when it throws
@@ -2061,7 +2127,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
     return rc;
 }
 
-int mdrq_stream_info(mdrq_store* s, uint64_t out[3]) {
+int mdrq_stream_info(mdrq_store* s, uint64_t out[4]) {
     return guard([&] {
         check_store(s);
         if (!out) raise(MDRQ_EINVAL, "null argument");
@@ -2069,6 +2135,7 @@ int mdrq_stream_info(mdrq_store* s, uint64_t out[3]) {
         out[0] = s->stream_d2h;
         out[1] = s->stream_packed;
         out[2] = s->stream_batches;
+        out[3] = uint64_t(s->stream_pack_share * 1000.0 + 0.5);
     });
 }
 

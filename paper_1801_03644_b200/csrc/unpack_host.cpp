@@ -9,6 +9,7 @@
 // two high halves by lane, and only a group with several ends goes id by id.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -51,6 +52,16 @@ void unpack_scalar(const uint16_t* lo16, uint32_t* out, uint64_t p, uint64_t p1,
 }
 
 #if defined(__x86_64__)
+template <bool NT>
+__attribute__((target("avx2"))) inline void store8(uint32_t* at, __m256i v) {
+    if (NT)
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(at), v);
+    else
+        _mm256_store_si256(reinterpret_cast<__m256i*>(at), v);
+}
+
+// NT: streaming stores (no read-for-ownership of the output lines)
+template <bool NT>
 __attribute__((target("avx2"))) void unpack_avx2(const uint16_t* lo16, uint32_t* out, uint64_t p, uint64_t p1,
                                                  Cursor& c) {
     // head up to a 64-byte aligned output position
@@ -93,8 +104,8 @@ __attribute__((target("avx2"))) void unpack_avx2(const uint16_t* lo16, uint32_t*
                 h1 = _mm256_load_si256(reinterpret_cast<const __m256i*>(tmp + 8));
             }
         }
-        _mm256_stream_si256(reinterpret_cast<__m256i*>(out + p), _mm256_or_si256(x0, h0));
-        _mm256_stream_si256(reinterpret_cast<__m256i*>(out + p + 8), _mm256_or_si256(x1, h1));
+        store8<NT>(out + p, _mm256_or_si256(x0, h0));
+        store8<NT>(out + p + 8, _mm256_or_si256(x1, h1));
     }
     unpack_scalar(lo16, out, p, p1, c);
     _mm_sfence();
@@ -110,7 +121,15 @@ void unpack_range(const uint16_t* lo16, const uint32_t* ends, const uint64_t* of
     c.load();
 #if defined(__x86_64__)
     if (__builtin_cpu_supports("avx2")) {
-        unpack_avx2(lo16, out, p0, p1, c);
+        // MDRQ_UNPACK_NT=0: regular stores (measurement switch)
+        static const bool nt = [] {
+            const char* e = getenv("MDRQ_UNPACK_NT");
+            return !(e && e[0] == '0');
+        }();
+        if (nt)
+            unpack_avx2<true>(lo16, out, p0, p1, c);
+        else
+            unpack_avx2<false>(lo16, out, p0, p1, c);
         return;
     }
 #endif

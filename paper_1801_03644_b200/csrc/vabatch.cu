@@ -1391,9 +1391,11 @@ __global__ void __launch_bounds__(256) vb_unpermute_ids_kernel(const uint32_t* _
                                                                const unsigned long long* __restrict__ cp,
                                                                const unsigned long long* __restrict__ offsets,
                                                                const uint32_t* __restrict__ src, uint64_t src_cap,
-                                                               uint32_t* __restrict__ dst, uint64_t cap, uint32_t nq) {
+                                                               uint32_t* __restrict__ dst, uint64_t cap, uint32_t nq,
+                                                               uint32_t q_from) {
     for (uint32_t i = blockIdx.x; i < nq; i += gridDim.x) {
         uint64_t n = cp[i];
+        if (perm[i] < q_from) continue;   // packed from slot order instead (pack.cu)
         const uint64_t d0 = offsets[perm[i]];
         // truncated result (either buffer too small): the caller grows the
         // pool and reruns
@@ -1535,14 +1537,15 @@ void launch_va_batch_scans(const VaBatchArgs& a, uint32_t q0, cudaStream_t st) {
 uint32_t launch_va_batch_unpermute(const uint32_t* perm, const unsigned long long* counts_p,
                                    const unsigned long long* offsets_p, unsigned long long* counts,
                                    unsigned long long* offsets, const uint32_t* ids_p, uint64_t src_cap,
-                                   uint32_t* ids, uint64_t cap, uint32_t nq, bool with_ids, cudaStream_t st) {
+                                   uint32_t* ids, uint64_t cap, uint32_t nq, bool with_ids, uint32_t q_from,
+                                   cudaStream_t st) {
     if (!nq) return 0;
     vb_unpermute_counts_kernel<<<(nq + 255) / 256, 256, 0, st>>>(perm, counts_p, counts, nq);
     vb_offsets_scan_kernel<<<1, 1024, 0, st>>>(counts, nq, offsets);
     if (!with_ids) return 2;
     // one CTA per id run (a run is a query's ids: ~5e5 on C5)
     vb_unpermute_ids_kernel<<<std::min<uint32_t>(nq, 65535), 256, 0, st>>>(perm, offsets_p, counts_p, offsets, ids_p,
-                                                                         src_cap, ids, cap, nq);
+                                                                         src_cap, ids, cap, nq, q_from);
     return 3;
 }
 

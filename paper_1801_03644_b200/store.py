@@ -261,13 +261,14 @@ class DeviceStore:
         if info is not None:
             info["h2d_bytes"] = int(h2d.value)
             info["totals"] = [int(t) for t in totals]
-            si = (ctypes.c_uint64 * 3)()
+            si = (ctypes.c_uint64 * 4)()
             with self._lock:
                 check(lib.mdrq_stream_info(self.handle, si))
             # device->host bytes of the call and how many of its batches left
             # the device packed (16-bit low halves + bucket ends, pack.cu)
             info["d2h_bytes"] = int(si[0])
             info["packed_batches"] = int(si[1])
+            info["packed_share"] = int(si[3]) / 1000.0   # of a packed batch's queries; the rest travel raw
         return out
 
     def stats(self, nq: int, mode: int = _lib.MODE_SCALAR):

@@ -418,7 +418,7 @@ def test_ids_stream_packed_copies(gpu, monkeypatch, pack, id_base):
             for (eo, ei), (offs, ids) in zip(exp, res):
                 assert np.array_equal(offs, eo)
                 assert np.array_equal(ids.astype(np.int64), ei + id_base)
-            out = (ctypes.c_uint64 * 3)()
+            out = (ctypes.c_uint64 * 4)()
             _lib.check(_lib.load().mdrq_stream_info(st_.handle, out))
             assert out[2] == len(batches)
             total = sum(int(o[-1]) for o, _ in res)
