@@ -411,7 +411,12 @@ def test_ids_stream_packed_copies(gpu, monkeypatch, pack, id_base):
         batches.append((lo, hi))
     exp = [oracle.ids_batch(v, lo, hi) for lo, hi in batches]
     with gpu.DeviceStore(v, layouts=1 | 4, va_bits=8, id_base=id_base) as st_:
-        for rep in range(2):   # the second round reuses warmed slots (automatic mode packs from here)
+        # rounds 0, 1: the steered share (the second round reuses warmed slots;
+        # automatic mode packs from there); then fixed shares: every query
+        # packed, a third packed and the rest raw
+        for rep in range(4 if pack == "1" else 2):
+            if rep >= 2:
+                monkeypatch.setenv("MDRQ_STREAM_PACK_SHARE", ("1.0", "0.3")[rep - 2])
             info = {}
             outs = [np.empty(ei.size + 16, np.uint32) for _, ei in exp]
             res = st_.ids_stream(batches, "auto", outs=outs, info=info)

@@ -8,4 +8,4 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 echo "torchrun rc=$?" >> $OUT/tr.err
 timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $OUT/ref.log 2> $OUT/ref.err
 echo "ref rc=$?" >> $OUT/ref.err
-tail -2 $OUT/tr.err $OUT/ref.err
+tail -n 2 $OUT/tr.err; tail -n 2 $OUT/ref.err
