@@ -955,16 +955,38 @@ uint64_t upload_bytes(const mdrq_batch* b) {
            b->vb_q16.size() * sizeof(uint32_t);
 }
 
-uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids) {
+uint32_t resolve_path(const mdrq_store* s, uint32_t path, uint32_t nq, bool ids, const float* lower = nullptr,
+                      const float* upper = nullptr) {
     if (path == MDRQ_PATH_AUTO) {
-        // planner, from the B200 per-query costs of C2:
-        // a bit-sliced VA pass of <= 256 queries costs about as much as ~10
-        // single-query VA scans (1.0 ms vs 102-124 us), so it wins from 10
-        // queries on; below that one query per pass over the code planes
-        // (VA) or the columns.
+        // planner.  A bit-sliced VA pass reads a table
+        // row per tuple and UNION dimension whatever the number of queries,
+        // a single-query VA scan a code per tuple and dimension of ITS query:
+        // on the B200 (tools/probe_planner.py, C2-C5) a row costs ~10x a
+        // code for unions of <= 16 dims (8.3 on C2 / C3 / C4, 12.4 on C5)
+        // and ~30x for the wider unions' (overlap, containment) rows, so the
+        // pass wins once  sum of the queries' dims >= 10 (30) x union dims:
+        // 10 full-match queries, ~25 of C3's (5 of 16 dims), ~130 of C4's
+        // when their union reaches 19 dims.
         const bool va = (s->layouts & MDRQ_LAYOUT_VAFILE) != 0;
         if (!(s->layouts & MDRQ_LAYOUT_COLUMNAR)) return MDRQ_PATH_ROWWISE;
-        if (va && nq >= 10) return MDRQ_PATH_VAFILE_BATCH;
+        if (va && nq >= 10) {
+            if (!lower || !upper || nq >= 1024) return MDRQ_PATH_VAFILE_BATCH;
+            uint64_t sum_k = 0;
+            std::vector<uint8_t> used(s->m, 0);
+            for (uint32_t q = 0; q < nq; ++q)
+                for (uint32_t j = 0; j < s->m; ++j) {
+                    const float l = lower[uint64_t(q) * s->m + j], h = upper[uint64_t(q) * s->m + j];
+                    if (!(is_neg_inf(l) && is_pos_inf(h))) {
+                        ++sum_k;
+                        used[j] = 1;
+                    }
+                }
+            uint64_t kb = 0;
+            for (uint32_t j = 0; j < s->m; ++j) kb += used[j];
+            const uint64_t row_cost = kb <= kVbPvDims ? 10 : 30;
+            if (sum_k >= row_cost * kb) return MDRQ_PATH_VAFILE_BATCH;
+            return MDRQ_PATH_VAFILE;
+        }
         if (va) return MDRQ_PATH_VAFILE;
         // multi-query columnar pass (<= 32 queries per read of the union's
         // columns): counts from 2 queries, ids from 4 (its masks + expansion
@@ -1481,7 +1503,7 @@ int query_ids_impl(mdrq_store* s, const float* lower, const float* upper, uint32
         static const bool tdbg = getenv("MDRQ_DEBUG_TIMING") != nullptr;
         auto now = [] { return std::chrono::steady_clock::now(); };
         const auto t0 = now();
-        build_descs(s, lower, upper, nq, resolve_path(s, path, nq, true), true, b);
+        build_descs(s, lower, upper, nq, resolve_path(s, path, nq, true, lower, upper), true, b);
         const auto t1 = now();
         // no synchronisation here: this call synchronises before it returns,
         // so the host descriptors stay untouched until their copies are done
@@ -1829,7 +1851,7 @@ int mdrq_query_count(mdrq_store* s, const float* lower, const float* upper, uint
         DeviceGuard dg(s->device);
         mdrq_batch* b = &s->scratch;
         b->owner = s;
-        build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false), true, b);
+        build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false, lower, upper), true, b);
         upload_batch(s, b, false);   // synchronised below, before the descriptors change
         enqueue(s, b, false, s->stream);
         // counts through the pinned bounce buffer (the cached ids, if any,
@@ -1965,7 +1987,8 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             }
             mdrq_batch* b = &sl.b;
             const uint32_t nq = nqs[k];
-            build_descs(s, lower + q0[k] * s->m, upper + q0[k] * s->m, nq, resolve_path(s, path, nq, true), true, b);
+            build_descs(s, lower + q0[k] * s->m, upper + q0[k] * s->m, nq,
+                        resolve_path(s, path, nq, true, lower + q0[k] * s->m, upper + q0[k] * s->m), true, b);
             upload_batch(s, b, false);
             b->own_pool = !want_pack(nq);
             sl.q_split = b->own_pool ? 0u
@@ -2221,7 +2244,7 @@ int mdrq_batch_prepare(mdrq_store* s, const float* lower, const float* upper, ui
         try {
             b->owner = s;
             // the ids flavour of AUTO is resolved at run time
-            build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false), true, b);
+            build_descs(s, lower, upper, nq, resolve_path(s, path, nq, false, lower, upper), true, b);
             upload_batch(s, b);
             s->batches.insert(b);
         } catch (...) {

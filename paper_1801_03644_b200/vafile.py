@@ -131,7 +131,8 @@ class VaFile:
             if q.m != self.m:
                 raise ValueError(f"query has {q.m} dimensions, grid has {self.m}")
         lo, hi = stack_queries(queries, self.m)
-        # the planner: >= 10 queries go through the bit-sliced multi-query
+        # the planner: a batch whose queries' dims sum to >= 10x the union's
+        # (10 full-match queries) goes through the bit-sliced multi-query
         # pass (<= 1024 queries per pass over the code planes)
         offs, ids = self.store.ids(lo, hi, "auto")
         if self._ids is not None:

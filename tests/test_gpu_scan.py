@@ -716,3 +716,35 @@ def test_reference_api_batches_use_the_multi_query_passes(gpu):
             assert np.array_equal(streamed[1].ids.astype(np.int64), exp_ids[:exp_offs[7]])
         finally:
             m.close()
+
+
+def test_planner_batches_when_the_rows_pay(gpu):
+    """MDRQ_PATH_AUTO on a VA-file store (store.cu resolve_path): the
+    bit-sliced pass when the queries' dims sum to >= 10x the union's dims (and
+    there are >= 10 queries), else one VA scan per query -- full-match
+    batches from 10 queries on, sparse partial-match batches later; either
+    way the ids are the oracle's."""
+    rng = np.random.default_rng(77)
+    n, m = 60_000, 12
+    v = rng.random((n, m), dtype=np.float32)
+
+    def batch(nq, k):
+        lo = np.full((nq, m), -np.inf, np.float32)
+        hi = np.full((nq, m), np.inf, np.float32)
+        for q in range(nq):
+            dims = rng.choice(m, size=k, replace=False)
+            a = rng.random(k) * 0.5
+            lo[q, dims] = a
+            hi[q, dims] = a + 0.5
+        return lo, hi
+
+    with gpu.DeviceStore(v, layouts=1 | 4, va_bits=8) as st_:
+        for nq, k, want in ((9, 12, "vafile"), (10, 12, "vafile_batch"), (16, 2, "vafile"),
+                            (59, 2, "vafile"), (64, 2, "vafile_batch"), (1024, 1, "vafile_batch")):
+            lo, hi = batch(nq, k)
+            b = st_.prepare(lo, hi, "auto")
+            assert b.info()["path"] == want, (nq, k, b.info())
+            b.close()
+            eo, ei = oracle.ids_batch(v, lo, hi)
+            offs, ids = st_.ids(lo, hi, "auto")
+            assert np.array_equal(offs, eo) and np.array_equal(ids.astype(np.int64), ei), (nq, k)
