@@ -422,6 +422,9 @@ def main():
     prof_count = batch.profile(ids=False, stream=sptr)
     stats_count = store.stats(nq)
     roof_count = roofline_of(binfo["path"], prof_count, stats_count, n, nq, 0, peak, peak_kind)
+    if binfo["path"] == "vafile_batch" and roof_count["class"] == "scan":
+        roof_count.update(ncu_traffic(f"va_batch_kernel<0, {binfo['max_union_dims']}, "
+                                      f"{vb_lw(min(nq, 1024), binfo['max_union_dims'])}>"))
     add_peaks(roof_count, rpeak)
 
     # ---- the single-query columnar scan kernel (HBM-bound by design), same

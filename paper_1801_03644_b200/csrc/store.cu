@@ -349,6 +349,7 @@ struct mdrq_store {
     // share of a packed batch's queries that travel packed (the rest raw):
     // steered so the PCIe copy and the host unpack of a batch take equally long
     double stream_pack_share = 0.85;
+    bool stream_no_pack = false;     // the host could not pin the packed copies' staging
     // pinned bounce buffer of the synchronous ids calls: the offsets, the VA
     // overflow flag and a speculative prefix of the ids come back in one
     // copy + one synchronisation; bounce_ids = ids of the last call held in
@@ -1930,7 +1931,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
         const uint32_t hb0 = s->id_base >> 16;
         const uint32_t nbuckets = s->n ? uint32_t(((uint64_t(s->id_base) + s->n - 1) >> 16) - hb0 + 1) : 1;
         auto want_pack = [&](uint32_t nq) {
-            if (!nq || !s->n || pk_mode == 0) return false;
+            if (!nq || !s->n || pk_mode == 0 || s->stream_no_pack) return false;
             if (pk_mode > 0) return true;
             return s->stream_per_query >= uint64_t(32) * nbuckets;
         };
@@ -1991,6 +1992,18 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
                         resolve_path(s, path, nq, true, lower + q0[k] * s->m, upper + q0[k] * s->m), true, b);
             upload_batch(s, b, false);
             b->own_pool = !want_pack(nq);
+            if (!b->own_pool) {
+                // the packed copy lands in pinned staging: if the host cannot
+                // pin it, this store's streams stay raw
+                try {
+                    sl.h_lo16.reserve(size_t(s->stream_hint + s->stream_hint / 8 + 4096));
+                    sl.h_ends.reserve(size_t(nq) * nbuckets);
+                } catch (const Error&) {
+                    cudaGetLastError();
+                    s->stream_no_pack = true;
+                    b->own_pool = true;
+                }
+            }
             sl.q_split = b->own_pool ? 0u
                                      : std::min<uint32_t>(nq, std::max<uint32_t>(1, uint32_t(s->stream_pack_share * nq + 0.5)));
             b->packed_to = sl.q_split;
