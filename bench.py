@@ -652,6 +652,15 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
     for _ in range(sync_n):
         store.ids(lo, hi, args.path, out=pinned[0])
     sync_s = (time.perf_counter() - t0) / sync_n
+    # count-only mode through the same API: one count_batch call per step
+    # (bounds host->device, the multi-query count passes, the counts back)
+    counts = method.count_batch(queries)   # warm
+    assert int(counts.sum()) == total_local, "count_batch differs from the ids total"
+    count_n = 5
+    t0 = time.perf_counter()
+    for _ in range(count_n):
+        method.count_batch(queries)
+    count_s = max_over_ranks((time.perf_counter() - t0) / count_n, world)
     e2e_s = max_over_ranks(e2e_s, world)
     sync_s = max_over_ranks(sync_s, world)
     # the bound of e2e: this box's pinned device->host bandwidth for one copy
@@ -689,6 +698,9 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
                              "peak_kind": "measured in this run: one pinned copy of min(result, 4 GB) per GPU"},
             "sync_call": {"value": n_total * nq / sync_s, "ms_per_step": sync_s * 1e3,
                           "api": "DeviceStore.ids into a pinned buffer, one synchronous call per step"},
+            "count_call": {"value": n_total * nq / count_s, "ms_per_step": count_s * 1e3,
+                           "d2h_bytes_per_step": nq * 8 * world,
+                           "api": "VaFile.count_batch (count-only mode), one synchronous call per step"},
             "pin_s": round(pin_s, 2)}
 
 

@@ -18,6 +18,8 @@ namespace mdrq {
 
 namespace {
 
+constexpr uint64_t kPackSeg = 16384;   // ids per CTA step within one list
+
 // One CTA per query run (grid-strided).  ends[q][b] = number of ids of query
 // q in buckets <= b (positions relative to the run), b relative to hb0.
 // Sorted bit-sliced batches (vabatch.cu) hold their lists in slot order: list
@@ -30,7 +32,9 @@ __global__ void __launch_bounds__(256) pack_ids16_kernel(const uint32_t* __restr
                                                          const uint32_t* __restrict__ perm,
                                                          const unsigned long long* __restrict__ src_off,
                                                          uint64_t src_cap) {
-    for (uint32_t i0 = blockIdx.x; i0 < nq; i0 += gridDim.x) {
+    // blockIdx.y strides over the lists, blockIdx.x over kPackSeg-id segments
+    // of one list (a batch of few long lists still fills the device)
+    for (uint32_t i0 = blockIdx.y; i0 < nq; i0 += gridDim.y) {
         const uint32_t q = perm ? perm[i0] : i0;
         if (q >= q_to) continue;   // this query's ids travel raw
         const uint64_t o0 = offsets[q], o1 = offsets[q + 1];
@@ -39,12 +43,15 @@ __global__ void __launch_bounds__(256) pack_ids16_kernel(const uint32_t* __restr
         if (perm && src_off[i0] + cnt > src_cap) continue;
         uint32_t* e = ends + uint64_t(q) * nbuckets;
         if (cnt == 0) {
-            for (uint32_t b = threadIdx.x; b < nbuckets; b += blockDim.x) e[b] = 0;
+            if (blockIdx.x == 0)
+                for (uint32_t b = threadIdx.x; b < nbuckets; b += blockDim.x) e[b] = 0;
             continue;
         }
         const uint32_t* s = ids + (perm ? src_off[i0] : o0);
         uint16_t* d = lo16 + o0;
-        for (uint64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        for (uint64_t seg = uint64_t(blockIdx.x) * kPackSeg; seg < cnt; seg += uint64_t(gridDim.x) * kPackSeg)
+        for (uint64_t i = seg + threadIdx.x, i1 = seg + kPackSeg < cnt ? seg + kPackSeg : cnt; i < i1;
+             i += blockDim.x) {
             const uint32_t id = __ldcs(s + i);
             d[i] = uint16_t(id);
             const uint32_t hb = (id >> 16) - hb0;
@@ -66,9 +73,11 @@ void launch_pack_ids16(const uint32_t* ids, const unsigned long long* offsets, u
                        cudaStream_t st) {
     if (!nq || !q_to) return;
     if (!perm) nq = std::min(nq, q_to);   // lists in query order: only the packed ones
-    const uint32_t grid = std::min<uint32_t>(nq, uint32_t(num_sms) * 8);
-    pack_ids16_kernel<<<grid, 256, 0, st>>>(ids, offsets, nq, q_to, cap, hb0, nbuckets, lo16, ends, perm, src_off,
-                                            src_cap);
+    const uint32_t want = uint32_t(num_sms) * 8;
+    const uint32_t gy = std::min<uint32_t>(nq, want);
+    const uint32_t gx = std::min<uint32_t>(64, std::max<uint32_t>(1, want / gy));
+    pack_ids16_kernel<<<dim3(gx, gy), 256, 0, st>>>(ids, offsets, nq, q_to, cap, hb0, nbuckets, lo16, ends, perm,
+                                                    src_off, src_cap);
 }
 
 }  // namespace mdrq

@@ -1996,8 +1996,13 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
                 // the packed copy lands in pinned staging: if the host cannot
                 // pin it, this store's streams stay raw
                 try {
-                    sl.h_lo16.reserve(size_t(s->stream_hint + s->stream_hint / 8 + 4096));
-                    sl.h_ends.reserve(size_t(nq) * nbuckets);
+                    const size_t need_lo = size_t(s->stream_hint + s->stream_hint / 8 + 4096);
+                    const size_t need_en = size_t(nq) * nbuckets;
+                    if (need_lo > sl.h_lo16.cap || need_en > sl.h_ends.cap) {
+                        sl.join();   // the slot's last unpack still reads the staging
+                        sl.h_lo16.reserve(need_lo);
+                        sl.h_ends.reserve(need_en);
+                    }
                 } catch (const Error&) {
                     cudaGetLastError();
                     s->stream_no_pack = true;
@@ -2124,6 +2129,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             uint32_t* out = ids_out[k];
             const uint32_t nq = sl.q_split;
             StreamSlot* slp = &sl;
+            sl.join();
             sl.unpack = std::thread([=] {
                 const auto t0 = std::chrono::steady_clock::now();
                 mdrq_unpack_ids16(lo, en, of, nq, hb0, nbuckets, out, pk_threads);

@@ -1,6 +1,6 @@
 // unpack_host.cpp -- host side of the 16-bit id packing (pack.cu): rebuild
 // the uint32 ids of a batch from their low halves and the per-query bucket
-// ends, on `threads` host threads (the queries split by id count).  Plain
+// ends, on `threads` host threads (equal shares of the ids).  Plain
 // C++ (g++), AVX2 where the CPU has it; exported as mdrq_unpack_ids16.
 //
 // A thread's queries are one contiguous range of the output, walked 16 ids
@@ -112,19 +112,26 @@ __attribute__((target("avx2"))) void unpack_avx2(const uint16_t* lo16, uint32_t*
 }
 #endif
 
-// queries [q0, q1): output positions offsets[q0] .. offsets[q1]
-void unpack_range(const uint16_t* lo16, const uint32_t* ends, const uint64_t* offsets, uint32_t q0, uint32_t q1,
-                  uint32_t hb0, uint32_t nbuckets, uint32_t* out) {
-    const uint64_t p0 = offsets[q0], p1 = offsets[q1];
+// output positions [p0, p1) of the queries [0, nq): the cursor starts in the
+// query and bucket that hold p0 (binary searches), so a thread's share is a
+// range of ids, not of queries -- a batch of few long lists still uses every
+// thread
+void unpack_range(const uint16_t* lo16, const uint32_t* ends, const uint64_t* offsets, uint32_t nq, uint64_t p0,
+                  uint64_t p1, uint32_t hb0, uint32_t nbuckets, uint32_t* out) {
     if (p0 >= p1) return;
-    Cursor c{ends, offsets, nbuckets, hb0, q0, q1, 0, 0, 0};
+    // last query whose list starts at or before p0 and is not empty up to p0
+    const uint32_t q = uint32_t(std::upper_bound(offsets, offsets + nq + 1, p0) - offsets) - 1;
+    const uint32_t* e = ends + uint64_t(q) * nbuckets;
+    const uint32_t rel = uint32_t(p0 - offsets[q]);
+    const uint32_t b = uint32_t(std::upper_bound(e, e + nbuckets, rel) - e);   // first bucket ending after rel
+    Cursor c{ends, offsets, nbuckets, hb0, q, nq, b < nbuckets ? b : nbuckets - 1, 0, 0};
     c.load();
 #if defined(__x86_64__)
     if (__builtin_cpu_supports("avx2")) {
         // MDRQ_UNPACK_NT=0: regular stores (measurement switch)
         static const bool nt = [] {
-            const char* e = getenv("MDRQ_UNPACK_NT");
-            return !(e && e[0] == '0');
+            const char* env = getenv("MDRQ_UNPACK_NT");
+            return !(env && env[0] == '0');
         }();
         if (nt)
             unpack_avx2<true>(lo16, out, p0, p1, c);
@@ -142,27 +149,21 @@ extern "C" int mdrq_unpack_ids16(const uint16_t* lo16, const uint32_t* ends, con
                                  uint32_t hb0, uint32_t nbuckets, uint32_t* out, int threads) {
     if (nq && (!lo16 || !ends || !offsets || !out || !nbuckets)) return -1;
     if (!nq) return 0;
-    int T = threads > 0 ? threads : int(std::thread::hardware_concurrency());
-    T = std::max(1, std::min<int>(T, int(nq)));
-    const uint64_t total = offsets[nq] - offsets[0];
-    if (T == 1 || total < (1u << 20)) {
-        unpack_range(lo16, ends, offsets, 0, nq, hb0, nbuckets, out);
+    int T = std::max(1, threads > 0 ? threads : int(std::thread::hardware_concurrency()));
+    const uint64_t first = offsets[0], total = offsets[nq] - offsets[0];
+    T = int(std::min<uint64_t>(uint64_t(T), std::max<uint64_t>(1, total >> 20)));   // >= 1 Mi ids per thread
+    if (T == 1) {
+        unpack_range(lo16, ends, offsets, nq, first, first + total, hb0, nbuckets, out);
         return 0;
     }
-    // query ranges of about equal id counts
-    std::vector<uint32_t> cut(size_t(T) + 1, nq);
-    cut[0] = 0;
-    uint32_t q = 0;
-    for (int t = 1; t < T; ++t) {
-        const uint64_t want = offsets[0] + total * uint64_t(t) / uint64_t(T);
-        while (q < nq && offsets[q] < want) ++q;
-        cut[t] = q;
-    }
+    // equal shares of the ids, cut at multiples of 16 positions
     std::vector<std::thread> th;
     th.reserve(size_t(T));
-    for (int t = 0; t < T; ++t)
-        if (cut[t] < cut[t + 1])
-            th.emplace_back(unpack_range, lo16, ends, offsets, cut[t], cut[t + 1], hb0, nbuckets, out);
+    for (int t = 0; t < T; ++t) {
+        const uint64_t a = first + (total * uint64_t(t) / uint64_t(T) & ~uint64_t(15));
+        const uint64_t b = t + 1 == T ? first + total : first + (total * uint64_t(t + 1) / uint64_t(T) & ~uint64_t(15));
+        if (a < b) th.emplace_back(unpack_range, lo16, ends, offsets, nq, a, b, hb0, nbuckets, out);
+    }
     for (auto& x : th) x.join();
     return 0;
 }

@@ -168,3 +168,22 @@ def test_unpack_ids16_rebuilds_the_ids(threads):
     assert rc == 0
     assert np.array_equal(out[: ids.size], ids)
     assert (out[ids.size:] == 0xDEADBEEF).all()
+
+
+def test_unpack_ids16_few_long_lists():
+    """Threads share the ids, not the queries: three lists (one empty between
+    two long ones) on 16 threads, every thread starting inside a list."""
+    from paper_1801_03644_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(3)
+    n = 40_000_000
+    runs = [np.sort(rng.choice(n, 6_000_000, replace=False)).astype(np.uint32), np.empty(0, np.uint32),
+            np.sort(rng.choice(n, 9_000_000, replace=False)).astype(np.uint32)]
+    offsets = np.concatenate([[0], np.cumsum([r.size for r in runs])]).astype(np.uint64)
+    ids = np.concatenate(runs)
+    nbuckets = ((n - 1) >> 16) + 1
+    lo16, ends = _pack_ids16(offsets.astype(np.int64), ids, 0, nbuckets)
+    out = np.zeros(ids.size, np.uint32)
+    rc = lib.mdrq_unpack_ids16(lo16.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)), ends.ctypes.data_as(_lib.u32p),
+                               offsets.ctypes.data_as(_lib.u64p), 3, 0, nbuckets, out.ctypes.data_as(_lib.u32p), 16)
+    assert rc == 0 and np.array_equal(out, ids)
