@@ -689,8 +689,8 @@ def measure_e2e(store, lo, hi, args, total_local, nq, n_total, world, stream):
             "packed_batches": f"{packed} of {e2e_steps}: ids leave the device as 16-bit low halves + per-query "
                               "bucket ends and are rebuilt to uint32 on the host threads (mdrq_unpack_ids16)",
             "packed_share": {"value": info.get("packed_share"),
-                             "note": "share of a batch's queries sent packed (the rest raw), steered so the PCIe "
-                                     "copy and the host unpack of a batch take about as long"},
+                             "note": "share of a batch's queries sent packed (the rest raw), steered to the "
+                                     "shortest measured step period of the stream"},
             "unpacked": {"ms_per_step": raw_s * 1e3, "value": n_total * nq / raw_s,
                          "note": f"MDRQ_STREAM_PACK=0, {raw_steps} steps: raw uint32 ids over PCIe"},
             "d2h_roofline": {"achieved_gbs": d2h / e2e_s / 1e9, "peak_gbs": d2h_peak,

@@ -206,9 +206,10 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
  * host step: out[offsets[q] + i] = (hb0 + b) << 16 | lo16[offsets[q] + i] for
  * ends[q][b-1] <= i < ends[q][b] (ends: nq x nbuckets, positions relative to
  * the query's list; offsets: nq + 1).  It needs no device.
- * A packed batch sends only a share of its queries packed and the rest raw,
- * the share steered so the PCIe copy and the host unpack of a batch take
- * about as long (MDRQ_STREAM_PACK_SHARE fixes it, 0..1).
+ * A packed batch sends only a share of its queries packed and the rest raw;
+ * the share follows the stream's measured step period (hill climbing: the
+ * copy and the unpack share the host's memory bandwidth;
+ * MDRQ_STREAM_PACK_SHARE fixes it, 0..1).
  * mdrq_stream_info: out[0] = device->host bytes of the store's last stream
  * call, out[1] = batches of it that were packed, out[2] = its batches,
  * out[3] = the current packed share of a batch's queries, in 1/1000.        */

@@ -347,8 +347,10 @@ struct mdrq_store {
     uint64_t stream_hint = 0;        // largest batch total seen by the stream (pre-sizes fresh slot pools)
     uint64_t stream_per_query = 0;   // largest ids-per-query average of a stream batch (packed copies or not)
     // share of a packed batch's queries that travel packed (the rest raw):
-    // steered so the PCIe copy and the host unpack of a batch take equally long
+    // steered to the shortest step period of the stream
     double stream_pack_share = 0.85;
+    double stream_hc_last = 0;       // hill climbing on the step period: the last window's mean
+    int stream_hc_dir = -1;          // and the direction of the last move
     bool stream_no_pack = false;     // the host could not pin the packed copies' staging
     // pinned bounce buffer of the synchronous ids calls: the offsets, the VA
     // overflow flag and a speculative prefix of the ids come back in one
@@ -1970,11 +1972,30 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             if (sdbg)
                 fprintf(stderr, "[stream] copy %.1f ms, unpack %.1f ms at packed share %.2f\n", copy_ms, sl.unpack_ms,
                         s->stream_pack_share);
-            if (sh_env || copy_ms <= 0 || sl.unpack_ms <= 0) return;
-            if (sl.unpack_ms > 1.10 * copy_ms)
-                s->stream_pack_share = std::max(0.5, s->stream_pack_share - 0.02);
-            else if (copy_ms > 1.10 * sl.unpack_ms)
-                s->stream_pack_share = std::min(1.0, s->stream_pack_share + 0.02);
+        };
+        // The share follows the stream's step period (the interval between two
+        // batches' copies being enqueued), not the two times above: copy and
+        // unpack share the host's memory bandwidth, so a longer copy can call
+        // for FEWER packed queries.  Hill climbing: every three packed
+        // batches the mean of the last two periods is compared with the
+        // previous window's; worse -> turn around; then one 0.04 step.
+        double hc_prev_t = -1, hc_acc = 0;
+        int hc_n = 0;
+        auto climb = [&](bool packed_batch) {
+            const double t = since();
+            const double period = hc_prev_t >= 0 ? t - hc_prev_t : -1;
+            hc_prev_t = t;
+            if (sh_env || !packed_batch || period <= 0) return;
+            if (++hc_n == 1) return;   // the first period after a move still mixes both shares
+            hc_acc += period;
+            if (hc_n < 3) return;
+            const double avg = hc_acc / 2;
+            hc_n = 0;
+            hc_acc = 0;
+            if (s->stream_hc_last > 0 && avg > 0.995 * s->stream_hc_last) s->stream_hc_dir = -s->stream_hc_dir;
+            s->stream_hc_last = avg;
+            s->stream_pack_share = std::min(1.0, std::max(0.4, s->stream_pack_share + 0.04 * s->stream_hc_dir));
+            if (sdbg) fprintf(stderr, "[stream] period %.1f ms -> packed share %.2f\n", avg, s->stream_pack_share);
         };
         s->stream_d2h = s->stream_packed = 0;
         s->stream_batches = nbatches;
@@ -2114,6 +2135,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             }
             CK(cudaEventRecord(sl.copy, s->copy_stream));
             sl.busy = true;
+            climb(sl.packed && k >= 2);
             if (sdbg) fprintf(stderr, "[stream] %8.1f finish %u: copies enqueued\n", since(), k);
         };
         // batch k's ids rebuilt from its packed copy, on host threads, while
