@@ -348,7 +348,7 @@ struct mdrq_store {
     uint64_t stream_per_query = 0;   // largest ids-per-query average of a stream batch (packed copies or not)
     // share of a packed batch's queries that travel packed (the rest raw):
     // steered to the shortest step period of the stream
-    double stream_pack_share = 0.85;
+    double stream_pack_share = 1.0;
     double stream_hc_last = 0;       // hill climbing on the step period: the last window's mean
     int stream_hc_dir = -1;          // and the direction of the last move
     bool stream_no_pack = false;     // the host could not pin the packed copies' staging
