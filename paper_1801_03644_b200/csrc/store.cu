@@ -1928,7 +1928,13 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             // one process per GPU: the node's ranks share the host threads
             const char* lw = getenv("LOCAL_WORLD_SIZE");
             const int ranks = lw ? std::max(1, std::atoi(lw)) : 1;
-            pk_threads = std::max(1, int(std::thread::hardware_concurrency()) / ranks);
+            // three quarters of the rank's share: the unpack is memory-bound
+            // well before that (25 G ids/s alone on 16 threads, 23 on 12) and
+            // the stream's own thread keeps building the next batches
+            // (C5 stream on a slow-host box: 349 / 337 / 336 ms per step on
+            // 16 / 12 / 8 threads)
+            const int hc = std::max(1, int(std::thread::hardware_concurrency()) / ranks);
+            pk_threads = std::max(1, hc - hc / 4);
         }
         const uint32_t hb0 = s->id_base >> 16;
         const uint32_t nbuckets = s->n ? uint32_t(((uint64_t(s->id_base) + s->n - 1) >> 16) - hb0 + 1) : 1;
