@@ -1964,20 +1964,21 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
                                   sl.d_ends.p, nullptr, nullptr, 0, s->num_sms, s->stream);
         };
         // MDRQ_STREAM_PACK_SHARE fixes the packed share of a batch's queries
-        // (0..1); otherwise it follows the measured copy and unpack times
+        // (0..1); otherwise it follows the stream's step period (climb, below)
         const char* sh_env = getenv("MDRQ_STREAM_PACK_SHARE");
         if (sh_env) s->stream_pack_share = std::min(1.0, std::max(0.0, std::atof(sh_env)));
-        auto steer = [&](StreamSlot& sl) {
+        // MDRQ_DEBUG_STREAM: the copy and unpack times of a slot's last batch
+        auto report_times = [&](StreamSlot& sl) {
             if (!sl.measured) return;
             sl.measured = false;
+            if (!sdbg) return;
             float copy_ms = 0;
             if (cudaEventElapsedTime(&copy_ms, sl.cp0, sl.cp1) != cudaSuccess) {
                 cudaGetLastError();
                 return;
             }
-            if (sdbg)
-                fprintf(stderr, "[stream] copy %.1f ms, unpack %.1f ms at packed share %.2f\n", copy_ms, sl.unpack_ms,
-                        s->stream_pack_share);
+            fprintf(stderr, "[stream] copy %.1f ms, unpack %.1f ms at packed share %.2f\n", copy_ms, sl.unpack_ms,
+                    s->stream_pack_share);
         };
         // The share follows the stream's step period (the interval between two
         // batches' copies being enqueued), not the two times above: copy and
@@ -2113,7 +2114,7 @@ int mdrq_query_ids_stream(mdrq_store* s, const float* lower, const float* upper,
             } else if (total && sl.packed) {
                 // the staging still feeds the unpack of the slot's previous batch
                 sl.join();
-                steer(sl);
+                report_times(sl);
                 // ids [0, split) belong to the packed queries, [split, total) travel raw
                 const uint64_t split = std::min<uint64_t>(sl.h_flags[2], total);
                 sl.h_lo16.reserve(size_t(total + total / 8 + 4096));
